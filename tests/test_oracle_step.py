@@ -1,0 +1,258 @@
+"""Pins of the oracle's collision step (A3-A9) against closed forms, limits,
+invariants and the literal recursive algorithm.  No GPU needed.
+
+Closed forms used (derivations in DESIGN.md §5):
+  Maxwell molecules, isotropic scattering, s = mu t / eps:
+    Pxx(s) - T = (Pxx0 - T) e^{-s/2}
+    y(s) = (y0 - |A|^2/2) e^{-s/3} + (|A|^2/2) e^{-s},  y = M4c - 15 T^2
+  one truncated step (eq. WST):  A <- R_m(tau) A,
+    R_m = (1 - tau) sum_{k<=m} tau^k C(2k,k)/4^k
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+
+
+def _hom(orc, cfg, v, offsets, **kw):
+    return orc.HomogeneousState(cfg, v[0], v[1], v[2], offsets, **kw)
+
+
+def _centred(vx, vy, vz):
+    v = np.stack([vx, vy, vz])
+    v = v - v.mean(1, keepdims=True)
+    P = v @ v.T / v.shape[1]
+    T = np.trace(P) / 3
+    A = P - T * np.eye(3)
+    M4c = ((v * v).sum(0) ** 2).mean()
+    return T, A, M4c
+
+
+@pytest.mark.parametrize("model,adaptive", [(0, 0), (1, 0), (1, 1), (0, 1)])
+def test_conservation_per_cell(orc, model, adaptive):
+    """Mass exact; momentum and energy per cell to 1e-12 (property (i))."""
+    vx, vy, vz, off = synth.ragged_cells(40, 300, seed=3)
+    cfg = orc.Config(model=model, adaptive=adaptive, m_fixed=6, m_init=2, m_cap=64, eps=0.3,
+                     dt=0.2, seed=4)
+    st = orc.HomogeneousState(cfg, vx, vy, vz, off)
+    m0 = st.moments()
+    st.step(5)
+    m1 = st.moments()
+    assert np.array_equal(m0[:, 0], m1[:, 0])
+    n = m0[:, 0:1]
+    scale = np.sqrt(m0[:, 6:7] * 2) + 1e-300        # sqrt(mean |v|^2) (rho = 1)
+    np.testing.assert_allclose(m1[:, 2:5] * n, m0[:, 2:5] * n, rtol=0, atol=1e-12 * (n * scale).max())
+    np.testing.assert_allclose(m1[:, 6], m0[:, 6], rtol=1e-12, atol=1e-300)
+    s = st.stats
+    assert np.all(s["leaves"] + s["untouched"] + s["thermalised"] == s["n"])
+
+
+def test_tau_to_zero_is_identity(orc):
+    """tau -> 0: no collisions, f^{n+1} = f^n."""
+    v = synth.two_maxwellians(5000, seed=2)
+    st = _hom(orc, orc.Config(model=1, eps=1.0, dt=1e-15), v, [0, 5000])
+    st.step(3)
+    assert np.array_equal(st.vx, v[0]) and np.array_equal(st.vz, v[2])
+
+
+def test_tau_to_one_is_maxwellian(orc):
+    """AP: mu dt/eps -> infinity gives the local Maxwellian with exact moments."""
+    from scipy import stats
+    v = synth.anisotropic_gaussian(50_000, seed=3)
+    st = _hom(orc, orc.Config(model=1, eps=1e-6, dt=0.05), v, [0, 50_000])
+    m0 = st.moments()[0]
+    st.step(1)
+    m1 = st.moments()[0]
+    assert st.stats["thermalised"][0] == 50_000 and st.stats["proposals"][0] == 0
+    np.testing.assert_allclose(m1[2:5], m0[2:5], atol=1e-14)
+    assert m1[5] == pytest.approx(m0[5], rel=1e-12)
+    T = m1[5]
+    for comp in (st.vx, st.vy, st.vz):
+        z = (comp - comp.mean()) / math.sqrt(T)
+        assert stats.kstest(z, "norm").pvalue > 1e-3
+    # isotropised: Pxx = T within sampling error
+    assert abs(m1[8] - T) < 5 * math.sqrt(2 / 50_000) * T
+
+
+def test_maxwell_closed_form_relaxation(orc):
+    """Config-1 shape (two Maxwellians at +-2): 20 steps of dt = 0.1, m = 64 (untruncated),
+    16 seeds: Pxx and centred M4 follow the Maxwell-molecule closed forms."""
+    n, steps, dt = 20_000, 20, 0.1
+    dP, dM = [], []
+    for seed in range(1, 17):
+        v = synth.two_maxwellians(n, seed=seed)
+        T, A, M4c0 = _centred(*v)
+        st = _hom(orc, orc.Config(model=0, m_fixed=64, eps=1.0, dt=dt, seed=seed), v, [0, n])
+        st.step(steps)
+        m = st.moments()[0]
+        s = steps * dt
+        a2 = (A * A).sum()
+        y0 = M4c0 - 15 * T * T
+        dP.append((m[8] - T) - A[0, 0] * math.exp(-s / 2))
+        dM.append((m[10] - 15 * T * T) - ((y0 - a2 / 2) * math.exp(-s / 3) + a2 / 2 * math.exp(-s)))
+    dP, dM = np.array(dP), np.array(dM)
+    # allowance 10/n: finite-N bias of the particle system (same for the literal algorithm)
+    assert abs(dP.mean()) < 4 * dP.std() / 4 + 10.0 / n * 5
+    assert abs(dM.mean()) < 4 * dM.std() / 4 + 10.0 / n * 80
+    # and the change itself is resolved: M4c moved by ~3 while the error is ~0.2
+    assert abs(dM.mean()) < 0.1 * 3.0
+
+
+@pytest.mark.parametrize("m,R", [(1, 0.625), (2, 0.671875)])
+def test_truncated_map_R_m(orc, m, R):
+    """One step at tau = 1/2 with truncation m: A <- R_m(tau) A (eq. WST with
+    r_k = C(2k,k)/4^k); m = 1, 2 are the paper's first/second-order TRMC."""
+    n = 100_000
+    ratios = []
+    for seed in range(1, 9):
+        v = synth.anisotropic_gaussian(n, seed=seed)
+        T, A, _ = _centred(*v)
+        st = _hom(orc, orc.Config(model=0, m_fixed=m, eps=1.0, dt=math.log(2.0), seed=seed),
+                  v, [0, n])
+        st.step(1)
+        T1, A1, _ = _centred(st.vx, st.vy, st.vz)
+        ratios.append(A1[0, 0] / A[0, 0])
+    r = np.array(ratios)
+    assert abs(r.mean() - R) < 4 * r.std() / math.sqrt(len(r)) + 2e-3
+    # resolves neighbouring orders
+    other = 0.671875 if m == 1 else 0.625
+    assert abs(r.mean() - other) > 10 * r.std() / math.sqrt(len(r))
+
+
+@pytest.mark.parametrize("model", [0, 1])
+def test_equilibrium_invariance(orc, model):
+    """A Maxwellian stays Maxwellian (Q(M,M) = 0): M4c = 15 T^2, Pxx = T."""
+    n = 50_000
+    zs4, zsx = [], []
+    for seed in range(1, 9):
+        v = synth.maxwellian(n, seed=seed, u=(0.5, -1.0, 0.2), T=1.5)
+        st = _hom(orc, orc.Config(model=model, m_fixed=16, eps=1.0, dt=0.2, seed=seed), v, [0, n])
+        st.step(4)
+        m = st.moments()[0]
+        T = m[5]
+        zs4.append(m[10] / (15 * T * T) - 1)
+        zsx.append(m[8] / T - 1)
+    for z, sd in ((np.array(zs4), math.sqrt(96 / 225 / n) * 2), (np.array(zsx), math.sqrt(2 / n))):
+        assert abs(z.mean()) < 4 * sd / math.sqrt(len(z)) + 1e-3
+
+
+@pytest.mark.parametrize("model", [0, 1])
+def test_literal_algorithm_equivalence(orc, model):
+    """LS realisation [R2] vs the literal recursive Alg 4.3/4.4: same law of the
+    post-step moments and of the collision count (64 seeds each)."""
+    n, steps = 2000, 3
+    out = {0: [], 1: []}
+    for lit in (0, 1):
+        for seed in range(1, 65):
+            v = synth.two_maxwellians(n, seed=seed)
+            cfg = orc.Config(model=model, m_fixed=8, eps=1.0, dt=0.25 if model == 0 else 0.05,
+                             seed=seed, literal=lit)
+            st = _hom(orc, cfg, v, [0, n])
+            props = 0.0
+            for _ in range(steps):
+                st.step(1)
+                props += st.stats["proposals"][0]
+            m = st.moments()[0]
+            out[lit].append([m[8], m[10], props])
+    a, b = np.array(out[0]), np.array(out[1])
+    for k in range(3):
+        se = math.sqrt(a[:, k].var() / len(a) + b[:, k].var() / len(b))
+        assert abs(a[:, k].mean() - b[:, k].mean()) < 4.5 * se + 1e-9, (k, a[:, k].mean(), b[:, k].mean(), se)
+
+
+def test_hs_majorant_bounds_pairwise_max(orc):
+    """Sigma' = 2 max|v_i - vbar| >= max_{ij} |v_i - v_j|, brute force n = 200."""
+    for seed in range(1, 6):
+        v = synth.two_maxwellians(200, seed=seed)
+        st = _hom(orc, orc.Config(model=1, eps=1.0, dt=0.01, seed=seed), v, [0, 200])
+        st.step(1)
+        V = np.stack(v, 1)
+        pair = np.sqrt(((V[:, None, :] - V[None, :, :]) ** 2).sum(-1)).max()
+        sig = st.stats["sigma"][0]
+        assert sig >= pair * (1 - 1e-15)
+        assert sig == pytest.approx(2 * np.sqrt(((V - V.mean(0)) ** 2).sum(1).max()), rel=1e-14)
+
+
+def test_hs_acceptance_fraction(orc):
+    """Dummy collisions: accepted/proposed = E|q|/Sigma' over the proposed pairs."""
+    n = 20_000
+    v = synth.anisotropic_gaussian(n, seed=5)
+    st = _hom(orc, orc.Config(model=1, eps=1.0, dt=0.05, seed=5), v, [0, n], log_cap=200_000)
+    V = np.stack(v, 1).copy()
+    st.step(1)
+    log = st.collisions()
+    lvl1 = log[log["level"] == 1]                     # level-1 inputs are untouched originals
+    q = np.linalg.norm(V[lvl1["slot_i"]] - V[lvl1["slot_k"]], axis=1)
+    p_acc = q / st.stats["sigma"][0]
+    acc = lvl1["accepted"]
+    se = math.sqrt((p_acc * (1 - p_acc)).sum()) / len(acc)
+    assert abs(acc.mean() - p_acc.mean()) < 4 * se + 1e-4
+
+
+def test_plan_structure(orc):
+    """Tree invariants: slots in range, disjoint within a level, each slot's levels
+    strictly increase (a sample of f_k is consumed only by a higher level), and the
+    per-level count is C_d = ceil((N_d + cons_d)/2)."""
+    n = 3000
+    v = synth.two_maxwellians(n, seed=7)
+    st = _hom(orc, orc.Config(model=1, m_fixed=12, eps=1.0, dt=0.2, seed=7), v, [0, n],
+              log_cap=100_000)
+    st.step(1)
+    log = st.collisions()
+    assert len(log) == st.stats["proposals"][0]
+    assert log["slot_i"].min() >= 0 and log["slot_k"].max() < n
+    for d in np.unique(log["level"]):
+        L = log[log["level"] == d]
+        s = np.concatenate([L["slot_i"], L["slot_k"]])
+        assert len(np.unique(s)) == len(s)
+        assert np.array_equal(np.sort(L["j"]), np.arange(len(L)))
+    last = {}
+    for r in log:                                       # log order = execution order
+        for s in (r["slot_i"], r["slot_k"]):
+            assert last.get(s, 0) < r["level"]
+            last[s] = r["level"]
+    # leaves are exactly the slots touched by collisions
+    assert len(last) == st.stats["leaves"][0]
+
+
+def test_rad_keep_and_extend_prefix(orc):
+    """RAD keeps the collisions of depth m and extends: attempt 0 of a
+    RAD step equals the fixed-m step with m = m_init, draw for draw."""
+    n = 4000
+    v = synth.two_maxwellians(n, seed=8)
+    a = _hom(orc, orc.Config(model=1, adaptive=1, m_init=2, m_cap=64, eps=1.0, dt=0.3, seed=8),
+             v, [0, n], log_cap=100_000)
+    b = _hom(orc, orc.Config(model=1, adaptive=0, m_fixed=2, eps=1.0, dt=0.3, seed=8),
+             v, [0, n], log_cap=100_000)
+    a.step(1)
+    b.step(1)
+    la, lb = a.collisions(), b.collisions()
+    assert a.stats["attempts"][0] > 1                  # far from equilibrium: E1 > delta2
+    np.testing.assert_array_equal(la[la["attempt"] == 0], lb)
+    assert a.stats["m_used"][0] in (4, 8, 16, 32, 64)
+
+
+def test_rad_decision_rule(orc):
+    """E1 < delta1 halves m_max, E1 > delta2 doubles up to the cap."""
+    n = 50_000
+    v = synth.maxwellian(n, seed=2)
+    st = _hom(orc, orc.Config(model=1, adaptive=1, m_init=16, m_cap=64, eps=1.0, dt=0.05,
+                              delta1=0.05, delta2=0.1, seed=2), v, [0, n])
+    seen = []
+    for _ in range(6):
+        st.step(1)
+        s = st.stats[0]
+        seen.append(int(s["m_next"]))
+        if s["E1"] < 0.05:
+            assert s["m_next"] == max(1, s["m_used"] // 2)
+        elif s["E1"] <= 0.1:
+            assert s["m_next"] == s["m_used"]
+    assert seen[-1] < 16                               # equilibrium: m_max shrinks
+    v = synth.two_maxwellians(n, seed=2)
+    st = _hom(orc, orc.Config(model=0, adaptive=1, m_init=2, m_cap=32, eps=1.0, dt=0.2,
+                              seed=2), v, [0, n])
+    st.step(1)
+    s = st.stats[0]
+    assert s["E1"] > 0.01 and s["m_used"] == 32 and s["m_next"] == 32   # forced accept at cap
