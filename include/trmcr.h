@@ -1,0 +1,180 @@
+/*
+ * trmcr.h — C ABI of the B200-native TRMC-R hot path (arXiv:1009.2768).
+ *
+ * One call of trmcr_step() advances every cell by one time step of the
+ * recursive Time-Relaxed Monte Carlo scheme:
+ *   (shock only) A1 free transport x <- x + v_x dt with inflow/outflow
+ *                reservoirs (splitting; boundary states P:971-988)
+ *   (shock only) A2 stable counting sort of the particles by cell
+ *   A3 per-cell moments and majorant Sigma = sigma(2 dv)
+ *   A4 split into collision sets, Alg 4.2 with IR rounding
+ *   A5 recursive collision trees of Alg 4.3/4.4, flattened into a
+ *      level-synchronous work list
+ *   A6 binary (dummy) collisions, eq. Maxwell_coll/n3d
+ *   A7 adaptive truncation TRMC-RAD
+ *   A8 conservative Maxwellian resampling of the truncated set
+ * Paper line numbers "P:nnn" refer to PAPER.md; readings "[Rnn]" to DESIGN.md §2.
+ *
+ * Conventions (all calls):
+ *   - Every call returns trmcr_status; nothing throws across the ABI.
+ *   - Argument errors return TRMCR_EINVAL and set trmcr_last_error(ctx).
+ *   - CUDA failures are sticky: the context returns TRMCR_ESTATE afterwards.
+ *   - A context owns all device buffers it allocates; caller memory passed to
+ *     trmcr_init is COPIED (the caller keeps ownership).  Output pointers
+ *     belong to the caller.
+ *   - One context per device and stream; calls are not thread safe.
+ *   - trmcr_step is asynchronous on the context's stream; calls that return
+ *     host data synchronise that stream.
+ *   - Units: K = 1/(4 pi) [R4]; homogeneous cells have rho = 1.
+ */
+#ifndef TRMCR_H
+#define TRMCR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct trmcr_ctx trmcr_ctx;
+
+typedef enum {
+  TRMCR_OK = 0,
+  TRMCR_EINVAL = 1,     /* bad argument (message in trmcr_last_error)              */
+  TRMCR_ENOMEM = 2,     /* device allocation failed                                */
+  TRMCR_ECUDA = 3,      /* CUDA runtime error                                      */
+  TRMCR_ENCCL = 4,      /* reserved: collective error                              */
+  TRMCR_ECAPACITY = 5,  /* particles or per-cell tree exceeded the capacity        */
+  TRMCR_ESTATE = 6      /* context unusable after an earlier sticky error          */
+} trmcr_status;
+
+typedef enum { TRMCR_MAXWELL = 0, TRMCR_HARD_SPHERE = 1 } trmcr_model;   /* alpha = 0 / 1 */
+typedef enum { TRMCR_F32 = 0, TRMCR_F64 = 1 } trmcr_dtype;
+typedef enum { TRMCR_HOMOGENEOUS = 0, TRMCR_SHOCK_1D = 1 } trmcr_geometry;
+typedef enum { TRMCR_IND_PXX = 0, TRMCR_IND_M4 = 1 } trmcr_indicator;  /* RAD indicator S */
+
+/* Particle ensemble handed to trmcr_init.  Structure of arrays of length n
+ * in `dtype`; device pointers unless `host` = 1.  x (positions) only for the
+ * shock geometry.  Homogeneous: particles must be grouped by cell as
+ * described by trmcr_cells.offsets.  Shock: any order (binned at init). */
+typedef struct {
+  int32_t dtype;             /* trmcr_dtype                                          */
+  int32_t host;              /* 1: pointers are host memory, 0: device memory        */
+  int64_t n;                 /* number of particles                                  */
+  int64_t capacity;          /* particle capacity (shock inflow headroom); 0: auto   */
+  const void *vx, *vy, *vz;  /* velocities                                           */
+  const void *x;             /* positions (shock) or NULL                            */
+} trmcr_particles;
+
+/* Cell geometry.
+ * HOMOGENEOUS: n_cells independent space-homogeneous gases (rho = 1), cell c
+ *   holding particles [offsets[c], offsets[c+1]) (host array of n_cells+1,
+ *   non-decreasing, offsets[0] = 0).
+ * SHOCK_1D: n_cells uniform cells on [x_min, x_max); weight = mass per
+ *   particle; reservoir states (rho,u,T)_{L,R} from Rankine-Hugoniot
+ *   (P:975-985).  offsets must be NULL.
+ * cell_base: global id of local cell 0 (keys the RNG: results do not depend
+ *   on how cells are split across devices). */
+typedef struct {
+  int32_t geometry;          /* trmcr_geometry                                       */
+  int32_t n_cells;
+  int32_t cell_base;
+  int32_t pad;
+  const int64_t *offsets;    /* HOMOGENEOUS: host [n_cells+1]; SHOCK_1D: NULL        */
+  double x_min, x_max, weight;
+  double rho_L, u_L, T_L, rho_R, u_R, T_R;
+} trmcr_cells;
+
+/* Collision kernel and truncation control. */
+typedef struct {
+  int32_t model;             /* trmcr_model                                          */
+  int32_t adaptive;          /* 0: fixed truncation m_fixed (TRMC-R); 1: TRMC-RAD     */
+  int32_t m_fixed;           /* e.g. 64                                              */
+  int32_t m_init;            /* RAD initial m_max (paper: 2)                   */
+  int32_t m_cap;             /* RAD largest m_max (<= 16384)                          */
+  int32_t indicator;         /* trmcr_indicator                                       */
+  double delta1, delta2;     /* RAD interval, 0 < delta1 < delta2 (paper 0.005, 0.01) */
+  uint64_t seed;             /* Philox4x32-10 key                                     */
+} trmcr_kernel;
+
+/* Per-cell statistics row (doubles), trmcr_stats(): */
+enum {
+  TRMCR_ST_N = 0, TRMCR_ST_P, TRMCR_ST_MU, TRMCR_ST_SIGMA, TRMCR_ST_S0, TRMCR_ST_SEST,
+  TRMCR_ST_E1, TRMCR_ST_MUSED, TRMCR_ST_MNEXT, TRMCR_ST_DEPTH, TRMCR_ST_ATTEMPTS,
+  TRMCR_ST_LEAVES, TRMCR_ST_UNTOUCHED, TRMCR_ST_THERMALISED, TRMCR_ST_PROPOSALS,
+  TRMCR_ST_ACCEPTED, TRMCR_ST_VIOLATIONS, TRMCR_ST_MAXW, TRMCR_NSTATS
+};
+/* Per-cell moment row (doubles), trmcr_moments(): */
+enum {
+  TRMCR_MO_N = 0, TRMCR_MO_RHO, TRMCR_MO_UX, TRMCR_MO_UY, TRMCR_MO_UZ, TRMCR_MO_T,
+  TRMCR_MO_E, TRMCR_MO_P, TRMCR_MO_PXX, TRMCR_MO_M4, TRMCR_MO_M4C, TRMCR_MO_MMAX,
+  TRMCR_NMOMENTS
+};
+
+/* Collision decision record (trmcr_get_log), one per tree node. */
+typedef struct {
+  int32_t cell, attempt, level, accepted;
+  int64_t j, slot_i, slot_k;
+} trmcr_coll_rec;
+
+/* Create a context on the current CUDA device, bound to `cuda_stream`
+ * (a cudaStream_t, NULL = legacy default stream).  eps: Knudsen number
+ * (P:127-129), dt: time step, both > 0.  Copies the particles (and bins them
+ * by cell for the shock).  Errors: EINVAL (bad sizes/arguments, eps or dt
+ * <= 0, delta1 >= delta2, offsets not monotone, particle outside the shock
+ * domain), ENOMEM, ECUDA. */
+trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *particles,
+                        const trmcr_cells *cells, double eps, double dt,
+                        const trmcr_kernel *kernel, void *cuda_stream);
+
+/* Advance n_steps >= 0 time steps (asynchronous). */
+trmcr_status trmcr_step(trmcr_ctx *ctx, int32_t n_steps);
+
+/* Per-cell moments of the current state, host out[n_cells * TRMCR_NMOMENTS]. Syncs. */
+trmcr_status trmcr_moments(trmcr_ctx *ctx, double *host_out);
+
+/* Per-cell statistics of the last step, host out[n_cells * TRMCR_NSTATS]. Syncs. */
+trmcr_status trmcr_stats(trmcr_ctx *ctx, double *host_out);
+
+/* Current particle count (shock: changes with inflow/outflow). Syncs. */
+trmcr_status trmcr_num_particles(trmcr_ctx *ctx, int64_t *n);
+
+/* Copy the current state out (cell-sorted).  Pointers are host (host = 1) or
+ * device memory of capacity >= trmcr_num_particles(); x may be NULL;
+ * offsets (n_cells+1 int64, same memory kind) may be NULL. Syncs. */
+trmcr_status trmcr_copy_particles(trmcr_ctx *ctx, void *vx, void *vy, void *vz, void *x,
+                                  int64_t *offsets, int32_t host);
+
+/* Overwrite the velocities (same count and cell layout as the current
+ * state) from host (host = 1) or device memory. Asynchronous. */
+trmcr_status trmcr_set_velocities(trmcr_ctx *ctx, const void *vx, const void *vy,
+                                  const void *vz, int32_t host);
+
+/* Host-buffer step (the e2e path): upload velocities from host memory,
+ * advance one step, download per-cell moments to host_moments
+ * [n_cells * TRMCR_NMOMENTS].  Homogeneous geometry only.  Syncs. */
+trmcr_status trmcr_step_host(trmcr_ctx *ctx, const void *vx, const void *vy, const void *vz,
+                             double *host_moments);
+
+/* Decision log for parity tests: capacity records (0 disables). */
+trmcr_status trmcr_set_log(trmcr_ctx *ctx, int64_t capacity);
+/* Copies min(count, capacity) records to host `out`, *count = records produced
+ * during the last step (may exceed the capacity). Syncs. */
+trmcr_status trmcr_get_log(trmcr_ctx *ctx, trmcr_coll_rec *out, int64_t *count);
+
+/* Number of kernel launches issued by this context so far. */
+int64_t trmcr_launch_count(const trmcr_ctx *ctx);
+
+/* Last error message of ctx (or of the last failed trmcr_init when ctx is NULL). */
+const char *trmcr_last_error(const trmcr_ctx *ctx);
+
+/* Library version / build string. */
+const char *trmcr_version(void);
+
+/* Release every resource of ctx (NULL is a no-op). */
+void trmcr_destroy(trmcr_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRMCR_H */

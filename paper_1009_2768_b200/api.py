@@ -1,0 +1,242 @@
+"""Thin Python binding of the C ABI in include/trmcr.h (argument marshalling only).
+
+Every step of the TRMC-R path runs in the CUDA kernels of libtrmcr.so; this
+module only converts arguments (torch CUDA tensors, numpy arrays) to pointers
+and back.  There is no CPU fallback: a missing library raises at import.
+PyTorch supplies device memory and the stream (P:nnn references: PAPER.md).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtrmcr.so")
+
+OK, EINVAL, ENOMEM, ECUDA, ENCCL, ECAPACITY, ESTATE = range(7)
+MAXWELL, HARD_SPHERE = 0, 1
+F32, F64 = 0, 1
+HOMOGENEOUS, SHOCK_1D = 0, 1
+IND_PXX, IND_M4 = 0, 1
+
+STAT_FIELDS = ["n", "p", "mu", "sigma", "S0", "S_est", "E1", "m_used", "m_next", "depth",
+               "attempts", "leaves", "untouched", "thermalised", "proposals", "accepted",
+               "violations", "maxw"]
+MOMENT_FIELDS = ["n", "rho", "ux", "uy", "uz", "T", "E", "p", "Pxx", "M4", "M4c", "m_max"]
+STATS_DTYPE = np.dtype([(f, "<f8") for f in STAT_FIELDS])
+COLL_DTYPE = np.dtype([("cell", "<i4"), ("attempt", "<i4"), ("level", "<i4"), ("accepted", "<i4"),
+                       ("j", "<i8"), ("slot_i", "<i8"), ("slot_k", "<i8")])
+
+
+class TrmcrError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"trmcr status {status}: {msg}")
+        self.status = status
+
+
+class _Particles(C.Structure):
+    _fields_ = [("dtype", C.c_int32), ("host", C.c_int32), ("n", C.c_int64), ("capacity", C.c_int64),
+                ("vx", C.c_void_p), ("vy", C.c_void_p), ("vz", C.c_void_p), ("x", C.c_void_p)]
+
+
+class _Cells(C.Structure):
+    _fields_ = [("geometry", C.c_int32), ("n_cells", C.c_int32), ("cell_base", C.c_int32),
+                ("pad", C.c_int32), ("offsets", C.POINTER(C.c_int64)),
+                ("x_min", C.c_double), ("x_max", C.c_double), ("weight", C.c_double),
+                ("rho_L", C.c_double), ("u_L", C.c_double), ("T_L", C.c_double),
+                ("rho_R", C.c_double), ("u_R", C.c_double), ("T_R", C.c_double)]
+
+
+class _Kernel(C.Structure):
+    _fields_ = [("model", C.c_int32), ("adaptive", C.c_int32), ("m_fixed", C.c_int32),
+                ("m_init", C.c_int32), ("m_cap", C.c_int32), ("indicator", C.c_int32),
+                ("delta1", C.c_double), ("delta2", C.c_double), ("seed", C.c_uint64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libtrmcr.so (built by __graft_entry__.build() / build.py).  Fails loudly."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1009_2768_b200.build` "
+                              "(no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        vp, P = C.c_void_p, C.POINTER
+        L.trmcr_init.argtypes = [P(vp), P(_Particles), P(_Cells), C.c_double, C.c_double, P(_Kernel), vp]
+        L.trmcr_step.argtypes = [vp, C.c_int32]
+        L.trmcr_moments.argtypes = [vp, P(C.c_double)]
+        L.trmcr_stats.argtypes = [vp, P(C.c_double)]
+        L.trmcr_num_particles.argtypes = [vp, P(C.c_int64)]
+        L.trmcr_copy_particles.argtypes = [vp, vp, vp, vp, vp, vp, C.c_int32]
+        L.trmcr_set_velocities.argtypes = [vp, vp, vp, vp, C.c_int32]
+        L.trmcr_step_host.argtypes = [vp, vp, vp, vp, P(C.c_double)]
+        L.trmcr_set_log.argtypes = [vp, C.c_int64]
+        L.trmcr_get_log.argtypes = [vp, vp, P(C.c_int64)]
+        L.trmcr_launch_count.argtypes = [vp]
+        L.trmcr_launch_count.restype = C.c_int64
+        L.trmcr_last_error.argtypes = [vp]
+        L.trmcr_last_error.restype = C.c_char_p
+        L.trmcr_version.restype = C.c_char_p
+        L.trmcr_destroy.argtypes = [vp]
+        for f in ("trmcr_init", "trmcr_step", "trmcr_moments", "trmcr_stats", "trmcr_num_particles",
+                  "trmcr_copy_particles", "trmcr_set_velocities", "trmcr_step_host", "trmcr_set_log",
+                  "trmcr_get_log"):
+            getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    """(pointer, is_host, dtype) of a torch tensor or numpy array (contiguous)."""
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            assert a.is_contiguous(), "tensor must be contiguous"
+            return a.data_ptr(), (0 if a.is_cuda else 1), {torch.float32: F32, torch.float64: F64}.get(a.dtype)
+    except ImportError:  # pragma: no cover
+        pass
+    assert isinstance(a, np.ndarray) and a.flags.c_contiguous, "numpy array must be contiguous"
+    return a.ctypes.data, 1, {np.dtype(np.float32): F32, np.dtype(np.float64): F64}.get(a.dtype)
+
+
+class Simulation:
+    """A TRMC-R simulation on the current CUDA device (one context per device/stream).
+
+    Homogeneous: pass `offsets` (cells of independent gases, rho = 1).
+    Shock: pass `shock` = dict(ncells, x_min, x_max, weight, rho_L, u_L, T_L,
+    rho_R, u_R, T_R) and positions `x` sorted by cell.
+    """
+
+    def __init__(self, vx, vy, vz, *, eps: float, dt: float, offsets=None, shock: Optional[dict] = None,
+                 x=None, model: int = HARD_SPHERE, adaptive: bool = False, m_fixed: int = 64,
+                 m_init: int = 2, m_cap: int = 4096, delta1: float = 0.005, delta2: float = 0.01,
+                 indicator: int = IND_PXX, seed: int = 1, cell_base: int = 0, capacity: int = 0,
+                 stream=None):
+        L = lib()
+        self._keep = [vx, vy, vz, x]
+        pvx, host, dt_code = _ptr(vx)
+        pvy, _, _ = _ptr(vy)
+        pvz, _, _ = _ptr(vz)
+        if dt_code is None:
+            raise TypeError("velocities must be float32 or float64")
+        self.dtype = dt_code
+        self.host_init = host
+        n = int(vx.shape[0])
+        px = _ptr(x)[0] if x is not None else None
+        part = _Particles(dt_code, host, n, int(capacity), pvx, pvy, pvz, px)
+        if shock is None:
+            off = np.ascontiguousarray(offsets, dtype=np.int64)
+            self._off = off
+            self.ncells = len(off) - 1
+            cells = _Cells(HOMOGENEOUS, self.ncells, cell_base, 0,
+                           off.ctypes.data_as(C.POINTER(C.c_int64)), 0, 0, 0, 0, 0, 0, 0, 0, 0)
+            self.geometry = HOMOGENEOUS
+        else:
+            self.ncells = int(shock["ncells"])
+            cells = _Cells(SHOCK_1D, self.ncells, cell_base, 0, None, shock["x_min"], shock["x_max"],
+                           shock["weight"], shock["rho_L"], shock["u_L"], shock["T_L"],
+                           shock["rho_R"], shock["u_R"], shock["T_R"])
+            self.geometry = SHOCK_1D
+        kern = _Kernel(model, int(bool(adaptive)), m_fixed, m_init, m_cap, indicator, delta1, delta2,
+                       seed & 0xFFFFFFFFFFFFFFFF)
+        if stream is None:
+            try:
+                import torch
+                stream = torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else 0
+            except ImportError:  # pragma: no cover
+                stream = 0
+        self.stream = stream
+        h = C.c_void_p()
+        st = L.trmcr_init(C.byref(h), C.byref(part), C.byref(cells), float(eps), float(dt),
+                          C.byref(kern), C.c_void_p(stream))
+        if st != OK:
+            raise TrmcrError(st, L.trmcr_last_error(None).decode())
+        self._h = h
+        self.n_init = n
+
+    # ------------------------------------------------------------------ helpers
+    def _check(self, st):
+        if st != OK:
+            raise TrmcrError(st, lib().trmcr_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().trmcr_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ ABI
+    def step(self, n: int = 1):
+        self._check(lib().trmcr_step(self._h, int(n)))
+        return self
+
+    def moments(self) -> np.ndarray:
+        out = np.zeros((self.ncells, len(MOMENT_FIELDS)))
+        self._check(lib().trmcr_moments(self._h, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def stats(self) -> np.ndarray:
+        out = np.zeros(self.ncells, dtype=STATS_DTYPE)
+        self._check(lib().trmcr_stats(self._h, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def num_particles(self) -> int:
+        n = C.c_int64()
+        self._check(lib().trmcr_num_particles(self._h, C.byref(n)))
+        return n.value
+
+    def particles(self) -> dict:
+        n = self.num_particles()
+        dt = np.float64 if self.dtype == F64 else np.float32
+        vx, vy, vz, x = (np.zeros(max(n, 1), dtype=dt) for _ in range(4))
+        off = np.zeros(self.ncells + 1, dtype=np.int64)
+        self._check(lib().trmcr_copy_particles(self._h, vx.ctypes.data, vy.ctypes.data, vz.ctypes.data,
+                                               x.ctypes.data, off.ctypes.data, 1))
+        out = dict(vx=vx[:n], vy=vy[:n], vz=vz[:n], offsets=off)
+        if self.geometry == SHOCK_1D:
+            out["x"] = x[:n]
+        return out
+
+    def set_velocities(self, vx, vy, vz):
+        p, host, _ = _ptr(vx)
+        self._check(lib().trmcr_set_velocities(self._h, p, _ptr(vy)[0], _ptr(vz)[0], host))
+
+    def step_host(self, vx, vy, vz, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """e2e path: host velocities in, one step, host per-cell moments out."""
+        if out is None:
+            out = np.zeros((self.ncells, len(MOMENT_FIELDS)))
+        self._check(lib().trmcr_step_host(self._h, _ptr(vx)[0], _ptr(vy)[0], _ptr(vz)[0],
+                                          out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def set_log(self, capacity: int):
+        self._check(lib().trmcr_set_log(self._h, int(capacity)))
+        self._log_cap = int(capacity)
+
+    def collisions(self) -> np.ndarray:
+        cnt = C.c_int64()
+        cap = getattr(self, "_log_cap", 0)
+        buf = np.zeros(max(cap, 1), dtype=COLL_DTYPE)
+        self._check(lib().trmcr_get_log(self._h, buf.ctypes.data, C.byref(cnt)))
+        if cnt.value > cap:
+            raise TrmcrError(ECAPACITY, f"log overflow: {cnt.value} > {cap}")
+        return buf[: cnt.value].copy()
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().trmcr_launch_count(self._h))
+
+
+def version() -> str:
+    return lib().trmcr_version().decode()

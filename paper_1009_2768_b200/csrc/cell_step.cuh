@@ -1,0 +1,590 @@
+// cell_step.cuh — one TRMC-R collision step of one cell, executed by one CTA.
+//
+// Rows A3..A8 of the hot path (SURVEY §8a / DESIGN.md §3):
+//   A3 moments + majorant
+//   A4 split into collision sets, Alg 4.2, IR rounding
+//   A5 recursive trees of Alg 4.3/4.4 flattened level-synchronously
+//   A6 binary / dummy collisions (eq. Maxwell_coll, n3d: P:381-395)
+//   A7 TRMC-RAD keep-and-extend
+//   A8 conservative Maxwellian of the truncated set
+//
+// The same routine runs with its working arrays in shared memory (cells up to
+// n_cap particles, the fast path) or in global memory (large cells, or a cell
+// whose tree overflowed the shared-memory plan; that CTA writes nothing and
+// hands the cell to the global-memory kernel).
+#pragma once
+#include "device_common.cuh"
+#include "../../include/trmcr.h"
+
+namespace trmcr {
+
+enum : int { kOk = 0, kOverflow = 1, kCapacity = 2 };
+// error bits of the context's device flag (read back by sync calls)
+enum : int { kErrPlanCapacity = 1, kErrParticleCapacity = 2, kErrInternal = 16 };
+
+struct StepParams {
+  int model, adaptive, m_fixed, m_cap, indicator, log_on;
+  double delta1, delta2, dt, eps;
+  uint32_t k0, k1, step, cell_base;
+  int shock;               // rho_c = n w / dx when 1, else 1
+  double w_over_dx;
+  int *err;                // device error bits
+  int debug_stop;          // debug: >0 stops after that many RAD retries (no Maxwellian)
+};
+
+// Per-CTA working set.  Index type: uint32.
+template <typename Real>
+struct CellBuf {
+  Real *vx, *vy, *vz;      // [n] cell velocities (smem copy or global, in place)
+  uint32_t *ctype;         // [K_cap] type a of collision (level d, j) at S[d]+j
+  uint32_t *crank;         // [K_cap] rank among same-type collisions of its level
+  uint32_t *cslot;         // [2 K_cap] input/output slots (side 0, side 1)
+  int32_t *Q;              // [L_cap+1] split quotas N_d
+  int32_t *C;              // [L_cap+1] collisions per level
+  int32_t *S;              // [L_cap+1] first collision index of level
+  int32_t *cons;           // [L_cap+1] demands on pool d
+  int32_t *base;           // [L_cap+1] running demand counter of pool d
+  int32_t *cnt;            // [L_cap+1] per-type counter of the current level
+  uint4 *rk;               // [L_cap+1] permutation keys of pools
+  uint32_t *mask;          // [ceil(n_cap/32)] Theta membership
+  double *red;             // [32*8] reduction scratch
+  int n_cap, K_cap, L_cap;
+};
+
+// Scalars shared by the CTA.
+struct CellShared {
+  double ux, uy, uz, S0, sigma, p, mu, S_est, E1;
+  double sums[8];
+  int n, m, m_cur, m_next, d, top, lo, hi, r, planned, flag, done;
+  int64_t rem;
+  int32_t L, Ltot, U, nT, budget, leaf_off, attempts;
+  unsigned long long prop, acc, viol;
+};
+
+template <typename Real> struct RealOps;
+template <> struct RealOps<double> {
+  __device__ static __forceinline__ double sqrt_(double x) { return sqrt(x); }
+  __device__ static __forceinline__ void sincospi_(double x, double *s, double *c) { sincospi(x, s, c); }
+};
+template <> struct RealOps<float> {
+  __device__ static __forceinline__ float sqrt_(float x) { return sqrtf(x); }
+  __device__ static __forceinline__ void sincospi_(float x, float *s, float *c) { sincospif(x, s, c); }
+};
+
+// IR at split level d with its keyed uniform; exact 0 when y < 2^-53.
+__device__ __forceinline__ int64_t ir_split(const RngKey &K, int d, double y) {
+  if (y < 0x1p-53) return 0;
+  const uint4 w = K(kSplit, 0, (uint32_t)d, 0);
+  const double fl = floor(y);
+  return (int64_t)fl + ((u53(w.x, w.y) < y - fl) ? 1 : 0);
+}
+
+// Alg 4.2 continued until rem == 0 or level m (thread 0 only).  Quotas above
+// L_cap cannot be stored: a non-zero one flags overflow.
+__device__ inline void split_extend(const RngKey &K, CellShared &sh, int m, int32_t *Q, int L_cap) {
+  while (sh.rem > 0 && sh.d < m) {
+    const double y = sh.p * (double)sh.rem;
+    if (y < 0x1p-53) {                     // every further IR is exactly 0
+      for (int d = sh.d + 1; d <= m && d <= L_cap; ++d) Q[d] = 0;
+      sh.d = m;
+      break;
+    }
+    sh.d++;
+    int64_t q = ir_split(K, sh.d, y);
+    if (q > sh.rem) q = sh.rem;
+    if (sh.d <= L_cap) Q[sh.d] = (int32_t)q;
+    else if (q > 0) sh.flag = kOverflow;
+    sh.rem -= q;
+  }
+}
+
+template <typename Real>
+__device__ __forceinline__ void load3(const Real *a, const Real *b, const Real *c, int64_t i, Real &x,
+                                      Real &y, Real &z) {
+  x = a[i]; y = b[i]; z = c[i];
+}
+
+// One (dummy) collision of a tree node (A6).  Returns accepted.
+template <typename Real>
+__device__ __forceinline__ int tree_collision(const StepParams &P, const RngKey &K, CellBuf<Real> &B,
+                                              Real sigma, int r, int d, uint32_t j, uint32_t si,
+                                              uint32_t sk, unsigned &viol) {
+  using O = RealOps<Real>;
+  Real xa, xi1, xi2;
+  if constexpr (sizeof(Real) == 8) {
+    const uint4 w = K(kColl, r, d, j);
+    const uint4 w2 = K(kColl2, r, d, j);
+    xa = u53(w.x, w.y); xi1 = u53(w.z, w.w); xi2 = u53(w2.x, w2.y);
+  } else {
+    const uint4 w = K(kColl, r, d, j);
+    xa = u24(w.x); xi1 = u24(w.y); xi2 = u24(w.z);
+  }
+  const Real ax = B.vx[si], ay = B.vy[si], az = B.vz[si];
+  const Real bx = B.vx[sk], by = B.vy[sk], bz = B.vz[sk];
+  const Real qx = ax - bx, qy = ay - by, qz = az - bz;
+  const Real q = O::sqrt_(qx * qx + qy * qy + qz * qz);
+  int acc = 1;
+  if (P.model == TRMCR_HARD_SPHERE) {       // accept iff xi Sigma' < |q|  [R7]
+    viol += (q > sigma) ? 1u : 0u;
+    acc = (xa * sigma < q);
+  }
+  if (acc) {
+    const Real c = Real(2) * xi1 - Real(1);
+    const Real s = O::sqrt_((Real(1) - c) * (Real(1) + c));
+    Real sp, cp;
+    O::sincospi_(Real(2) * xi2, &sp, &cp);
+    const Real h = Real(0.5) * q;
+    const Real hx = h * (s * cp), hy = h * (s * sp), hz = h * c;
+    const Real gx = Real(0.5) * (ax + bx), gy = Real(0.5) * (ay + by), gz = Real(0.5) * (az + bz);
+    B.vx[si] = gx + hx; B.vy[si] = gy + hy; B.vz[si] = gz + hz;
+    B.vx[sk] = gx - hx; B.vy[sk] = gy - hy; B.vz[sk] = gz - hz;
+  }
+  return acc;
+}
+
+// Draw three standard normals for Theta slot `slot` (Box-Muller).
+template <typename Real>
+__device__ __forceinline__ void gauss3(const RngKey &K, uint32_t slot, Real &g0, Real &g1, Real &g2) {
+  if constexpr (sizeof(Real) == 8) {
+    const uint4 w = K(kMaxw, 0, 0, slot);
+    const uint4 w2 = K(kMaxw2, 0, 0, slot);
+    const double u1 = u53(w.x, w.y), u2 = u53(w.z, w.w), u3 = u53(w2.x, w2.y), u4 = u53(w2.z, w2.w);
+    const double r1 = sqrt(-2.0 * log(u1)), r3 = sqrt(-2.0 * log(u3));
+    double s2, c2, s4, c4;
+    sincospi(2.0 * u2, &s2, &c2);
+    sincospi(2.0 * u4, &s4, &c4);
+    g0 = r1 * c2; g1 = r1 * s2; g2 = r3 * c4;
+  } else {
+    const uint4 w = K(kMaxw, 0, 0, slot);
+    const float u1 = u24(w.x), u2 = u24(w.y), u3 = u24(w.z), u4 = u24(w.w);
+    const float r1 = sqrtf(-2.0f * __logf(u1)), r3 = sqrtf(-2.0f * __logf(u3));
+    float s2, c2;
+    __sincosf(6.283185307179586f * u2, &s2, &c2);
+    const float c4 = __cosf(6.283185307179586f * u4);
+    g0 = r1 * c2; g1 = r1 * s2; g2 = r3 * c4;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Plan (A5), top-down: C_d = ceil((Q_d + cons_d)/2) collisions per level,
+// each with a type a uniform in {0..d-1} consuming one sample of f_a
+// and one of f_{d-1-a}.  Quotas only on [lo, hi].  Guard: if the
+// leaves cons_0 exceed `budget`, drop the top quota level and re-plan.
+// ---------------------------------------------------------------------------
+template <typename Real>
+__device__ void plan_counts(const RngKey &K, CellBuf<Real> &B, CellShared &sh) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int top = sh.hi;
+    while (top >= sh.lo && B.Q[top] == 0) top--;
+    sh.top = top;
+    sh.planned = 0;
+    sh.done = 0;
+  }
+  __syncthreads();
+  for (;;) {
+    if (sh.top < sh.lo || sh.top < 1) {    // nothing to plan
+      if (tid == 0) { sh.top = 0; sh.L = 0; }
+      __syncthreads();
+      return;
+    }
+    if (sh.top > B.L_cap) {
+      if (tid == 0) sh.flag = kOverflow;
+      __syncthreads();
+      return;
+    }
+    const int top = sh.top;
+    for (int d = tid; d <= top; d += blockDim.x) B.cons[d] = 0;
+    __syncthreads();
+    int Sacc = 0;
+    for (int d = top; d >= 1; --d) {
+      const int Qd = (d >= sh.lo) ? B.Q[d] : 0;
+      const int Cd = (Qd + B.cons[d] + 1) >> 1;   // all threads read the same value
+      if ((int64_t)Sacc + Cd > B.K_cap) {
+        __syncthreads();
+        if (tid == 0) sh.flag = kOverflow;
+        __syncthreads();
+        return;
+      }
+      __syncthreads();                            // every thread has read cons[d]
+      if (tid == 0) { B.C[d] = Cd; B.S[d] = Sacc; }
+      for (int j = tid; j < Cd; j += blockDim.x) {
+        const uint32_t w = K(kType, sh.r, d, j).x;
+        const uint32_t a = __umulhi(w, (uint32_t)d);  // floor(w d / 2^32)
+        B.ctype[Sacc + j] = a;
+        atomicAdd(&B.cons[a], 1);
+        atomicAdd(&B.cons[d - 1 - a], 1);
+      }
+      Sacc += Cd;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      if (B.cons[0] <= sh.budget) {
+        sh.L = B.cons[0];
+        sh.done = 1;
+      } else {                                    // drop the top quota level
+        int t = sh.top - 1;
+        while (t >= sh.lo && B.Q[t] == 0) t--;
+        sh.top = t;
+      }
+    }
+    __syncthreads();
+    if (sh.done) return;
+  }
+}
+
+// Bottom-up slot resolution + execution (A5, A6): level d's demand on pool p
+// has rank base_p + (in-level rank); side-0 demands (type p) precede side-1
+// demands (type d-1-p).  Pool p's t-th demand takes output pi_p(t) of level
+// p (pi_0 = leaf order of the cell).  Output side s of a collision keeps the
+// slot of its input side s; collisions of one level touch disjoint slots.
+template <typename Real>
+__device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real> &B, CellShared &sh,
+                             const Perm &pi0, Real sigma, trmcr_coll_rec *log,
+                             unsigned long long *log_count, int64_t log_cap) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int top = sh.top;
+  if (top < 1) return;
+  for (int d = tid; d <= top; d += blockDim.x) {
+    B.base[d] = 0;
+    B.cnt[d] = 0;
+    if (d >= 1) B.rk[d] = K(kPerm, sh.r, d, 0);
+  }
+  __syncthreads();
+  unsigned acc = 0, viol = 0;
+  const int r = sh.r;
+  const int leaf_off = sh.leaf_off;
+  for (int d = 1; d <= top; ++d) {
+    const int Cd = B.C[d], Sd = B.S[d];
+    if (Cd == 0) continue;
+    // in-level stable ranks per type (one warp, 32 collisions per round)
+    if (warp == 0) {
+      for (int j0 = 0; j0 < Cd; j0 += 32) {
+        const int j = j0 + lane;
+        const bool valid = j < Cd;
+        const uint32_t a = valid ? B.ctype[Sd + j] : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xffffffffu, a);
+        const unsigned lt = (1u << lane) - 1u;
+        int c0 = 0;
+        if (valid) c0 = B.cnt[a];
+        __syncwarp();
+        if (valid) {
+          B.crank[Sd + j] = (uint32_t)(c0 + __popc(peers & lt));
+          if ((peers & lt) == 0u) B.cnt[a] = c0 + __popc(peers);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int j = tid; j < Cd; j += blockDim.x) {
+      const uint32_t a = B.ctype[Sd + j], b = (uint32_t)d - 1u - a;
+      const uint32_t rank = B.crank[Sd + j];
+      const uint32_t t[2] = {(uint32_t)B.base[a] + rank, (uint32_t)(B.base[b] + B.cnt[b]) + rank};
+      const uint32_t pool[2] = {a, b};
+      uint32_t slot[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        if (pool[s] == 0) {
+          slot[s] = pi0((uint32_t)leaf_off + t[s]);
+        } else {
+          Perm pp;
+          pp.init(B.rk[pool[s]], 2u * (uint32_t)B.C[pool[s]]);
+          const uint32_t o = pp(t[s]);
+          slot[s] = o == 0xFFFFFFFFu ? o : B.cslot[2u * (uint32_t)B.S[pool[s]] + o];
+        }
+        if (slot[s] >= (uint32_t)sh.n) {   // cannot happen: internal fault, never hang
+          atomicOr(P.err, kErrInternal);
+          slot[s] = 0;
+        }
+      }
+      B.cslot[2 * (Sd + j)] = slot[0];
+      B.cslot[2 * (Sd + j) + 1] = slot[1];
+      const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, slot[0], slot[1], viol);
+      acc += ok;
+      if (P.log_on) {
+        const unsigned long long at = atomicAdd(log_count, 1ull);
+        if ((int64_t)at < log_cap) {
+          trmcr_coll_rec rec;
+          rec.cell = (int32_t)K.cell; rec.attempt = r; rec.level = d; rec.accepted = ok;
+          rec.j = j; rec.slot_i = slot[0]; rec.slot_k = slot[1];
+          log[at] = rec;
+        }
+      }
+    }
+    __syncthreads();
+    for (int j = tid; j < Cd; j += blockDim.x) {
+      const uint32_t a = B.ctype[Sd + j];
+      atomicAdd(&B.base[a], 1);
+      atomicAdd(&B.base[d - 1 - a], 1);
+      B.cnt[a] = 0;
+    }
+    if (tid == 0) atomicAdd(&sh.prop, (unsigned long long)Cd);
+    __syncthreads();
+  }
+  atomicAdd(&sh.acc, (unsigned long long)acc);
+  atomicAdd(&sh.viol, (unsigned long long)viol);
+  __syncthreads();
+}
+
+// RAD indicator estimate with Theta taken analytically.
+template <typename Real>
+__device__ void rad_estimate(const StepParams &P, CellBuf<Real> &B, CellShared &sh, const Perm &pi0) {
+  const int tid = threadIdx.x, n = sh.n, nT = sh.nT;
+  const int nwords = (n + 31) >> 5;
+  for (int i = tid; i < nwords; i += blockDim.x) B.mask[i] = 0u;
+  __syncthreads();
+  for (int q = tid; q < nT; q += blockDim.x) {
+    const uint32_t s = pi0((uint32_t)(sh.Ltot + q));
+    if (s >= (uint32_t)n) { atomicOr(P.err, kErrInternal); continue; }
+    atomicOr(&B.mask[s >> 5], 1u << (s & 31));
+  }
+  __syncthreads();
+  double v[4] = {0, 0, 0, 0};  // non-Theta indicator sum, Theta momentum
+  for (int i = tid; i < n; i += blockDim.x) {
+    const double x = B.vx[i], y = B.vy[i], z = B.vz[i];
+    if ((B.mask[i >> 5] >> (i & 31)) & 1u) {
+      v[1] += x; v[2] += y; v[3] += z;
+    } else if (P.indicator == TRMCR_IND_PXX) {
+      const double dx = x - sh.ux;
+      v[0] += dx * dx;
+    } else {
+      const double v2 = x * x + y * y + z * z;
+      v[0] += v2 * v2;
+    }
+  }
+  block_sum<4>(v, B.red);
+  double tx = 0, ty = 0, tz = 0;
+  if (nT > 0) { tx = v[1] / nT; ty = v[2] / nT; tz = v[3] / nT; }
+  double e[1] = {0};
+  for (int i = tid; i < n; i += blockDim.x) {
+    if ((B.mask[i >> 5] >> (i & 31)) & 1u) {
+      const double dx = B.vx[i] - tx, dy = B.vy[i] - ty, dz = B.vz[i] - tz;
+      e[0] += dx * dx + dy * dy + dz * dz;
+    }
+  }
+  block_sum<1>(e, B.red);
+  if (tid == 0) {
+    double s = v[0];
+    if (nT > 0) {
+      const double T = e[0] / (3.0 * nT);
+      if (P.indicator == TRMCR_IND_PXX) {
+        s += (double)nT * (T + (tx - sh.ux) * (tx - sh.ux));
+      } else {
+        const double u2 = tx * tx + ty * ty + tz * tz;
+        s += (double)nT * (u2 * u2 + 10.0 * u2 * T + 15.0 * T * T);
+      }
+    }
+    sh.S_est = s / n;
+    if (sh.S0 != 0.0) sh.E1 = fabs(sh.S_est - sh.S0) / fabs(sh.S0);
+    else sh.E1 = (sh.S_est == 0.0) ? 0.0 : INFINITY;
+  }
+  __syncthreads();
+}
+
+// Conservative Maxwellian (A8) over Theta = pi0 positions [Ltot, Ltot+nT).
+template <typename Real>
+__device__ void maxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> &B, CellShared &sh,
+                           const Perm &pi0, double ec_all) {
+  const int tid = threadIdx.x, nT = sh.nT;
+  if (nT < 2) return;
+  const bool full = (nT == sh.n);          // Theta = every slot: skip the permutation
+  double ux, uy, uz, ec;
+  if (full) {
+    ux = sh.ux; uy = sh.uy; uz = sh.uz; ec = ec_all;
+  } else {
+    double v[3] = {0, 0, 0};
+    for (int q = tid; q < nT; q += blockDim.x) {
+      const uint32_t s = pi0((uint32_t)(sh.Ltot + q));
+      if (s >= (uint32_t)sh.n) { atomicOr(P.err, kErrInternal); continue; }
+      v[0] += (double)B.vx[s]; v[1] += (double)B.vy[s]; v[2] += (double)B.vz[s];
+    }
+    block_sum<3>(v, B.red);
+    ux = v[0] / nT; uy = v[1] / nT; uz = v[2] / nT;
+    ec = 0;
+  }
+  double g[5] = {0, 0, 0, 0, 0};   // sum g (3), sum |g|^2, centred energy of Theta
+  for (int q = tid; q < nT; q += blockDim.x) {
+    const uint32_t s = full ? (uint32_t)q : pi0((uint32_t)(sh.Ltot + q));
+    if (s >= (uint32_t)sh.n) { atomicOr(P.err, kErrInternal); continue; }
+    if (!full) {
+      const double dx = B.vx[s] - ux, dy = B.vy[s] - uy, dz = B.vz[s] - uz;
+      g[4] += dx * dx + dy * dy + dz * dz;
+    }
+    Real g0, g1, g2;
+    gauss3<Real>(K, s, g0, g1, g2);
+    B.vx[s] = g0; B.vy[s] = g1; B.vz[s] = g2;   // park g in place (same thread rewrites)
+    g[0] += g0; g[1] += g1; g[2] += g2;
+    g[3] += (double)g0 * g0 + (double)g1 * g1 + (double)g2 * g2;
+  }
+  block_sum<5>(g, B.red);
+  if (!full) ec = g[4];
+  const double gx = g[0] / nT, gy = g[1] / nT, gz = g[2] / nT;
+  const double D = g[3] - nT * (gx * gx + gy * gy + gz * gz);
+  const double sc = (D > 0.0 && ec > 0.0) ? sqrt(ec / D) : 0.0;
+  const Real rsc = (Real)sc, rgx = (Real)gx, rgy = (Real)gy, rgz = (Real)gz;
+  const Real rux = (Real)ux, ruy = (Real)uy, ruz = (Real)uz;
+  for (int q = tid; q < nT; q += blockDim.x) {
+    const uint32_t s = full ? (uint32_t)q : pi0((uint32_t)(sh.Ltot + q));
+    if (s >= (uint32_t)sh.n) continue;
+    B.vx[s] = rux + rsc * (B.vx[s] - rgx);
+    B.vy[s] = ruy + rsc * (B.vy[s] - rgy);
+    B.vz[s] = ruz + rsc * (B.vz[s] - rgz);
+  }
+  __syncthreads();
+}
+
+// Full per-cell step.  in_* = the cell's particles (global), out_* = where the
+// result goes (may alias in_*).  kLoad: copy in_* into B's arrays first;
+// otherwise B.v* already hold the cell (staged in shared memory by a gather,
+// or aliasing global memory).  kStore: write B.v* to out_* at the end.
+template <typename Real, bool kLoad, bool kStore>
+__device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &sh, const Real *in_x,
+                            const Real *in_y, const Real *in_z, Real *out_x, Real *out_y, Real *out_z,
+                            int n, uint32_t gcell, int32_t *m_state, double *stats_row,
+                            trmcr_coll_rec *log, unsigned long long *log_count, int64_t log_cap) {
+  const int tid = threadIdx.x;
+  if (n > B.n_cap) return kOverflow;
+  const RngKey K{P.k0, P.k1, gcell, P.step};
+  const int m0 = P.adaptive ? *m_state : P.m_fixed;
+  if (n == 0) {
+    if (tid == 0 && stats_row) {
+      for (int k = 0; k < TRMCR_NSTATS; ++k) stats_row[k] = 0.0;
+      stats_row[TRMCR_ST_MUSED] = m0;
+      stats_row[TRMCR_ST_MNEXT] = m0;
+    }
+    return kOk;
+  }
+  // ---- A3: moments ----
+  double s3[3] = {0, 0, 0};
+  for (int i = tid; i < n; i += blockDim.x) {
+    Real x, y, z;
+    if (kLoad) load3(in_x, in_y, in_z, i, x, y, z);
+    else { x = B.vx[i]; y = B.vy[i]; z = B.vz[i]; }
+    if (kLoad) { B.vx[i] = x; B.vy[i] = y; B.vz[i] = z; }
+    s3[0] += x; s3[1] += y; s3[2] += z;
+  }
+  block_sum<3>(s3, B.red);
+  const double ux = s3[0] / n, uy = s3[1] / n, uz = s3[2] / n;
+  double c3[3] = {0, 0, 0};  // Pxx sum, M4 sum, centred energy
+  double dv2 = 0.0;
+  for (int i = tid; i < n; i += blockDim.x) {
+    const double x = B.vx[i], y = B.vy[i], z = B.vz[i];
+    const double dx = x - ux, dy = y - uy, dz = z - uz;
+    const double r2 = dx * dx + dy * dy + dz * dz;
+    dv2 = fmax(dv2, r2);
+    c3[0] += dx * dx;
+    const double v2 = x * x + y * y + z * z;
+    c3[1] += v2 * v2;
+    c3[2] += r2;
+  }
+  block_sum<3>(c3, B.red);
+  dv2 = block_max(dv2, B.red);
+  if (tid == 0) {
+    sh.n = n; sh.ux = ux; sh.uy = uy; sh.uz = uz;
+    sh.S0 = (P.indicator == TRMCR_IND_PXX ? c3[0] : c3[1]) / n;
+    const double rho_c = P.shock ? n * P.w_over_dx : 1.0;
+    if (P.model == TRMCR_HARD_SPHERE) {
+      sh.sigma = 2.0 * sqrt(dv2);            // Sigma' = 2 dv  [R4]
+      sh.mu = rho_c * sh.sigma;              // mu = 4 pi rho Sigma  [R5]
+    } else {
+      sh.sigma = 0.0;
+      sh.mu = rho_c;
+    }
+    const double x = sh.mu * P.dt / P.eps;
+    sh.p = exp(-x);
+    sh.m = m0; sh.m_cur = m0; sh.flag = kOk;
+    sh.prop = 0; sh.acc = 0; sh.viol = 0;
+    // ---- A4: split (Alg 4.2) ----
+    const int64_t N0 = ir_split(K, 0, sh.p * (double)n);
+    B.Q[0] = (int32_t)N0;
+    sh.rem = n - N0;
+    sh.d = 0;
+    split_extend(K, sh, m0, B.Q, B.L_cap);
+    // quotas above L_cap are zero (else split_extend flagged overflow)
+    sh.r = 0; sh.lo = 1; sh.hi = sh.d < B.L_cap ? sh.d : B.L_cap;
+    sh.budget = n; sh.leaf_off = 0;
+  }
+  __syncthreads();
+  if (sh.flag != kOk) return sh.flag;
+  Perm pi0;
+  pi0.init(K(kPerm, 0, 0, 0), (uint32_t)n);
+  const Real sigma = (Real)sh.sigma;
+  // ---- A5/A6: attempt 0 ----
+  plan_counts<Real>(K, B, sh);
+  if (sh.flag != kOk) return sh.flag;
+  plan_execute<Real>(P, K, B, sh, pi0, sigma, log, log_count, log_cap);
+  if (tid == 0) {
+    sh.Ltot = sh.L;
+    sh.U = B.Q[0] < n - sh.Ltot ? B.Q[0] : n - sh.Ltot;
+    sh.nT = n - sh.Ltot - sh.U;
+    sh.m_next = sh.m_cur;
+    sh.S_est = sh.S0; sh.E1 = 0.0;
+  }
+  __syncthreads();
+  // ---- A7: TRMC-RAD ----
+  if (P.adaptive) {
+    for (;;) {
+      rad_estimate<Real>(P, B, sh, pi0);
+      if (tid == 0) {
+        sh.done = 1;
+        if (sh.E1 > P.delta2 && sh.m_cur < P.m_cap) {
+          const int m_new = 2 * sh.m_cur < P.m_cap ? 2 * sh.m_cur : P.m_cap;
+          split_extend(K, sh, m_new, B.Q, B.L_cap);
+          sh.r += 1;
+          sh.lo = sh.m_cur + 1;
+          sh.hi = sh.d < B.L_cap ? sh.d : B.L_cap;
+          sh.budget = sh.nT;
+          sh.leaf_off = sh.Ltot;
+          sh.m_cur = m_new;
+          sh.done = 0;
+        }
+      }
+      __syncthreads();
+      if (sh.flag != kOk) return sh.flag;
+      if (sh.done) break;
+      plan_counts<Real>(K, B, sh);
+      if (sh.flag != kOk) return sh.flag;
+      plan_execute<Real>(P, K, B, sh, pi0, sigma, log, log_count, log_cap);
+      if (tid == 0) { sh.Ltot += sh.L; sh.nT -= sh.L; }
+      __syncthreads();
+      if (P.debug_stop > 0 && sh.r >= P.debug_stop) {
+        if (kStore)
+          for (int i = tid; i < n; i += blockDim.x) { out_x[i] = B.vx[i]; out_y[i] = B.vy[i]; out_z[i] = B.vz[i]; }
+        return kOk;
+      }
+    }
+    if (tid == 0) {
+      sh.m_next = (sh.E1 < P.delta1) ? (sh.m_cur / 2 > 1 ? sh.m_cur / 2 : 1) : sh.m_cur;
+    }
+    __syncthreads();
+  }
+  if (P.debug_stop < 0) {   // debug: stop before the Maxwellian
+    if (kStore)
+      for (int i = tid; i < n; i += blockDim.x) { out_x[i] = B.vx[i]; out_y[i] = B.vy[i]; out_z[i] = B.vz[i]; }
+    return kOk;
+  }
+  // ---- A8: Maxwellian of Theta ----
+  maxwellian<Real>(P, K, B, sh, pi0, c3[2]);
+  // ---- write back + stats ----
+  if (kStore) {
+    for (int i = tid; i < n; i += blockDim.x) {
+      out_x[i] = B.vx[i]; out_y[i] = B.vy[i]; out_z[i] = B.vz[i];
+    }
+  }
+  if (tid == 0) {
+    if (P.adaptive) *m_state = sh.m_next;
+    if (stats_row) {
+      double *s = stats_row;
+      s[TRMCR_ST_N] = n; s[TRMCR_ST_P] = sh.p; s[TRMCR_ST_MU] = sh.mu; s[TRMCR_ST_SIGMA] = sh.sigma;
+      s[TRMCR_ST_S0] = sh.S0; s[TRMCR_ST_SEST] = sh.S_est; s[TRMCR_ST_E1] = sh.E1;
+      s[TRMCR_ST_MUSED] = sh.m_cur; s[TRMCR_ST_MNEXT] = sh.m_next; s[TRMCR_ST_DEPTH] = sh.d;
+      s[TRMCR_ST_ATTEMPTS] = sh.r + 1; s[TRMCR_ST_LEAVES] = sh.Ltot; s[TRMCR_ST_UNTOUCHED] = sh.U;
+      s[TRMCR_ST_THERMALISED] = sh.nT; s[TRMCR_ST_PROPOSALS] = (double)sh.prop;
+      s[TRMCR_ST_ACCEPTED] = (double)sh.acc; s[TRMCR_ST_VIOLATIONS] = (double)sh.viol;
+      s[TRMCR_ST_MAXW] = sh.nT >= 2 ? sh.nT : 0;
+    }
+  }
+  return kOk;
+}
+
+}  // namespace trmcr

@@ -1,0 +1,204 @@
+// ctx.cuh — host-side context of a TRMC-R simulation and shared helpers.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/trmcr.h"
+#include "cell_step.cuh"
+
+namespace trmcr {
+
+constexpr int kSmemThreads = 256;
+constexpr int kGmemThreads = 1024;
+
+// ---- shared-memory layout of cell_step_smem ----
+struct SmemLayout {
+  int n_cap, K_cap, L_cap;
+  size_t real_size;
+  size_t off_v, off_ctype, off_crank, off_cslot, off_ints, off_rk, off_mask, off_red, total;
+  void build(int n, int K, int L, size_t rs) {
+    n_cap = n; K_cap = K; L_cap = L; real_size = rs;
+    size_t o = 0;
+    auto al = [&](size_t a) { o = (o + a - 1) / a * a; };
+    off_red = o; o += 32 * 8 * sizeof(double);
+    al(16); off_rk = o; o += (size_t)(L + 1) * sizeof(uint4);
+    al(16); off_v = o; o += 3 * (size_t)n * rs;
+    al(16); off_ctype = o; o += (size_t)K * 4;
+    off_crank = o; o += (size_t)K * 4;
+    off_cslot = o; o += (size_t)K * 8;
+    off_ints = o; o += 6 * (size_t)(L + 1) * 4;
+    off_mask = o; o += (size_t)((n + 31) / 32) * 4;
+    al(16); total = o;
+  }
+};
+
+template <typename Real>
+__device__ __forceinline__ void bind_smem(CellBuf<Real> &B, unsigned char *base, const SmemLayout &Lay) {
+  B.red = reinterpret_cast<double *>(base + Lay.off_red);
+  B.rk = reinterpret_cast<uint4 *>(base + Lay.off_rk);
+  Real *v = reinterpret_cast<Real *>(base + Lay.off_v);
+  B.vx = v; B.vy = v + Lay.n_cap; B.vz = v + 2 * Lay.n_cap;
+  B.ctype = reinterpret_cast<uint32_t *>(base + Lay.off_ctype);
+  B.crank = reinterpret_cast<uint32_t *>(base + Lay.off_crank);
+  B.cslot = reinterpret_cast<uint32_t *>(base + Lay.off_cslot);
+  int32_t *ints = reinterpret_cast<int32_t *>(base + Lay.off_ints);
+  const int Lp = Lay.L_cap + 1;
+  B.Q = ints; B.C = ints + Lp; B.S = ints + 2 * Lp; B.cons = ints + 3 * Lp;
+  B.base = ints + 4 * Lp; B.cnt = ints + 5 * Lp;
+  B.mask = reinterpret_cast<uint32_t *>(base + Lay.off_mask);
+  B.n_cap = Lay.n_cap; B.K_cap = Lay.K_cap; B.L_cap = Lay.L_cap;
+}
+
+struct GmemScratch {
+  unsigned char *base;
+  size_t stride;
+  int n_cap, K_cap, L_cap;
+};
+
+// Bind the plan arrays of CTA blockIdx.x to its slab of global scratch.
+template <typename Real>
+__device__ __forceinline__ void bind_gmem(CellBuf<Real> &B, const GmemScratch &G, double *red) {
+  unsigned char *p = G.base + (size_t)blockIdx.x * G.stride;
+  const int Lp = G.L_cap + 1;
+  B.red = red;
+  B.rk = reinterpret_cast<uint4 *>(p); p += (size_t)Lp * sizeof(uint4);
+  B.ctype = reinterpret_cast<uint32_t *>(p); p += (size_t)G.K_cap * 4;
+  B.crank = reinterpret_cast<uint32_t *>(p); p += (size_t)G.K_cap * 4;
+  B.cslot = reinterpret_cast<uint32_t *>(p); p += (size_t)G.K_cap * 8;
+  int32_t *ints = reinterpret_cast<int32_t *>(p); p += 6 * (size_t)Lp * 4;
+  B.Q = ints; B.C = ints + Lp; B.S = ints + 2 * Lp; B.cons = ints + 3 * Lp;
+  B.base = ints + 4 * Lp; B.cnt = ints + 5 * Lp;
+  B.mask = reinterpret_cast<uint32_t *>(p);
+  B.n_cap = G.n_cap; B.K_cap = G.K_cap; B.L_cap = G.L_cap;
+}
+
+inline size_t gmem_stride(int n_cap, int64_t K_cap, int L_cap) {
+  size_t s = (size_t)(L_cap + 1) * 16 + (size_t)K_cap * 16 + 6 * (size_t)(L_cap + 1) * 4 +
+             (size_t)((n_cap + 31) / 32) * 4 + 256;
+  return (s + 255) / 256 * 256;
+}
+
+struct QueueArgs {
+  int *ovf_count;
+  int *ovf_list;
+  int *err;
+  trmcr_coll_rec *log;
+  unsigned long long *log_count;
+  int64_t log_cap;
+};
+
+// Shock geometry state (A1, A2): see shock.cuh.
+struct ShockState {
+  int C = 0;
+  double x_min = 0, x_max = 1, inv_dx = 1, weight = 1;
+  double rho[2] = {1, 1}, u[2] = {0, 0}, T[2] = {1, 1}, Lg[2] = {0, 0};
+  int cap_g = 0;
+  int64_t *d_off[2] = {nullptr, nullptr};   // offsets double buffer
+  int32_t *d_dest = nullptr;                // [cap] destination cell (-1: left the domain)
+  int32_t *d_gdest[2] = {nullptr, nullptr}; // [cap_g] per side
+  void *gx[2] = {nullptr, nullptr};         // ghost positions (after transport)
+  void *gv[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  int32_t *d_counts = nullptr;              // [C] particles per destination cell
+  int *d_ng = nullptr;                      // [2] ghosts generated this step
+  int *d_W = nullptr;                       // max |destination - source| cell
+  unsigned long long *d_acct = nullptr;     // [4] injected L, injected R, dropped, generated
+};
+
+thread_local inline std::string g_init_error;
+
+}  // namespace trmcr
+
+
+// ======================================================================
+// context
+// ======================================================================
+struct trmcr_ctx {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  int dtype = TRMCR_F32, geometry = TRMCR_HOMOGENEOUS;
+  size_t rs = 4;
+  int64_t n = 0, cap = 0;
+  int ncells = 0, cell_base = 0;
+  double eps = 1, dt = 0.1;
+  trmcr_kernel kern{};
+  // particle state (double buffered for the shock)
+  void *v[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  void *x[2] = {nullptr, nullptr};
+  int cur = 0;
+  int64_t *d_offsets = nullptr;
+  std::vector<int64_t> h_offsets;
+  int32_t *d_mstate = nullptr;
+  double *d_stats = nullptr, *d_moments = nullptr;
+  int *d_ovf_count = nullptr, *d_ovf_list = nullptr, *d_err = nullptr;
+  unsigned char *d_scratch = nullptr;
+  trmcr::GmemScratch gs{};
+  int G = 1;
+  int gmem_threads = trmcr::kGmemThreads;
+  trmcr::SmemLayout lay{};
+  trmcr::StepParams P{};
+  uint32_t step = 0;
+  trmcr_coll_rec *d_log = nullptr;
+  unsigned long long *d_log_count = nullptr;
+  int64_t log_cap = 0;
+  int64_t launches = 0;
+  trmcr::ShockState shock{};
+  std::vector<void *> allocs;
+  std::string err;
+  int sticky = 0;
+};
+
+namespace trmcr {
+
+inline trmcr_status fail(trmcr_ctx *c, trmcr_status s, const std::string &msg) {
+  if (c) {
+    c->err = msg;
+    if (s == TRMCR_ECUDA || s == TRMCR_ENOMEM) c->sticky = 1;
+  } else {
+    g_init_error = msg;
+  }
+  return s;
+}
+
+#define CUDA_TRY(ctx, call)                                                               \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(ctx, TRMCR_ECUDA, std::string(#call " failed: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <typename T>
+inline trmcr_status dalloc(trmcr_ctx *c, T **p, size_t bytes) {
+  void *q = nullptr;
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, TRMCR_ENOMEM, std::string("cudaMalloc(") + std::to_string(bytes) + ") failed");
+  }
+  c->allocs.push_back(q);
+  *p = reinterpret_cast<T *>(q);
+  return TRMCR_OK;
+}
+
+inline trmcr_status check_launch(trmcr_ctx *c, const char *what) {
+  c->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, TRMCR_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return TRMCR_OK;
+}
+
+inline trmcr_status sync_check(trmcr_ctx *c) {
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  int err = 0;
+  CUDA_TRY(c, cudaMemcpy(&err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err & 1) return fail(c, TRMCR_ECAPACITY, "a cell's collision tree exceeded the global-memory plan capacity");
+  if (err & 2) return fail(c, TRMCR_ECAPACITY, "particle capacity exceeded (shock inflow)");
+  if (err & 16) return fail(c, TRMCR_ECUDA, "internal fault: tree index out of range");
+  return TRMCR_OK;
+}
+
+}  // namespace trmcr
+

@@ -1,0 +1,420 @@
+// shock.cuh — 1D stationary shock: reservoirs + free transport (A1) and the
+// stable counting sort by cell (A2), fused with the per-cell collision step.
+//
+// Step (all on the context stream, no host round trip):
+//   ghost_count / ghost_gen   ghost slabs [x_min-Lg, x_min) and [x_max, x_max+Lg),
+//                             Lg = (|u_B| + 6 sqrt(T_B)) dt, refilled with
+//                             IR(rho_B Lg / w) particles of M(rho_B,u_B,T_B) [R26];
+//                             transported; survivors counted per destination cell
+//   transport_kernel          x <- x + v_x dt (splitting); destination
+//                             cell; per-cell counts; max displacement W
+//   scan_offsets              exclusive scan -> new offsets (capacity check)
+//   shock_collide_smem/gmem   per destination cell: stable gather of its
+//                             particles from the source window [c-W, c+W] in
+//                             canonical order (left ghosts, interior in array
+//                             order, right ghosts), then the collision step
+//                             (cell_step.cuh) with rho_c = n_c w / dx, written
+//                             to the other buffer.
+#pragma once
+#include "ctx.cuh"
+
+namespace trmcr {
+
+struct ShockDev {
+  int C;
+  double x_min, x_max, inv_dx, dt;
+  double rho[2], u[2], T[2], Lg[2], y[2];
+  int cap_g;
+};
+
+__device__ __forceinline__ int cell_of(const ShockDev &S, double x) {
+  const double f = floor((x - S.x_min) * S.inv_dx);
+  return f < 0.0 ? 0 : (f >= (double)S.C ? S.C - 1 : (int)f);
+}
+
+template <typename Real> __device__ __forceinline__ Real add_rn(Real a, Real b);
+template <> __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+template <> __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+template <typename Real> __device__ __forceinline__ Real mul_rn(Real a, Real b);
+template <> __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+template <> __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+
+// warp-aggregated atomicAdd(&counts[key], 1) for lanes with key >= 0
+__device__ __forceinline__ void count_key(int32_t *counts, int key) {
+  const unsigned act = __activemask();
+  const unsigned peers = __match_any_sync(act, key);
+  const int lane = threadIdx.x & 31;
+  if (key >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(&counts[key], __popc(peers));
+}
+
+// ---- init: check the particles lie in the domain, sorted by cell; count ----
+template <typename Real>
+__global__ void shock_bin_init(ShockDev S, const Real *__restrict__ x, int64_t n, int32_t *counts, int *err) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double xi = (double)x[i];
+  if (!(xi >= S.x_min && xi < S.x_max)) { atomicOr(err, 4); return; }
+  const int c = cell_of(S, xi);
+  if (i > 0 && cell_of(S, (double)x[i - 1]) > c) atomicOr(err, 8);
+  atomicAdd(&counts[c], 1);
+}
+
+// exclusive scan of counts[0..C) into off[0..C], off[C] = total (one CTA)
+__global__ void __launch_bounds__(1024) scan_offsets(const int32_t *__restrict__ counts, int C, int64_t *off,
+                                                     int64_t cap, int *err) {
+  __shared__ int64_t wsum[32];
+  __shared__ int64_t carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int ITEMS = 16;
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < C; base += 1024 * ITEMS) {
+    int64_t v[ITEMS];
+    int64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const int i = base + tid * ITEMS + k;
+      v[k] = i < C ? counts[i] : 0;
+      s += v[k];
+    }
+    int64_t incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t w = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t t = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += t;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    int64_t run = carry + (warp > 0 ? wsum[warp - 1] : 0) + incl - s;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const int i = base + tid * ITEMS + k;
+      if (i < C) off[i] = run;
+      run += v[k];
+    }
+    __syncthreads();
+    if (tid == 0) carry += wsum[31];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    off[C] = carry;
+    if (carry > cap) atomicOr(err, 2);
+  }
+}
+
+// ---- A1: reservoir ghost counts IR(rho_B Lg / w) ----
+__global__ void ghost_count(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, int *ng, int *err) {
+  const int side = threadIdx.x;
+  if (side > 1) return;
+  const RngKey K{k0, k1, 0xFFFFFFF0u + (uint32_t)side, step};
+  const uint4 w = K(kResv, side, 0, 0);
+  const double y = S.y[side];
+  const double fl = floor(y);
+  int64_t N = (int64_t)fl + ((u53(w.x, w.y) < y - fl) ? 1 : 0);
+  if (N > S.cap_g) { atomicOr(err, 2); N = S.cap_g; }
+  ng[side] = (int)N;
+}
+
+// ---- A1: ghost particles, transported; survivors counted ----
+template <typename Real>
+__global__ void ghost_gen(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, const int *ng, Real *gx0,
+                          Real *gx1, Real *gvx0, Real *gvy0, Real *gvz0, Real *gvx1, Real *gvy1, Real *gvz1,
+                          int32_t *gd0, int32_t *gd1, int32_t *counts, int *W, unsigned long long *acct) {
+  const int side = blockIdx.y;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= ng[side]) return;
+  const RngKey K{k0, k1, 0xFFFFFFF0u + (uint32_t)side, step};
+  const uint4 a = K(kResv, side, 1, k), b = K(kResv, side, 2, k), c = K(kResv, side, 3, k);
+  const double upos = u53(a.x, a.y), u1 = u53(a.z, a.w), u2 = u53(b.x, b.y), u3 = u53(b.z, b.w);
+  const double u4 = u53(c.x, c.y);
+  const double Lg = S.Lg[side];
+  const double xg = side ? __dadd_rn(S.x_max, __dmul_rn(Lg, upos))
+                         : __dadd_rn(__dsub_rn(S.x_min, Lg), __dmul_rn(Lg, upos));
+  const double r1 = sqrt(-2.0 * log(u1)), r3 = sqrt(-2.0 * log(u3));
+  double s2, c2, s4, c4;
+  sincospi(2.0 * u2, &s2, &c2);
+  sincospi(2.0 * u4, &s4, &c4);
+  const double sT = sqrt(S.T[side]);
+  const Real vx = (Real)(S.u[side] + sT * (r1 * c2));
+  const Real vy = (Real)(sT * (r1 * s2));
+  const Real vz = (Real)(sT * (r3 * c4));
+  const Real xn = add_rn<Real>((Real)xg, mul_rn<Real>(vx, (Real)S.dt));
+  const double xd = (double)xn;
+  const bool keep = xd >= S.x_min && xd < S.x_max;
+  const int d = keep ? cell_of(S, xd) : -1;
+  Real *gx = side ? gx1 : gx0;
+  Real *gvx = side ? gvx1 : gvx0, *gvy = side ? gvy1 : gvy0, *gvz = side ? gvz1 : gvz0;
+  int32_t *gd = side ? gd1 : gd0;
+  gx[k] = xn; gvx[k] = vx; gvy[k] = vy; gvz[k] = vz; gd[k] = d;
+  if (keep) {
+    atomicAdd(&counts[d], 1);
+    atomicMax(W, side ? S.C - d : d + 1);
+    atomicAdd(&acct[side], 1ull);
+  }
+}
+
+// ---- A1: free transport of the interior particles ----
+template <typename Real>
+__global__ void __launch_bounds__(256)
+transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const Real *__restrict__ vx,
+                 int32_t *dest, int32_t *counts, int *W, unsigned long long *acct) {
+  const int64_t n = off_old[S.C];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Real xo = x[i];
+  const int src = cell_of(S, (double)xo);
+  const Real xn = add_rn<Real>(xo, mul_rn<Real>(vx[i], (Real)S.dt));
+  x[i] = xn;
+  const double xd = (double)xn;
+  const bool keep = xd >= S.x_min && xd < S.x_max;
+  const int d = keep ? cell_of(S, xd) : -1;
+  dest[i] = d;
+  count_key(counts, d);
+  int disp = keep ? abs(d - src) : 0;
+  const unsigned act = __activemask();
+  disp = __reduce_max_sync(act, disp);
+  const unsigned dropped = __popc(__ballot_sync(act, !keep));
+  if ((threadIdx.x & 31) == (__ffs(act) - 1)) {
+    if (disp > 0) atomicMax(W, disp);
+    if (dropped) atomicAdd(&acct[2], (unsigned long long)dropped);
+  }
+}
+
+struct GatherSrc {
+  const int64_t *off_old;
+  const int *ng;
+  const int *W;
+  const void *x, *vx, *vy, *vz;      // interior (source buffer, transported positions)
+  const int32_t *dest;
+  const void *gx[2], *gvx[2], *gvy[2], *gvz[2];
+  const int32_t *gdest[2];
+};
+
+// Stable gather of destination cell c into (bx,by,bz) [velocities] and ox
+// [positions, global] in canonical source order.  Returns the count.
+template <typename Real>
+__device__ int gather_cell(const ShockDev &S, const GatherSrc &G, int c, Real *bx, Real *by, Real *bz,
+                           Real *ox, int *wcnt) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int W = *G.W;
+  int running = 0;
+  for (int seg = 0; seg < 3; ++seg) {
+    int64_t lo, hi;
+    const Real *sx, *svx, *svy, *svz;
+    const int32_t *sd;
+    if (seg == 1) {
+      const int a = max(c - W, 0), b = min(c + W, S.C - 1);
+      lo = G.off_old[a]; hi = G.off_old[b + 1];
+      sx = (const Real *)G.x; svx = (const Real *)G.vx; svy = (const Real *)G.vy; svz = (const Real *)G.vz;
+      sd = G.dest;
+    } else {
+      const int side = seg == 0 ? 0 : 1;
+      const bool in = side == 0 ? (c - W <= -1) : (c + W >= S.C);
+      if (!in) continue;
+      lo = 0; hi = G.ng[side];
+      sx = (const Real *)G.gx[side]; svx = (const Real *)G.gvx[side];
+      svy = (const Real *)G.gvy[side]; svz = (const Real *)G.gvz[side];
+      sd = G.gdest[side];
+    }
+    for (int64_t b0 = lo; b0 < hi; b0 += blockDim.x) {
+      const int64_t i = b0 + tid;
+      const bool match = i < hi && sd[i] == c;
+      const unsigned bal = __ballot_sync(0xffffffffu, match);
+      if (lane == 0) wcnt[warp] = __popc(bal);
+      __syncthreads();
+      int wb = 0, tot = 0;
+      for (int w = 0; w < nw; ++w) {
+        const int t = wcnt[w];
+        wb += (w < warp) ? t : 0;
+        tot += t;
+      }
+      if (match) {
+        const int pos = running + wb + __popc(bal & ((1u << lane) - 1u));
+        bx[pos] = svx[i]; by[pos] = svy[i]; bz[pos] = svz[i];
+        ox[pos] = sx[i];
+      }
+      running += tot;
+      __syncthreads();
+    }
+  }
+  return running;
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(kSmemThreads)
+shock_collide_smem(StepParams P, SmemLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
+                   Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, QueueArgs Q) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ CellShared sh;
+  __shared__ int wcnt[32];
+  const int c = blockIdx.x;
+  CellBuf<Real> B;
+  bind_smem(B, smem, Lay);
+  const int64_t base = off_new[c];
+  const int n = (int)(off_new[c + 1] - base);
+  int rc = kOverflow;
+  if (n <= B.n_cap) {
+    gather_cell<Real>(S, G, c, B.vx, B.vy, B.vz, ox + base, wcnt);
+    __syncthreads();
+    rc = process_cell<Real, false, true>(P, B, sh, nullptr, nullptr, nullptr, ovx + base, ovy + base,
+                                         ovz + base, n, P.cell_base + (uint32_t)c, m_state + c,
+                                         stats + (size_t)c * TRMCR_NSTATS, Q.log, Q.log_count, Q.log_cap);
+  }
+  if (rc != kOk && threadIdx.x == 0) {
+    const int k = atomicAdd(Q.ovf_count, 1);
+    Q.ovf_list[k] = c;
+  }
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(kGmemThreads)
+shock_collide_gmem(StepParams P, GmemScratch GS, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
+                   Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, QueueArgs Q) {
+  __shared__ CellShared sh;
+  __shared__ double red[32 * 8];
+  __shared__ int wcnt[32];
+  const int count = *Q.ovf_count;
+  CellBuf<Real> B;
+  bind_gmem(B, GS, red);
+  for (int k = blockIdx.x; k < count; k += gridDim.x) {
+    const int c = Q.ovf_list[k];
+    const int64_t base = off_new[c];
+    const int n = (int)(off_new[c + 1] - base);
+    B.vx = ovx + base; B.vy = ovy + base; B.vz = ovz + base;
+    gather_cell<Real>(S, G, c, B.vx, B.vy, B.vz, ox + base, wcnt);
+    __syncthreads();
+    const int rc = process_cell<Real, false, false>(P, B, sh, nullptr, nullptr, nullptr, B.vx, B.vy, B.vz, n,
+                                                    P.cell_base + (uint32_t)c, m_state + c,
+                                                    stats + (size_t)c * TRMCR_NSTATS, Q.log, Q.log_count,
+                                                    Q.log_cap);
+    if (rc != kOk && threadIdx.x == 0) atomicOr(Q.err, 1);
+    __syncthreads();
+  }
+}
+
+inline ShockDev shock_dev(const trmcr_ctx *c) {
+  const ShockState &s = c->shock;
+  ShockDev d;
+  d.C = s.C; d.x_min = s.x_min; d.x_max = s.x_max; d.inv_dx = s.inv_dx; d.dt = c->dt;
+  for (int k = 0; k < 2; ++k) {
+    d.rho[k] = s.rho[k]; d.u[k] = s.u[k]; d.T[k] = s.T[k]; d.Lg[k] = s.Lg[k];
+    d.y[k] = s.rho[k] * s.Lg[k] / s.weight;
+  }
+  d.cap_g = s.cap_g;
+  return d;
+}
+
+// Allocate shock state, validate + count the initial particles (sorted by
+// cell), build offsets.  Synchronises (init only).  *max_cell: largest cell.
+inline trmcr_status shock_init(trmcr_ctx *c, const trmcr_cells *cc, int *max_cell) {
+  ShockState &s = c->shock;
+  s.C = cc->n_cells;
+  s.x_min = cc->x_min; s.x_max = cc->x_max; s.weight = cc->weight;
+  s.inv_dx = (double)cc->n_cells / (cc->x_max - cc->x_min);
+  s.rho[0] = cc->rho_L; s.u[0] = cc->u_L; s.T[0] = cc->T_L;
+  s.rho[1] = cc->rho_R; s.u[1] = cc->u_R; s.T[1] = cc->T_R;
+  double ymax = 0;
+  for (int k = 0; k < 2; ++k) {
+    s.Lg[k] = (fabs(s.u[k]) + 6.0 * sqrt(s.T[k])) * c->dt;
+    ymax = std::max(ymax, s.rho[k] * s.Lg[k] / s.weight);
+  }
+  if (ymax > 1e9) return fail(c, TRMCR_EINVAL, "reservoir ghost slab too large (dt / weight)");
+  s.cap_g = (int)floor(ymax) + 2;   // IR(y) <= floor(y) + 1
+  if (dalloc(c, &s.d_off[0], sizeof(int64_t) * (s.C + 1)) || dalloc(c, &s.d_off[1], sizeof(int64_t) * (s.C + 1)) ||
+      dalloc(c, &s.d_dest, sizeof(int32_t) * (size_t)c->cap) || dalloc(c, &s.d_counts, sizeof(int32_t) * s.C) ||
+      dalloc(c, &s.d_ng, sizeof(int) * 2) || dalloc(c, &s.d_W, sizeof(int)) ||
+      dalloc(c, &s.d_acct, sizeof(unsigned long long) * 4))
+    return TRMCR_ENOMEM;
+  for (int k = 0; k < 2; ++k) {
+    if (dalloc(c, &s.d_gdest[k], sizeof(int32_t) * s.cap_g) || dalloc(c, &s.gx[k], c->rs * s.cap_g)) return TRMCR_ENOMEM;
+    for (int j = 0; j < 3; ++j)
+      if (dalloc(c, &s.gv[k][j], c->rs * s.cap_g)) return TRMCR_ENOMEM;
+  }
+  CUDA_TRY(c, cudaMemsetAsync(s.d_counts, 0, sizeof(int32_t) * s.C, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(s.d_acct, 0, sizeof(unsigned long long) * 4, c->stream));
+  const ShockDev d = shock_dev(c);
+  if (c->n > 0) {
+    const unsigned blocks = (unsigned)((c->n + 255) / 256);
+    if (c->dtype == TRMCR_F64)
+      shock_bin_init<double><<<blocks, 256, 0, c->stream>>>(d, (const double *)c->x[0], c->n, s.d_counts, c->d_err);
+    else
+      shock_bin_init<float><<<blocks, 256, 0, c->stream>>>(d, (const float *)c->x[0], c->n, s.d_counts, c->d_err);
+    if (auto e = check_launch(c, "shock_bin_init")) return e;
+  }
+  scan_offsets<<<1, 1024, 0, c->stream>>>(s.d_counts, s.C, s.d_off[0], c->cap, c->d_err);
+  if (auto e = check_launch(c, "scan_offsets")) return e;
+  std::vector<int32_t> counts(s.C);
+  CUDA_TRY(c, cudaMemcpyAsync(counts.data(), s.d_counts, sizeof(int32_t) * s.C, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  int err = 0;
+  CUDA_TRY(c, cudaMemcpy(&err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err & 4) return fail(c, TRMCR_EINVAL, "particle outside the shock domain");
+  if (err & 8) return fail(c, TRMCR_EINVAL, "shock particles must be sorted by cell (stable order)");
+  *max_cell = 0;
+  for (int32_t v : counts) *max_cell = std::max(*max_cell, (int)v);
+  c->cur = 0;
+  c->d_offsets = s.d_off[0];
+  return TRMCR_OK;
+}
+
+// One full shock step: A1 + A2 + A3..A8.
+template <typename Real>
+trmcr_status shock_step(trmcr_ctx *c) {
+  ShockState &s = c->shock;
+  const ShockDev d = shock_dev(c);
+  const int cur = c->cur, nxt = cur ^ 1;
+  CUDA_TRY(c, cudaMemsetAsync(s.d_counts, 0, sizeof(int32_t) * s.C, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(s.d_W, 0, sizeof(int), c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(s.d_acct, 0, sizeof(unsigned long long) * 4, c->stream));
+  ghost_count<<<1, 32, 0, c->stream>>>(d, c->P.k0, c->P.k1, c->step, s.d_ng, c->d_err);
+  if (auto e = check_launch(c, "ghost_count")) return e;
+  {
+    dim3 grid((unsigned)((s.cap_g + 255) / 256), 2);
+    ghost_gen<Real><<<grid, 256, 0, c->stream>>>(
+        d, c->P.k0, c->P.k1, c->step, s.d_ng, (Real *)s.gx[0], (Real *)s.gx[1], (Real *)s.gv[0][0],
+        (Real *)s.gv[0][1], (Real *)s.gv[0][2], (Real *)s.gv[1][0], (Real *)s.gv[1][1], (Real *)s.gv[1][2],
+        s.d_gdest[0], s.d_gdest[1], s.d_counts, s.d_W, s.d_acct);
+    if (auto e = check_launch(c, "ghost_gen")) return e;
+  }
+  {
+    const unsigned blocks = (unsigned)((c->cap + 255) / 256);
+    transport_kernel<Real><<<blocks, 256, 0, c->stream>>>(d, s.d_off[cur], (Real *)c->x[cur],
+                                                          (const Real *)c->v[cur][0], s.d_dest, s.d_counts,
+                                                          s.d_W, s.d_acct);
+    if (auto e = check_launch(c, "transport_kernel")) return e;
+  }
+  scan_offsets<<<1, 1024, 0, c->stream>>>(s.d_counts, s.C, s.d_off[nxt], c->cap, c->d_err);
+  if (auto e = check_launch(c, "scan_offsets")) return e;
+
+  GatherSrc G;
+  G.off_old = s.d_off[cur]; G.ng = s.d_ng; G.W = s.d_W;
+  G.x = c->x[cur]; G.vx = c->v[cur][0]; G.vy = c->v[cur][1]; G.vz = c->v[cur][2]; G.dest = s.d_dest;
+  for (int k = 0; k < 2; ++k) {
+    G.gx[k] = s.gx[k]; G.gvx[k] = s.gv[k][0]; G.gvy[k] = s.gv[k][1]; G.gvz[k] = s.gv[k][2];
+    G.gdest[k] = s.d_gdest[k];
+  }
+  QueueArgs Q{c->d_ovf_count, c->d_ovf_list, c->d_err, c->d_log, c->d_log_count, c->log_cap};
+  c->P.step = c->step;
+  Real *ox = (Real *)c->x[nxt], *ovx = (Real *)c->v[nxt][0], *ovy = (Real *)c->v[nxt][1], *ovz = (Real *)c->v[nxt][2];
+  shock_collide_smem<Real><<<s.C, kSmemThreads, c->lay.total, c->stream>>>(
+      c->P, c->lay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, Q);
+  if (auto e = check_launch(c, "shock_collide_smem")) return e;
+  shock_collide_gmem<Real><<<c->G, c->gmem_threads, 0, c->stream>>>(c->P, c->gs, d, G, s.d_off[nxt], ox, ovx, ovy,
+                                                                 ovz, c->d_mstate, c->d_stats, Q);
+  if (auto e = check_launch(c, "shock_collide_gmem")) return e;
+  c->cur = nxt;
+  c->d_offsets = s.d_off[nxt];
+  return TRMCR_OK;
+}
+
+}  // namespace trmcr

@@ -1,0 +1,478 @@
+// trmcr.cu — kernels and host runtime behind include/trmcr.h (sm_100a).
+//
+// Step pipeline (homogeneous geometry), all on the context stream:
+//   cell_step_smem<Real>   one CTA per cell, working set in shared memory;
+//                          cells larger than n_cap, or whose tree overflows the
+//                          shared-memory plan, are queued (nothing written)
+//   cell_step_gmem<Real>   persistent CTAs drain that queue with the working
+//                          set in global memory (L2-resident for C1/C2 sizes)
+// Shock geometry adds transport/binning kernels (shock.cuh) in front.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/trmcr.h"
+#include "cell_step.cuh"
+#include "ctx.cuh"
+#include "shock.cuh"
+
+using namespace trmcr;
+
+#define TRMCR_VERSION "trmcr 0.1 (sm_100a)"
+
+namespace {
+
+template <typename Real>
+__global__ void __launch_bounds__(kSmemThreads)
+cell_step_smem(StepParams P, SmemLayout Lay, const int64_t *__restrict__ offsets, int ncells,
+               Real *vx, Real *vy, Real *vz, int32_t *m_state, double *stats, QueueArgs Q) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ CellShared sh;
+  const int c = blockIdx.x;
+  if (c >= ncells) return;
+  CellBuf<Real> B;
+  bind_smem(B, smem, Lay);
+  const int64_t off = offsets[c];
+  const int n = (int)(offsets[c + 1] - off);
+  const int rc = process_cell<Real, true, true>(P, B, sh, vx + off, vy + off, vz + off, vx + off, vy + off,
+                                          vz + off, n, P.cell_base + (uint32_t)c, m_state + c,
+                                          stats + (size_t)c * TRMCR_NSTATS, Q.log, Q.log_count,
+                                          Q.log_cap);
+  if (rc != kOk && threadIdx.x == 0) {
+    const int k = atomicAdd(Q.ovf_count, 1);
+    Q.ovf_list[k] = c;
+  }
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(kGmemThreads)
+cell_step_gmem(StepParams P, GmemScratch G, const int64_t *__restrict__ offsets, Real *vx, Real *vy,
+               Real *vz, int32_t *m_state, double *stats, QueueArgs Q) {
+  __shared__ CellShared sh;
+  __shared__ double red[32 * 8];
+  const int count = *Q.ovf_count;
+  CellBuf<Real> B;
+  bind_gmem(B, G, red);
+  for (int k = blockIdx.x; k < count; k += gridDim.x) {
+    const int c = Q.ovf_list[k];
+    const int64_t off = offsets[c];
+    const int n = (int)(offsets[c + 1] - off);
+    B.vx = vx + off; B.vy = vy + off; B.vz = vz + off;
+    const int rc = process_cell<Real, false, false>(P, B, sh, vx + off, vy + off, vz + off, vx + off,
+                                             vy + off, vz + off, n, P.cell_base + (uint32_t)c,
+                                             m_state + c, stats + (size_t)c * TRMCR_NSTATS, Q.log,
+                                             Q.log_count, Q.log_cap);
+    if (rc != kOk && threadIdx.x == 0) atomicOr(Q.err, 1);
+    __syncthreads();
+  }
+}
+
+// A9: per-cell moments, one CTA per cell (two passes).
+template <typename Real>
+__global__ void __launch_bounds__(256)
+moments_kernel(const int64_t *__restrict__ offsets, int ncells, const Real *__restrict__ vx,
+               const Real *__restrict__ vy, const Real *__restrict__ vz,
+               const int32_t *__restrict__ m_state, int shock, double w_over_dx, double *out) {
+  __shared__ double red[8 * 8];
+  const int c = blockIdx.x;
+  if (c >= ncells) return;
+  const int64_t off = offsets[c];
+  const int n = (int)(offsets[c + 1] - off);
+  double s[3] = {0, 0, 0};
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    s[0] += (double)vx[off + i]; s[1] += (double)vy[off + i]; s[2] += (double)vz[off + i];
+  }
+  block_sum<3>(s, red);
+  const double ux = n ? s[0] / n : 0.0, uy = n ? s[1] / n : 0.0, uz = n ? s[2] / n : 0.0;
+  double t[4] = {0, 0, 0, 0};
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double x = vx[off + i], y = vy[off + i], z = vz[off + i];
+    const double dx = x - ux, dy = y - uy, dz = z - uz;
+    const double c2 = dx * dx + dy * dy + dz * dz, v2 = x * x + y * y + z * z;
+    t[0] += c2; t[1] += dx * dx; t[2] += v2 * v2; t[3] += c2 * c2;
+  }
+  block_sum<4>(t, red);
+  if (threadIdx.x == 0) {
+    double *r = out + (size_t)c * TRMCR_NMOMENTS;
+    const double rho = shock ? n * w_over_dx : 1.0;
+    const double T = n ? t[0] / (3.0 * n) : 0.0;
+    r[TRMCR_MO_N] = n; r[TRMCR_MO_RHO] = rho;
+    r[TRMCR_MO_UX] = ux; r[TRMCR_MO_UY] = uy; r[TRMCR_MO_UZ] = uz; r[TRMCR_MO_T] = T;
+    r[TRMCR_MO_E] = 0.5 * rho * (ux * ux + uy * uy + uz * uz + 3.0 * T);
+    r[TRMCR_MO_P] = rho * T;
+    r[TRMCR_MO_PXX] = n ? t[1] / n : 0.0;
+    r[TRMCR_MO_M4] = n ? t[2] / n : 0.0;
+    r[TRMCR_MO_M4C] = n ? t[3] / n : 0.0;
+    r[TRMCR_MO_MMAX] = m_state[c];
+  }
+}
+
+__global__ void fill_i32(int32_t *a, int n, int32_t v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = v;
+}
+
+}  // namespace
+
+namespace {
+
+template <typename Real>
+trmcr_status launch_collide(trmcr_ctx *c) {
+  Real *vx = (Real *)c->v[c->cur][0], *vy = (Real *)c->v[c->cur][1], *vz = (Real *)c->v[c->cur][2];
+  QueueArgs Q{c->d_ovf_count, c->d_ovf_list, c->d_err, c->d_log, c->d_log_count, c->log_cap};
+  c->P.step = c->step;
+  if (c->ncells > 0) {
+    cell_step_smem<Real><<<c->ncells, kSmemThreads, c->lay.total, c->stream>>>(
+        c->P, c->lay, c->d_offsets, c->ncells, vx, vy, vz, c->d_mstate, c->d_stats, Q);
+    if (auto s = check_launch(c, "cell_step_smem")) return s;
+    cell_step_gmem<Real><<<c->G, c->gmem_threads, 0, c->stream>>>(c->P, c->gs, c->d_offsets, vx, vy, vz,
+                                                               c->d_mstate, c->d_stats, Q);
+    if (auto s = check_launch(c, "cell_step_gmem")) return s;
+  }
+  return TRMCR_OK;
+}
+
+template <typename Real>
+trmcr_status launch_moments(trmcr_ctx *c) {
+  if (c->ncells == 0) return TRMCR_OK;
+  moments_kernel<Real><<<c->ncells, 256, 0, c->stream>>>(
+      c->d_offsets, c->ncells, (const Real *)c->v[c->cur][0], (const Real *)c->v[c->cur][1],
+      (const Real *)c->v[c->cur][2], c->d_mstate, c->P.shock, c->P.w_over_dx, c->d_moments);
+  return check_launch(c, "moments_kernel");
+}
+
+trmcr_status do_step(trmcr_ctx *c) {
+  CUDA_TRY(c, cudaMemsetAsync(c->d_ovf_count, 0, sizeof(int), c->stream));
+  if (c->log_cap > 0)
+    CUDA_TRY(c, cudaMemsetAsync(c->d_log_count, 0, sizeof(unsigned long long), c->stream));
+  trmcr_status s;
+  if (c->geometry == TRMCR_SHOCK_1D)
+    s = c->dtype == TRMCR_F64 ? shock_step<double>(c) : shock_step<float>(c);
+  else
+    s = c->dtype == TRMCR_F64 ? launch_collide<double>(c) : launch_collide<float>(c);
+  if (s) return s;
+  c->step++;
+  return TRMCR_OK;
+}
+
+}  // namespace
+
+// ======================================================================
+// ABI
+// ======================================================================
+extern "C" {
+
+const char *trmcr_version(void) { return TRMCR_VERSION; }
+
+const char *trmcr_last_error(const trmcr_ctx *ctx) {
+  return ctx ? ctx->err.c_str() : g_init_error.c_str();
+}
+
+int64_t trmcr_launch_count(const trmcr_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+void trmcr_destroy(trmcr_ctx *ctx) {
+  if (!ctx) return;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (void *p : ctx->allocs) cudaFree(p);
+  delete ctx;
+}
+
+trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_cells *cc, double eps,
+                        double dt, const trmcr_kernel *kk, void *cuda_stream) {
+  if (!out || !pp || !cc || !kk) return fail(nullptr, TRMCR_EINVAL, "null argument");
+  *out = nullptr;
+  if (!(eps > 0) || !(dt > 0)) return fail(nullptr, TRMCR_EINVAL, "eps and dt must be > 0");
+  if (pp->dtype != TRMCR_F32 && pp->dtype != TRMCR_F64) return fail(nullptr, TRMCR_EINVAL, "bad dtype");
+  if (pp->n < 0 || pp->n > 0x7FFFFFFFLL) return fail(nullptr, TRMCR_EINVAL, "bad particle count");
+  if (pp->n > 0 && (!pp->vx || !pp->vy || !pp->vz)) return fail(nullptr, TRMCR_EINVAL, "null velocity pointer");
+  if (kk->model != TRMCR_MAXWELL && kk->model != TRMCR_HARD_SPHERE) return fail(nullptr, TRMCR_EINVAL, "bad model");
+  if (kk->indicator != TRMCR_IND_PXX && kk->indicator != TRMCR_IND_M4) return fail(nullptr, TRMCR_EINVAL, "bad indicator");
+  if (kk->adaptive) {
+    if (kk->m_init < 1 || kk->m_cap < kk->m_init || kk->m_cap > 16384)
+      return fail(nullptr, TRMCR_EINVAL, "need 1 <= m_init <= m_cap <= 16384");
+    if (!(kk->delta1 > 0) || !(kk->delta1 < kk->delta2)) return fail(nullptr, TRMCR_EINVAL, "need 0 < delta1 < delta2");
+  } else if (kk->m_fixed < 0 || kk->m_fixed > 16384) {
+    return fail(nullptr, TRMCR_EINVAL, "need 0 <= m_fixed <= 16384");
+  }
+  if (cc->geometry != TRMCR_HOMOGENEOUS && cc->geometry != TRMCR_SHOCK_1D)
+    return fail(nullptr, TRMCR_EINVAL, "bad geometry");
+  if (cc->n_cells < 0 || cc->cell_base < 0) return fail(nullptr, TRMCR_EINVAL, "bad cell count");
+
+  trmcr_ctx *c = new trmcr_ctx();
+  c->stream = (cudaStream_t)cuda_stream;
+  cudaGetDevice(&c->dev);
+  c->dtype = pp->dtype;
+  c->rs = pp->dtype == TRMCR_F64 ? 8 : 4;
+  c->geometry = cc->geometry;
+  c->n = pp->n;
+  c->ncells = cc->n_cells;
+  c->cell_base = cc->cell_base;
+  c->eps = eps; c->dt = dt; c->kern = *kk;
+  auto bail = [&](trmcr_status s) { g_init_error = c->err; trmcr_destroy(c); return s; };
+
+  int max_cell = 0;
+  if (c->geometry == TRMCR_HOMOGENEOUS) {
+    if (!cc->offsets) { fail(c, TRMCR_EINVAL, "homogeneous geometry needs offsets"); return bail(TRMCR_EINVAL); }
+    c->h_offsets.assign(cc->offsets, cc->offsets + c->ncells + 1);
+    if (c->h_offsets[0] != 0 || c->h_offsets[c->ncells] != c->n) {
+      fail(c, TRMCR_EINVAL, "offsets must start at 0 and end at n");
+      return bail(TRMCR_EINVAL);
+    }
+    for (int i = 0; i < c->ncells; ++i) {
+      const int64_t d = c->h_offsets[i + 1] - c->h_offsets[i];
+      if (d < 0) { fail(c, TRMCR_EINVAL, "offsets not monotone"); return bail(TRMCR_EINVAL); }
+      max_cell = (int)std::max<int64_t>(max_cell, d);
+    }
+    c->cap = c->n;
+  } else {
+    if (cc->offsets) { fail(c, TRMCR_EINVAL, "shock geometry takes no offsets"); return bail(TRMCR_EINVAL); }
+    if (!pp->x && pp->n > 0) { fail(c, TRMCR_EINVAL, "shock geometry needs positions"); return bail(TRMCR_EINVAL); }
+    if (!(cc->x_max > cc->x_min) || !(cc->weight > 0) || c->ncells < 1) {
+      fail(c, TRMCR_EINVAL, "bad shock domain");
+      return bail(TRMCR_EINVAL);
+    }
+    if (!(cc->rho_L > 0) || !(cc->rho_R > 0) || !(cc->T_L > 0) || !(cc->T_R > 0)) {
+      fail(c, TRMCR_EINVAL, "reservoir states need rho, T > 0");
+      return bail(TRMCR_EINVAL);
+    }
+    c->cap = pp->capacity > 0 ? pp->capacity : c->n + c->n / 4 + 65536;
+    if (c->cap < c->n || c->cap > 0x7FFFFFFFLL) { fail(c, TRMCR_EINVAL, "bad capacity"); return bail(TRMCR_EINVAL); }
+  }
+
+  // ---- parameters ----
+  StepParams &P = c->P;
+  P.model = kk->model; P.adaptive = kk->adaptive; P.m_fixed = kk->m_fixed; P.m_cap = kk->m_cap;
+  P.indicator = kk->indicator; P.log_on = 0;
+  P.delta1 = kk->delta1; P.delta2 = kk->delta2; P.dt = dt; P.eps = eps;
+  P.k0 = (uint32_t)kk->seed; P.k1 = (uint32_t)(kk->seed >> 32);
+  P.step = 0; P.cell_base = (uint32_t)cc->cell_base;
+  P.shock = c->geometry == TRMCR_SHOCK_1D;
+  P.err = nullptr;   // set once d_err exists
+  P.debug_stop = getenv("TRMCR_DEBUG_STOP") ? atoi(getenv("TRMCR_DEBUG_STOP")) : 0;
+  P.w_over_dx = P.shock ? cc->weight / ((cc->x_max - cc->x_min) / cc->n_cells) : 0.0;
+
+  // ---- buffers ----
+  const int nbuf = c->geometry == TRMCR_SHOCK_1D ? 2 : 1;
+  for (int b = 0; b < nbuf; ++b) {
+    for (int k = 0; k < 3; ++k)
+      if (dalloc(c, &c->v[b][k], (size_t)c->cap * c->rs)) return bail(TRMCR_ENOMEM);
+    if (c->geometry == TRMCR_SHOCK_1D && dalloc(c, &c->x[b], (size_t)c->cap * c->rs)) return bail(TRMCR_ENOMEM);
+  }
+  if (dalloc(c, &c->d_offsets, sizeof(int64_t) * (c->ncells + 1)) ||
+      dalloc(c, &c->d_mstate, sizeof(int32_t) * std::max(c->ncells, 1)) ||
+      dalloc(c, &c->d_stats, sizeof(double) * TRMCR_NSTATS * std::max(c->ncells, 1)) ||
+      dalloc(c, &c->d_moments, sizeof(double) * TRMCR_NMOMENTS * std::max(c->ncells, 1)) ||
+      dalloc(c, &c->d_ovf_count, sizeof(int)) ||
+      dalloc(c, &c->d_ovf_list, sizeof(int) * std::max(c->ncells, 1)) ||
+      dalloc(c, &c->d_err, sizeof(int)) || dalloc(c, &c->d_log_count, sizeof(unsigned long long)))
+    return bail(TRMCR_ENOMEM);
+  c->P.err = c->d_err;
+  if (cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->d_stats, 0, sizeof(double) * TRMCR_NSTATS * std::max(c->ncells, 1), c->stream) != cudaSuccess) {
+    fail(c, TRMCR_ECUDA, "memset failed");
+    return bail(TRMCR_ECUDA);
+  }
+  const int m0 = kk->adaptive ? kk->m_init : kk->m_fixed;
+  if (c->ncells > 0) {
+    fill_i32<<<(c->ncells + 255) / 256, 256, 0, c->stream>>>(c->d_mstate, c->ncells, m0);
+    if (check_launch(c, "fill_i32")) return bail(TRMCR_ECUDA);
+  }
+
+  // ---- copy particles in ----
+  const cudaMemcpyKind kind = pp->host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  const void *src[3] = {pp->vx, pp->vy, pp->vz};
+  for (int k = 0; k < 3 && c->n > 0; ++k)
+    if (cudaMemcpyAsync(c->v[0][k], src[k], (size_t)c->n * c->rs, kind, c->stream) != cudaSuccess) {
+      fail(c, TRMCR_ECUDA, "particle copy failed");
+      return bail(TRMCR_ECUDA);
+    }
+  if (c->geometry == TRMCR_SHOCK_1D && c->n > 0)
+    if (cudaMemcpyAsync(c->x[0], pp->x, (size_t)c->n * c->rs, kind, c->stream) != cudaSuccess) {
+      fail(c, TRMCR_ECUDA, "position copy failed");
+      return bail(TRMCR_ECUDA);
+    }
+  if (c->geometry == TRMCR_HOMOGENEOUS) {
+    if (cudaMemcpyAsync(c->d_offsets, c->h_offsets.data(), sizeof(int64_t) * (c->ncells + 1),
+                        cudaMemcpyHostToDevice, c->stream) != cudaSuccess) {
+      fail(c, TRMCR_ECUDA, "offsets copy failed");
+      return bail(TRMCR_ECUDA);
+    }
+  }
+
+  if (c->geometry == TRMCR_SHOCK_1D) {
+    trmcr_status s = shock_init(c, cc, &max_cell);
+    if (s) return bail(s);
+  }
+
+  // ---- shared-memory plan capacity ----
+  int smem_max = 0;
+  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
+  if (smem_max <= 0) smem_max = 227 * 1024;
+  const int budget = std::min(smem_max - 4096, 160 * 1024);
+  int n_cap = 0;
+  if (c->geometry == TRMCR_HOMOGENEOUS) n_cap = std::max(32, (max_cell + 31) / 32 * 32);
+  else n_cap = std::max(64, (2 * max_cell + 31) / 32 * 32);   // shock cells fluctuate
+  const int L_cap = 64;
+  // debug knobs: TRMCR_FORCE_GMEM=1 routes every cell through the global-memory
+  // path; TRMCR_SMEM_KCAP overrides the shared-memory tree capacity.
+  const char *force_g = getenv("TRMCR_FORCE_GMEM");
+  const char *kcap_env = getenv("TRMCR_SMEM_KCAP");
+  for (;;) {
+    const int K_cap = kcap_env ? atoi(kcap_env) : std::max(256, n_cap / 2);
+    c->lay.build(n_cap, K_cap, L_cap, c->rs);
+    if ((int)c->lay.total <= budget || n_cap <= 32) break;
+    n_cap = std::max(32, n_cap / 2 / 32 * 32);
+  }
+  if (force_g && atoi(force_g)) c->lay.n_cap = 0;
+  if (const char *gt = getenv("TRMCR_GMEM_THREADS")) c->gmem_threads = std::max(32, std::min(1024, atoi(gt)));
+  const int dyn = (int)c->lay.total;
+  cudaError_t ea;
+  if (c->geometry == TRMCR_SHOCK_1D)
+    ea = c->dtype == TRMCR_F64
+             ? cudaFuncSetAttribute(shock_collide_smem<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)
+             : cudaFuncSetAttribute(shock_collide_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  else
+    ea = c->dtype == TRMCR_F64
+             ? cudaFuncSetAttribute(cell_step_smem<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)
+             : cudaFuncSetAttribute(cell_step_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  if (ea != cudaSuccess) { fail(c, TRMCR_ECUDA, "cudaFuncSetAttribute failed"); return bail(TRMCR_ECUDA); }
+
+  // ---- global-memory plan scratch for large / overflowing cells ----
+  int big = 0;   // cells that will not fit the smem path at all
+  if (c->geometry == TRMCR_HOMOGENEOUS)
+    for (int i = 0; i < c->ncells; ++i) big += (c->h_offsets[i + 1] - c->h_offsets[i]) > c->lay.n_cap;
+  const int n_cap_g = c->geometry == TRMCR_HOMOGENEOUS
+                          ? std::max(max_cell, 32)
+                          : (int)std::min<int64_t>(c->cap, std::max(16 * max_cell, 65536));
+  const int L_cap_g = std::max(kk->adaptive ? kk->m_cap : kk->m_fixed, 64) + 1;
+  const int64_t K_cap_g = std::min<int64_t>(4LL * n_cap_g + 65536, 0x3FFFFFFFLL);
+  const size_t stride = gmem_stride(n_cap_g, K_cap_g, L_cap_g);
+  int G = std::max(1, std::min(c->ncells, big > 0 ? 148 : (c->geometry == TRMCR_SHOCK_1D ? 16 : 8)));
+  while (G > 1 && (double)G * stride > 4e9) G /= 2;
+  c->G = G;
+  if (dalloc(c, &c->d_scratch, stride * G)) return bail(TRMCR_ENOMEM);
+  c->gs = GmemScratch{c->d_scratch, stride, n_cap_g, (int)K_cap_g, L_cap_g};
+
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    fail(c, TRMCR_ECUDA, "init synchronisation failed");
+    return bail(TRMCR_ECUDA);
+  }
+  *out = c;
+  return TRMCR_OK;
+}
+
+trmcr_status trmcr_step(trmcr_ctx *c, int32_t n_steps) {
+  if (!c) return fail(nullptr, TRMCR_EINVAL, "null ctx");
+  if (c->sticky) return TRMCR_ESTATE;
+  if (n_steps < 0) return fail(c, TRMCR_EINVAL, "n_steps < 0");
+  for (int k = 0; k < n_steps; ++k)
+    if (trmcr_status s = do_step(c)) return s;
+  return TRMCR_OK;
+}
+
+trmcr_status trmcr_moments(trmcr_ctx *c, double *host_out) {
+  if (!c || !host_out) return fail(c, TRMCR_EINVAL, "null argument");
+  if (c->sticky) return TRMCR_ESTATE;
+  trmcr_status s = c->dtype == TRMCR_F64 ? launch_moments<double>(c) : launch_moments<float>(c);
+  if (s) return s;
+  if ((s = sync_check(c))) return s;
+  CUDA_TRY(c, cudaMemcpy(host_out, c->d_moments, sizeof(double) * TRMCR_NMOMENTS * c->ncells,
+                         cudaMemcpyDeviceToHost));
+  return TRMCR_OK;
+}
+
+trmcr_status trmcr_stats(trmcr_ctx *c, double *host_out) {
+  if (!c || !host_out) return fail(c, TRMCR_EINVAL, "null argument");
+  if (c->sticky) return TRMCR_ESTATE;
+  if (trmcr_status s = sync_check(c)) return s;
+  CUDA_TRY(c, cudaMemcpy(host_out, c->d_stats, sizeof(double) * TRMCR_NSTATS * c->ncells,
+                         cudaMemcpyDeviceToHost));
+  return TRMCR_OK;
+}
+
+trmcr_status trmcr_num_particles(trmcr_ctx *c, int64_t *n) {
+  if (!c || !n) return fail(c, TRMCR_EINVAL, "null argument");
+  if (c->sticky) return TRMCR_ESTATE;
+  if (trmcr_status s = sync_check(c)) return s;
+  if (c->geometry == TRMCR_SHOCK_1D) {
+    int64_t last = 0;
+    CUDA_TRY(c, cudaMemcpy(&last, c->d_offsets + c->ncells, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    c->n = last;
+  }
+  *n = c->n;
+  return TRMCR_OK;
+}
+
+trmcr_status trmcr_copy_particles(trmcr_ctx *c, void *vx, void *vy, void *vz, void *x, int64_t *offsets,
+                                  int32_t host) {
+  if (!c || !vx || !vy || !vz) return fail(c, TRMCR_EINVAL, "null argument");
+  int64_t n = 0;
+  if (trmcr_status s = trmcr_num_particles(c, &n)) return s;
+  const cudaMemcpyKind kind = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  void *dst[3] = {vx, vy, vz};
+  for (int k = 0; k < 3; ++k)
+    if (n > 0) CUDA_TRY(c, cudaMemcpyAsync(dst[k], c->v[c->cur][k], (size_t)n * c->rs, kind, c->stream));
+  if (x && c->geometry == TRMCR_SHOCK_1D && n > 0)
+    CUDA_TRY(c, cudaMemcpyAsync(x, c->x[c->cur], (size_t)n * c->rs, kind, c->stream));
+  if (offsets)
+    CUDA_TRY(c, cudaMemcpyAsync(offsets, c->d_offsets, sizeof(int64_t) * (c->ncells + 1), kind, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TRMCR_OK;
+}
+
+trmcr_status trmcr_set_velocities(trmcr_ctx *c, const void *vx, const void *vy, const void *vz, int32_t host) {
+  if (!c || !vx || !vy || !vz) return fail(c, TRMCR_EINVAL, "null argument");
+  if (c->sticky) return TRMCR_ESTATE;
+  if (c->geometry == TRMCR_SHOCK_1D) {
+    int64_t n = 0;
+    if (trmcr_status s = trmcr_num_particles(c, &n)) return s;
+  }
+  const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  const void *src[3] = {vx, vy, vz};
+  for (int k = 0; k < 3; ++k)
+    if (c->n > 0) CUDA_TRY(c, cudaMemcpyAsync(c->v[c->cur][k], src[k], (size_t)c->n * c->rs, kind, c->stream));
+  return TRMCR_OK;
+}
+
+trmcr_status trmcr_step_host(trmcr_ctx *c, const void *vx, const void *vy, const void *vz, double *host_moments) {
+  if (!c || !host_moments) return fail(c, TRMCR_EINVAL, "null argument");
+  if (c->geometry != TRMCR_HOMOGENEOUS) return fail(c, TRMCR_EINVAL, "trmcr_step_host: homogeneous geometry only");
+  if (trmcr_status s = trmcr_set_velocities(c, vx, vy, vz, 1)) return s;
+  if (trmcr_status s = do_step(c)) return s;
+  return trmcr_moments(c, host_moments);
+}
+
+trmcr_status trmcr_set_log(trmcr_ctx *c, int64_t capacity) {
+  if (!c || capacity < 0) return fail(c, TRMCR_EINVAL, "bad argument");
+  if (c->sticky) return TRMCR_ESTATE;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->d_log = nullptr;
+  c->log_cap = 0;
+  c->P.log_on = 0;
+  if (capacity > 0) {
+    if (dalloc(c, &c->d_log, sizeof(trmcr_coll_rec) * (size_t)capacity)) return TRMCR_ENOMEM;
+    c->log_cap = capacity;
+    c->P.log_on = 1;
+  }
+  CUDA_TRY(c, cudaMemset(c->d_log_count, 0, sizeof(unsigned long long)));
+  return TRMCR_OK;
+}
+
+trmcr_status trmcr_get_log(trmcr_ctx *c, trmcr_coll_rec *out, int64_t *count) {
+  if (!c || !count) return fail(c, TRMCR_EINVAL, "null argument");
+  if (trmcr_status s = sync_check(c)) return s;
+  unsigned long long k = 0;
+  CUDA_TRY(c, cudaMemcpy(&k, c->d_log_count, sizeof(k), cudaMemcpyDeviceToHost));
+  *count = (int64_t)k;
+  const int64_t m = std::min<int64_t>((int64_t)k, c->log_cap);
+  if (out && m > 0)
+    CUDA_TRY(c, cudaMemcpy(out, c->d_log, sizeof(trmcr_coll_rec) * (size_t)m, cudaMemcpyDeviceToHost));
+  return TRMCR_OK;
+}
+
+}  // extern "C"
