@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""TRMC-R benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c5|c4|c2|c1]
+                    [--impl trmcr|reference]
+
+Prints ONE JSON line (rank 0).  Metric: particle-updates/s of the TRMC-R
+step (BASELINE.json).  Default workload: configs[2], the batched ensemble of
+16,384 independent hard-sphere cells x 1,024 particles (16.8 M particles,
+fp32, eps = 0.01, dt = 0.1) sharded across GPUs by cell with an NCCL
+all-reduce of the global moments every step (DESIGN.md §7 explains the
+choice).  Inputs (201 MB) are larger than L2 (126 MB): no flush needed.
+
+--impl reference times the CPU oracle (oracle/, single-threaded, fp64) on a
+bounded sample of the same workload (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "TRMC-R particle-updates/s"
+UNIT = "particle-updates/s"
+
+
+# ----------------------------------------------------------------------------- workloads
+def workload(name: str, rank: int = 0, world: int = 1, eps_override=None):
+    """Synthetic inputs shaped like BASELINE.json configs."""
+    if name == "c3":
+        ncells, ppc = 16_384, 1024
+        lo, hi = rank * ncells // world, (rank + 1) * ncells // world
+        vx, vy, vz, off = synth.bimodal_cells(ncells, ppc, seed=1)
+        sl = slice(lo * ppc, hi * ppc)
+        return dict(kind="hom", vx=vx[sl], vy=vy[sl], vz=vz[sl], offsets=off[lo:hi + 1] - off[lo],
+                    cell_base=lo, dtype=np.float32,
+                    kw=dict(model=1, m_fixed=64, eps=eps_override or 0.01, dt=0.1, seed=1),
+                    cfg=dict(workload="configs[2] batched homogeneous hard spheres", cells=ncells,
+                             ppc=ppc, particles=ncells * ppc, eps=eps_override or 0.01, dt=0.1,
+                             truncation="TRMC-R m=64", sharding="cells", global_moments="allreduce/step"),
+                    global_cells=ncells)
+    if name in ("c4", "c5"):
+        if world > 1:
+            raise SystemExit("shock slab decomposition across GPUs is not implemented yet (DESIGN.md §8)")
+        if name == "c4":
+            setup = synth.shock_setup(mach=3.0, ncells=2000, n_total=1_000_000, x_min=-20, x_max=20)
+            eps = eps_override or 1.0
+        else:
+            setup = synth.shock_setup(mach=5.0, ncells=65_536, n_total=65_536_000, x_min=-50, x_max=50)
+            eps = eps_override or 0.01
+        x, vx, vy, vz = synth.shock_particles(setup, seed=1, dtype=np.float32)
+        inv = setup["ncells"] / (setup["x_max"] - setup["x_min"])
+        cell = np.clip(np.floor((x.astype(np.float64) - setup["x_min"]) * inv), 0, setup["ncells"] - 1)
+        order = np.argsort(cell, kind="stable")
+        return dict(kind="shock", x=x[order], vx=vx[order], vy=vy[order], vz=vz[order], setup=setup,
+                    dtype=np.float32,
+                    kw=dict(model=1, adaptive=True, m_init=2, m_cap=64, eps=eps, dt=setup["dt"], seed=1),
+                    cfg=dict(workload=f"configs[{3 if name == 'c4' else 4}] 1D Mach-{setup['mach']:g} shock",
+                             cells=setup["ncells"], particles=len(x), eps=eps, dt=setup["dt"],
+                             truncation="TRMC-RAD m_init=2 m_cap=64", sharding="none"),
+                    global_cells=setup["ncells"])
+    if name == "c2":
+        n = 1_000_000
+        vx, vy, vz = synth.anisotropic_gaussian(n, seed=1)
+        eps = eps_override or 1.0
+        return dict(kind="hom", vx=vx.astype(np.float32), vy=vy.astype(np.float32),
+                    vz=vz.astype(np.float32), offsets=np.array([0, n]), cell_base=0, dtype=np.float32,
+                    kw=dict(model=1, adaptive=True, m_init=2, m_cap=4096, eps=eps, dt=0.05, seed=1),
+                    cfg=dict(workload="configs[1] homogeneous hard spheres, one cell", cells=1,
+                             particles=n, eps=eps, dt=0.05, truncation="TRMC-RAD"), global_cells=1)
+    if name == "c1":
+        vx, vy, vz = synth.two_maxwellians(10_000, seed=1)
+        return dict(kind="hom", vx=vx, vy=vy, vz=vz, offsets=np.array([0, 10_000]), cell_base=0,
+                    dtype=np.float64, kw=dict(model=0, m_fixed=64, eps=1.0, dt=0.1, seed=1),
+                    cfg=dict(workload="configs[0] Maxwell molecules, one cell", cells=1, particles=10_000,
+                             eps=1.0, dt=0.1, truncation="TRMC-R m=64"), global_cells=1)
+    raise SystemExit(f"unknown workload {name}")
+
+
+# ----------------------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(workload_name):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload_name)
+    except (OSError, ValueError):
+        return None
+
+
+def oracle_rate(W, seconds=12.0, min_steps=1, max_steps=10**9):
+    """Time the CPU oracle (as it stands) on a bounded sample of workload W."""
+    from oracle import oracle as O
+    kw = dict(W["kw"])
+    cfg = O.Config(model=kw.get("model", 1), adaptive=int(bool(kw.get("adaptive", 0))),
+                   m_fixed=kw.get("m_fixed", 64), m_init=kw.get("m_init", 2), m_cap=kw.get("m_cap", 4096),
+                   eps=kw["eps"], dt=kw["dt"], seed=kw.get("seed", 1))
+    if W["kind"] == "hom":
+        off = W["offsets"]
+        ncs = len(off) - 1
+        take = ncs
+        # bounded sample: the first cells, about 1 M particles
+        while take > 1 and off[take] > 1_000_000:
+            take //= 2
+        o = O.HomogeneousState(cfg, W["vx"][: off[take]].astype(np.float64),
+                               W["vy"][: off[take]].astype(np.float64),
+                               W["vz"][: off[take]].astype(np.float64), off[: take + 1],
+                               gcell0=W.get("cell_base", 0))
+        per_step = int(off[take])
+        sample = f"first {take} of {ncs} cells ({per_step} particles), same per-cell workload"
+    else:
+        s = dict(W["setup"])
+        # a 1,024-cell window of the same grid (same dx, dt, w, ppc) around the shock
+        cells = min(1024, s["ncells"])
+        half = cells * s["dx"] / 2
+        s.update(ncells=cells, x_min=-half, x_max=half)
+        x, vx, vy, vz = synth.shock_particles(s, seed=1)
+        o = O.ShockState(cfg, s, x, vx, vy, vz)
+        per_step = o.n
+        sample = f"{cells}-cell window of the same grid around the shock ({per_step} particles)"
+    t0 = time.perf_counter()
+    steps = 0
+    parts = 0
+    while (steps < min_steps or time.perf_counter() - t0 < seconds) and steps < max_steps:
+        n_before = o.n if W["kind"] == "shock" else per_step
+        o.step(1)
+        parts += n_before
+        steps += 1
+    dt = time.perf_counter() - t0
+    return parts / dt, dict(sample=f"{sample}; {steps} steps, {dt:.1f} s", cores=1, steps=steps,
+                            seconds=dt)
+
+
+# ----------------------------------------------------------------------------- arms
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    W = workload(args.workload, 0, 1, args.eps)
+    # warmup steps then K timed steps, each step a bounded sample of the workload
+    from oracle import oracle as O  # noqa: F401
+    rate_w, _ = oracle_rate(W, seconds=0.0, min_steps=args.warmup, max_steps=args.warmup)
+    rate, info = oracle_rate(W, seconds=0.0, min_steps=args.steps, max_steps=args.steps)
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "ms_per_step": 1e3 * info["seconds"] / max(info["steps"], 1), "dtype": "f64",
+            "data": "synthetic", "config": W["cfg"],
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": info["sample"]},
+            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_trmcr(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_1009_2768_b200 import api
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    W = workload(args.workload, rank, world, args.eps)
+    td = torch.float32 if W["dtype"] == np.float32 else torch.float64
+    T = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(device=dev, dtype=td)
+    stream = torch.cuda.current_stream(dev)
+    if W["kind"] == "hom":
+        sim = api.Simulation(T(W["vx"]), T(W["vy"]), T(W["vz"]), offsets=W["offsets"],
+                             cell_base=W["cell_base"], stream=stream.cuda_stream, **W["kw"])
+        n_local = int(W["offsets"][-1])
+    else:
+        sim = api.Simulation(T(W["vx"]), T(W["vy"]), T(W["vz"]), x=T(W["x"]), shock=W["setup"],
+                             stream=stream.cuda_stream, **W["kw"])
+        n_local = sim.num_particles()
+    gm = torch.zeros(len(api.GLOBAL_FIELDS), dtype=torch.float64, device=dev)
+
+    def one_step():
+        sim.step(1)
+        if W["kind"] == "hom":
+            sim.global_moments(gm)
+            if world > 1:
+                dist.all_reduce(gm)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    n_before = sim.num_particles()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = sim.launch_count
+    sim.set_profiling(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            one_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_local = e0.elapsed_time(e1)
+    ktimes = sim.kernel_times()
+    sim.set_profiling(False)
+    launches = sim.launch_count - launches0
+    n_after = sim.num_particles()
+    updates_local = 0.5 * (n_before + n_after) * args.steps
+    t = torch.tensor([ms_local, updates_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        tm = t[:1].clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        tu = t[1:].clone()
+        dist.all_reduce(tu, op=dist.ReduceOp.SUM)
+        ms, updates = float(tm.item()), float(tu.item())
+    else:
+        ms, updates = ms_local, updates_local
+    value = updates / (ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (algorithmic bytes) ----
+    dom, (dom_ms, dom_n) = max(ktimes.items(), key=lambda kv: kv[1][0])
+    rs = 4 if td == torch.float32 else 8
+    if dom in ("cell_step_smem", "cell_step_gmem"):
+        bytes_per = 2 * 3 * rs            # read v, write the changed v (f_chg = 1 here)
+        if W["kind"] == "hom" and W["kw"]["eps"] > 0.05:
+            bytes_per = 2 * 3 * rs        # upper bound; changed fraction < 1 (dense write-back)
+    elif dom in ("shock_collide_smem", "shock_collide_gmem"):
+        bytes_per = 2 * 4 * rs            # read (x, v), write (x, v) once
+    elif dom == "transport_kernel":
+        bytes_per = 3 * rs                # read x, v_x; write x
+    else:
+        bytes_per = 3 * rs
+    peak, peak_kind = measured_peaks()
+    achieved = bytes_per * 0.5 * (n_before + n_after) / (dom_ms / dom_n * 1e-3) / 1e9
+    traffic = ncu_traffic(args.workload)
+    roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "traffic": traffic, "algorithmic_bytes_per_particle": bytes_per,
+            "kernel_share_of_step": round(dom_ms / ms_local, 4),
+            "kernel_ms": {k: round(v[0] / max(v[1], 1), 4) for k, v in ktimes.items()}}
+
+    # ---- e2e: host buffers through the public API (homogeneous: step_host) ----
+    e2e = None
+    if W["kind"] == "hom":
+        hv = [torch.as_tensor(np.ascontiguousarray(W[k])).to(td).pin_memory().numpy() for k in ("vx", "vy", "vz")]
+        out = np.zeros((sim.ncells, len(api.MOMENT_FIELDS)))
+        ke = max(3, min(args.steps, 20))
+        sim.step_host(*hv, out=out)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            sim.step_host(*hv, out=out)
+        t_e2e = time.perf_counter() - t0
+        tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_local * world * ke / float(tt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(3 * rs * n_local * world),
+               "d2h_bytes_per_step": int(out.nbytes * world), "steps": ke,
+               "path": "Simulation.step_host (trmcr_step_host): pinned host velocities in, per-cell moments out"}
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        rate, info = oracle_rate(W, seconds=args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": info["cores"], "kind": "oracle",
+               "sample": info["sample"]}
+    clocks = clk.summary()
+    cfg = dict(W["cfg"])
+    cfg.update(parallelism=f"{'cells' if W['kind'] == 'hom' else 'single'}x{world}",
+               l2="inputs larger than L2 (no flush)" if n_local * 3 * rs > 126e6 else "inputs L2-resident")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if td == torch.float32 else "f64", "data": "synthetic", "config": cfg,
+            "roofline": roof, "cpu_baseline": cpu, "clocks": clocks, "e2e": e2e,
+            "gpu_launches": int(launches), "impl": "trmcr"}
+    print(json.dumps(line), flush=True)
+    sim.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--eps", type=float, default=None)
+    ap.add_argument("--impl", default="trmcr", choices=["trmcr", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_trmcr(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

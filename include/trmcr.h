@@ -56,7 +56,8 @@ typedef enum { TRMCR_IND_PXX = 0, TRMCR_IND_M4 = 1 } trmcr_indicator;  /* RAD in
 /* Particle ensemble handed to trmcr_init.  Structure of arrays of length n
  * in `dtype`; device pointers unless `host` = 1.  x (positions) only for the
  * shock geometry.  Homogeneous: particles must be grouped by cell as
- * described by trmcr_cells.offsets.  Shock: any order (binned at init). */
+ * described by trmcr_cells.offsets.  Shock: positions inside [x_min, x_max)
+ * and sorted by cell (non-decreasing cell index; validated, EINVAL if not). */
 typedef struct {
   int32_t dtype;             /* trmcr_dtype                                          */
   int32_t host;              /* 1: pointers are host memory, 0: device memory        */
@@ -102,7 +103,14 @@ enum {
   TRMCR_ST_N = 0, TRMCR_ST_P, TRMCR_ST_MU, TRMCR_ST_SIGMA, TRMCR_ST_S0, TRMCR_ST_SEST,
   TRMCR_ST_E1, TRMCR_ST_MUSED, TRMCR_ST_MNEXT, TRMCR_ST_DEPTH, TRMCR_ST_ATTEMPTS,
   TRMCR_ST_LEAVES, TRMCR_ST_UNTOUCHED, TRMCR_ST_THERMALISED, TRMCR_ST_PROPOSALS,
-  TRMCR_ST_ACCEPTED, TRMCR_ST_VIOLATIONS, TRMCR_ST_MAXW, TRMCR_NSTATS
+  TRMCR_ST_ACCEPTED, TRMCR_ST_VIOLATIONS, TRMCR_ST_MAXW,
+  TRMCR_ST_PX, TRMCR_ST_PY, TRMCR_ST_PZ, TRMCR_ST_ENERGY,   /* sum v, sum |v|^2 (conserved by the step) */
+  TRMCR_NSTATS
+};
+/* Global sums over this context's cells, trmcr_global_moments(): */
+enum {
+  TRMCR_GM_N = 0, TRMCR_GM_PX, TRMCR_GM_PY, TRMCR_GM_PZ, TRMCR_GM_ENERGY, TRMCR_GM_NPXX,
+  TRMCR_GM_PROPOSALS, TRMCR_GM_ACCEPTED, TRMCR_GM_MAXW, TRMCR_GM_COST, TRMCR_NGLOBAL
 };
 /* Per-cell moment row (doubles), trmcr_moments(): */
 enum {
@@ -119,8 +127,8 @@ typedef struct {
 
 /* Create a context on the current CUDA device, bound to `cuda_stream`
  * (a cudaStream_t, NULL = legacy default stream).  eps: Knudsen number
- * (P:127-129), dt: time step, both > 0.  Copies the particles (and bins them
- * by cell for the shock).  Errors: EINVAL (bad sizes/arguments, eps or dt
+ * (P:127-129), dt: time step, both > 0.  Copies the particles (and builds
+ * the cell offsets for the shock).  Errors: EINVAL (bad sizes/arguments, eps or dt
  * <= 0, delta1 >= delta2, offsets not monotone, particle outside the shock
  * domain), ENOMEM, ECUDA. */
 trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *particles,
@@ -135,6 +143,11 @@ trmcr_status trmcr_moments(trmcr_ctx *ctx, double *host_out);
 
 /* Per-cell statistics of the last step, host out[n_cells * TRMCR_NSTATS]. Syncs. */
 trmcr_status trmcr_stats(trmcr_ctx *ctx, double *host_out);
+
+/* Global sums (TRMCR_NGLOBAL doubles) of the last step's per-cell statistics,
+ * written asynchronously to DEVICE memory `dev_out` (e.g. the buffer of an
+ * NCCL all-reduce across ranks).  cost = proposals + maxw/2. */
+trmcr_status trmcr_global_moments(trmcr_ctx *ctx, double *dev_out);
 
 /* Current particle count (shock: changes with inflow/outflow). Syncs. */
 trmcr_status trmcr_num_particles(trmcr_ctx *ctx, int64_t *n);
@@ -164,6 +177,18 @@ trmcr_status trmcr_get_log(trmcr_ctx *ctx, trmcr_coll_rec *out, int64_t *count);
 
 /* Number of kernel launches issued by this context so far. */
 int64_t trmcr_launch_count(const trmcr_ctx *ctx);
+
+/* Per-kernel device timing (CUDA events recorded around every launch on the
+ * context stream while enabled).  Kernel ids: */
+enum {
+  TRMCR_K_CELL_SMEM = 0, TRMCR_K_CELL_GMEM, TRMCR_K_MOMENTS, TRMCR_K_GHOST_COUNT, TRMCR_K_GHOST_GEN,
+  TRMCR_K_TRANSPORT, TRMCR_K_SCAN, TRMCR_K_SHOCK_SMEM, TRMCR_K_SHOCK_GMEM, TRMCR_NKERNELS
+};
+trmcr_status trmcr_set_profiling(trmcr_ctx *ctx, int32_t on);
+/* Sums, per kernel id, the device time (ms) and launch count recorded since
+ * the previous call (or since profiling was enabled), then resets. Syncs.
+ * ms and launches are host arrays of TRMCR_NKERNELS entries. */
+trmcr_status trmcr_kernel_times(trmcr_ctx *ctx, double *ms, int64_t *launches);
 
 /* Last error message of ctx (or of the last failed trmcr_init when ctx is NULL). */
 const char *trmcr_last_error(const trmcr_ctx *ctx);

@@ -24,8 +24,11 @@ IND_PXX, IND_M4 = 0, 1
 
 STAT_FIELDS = ["n", "p", "mu", "sigma", "S0", "S_est", "E1", "m_used", "m_next", "depth",
                "attempts", "leaves", "untouched", "thermalised", "proposals", "accepted",
-               "violations", "maxw"]
+               "violations", "maxw", "px", "py", "pz", "energy"]
+GLOBAL_FIELDS = ["n", "px", "py", "pz", "energy", "nPxx", "proposals", "accepted", "maxw", "cost"]
 MOMENT_FIELDS = ["n", "rho", "ux", "uy", "uz", "T", "E", "p", "Pxx", "M4", "M4c", "m_max"]
+KERNELS = ["cell_step_smem", "cell_step_gmem", "moments_kernel", "ghost_count", "ghost_gen",
+           "transport_kernel", "scan_offsets", "shock_collide_smem", "shock_collide_gmem"]
 STATS_DTYPE = np.dtype([(f, "<f8") for f in STAT_FIELDS])
 COLL_DTYPE = np.dtype([("cell", "<i4"), ("attempt", "<i4"), ("level", "<i4"), ("accepted", "<i4"),
                        ("j", "<i8"), ("slot_i", "<i8"), ("slot_k", "<i8")])
@@ -78,6 +81,12 @@ def lib():
         L.trmcr_step_host.argtypes = [vp, vp, vp, vp, P(C.c_double)]
         L.trmcr_set_log.argtypes = [vp, C.c_int64]
         L.trmcr_get_log.argtypes = [vp, vp, P(C.c_int64)]
+        L.trmcr_global_moments.argtypes = [vp, vp]
+        L.trmcr_global_moments.restype = C.c_int
+        L.trmcr_set_profiling.argtypes = [vp, C.c_int32]
+        L.trmcr_set_profiling.restype = C.c_int
+        L.trmcr_kernel_times.argtypes = [vp, P(C.c_double), P(C.c_int64)]
+        L.trmcr_kernel_times.restype = C.c_int
         L.trmcr_launch_count.argtypes = [vp]
         L.trmcr_launch_count.restype = C.c_int64
         L.trmcr_last_error.argtypes = [vp]
@@ -232,6 +241,23 @@ class Simulation:
         if cnt.value > cap:
             raise TrmcrError(ECAPACITY, f"log overflow: {cnt.value} > {cap}")
         return buf[: cnt.value].copy()
+
+    def global_moments(self, dev_out):
+        """Asynchronously write the global sums (GLOBAL_FIELDS) into a device float64 tensor."""
+        p, host, _ = _ptr(dev_out)
+        assert not host and dev_out.numel() >= len(GLOBAL_FIELDS)
+        self._check(lib().trmcr_global_moments(self._h, C.c_void_p(p)))
+
+    def set_profiling(self, on: bool = True):
+        self._check(lib().trmcr_set_profiling(self._h, int(bool(on))))
+
+    def kernel_times(self) -> dict:
+        """{kernel name: (total ms, launches)} since the last call (device events)."""
+        ms = np.zeros(len(KERNELS))
+        cnt = np.zeros(len(KERNELS), dtype=np.int64)
+        self._check(lib().trmcr_kernel_times(self._h, ms.ctypes.data_as(C.POINTER(C.c_double)),
+                                             cnt.ctypes.data_as(C.POINTER(C.c_int64))))
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNELS) if cnt[i] > 0}
 
     @property
     def launch_count(self) -> int:

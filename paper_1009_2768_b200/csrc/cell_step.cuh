@@ -481,6 +481,8 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
   dv2 = block_max(dv2, B.red);
   if (tid == 0) {
     sh.n = n; sh.ux = ux; sh.uy = uy; sh.uz = uz;
+    sh.sums[0] = s3[0]; sh.sums[1] = s3[1]; sh.sums[2] = s3[2];
+    sh.sums[3] = c3[2] + n * (ux * ux + uy * uy + uz * uz);   // sum |v|^2
     sh.S0 = (P.indicator == TRMCR_IND_PXX ? c3[0] : c3[1]) / n;
     const double rho_c = P.shock ? n * P.w_over_dx : 1.0;
     if (P.model == TRMCR_HARD_SPHERE) {
@@ -582,6 +584,8 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
       s[TRMCR_ST_THERMALISED] = sh.nT; s[TRMCR_ST_PROPOSALS] = (double)sh.prop;
       s[TRMCR_ST_ACCEPTED] = (double)sh.acc; s[TRMCR_ST_VIOLATIONS] = (double)sh.viol;
       s[TRMCR_ST_MAXW] = sh.nT >= 2 ? sh.nT : 0;
+      s[TRMCR_ST_PX] = sh.sums[0]; s[TRMCR_ST_PY] = sh.sums[1]; s[TRMCR_ST_PZ] = sh.sums[2];
+      s[TRMCR_ST_ENERGY] = sh.sums[3];
     }
   }
   return kOk;

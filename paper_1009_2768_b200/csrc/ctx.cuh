@@ -144,6 +144,11 @@ struct trmcr_ctx {
   unsigned long long *d_log_count = nullptr;
   int64_t log_cap = 0;
   int64_t launches = 0;
+  // per-kernel timing (trmcr_set_profiling)
+  int prof = 0;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<int> ev_kid;
   trmcr::ShockState shock{};
   std::vector<void *> allocs;
   std::string err;
@@ -183,7 +188,24 @@ inline trmcr_status dalloc(trmcr_ctx *c, T **p, size_t bytes) {
   return TRMCR_OK;
 }
 
-inline trmcr_status check_launch(trmcr_ctx *c, const char *what) {
+// Profiling brackets around a launch: prof_begin records the start event,
+// check_launch (with kid >= 0) records the stop event.
+inline void prof_event(trmcr_ctx *c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  cudaEventRecord(c->ev_pool[c->ev_used++], c->stream);
+}
+inline void prof_begin(trmcr_ctx *c, int kid) {
+  if (!c->prof) return;
+  c->ev_kid.push_back(kid);
+  prof_event(c);
+}
+
+inline trmcr_status check_launch(trmcr_ctx *c, const char *what, int kid = -1) {
+  if (c->prof && kid >= 0) prof_event(c);
   c->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(c, TRMCR_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));

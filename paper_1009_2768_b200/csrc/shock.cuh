@@ -376,25 +376,29 @@ trmcr_status shock_step(trmcr_ctx *c) {
   CUDA_TRY(c, cudaMemsetAsync(s.d_counts, 0, sizeof(int32_t) * s.C, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(s.d_W, 0, sizeof(int), c->stream));
   CUDA_TRY(c, cudaMemsetAsync(s.d_acct, 0, sizeof(unsigned long long) * 4, c->stream));
+  prof_begin(c, TRMCR_K_GHOST_COUNT);
   ghost_count<<<1, 32, 0, c->stream>>>(d, c->P.k0, c->P.k1, c->step, s.d_ng, c->d_err);
-  if (auto e = check_launch(c, "ghost_count")) return e;
+  if (auto e = check_launch(c, "ghost_count", TRMCR_K_GHOST_COUNT)) return e;
   {
     dim3 grid((unsigned)((s.cap_g + 255) / 256), 2);
+    prof_begin(c, TRMCR_K_GHOST_GEN);
     ghost_gen<Real><<<grid, 256, 0, c->stream>>>(
         d, c->P.k0, c->P.k1, c->step, s.d_ng, (Real *)s.gx[0], (Real *)s.gx[1], (Real *)s.gv[0][0],
         (Real *)s.gv[0][1], (Real *)s.gv[0][2], (Real *)s.gv[1][0], (Real *)s.gv[1][1], (Real *)s.gv[1][2],
         s.d_gdest[0], s.d_gdest[1], s.d_counts, s.d_W, s.d_acct);
-    if (auto e = check_launch(c, "ghost_gen")) return e;
+    if (auto e = check_launch(c, "ghost_gen", TRMCR_K_GHOST_GEN)) return e;
   }
   {
     const unsigned blocks = (unsigned)((c->cap + 255) / 256);
+    prof_begin(c, TRMCR_K_TRANSPORT);
     transport_kernel<Real><<<blocks, 256, 0, c->stream>>>(d, s.d_off[cur], (Real *)c->x[cur],
                                                           (const Real *)c->v[cur][0], s.d_dest, s.d_counts,
                                                           s.d_W, s.d_acct);
-    if (auto e = check_launch(c, "transport_kernel")) return e;
+    if (auto e = check_launch(c, "transport_kernel", TRMCR_K_TRANSPORT)) return e;
   }
+  prof_begin(c, TRMCR_K_SCAN);
   scan_offsets<<<1, 1024, 0, c->stream>>>(s.d_counts, s.C, s.d_off[nxt], c->cap, c->d_err);
-  if (auto e = check_launch(c, "scan_offsets")) return e;
+  if (auto e = check_launch(c, "scan_offsets", TRMCR_K_SCAN)) return e;
 
   GatherSrc G;
   G.off_old = s.d_off[cur]; G.ng = s.d_ng; G.W = s.d_W;
@@ -406,12 +410,14 @@ trmcr_status shock_step(trmcr_ctx *c) {
   QueueArgs Q{c->d_ovf_count, c->d_ovf_list, c->d_err, c->d_log, c->d_log_count, c->log_cap};
   c->P.step = c->step;
   Real *ox = (Real *)c->x[nxt], *ovx = (Real *)c->v[nxt][0], *ovy = (Real *)c->v[nxt][1], *ovz = (Real *)c->v[nxt][2];
+  prof_begin(c, TRMCR_K_SHOCK_SMEM);
   shock_collide_smem<Real><<<s.C, kSmemThreads, c->lay.total, c->stream>>>(
       c->P, c->lay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, Q);
-  if (auto e = check_launch(c, "shock_collide_smem")) return e;
+  if (auto e = check_launch(c, "shock_collide_smem", TRMCR_K_SHOCK_SMEM)) return e;
+  prof_begin(c, TRMCR_K_SHOCK_GMEM);
   shock_collide_gmem<Real><<<c->G, c->gmem_threads, 0, c->stream>>>(c->P, c->gs, d, G, s.d_off[nxt], ox, ovx, ovy,
                                                                  ovz, c->d_mstate, c->d_stats, Q);
-  if (auto e = check_launch(c, "shock_collide_gmem")) return e;
+  if (auto e = check_launch(c, "shock_collide_gmem", TRMCR_K_SHOCK_GMEM)) return e;
   c->cur = nxt;
   c->d_offsets = s.d_off[nxt];
   return TRMCR_OK;

@@ -112,6 +112,28 @@ moments_kernel(const int64_t *__restrict__ offsets, int ncells, const Real *__re
   }
 }
 
+// Global sums of the per-cell statistics rows (one CTA, fixed order).
+__global__ void __launch_bounds__(256) global_moments_kernel(const double *__restrict__ stats, int ncells,
+                                                             double *out) {
+  __shared__ double red[8 * 8];
+  double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int c = threadIdx.x; c < ncells; c += blockDim.x) {
+    const double *r = stats + (size_t)c * TRMCR_NSTATS;
+    v[0] += r[TRMCR_ST_N]; v[1] += r[TRMCR_ST_PX]; v[2] += r[TRMCR_ST_PY]; v[3] += r[TRMCR_ST_PZ];
+    v[4] += r[TRMCR_ST_ENERGY]; v[5] += r[TRMCR_ST_N] * r[TRMCR_ST_S0];
+    v[6] += r[TRMCR_ST_PROPOSALS]; v[7] += r[TRMCR_ST_ACCEPTED];
+  }
+  block_sum<8>(v, red);
+  double w[1] = {0};
+  for (int c = threadIdx.x; c < ncells; c += blockDim.x) w[0] += stats[(size_t)c * TRMCR_NSTATS + TRMCR_ST_MAXW];
+  block_sum<1>(w, red);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 8; ++k) out[k] = v[k];
+    out[TRMCR_GM_MAXW] = w[0];
+    out[TRMCR_GM_COST] = v[6] + 0.5 * w[0];
+  }
+}
+
 __global__ void fill_i32(int32_t *a, int n, int32_t v) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = v;
@@ -127,12 +149,14 @@ trmcr_status launch_collide(trmcr_ctx *c) {
   QueueArgs Q{c->d_ovf_count, c->d_ovf_list, c->d_err, c->d_log, c->d_log_count, c->log_cap};
   c->P.step = c->step;
   if (c->ncells > 0) {
+    prof_begin(c, TRMCR_K_CELL_SMEM);
     cell_step_smem<Real><<<c->ncells, kSmemThreads, c->lay.total, c->stream>>>(
         c->P, c->lay, c->d_offsets, c->ncells, vx, vy, vz, c->d_mstate, c->d_stats, Q);
-    if (auto s = check_launch(c, "cell_step_smem")) return s;
+    if (auto s = check_launch(c, "cell_step_smem", TRMCR_K_CELL_SMEM)) return s;
+    prof_begin(c, TRMCR_K_CELL_GMEM);
     cell_step_gmem<Real><<<c->G, c->gmem_threads, 0, c->stream>>>(c->P, c->gs, c->d_offsets, vx, vy, vz,
                                                                c->d_mstate, c->d_stats, Q);
-    if (auto s = check_launch(c, "cell_step_gmem")) return s;
+    if (auto s = check_launch(c, "cell_step_gmem", TRMCR_K_CELL_GMEM)) return s;
   }
   return TRMCR_OK;
 }
@@ -140,10 +164,11 @@ trmcr_status launch_collide(trmcr_ctx *c) {
 template <typename Real>
 trmcr_status launch_moments(trmcr_ctx *c) {
   if (c->ncells == 0) return TRMCR_OK;
+  prof_begin(c, TRMCR_K_MOMENTS);
   moments_kernel<Real><<<c->ncells, 256, 0, c->stream>>>(
       c->d_offsets, c->ncells, (const Real *)c->v[c->cur][0], (const Real *)c->v[c->cur][1],
       (const Real *)c->v[c->cur][2], c->d_mstate, c->P.shock, c->P.w_over_dx, c->d_moments);
-  return check_launch(c, "moments_kernel");
+  return check_launch(c, "moments_kernel", TRMCR_K_MOMENTS);
 }
 
 trmcr_status do_step(trmcr_ctx *c) {
@@ -175,9 +200,43 @@ const char *trmcr_last_error(const trmcr_ctx *ctx) {
 
 int64_t trmcr_launch_count(const trmcr_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
+trmcr_status trmcr_global_moments(trmcr_ctx *c, double *dev_out) {
+  if (!c || !dev_out) return fail(c, TRMCR_EINVAL, "null argument");
+  if (c->sticky) return TRMCR_ESTATE;
+  global_moments_kernel<<<1, 256, 0, c->stream>>>(c->d_stats, c->ncells, dev_out);
+  return check_launch(c, "global_moments_kernel");
+}
+
+trmcr_status trmcr_set_profiling(trmcr_ctx *c, int32_t on) {
+  if (!c) return fail(nullptr, TRMCR_EINVAL, "null ctx");
+  if (c->sticky) return TRMCR_ESTATE;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->prof = on ? 1 : 0;
+  c->ev_used = 0;
+  c->ev_kid.clear();
+  return TRMCR_OK;
+}
+
+trmcr_status trmcr_kernel_times(trmcr_ctx *c, double *ms, int64_t *launches) {
+  if (!c || !ms || !launches) return fail(c, TRMCR_EINVAL, "null argument");
+  if (c->sticky) return TRMCR_ESTATE;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < TRMCR_NKERNELS; ++k) { ms[k] = 0.0; launches[k] = 0; }
+  for (size_t i = 0; i < c->ev_kid.size(); ++i) {
+    float t = 0.f;
+    CUDA_TRY(c, cudaEventElapsedTime(&t, c->ev_pool[2 * i], c->ev_pool[2 * i + 1]));
+    ms[c->ev_kid[i]] += t;
+    launches[c->ev_kid[i]] += 1;
+  }
+  c->ev_used = 0;
+  c->ev_kid.clear();
+  return TRMCR_OK;
+}
+
 void trmcr_destroy(trmcr_ctx *ctx) {
   if (!ctx) return;
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   for (void *p : ctx->allocs) cudaFree(p);
   delete ctx;
 }
