@@ -182,7 +182,8 @@ int64_t trmcr_launch_count(const trmcr_ctx *ctx);
  * context stream while enabled).  Kernel ids: */
 enum {
   TRMCR_K_CELL_SMEM = 0, TRMCR_K_CELL_GMEM, TRMCR_K_MOMENTS, TRMCR_K_GHOST_COUNT, TRMCR_K_GHOST_GEN,
-  TRMCR_K_TRANSPORT, TRMCR_K_SCAN, TRMCR_K_SHOCK_SMEM, TRMCR_K_SHOCK_GMEM, TRMCR_NKERNELS
+  TRMCR_K_TRANSPORT, TRMCR_K_SCAN, TRMCR_K_SHOCK_SMEM, TRMCR_K_SHOCK_GMEM, TRMCR_K_THERMAL,
+  TRMCR_NKERNELS
 };
 trmcr_status trmcr_set_profiling(trmcr_ctx *ctx, int32_t on);
 /* Sums, per kernel id, the device time (ms) and launch count recorded since

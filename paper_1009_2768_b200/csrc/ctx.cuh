@@ -133,6 +133,13 @@ struct trmcr_ctx {
   int32_t *d_mstate = nullptr;
   double *d_stats = nullptr, *d_moments = nullptr;
   int *d_ovf_count = nullptr, *d_ovf_list = nullptr, *d_err = nullptr;
+  // thermal fast path (thermal.cuh): cells it defers go to the general kernel
+  int *d_defer_count = nullptr, *d_defer_list = nullptr;
+  int *h_defer = nullptr;          // pinned copy of the last defer count
+  double *d_gm_partial = nullptr;  // global-moments partial sums
+  unsigned *d_gm_done = nullptr;
+  cudaEvent_t ev_defer = nullptr;
+  int fast_ok = 1, fast_pending = 0, fast_grid = 0, smem_grid = 0, last_defer = -1, last_ovf = -1;
   unsigned char *d_scratch = nullptr;
   trmcr::GmemScratch gs{};
   int G = 1;

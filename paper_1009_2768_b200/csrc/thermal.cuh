@@ -1,0 +1,404 @@
+// thermal.cuh — warp-per-cell fast path of the collision step for cells in
+// the fluid regime, where the split (Alg 4.2) provably assigns
+// every particle to N_{m+1}: p n < 2^-53 makes every IR draw exactly 0
+// (DESIGN.md §3.2), so the step is "replace the cell by a Maxwellian with its
+// own momentum and energy" (AP property (ii); conservative
+// sampling P:558-561).  No tree, no permutation: Theta is every slot.
+//
+// One warp owns one cell at a time (persistent grid); the cell is staged in
+// the warp's shared-memory slab, reductions are warp butterflies (bitwise
+// identical on every lane), and no CTA barrier is needed.  A cell that is not
+// in this regime (or larger than the slab) is queued, untouched, for the
+// general kernel (cell_step.cuh).  Results equal the general path's: same
+// keyed draws, same formulas.
+#pragma once
+#include "cell_step.cuh"
+
+namespace trmcr {
+
+template <typename Real> struct ThermalCap;
+template <> struct ThermalCap<float> { static constexpr int value = 1024; };
+template <> struct ThermalCap<double> { static constexpr int value = 512; };
+constexpr int kThermalWarps = 8;
+
+// 16-byte vector of Real (4 floats or 2 doubles) for coalesced, batched I/O.
+template <typename Real> struct Vec;
+template <> struct Vec<float> { using T = float4; static constexpr int W = 4; };
+template <> struct Vec<double> { using T = double2; static constexpr int W = 2; };
+template <typename V, typename Real> __device__ __forceinline__ Real vget(const V &v, int k);
+template <> __device__ __forceinline__ float vget<float4, float>(const float4 &v, int k) {
+  return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+}
+template <> __device__ __forceinline__ double vget<double2, double>(const double2 &v, int k) {
+  return k == 0 ? v.x : v.y;
+}
+template <typename V, typename Real> __device__ __forceinline__ void vset(V &v, int k, Real a);
+template <> __device__ __forceinline__ void vset<float4, float>(float4 &v, int k, float a) {
+  if (k == 0) v.x = a; else if (k == 1) v.y = a; else if (k == 2) v.z = a; else v.w = a;
+}
+template <> __device__ __forceinline__ void vset<double2, double>(double2 &v, int k, double a) {
+  if (k == 0) v.x = a; else v.y = a;
+}
+
+// Moments of the staged cell (pass 2) and the thermal decision; returns true
+// when the cell is in the fluid regime (p n < 2^-53).
+struct ThermalMoments {
+  double Sx, Sy, Sz, ux, uy, uz, E, S0, sigma, mu, p;
+};
+
+template <typename Real>
+__device__ __forceinline__ void thermal_finish(const StepParams &P, const ThermalMoments &M, int n, int c,
+                                               int32_t *m_state, double *stats) {
+  // A7 in closed form: every retry plan is empty, E1 is fixed.
+  int m = P.adaptive ? m_state[c] : P.m_fixed;
+  int r = 0;
+  double S_est = M.S0, E1 = 0.0;
+  int m_next = m;
+  if (P.adaptive) {
+    const double T = M.E / (3.0 * n);
+    if (P.indicator == TRMCR_IND_PXX) {
+      S_est = T;
+    } else {
+      const double u2 = M.ux * M.ux + M.uy * M.uy + M.uz * M.uz;
+      S_est = u2 * u2 + 10.0 * u2 * T + 15.0 * T * T;
+    }
+    E1 = M.S0 != 0.0 ? fabs(S_est - M.S0) / fabs(M.S0) : (S_est == 0.0 ? 0.0 : INFINITY);
+    while (E1 > P.delta2 && m < P.m_cap) { m = 2 * m < P.m_cap ? 2 * m : P.m_cap; ++r; }
+    m_next = E1 < P.delta1 ? (m / 2 > 1 ? m / 2 : 1) : m;
+    m_state[c] = m_next;
+  }
+  double *s = stats + (size_t)c * TRMCR_NSTATS;
+  s[TRMCR_ST_N] = n; s[TRMCR_ST_P] = M.p; s[TRMCR_ST_MU] = M.mu; s[TRMCR_ST_SIGMA] = M.sigma;
+  s[TRMCR_ST_S0] = M.S0; s[TRMCR_ST_SEST] = S_est; s[TRMCR_ST_E1] = E1;
+  s[TRMCR_ST_MUSED] = m; s[TRMCR_ST_MNEXT] = m_next; s[TRMCR_ST_DEPTH] = m;
+  s[TRMCR_ST_ATTEMPTS] = r + 1; s[TRMCR_ST_LEAVES] = 0; s[TRMCR_ST_UNTOUCHED] = 0;
+  s[TRMCR_ST_THERMALISED] = n; s[TRMCR_ST_PROPOSALS] = 0; s[TRMCR_ST_ACCEPTED] = 0;
+  s[TRMCR_ST_VIOLATIONS] = 0; s[TRMCR_ST_MAXW] = n >= 2 ? n : 0;
+  s[TRMCR_ST_PX] = M.Sx; s[TRMCR_ST_PY] = M.Sy; s[TRMCR_ST_PZ] = M.Sz;
+  s[TRMCR_ST_ENERGY] = M.E + n * (M.ux * M.ux + M.uy * M.uy + M.uz * M.uz);
+}
+
+__device__ __forceinline__ void thermal_decide(const StepParams &P, ThermalMoments &M, int n, double PXX,
+                                               double M4, double dv2) {
+  M.S0 = (P.indicator == TRMCR_IND_PXX ? PXX : M4) / n;
+  M.sigma = 0.0;
+  M.mu = 1.0;
+  if (P.model == TRMCR_HARD_SPHERE) { M.sigma = 2.0 * sqrt(dv2); M.mu = M.sigma; }
+  M.p = exp(-(M.mu * P.dt / P.eps));
+}
+
+// Vector path: cell start and length multiples of the vector width.  Each lane
+// owns whole 16-byte groups; loads/stores are 16 B per lane (512 B per warp
+// instruction), the Box-Muller draws of a group are independent (ILP).
+template <typename Real, int CAP>
+__device__ __forceinline__ bool thermal_cell_vec(const StepParams &P, Real *vx, Real *vy, Real *vz,
+                                                 int64_t off, int n, int c, Real *wx, Real *wy, Real *wz,
+                                                 int32_t *m_state, double *stats) {
+  using V = typename Vec<Real>::T;
+  constexpr int W = Vec<Real>::W;
+  constexpr int G = CAP / W / 32;          // groups per lane at n = CAP
+  const int lane = threadIdx.x & 31;
+  const int ng = n / W;
+  V *gx = reinterpret_cast<V *>(vx + off), *gy = reinterpret_cast<V *>(vy + off), *gz = reinterpret_cast<V *>(vz + off);
+  V *sx4 = reinterpret_cast<V *>(wx), *sy4 = reinterpret_cast<V *>(wy), *sz4 = reinterpret_cast<V *>(wz);
+  // pass 1: batched 16-byte loads (all in flight), stage + sums
+  double sx = 0, sy = 0, sz = 0;
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    const int g = lane + 32 * k;
+    if (g < ng) {
+      const V a = __ldcs(gx + g), b = __ldcs(gy + g), d = __ldcs(gz + g);
+      sx4[g] = a; sy4[g] = b; sz4[g] = d;
+#pragma unroll
+      for (int w = 0; w < W; ++w) { sx += vget<V, Real>(a, w); sy += vget<V, Real>(b, w); sz += vget<V, Real>(d, w); }
+    }
+  }
+  ThermalMoments M;
+  M.Sx = warp_sum(sx); M.Sy = warp_sum(sy); M.Sz = warp_sum(sz);
+  M.ux = M.Sx / n; M.uy = M.Sy / n; M.uz = M.Sz / n;
+  const Real rux = (Real)M.ux, ruy = (Real)M.uy, ruz = (Real)M.uz;
+  double e = 0, pxx = 0, m4 = 0;
+  Real mx = 0;
+#pragma unroll 4
+  for (int g = lane; g < ng; g += 32) {
+    const V a = sx4[g], b = sy4[g], d = sz4[g];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const Real x = vget<V, Real>(a, w), y = vget<V, Real>(b, w), z = vget<V, Real>(d, w);
+      const Real dx = x - rux, dy = y - ruy, dz = z - ruz;
+      const Real r2 = dx * dx + dy * dy + dz * dz;
+      e += r2;
+      mx = r2 > mx ? r2 : mx;
+      pxx += dx * dx;
+      const Real v2 = x * x + y * y + z * z;
+      m4 += v2 * v2;
+    }
+  }
+  M.E = warp_sum(e);
+  thermal_decide(P, M, n, warp_sum(pxx), warp_sum(m4), warp_max((double)mx));
+  if (!(M.p * (double)n < 0x1p-53)) return false;
+  const RngKey K{P.k0, P.k1, P.cell_base + (uint32_t)c, P.step};
+  if (n >= 2) {
+    double ax = 0, ay = 0, az = 0, a2 = 0;
+#pragma unroll 2
+    for (int g = lane; g < ng; g += 32) {
+      V a, b, d;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        Real g0, g1, g2;
+        gauss3<Real>(K, (uint32_t)(g * W + w), g0, g1, g2);
+        vset<V, Real>(a, w, g0); vset<V, Real>(b, w, g1); vset<V, Real>(d, w, g2);
+        ax += g0; ay += g1; az += g2;
+        a2 += (double)(g0 * g0 + g1 * g1 + g2 * g2);
+      }
+      sx4[g] = a; sy4[g] = b; sz4[g] = d;
+    }
+    const double Gx = warp_sum(ax) / n, Gy = warp_sum(ay) / n, Gz = warp_sum(az) / n;
+    const double D = warp_sum(a2) - n * (Gx * Gx + Gy * Gy + Gz * Gz);
+    const double sc = (D > 0.0 && M.E > 0.0) ? sqrt(M.E / D) : 0.0;
+    const Real rs = (Real)sc, rgx = (Real)Gx, rgy = (Real)Gy, rgz = (Real)Gz;
+#pragma unroll 4
+    for (int g = lane; g < ng; g += 32) {
+      V a = sx4[g], b = sy4[g], d = sz4[g];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        vset<V, Real>(a, w, rux + rs * (vget<V, Real>(a, w) - rgx));
+        vset<V, Real>(b, w, ruy + rs * (vget<V, Real>(b, w) - rgy));
+        vset<V, Real>(d, w, ruz + rs * (vget<V, Real>(d, w) - rgz));
+      }
+      __stcs(gx + g, a); __stcs(gy + g, b); __stcs(gz + g, d);
+    }
+  }
+  if (lane == 0) thermal_finish<Real>(P, M, n, c, m_state, stats);
+  return true;
+}
+
+// Scalar path for unaligned cells.
+template <typename Real>
+__device__ __forceinline__ bool thermal_cell_scalar(const StepParams &P, Real *vx, Real *vy, Real *vz,
+                                                    int64_t off, int n, int c, Real *wx, Real *wy, Real *wz,
+                                                    int32_t *m_state, double *stats) {
+  const int lane = threadIdx.x & 31;
+  double sx = 0, sy = 0, sz = 0;
+#pragma unroll 4
+  for (int i = lane; i < n; i += 32) {
+    const Real a = vx[off + i], b = vy[off + i], d = vz[off + i];
+    wx[i] = a; wy[i] = b; wz[i] = d;
+    sx += a; sy += b; sz += d;
+  }
+  ThermalMoments M;
+  M.Sx = warp_sum(sx); M.Sy = warp_sum(sy); M.Sz = warp_sum(sz);
+  M.ux = M.Sx / n; M.uy = M.Sy / n; M.uz = M.Sz / n;
+  const Real rux = (Real)M.ux, ruy = (Real)M.uy, ruz = (Real)M.uz;
+  double e = 0, pxx = 0, m4 = 0;
+  Real mx = 0;
+  for (int i = lane; i < n; i += 32) {
+    const Real x = wx[i], y = wy[i], z = wz[i];
+    const Real dx = x - rux, dy = y - ruy, dz = z - ruz;
+    const Real r2 = dx * dx + dy * dy + dz * dz;
+    e += r2;
+    mx = r2 > mx ? r2 : mx;
+    pxx += dx * dx;
+    const Real v2 = x * x + y * y + z * z;
+    m4 += v2 * v2;
+  }
+  M.E = warp_sum(e);
+  thermal_decide(P, M, n, warp_sum(pxx), warp_sum(m4), warp_max((double)mx));
+  if (!(M.p * (double)n < 0x1p-53)) return false;
+  const RngKey K{P.k0, P.k1, P.cell_base + (uint32_t)c, P.step};
+  if (n >= 2) {
+    double gx = 0, gy = 0, gz = 0, g2 = 0;
+    for (int i = lane; i < n; i += 32) {
+      Real a, b, d;
+      gauss3<Real>(K, (uint32_t)i, a, b, d);
+      wx[i] = a; wy[i] = b; wz[i] = d;
+      gx += a; gy += b; gz += d;
+      g2 += (double)(a * a + b * b + d * d);
+    }
+    const double Gx = warp_sum(gx) / n, Gy = warp_sum(gy) / n, Gz = warp_sum(gz) / n;
+    const double D = warp_sum(g2) - n * (Gx * Gx + Gy * Gy + Gz * Gz);
+    const double sc = (D > 0.0 && M.E > 0.0) ? sqrt(M.E / D) : 0.0;
+    const Real rs = (Real)sc, rgx = (Real)Gx, rgy = (Real)Gy, rgz = (Real)Gz;
+    for (int i = lane; i < n; i += 32) {
+      vx[off + i] = rux + rs * (wx[i] - rgx);
+      vy[off + i] = ruy + rs * (wy[i] - rgy);
+      vz[off + i] = ruz + rs * (wz[i] - rgz);
+    }
+  }
+  if (lane == 0) thermal_finish<Real>(P, M, n, c, m_state, stats);
+  return true;
+}
+
+// ---- fp32 production path (C3-class cells): cp.async staging, fp32 lane sums ----
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem_src) : "memory");
+}
+// Bulk prefetch of a contiguous global range into L2 (sm_90+): one instruction
+// per array, used to pull the warp's next cell in while it works on this one.
+__device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+// (k + 1/2) 2^-23 for k = w >> 9, built from the mantissa bits (no I2F):
+// b = 1 + k 2^-23 in [1,2); b - (1 - 2^-24) = (2k+1) 2^-24 is representable, so
+// the single FADD is exact and the value is bit-identical to u24().
+__device__ __forceinline__ float u24_bits(uint32_t w) {
+  return __uint_as_float(0x3F800000u | (w >> 9)) + (-1.0f + 0x1p-24f);
+}
+// Box-Muller for the statistical fp32 path: MUFU lg2 / rsqrt / sin / cos.
+// r = sqrt(-2 ln u) = a rsqrt(a), a = (-2 ln 2) log2(u) > 0 since u < 1.
+__device__ __forceinline__ void gauss3_fast(const RngKey &K, uint32_t slot, float &g0, float &g1, float &g2) {
+  const uint4 w = K(kMaxw, 0, 0, slot);
+  const float u1 = u24_bits(w.x), u2 = u24_bits(w.y), u3 = u24_bits(w.z), u4 = u24_bits(w.w);
+  constexpr float kM2Ln2 = -1.3862943611198906f;   // -2 ln 2
+  const float a1 = kM2Ln2 * __log2f(u1), a3 = kM2Ln2 * __log2f(u3);
+  const float r1 = a1 * rsqrtf(a1), r3 = a3 * rsqrtf(a3);
+  float s2, c2;
+  __sincosf(6.283185307179586f * u2, &s2, &c2);
+  const float c4 = __cosf(6.283185307179586f * u4);
+  g0 = r1 * c2; g1 = r1 * s2; g2 = r3 * c4;
+}
+
+__device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, float *vx, float *vy, float *vz, int64_t off,
+                                                 int n, int c, float *wx, float *wy, float *wz,
+                                                 int32_t *m_state, double *stats) {
+  constexpr int CAP = ThermalCap<float>::value;
+  constexpr int G = CAP / 4 / 32;                 // float4 groups per lane at n = CAP
+  const int lane = threadIdx.x & 31;
+  const int ng = n >> 2;
+  float4 *gx = reinterpret_cast<float4 *>(vx + off), *gy = reinterpret_cast<float4 *>(vy + off);
+  float4 *gz = reinterpret_cast<float4 *>(vz + off);
+  float4 *sx4 = reinterpret_cast<float4 *>(wx), *sy4 = reinterpret_cast<float4 *>(wy);
+  float4 *sz4 = reinterpret_cast<float4 *>(wz);
+  // pass 1: every 16-byte load of the cell in flight at once (global -> shared)
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    const int g = lane + 32 * k;
+    if (g < ng) { cp_async16(sx4 + g, gx + g); cp_async16(sy4 + g, gy + g); cp_async16(sz4 + g, gz + g); }
+  }
+  cp_async_wait_all();
+  __syncwarp();
+  float sx = 0, sy = 0, sz = 0;
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    const int g = lane + 32 * k;
+    if (g < ng) {
+      const float4 a = sx4[g], b = sy4[g], d = sz4[g];
+      sx += (a.x + a.y) + (a.z + a.w); sy += (b.x + b.y) + (b.z + b.w); sz += (d.x + d.y) + (d.z + d.w);
+    }
+  }
+  ThermalMoments M;
+  M.Sx = warp_sum((double)sx); M.Sy = warp_sum((double)sy); M.Sz = warp_sum((double)sz);
+  M.ux = M.Sx / n; M.uy = M.Sy / n; M.uz = M.Sz / n;
+  const float rux = (float)M.ux, ruy = (float)M.uy, ruz = (float)M.uz;
+  float e = 0, pxx = 0, m4 = 0, mx = 0;
+  const bool want_m4 = P.indicator == TRMCR_IND_M4;
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    const int g = lane + 32 * k;
+    if (g < ng) {
+      const float4 a = sx4[g], b = sy4[g], d = sz4[g];
+      const float xs[4] = {a.x, a.y, a.z, a.w}, ys[4] = {b.x, b.y, b.z, b.w}, zs[4] = {d.x, d.y, d.z, d.w};
+      float eg = 0, pg = 0, mg = 0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float dx = xs[w] - rux, dy = ys[w] - ruy, dz = zs[w] - ruz;
+        const float px = dx * dx;
+        const float r2 = px + dy * dy + dz * dz;
+        eg += r2;
+        mx = fmaxf(mx, r2);
+        pg += px;
+        if (want_m4) {
+          const float v2 = xs[w] * xs[w] + ys[w] * ys[w] + zs[w] * zs[w];
+          mg += v2 * v2;
+        }
+      }
+      e += eg; pxx += pg; m4 += mg;
+    }
+  }
+  M.E = warp_sum((double)e);
+  thermal_decide(P, M, n, warp_sum((double)pxx), warp_sum((double)m4), warp_max((double)mx));
+  if (!(M.p * (double)n < 0x1p-53)) return false;
+  const RngKey K{P.k0, P.k1, P.cell_base + (uint32_t)c, P.step};
+  if (n >= 2) {
+    float ax = 0, ay = 0, az = 0, a2 = 0;
+#pragma unroll 2
+    for (int k = 0; k < G; ++k) {
+      const int g = lane + 32 * k;
+      if (g < ng) {
+        float4 a, b, d;
+        gauss3_fast(K, (uint32_t)(4 * g + 0), a.x, b.x, d.x);
+        gauss3_fast(K, (uint32_t)(4 * g + 1), a.y, b.y, d.y);
+        gauss3_fast(K, (uint32_t)(4 * g + 2), a.z, b.z, d.z);
+        gauss3_fast(K, (uint32_t)(4 * g + 3), a.w, b.w, d.w);
+        sx4[g] = a; sy4[g] = b; sz4[g] = d;
+        ax += (a.x + a.y) + (a.z + a.w); ay += (b.x + b.y) + (b.z + b.w); az += (d.x + d.y) + (d.z + d.w);
+        a2 += ((a.x * a.x + b.x * b.x + d.x * d.x) + (a.y * a.y + b.y * b.y + d.y * d.y)) +
+              ((a.z * a.z + b.z * b.z + d.z * d.z) + (a.w * a.w + b.w * b.w + d.w * d.w));
+      }
+    }
+    const double Gx = warp_sum((double)ax) / n, Gy = warp_sum((double)ay) / n, Gz = warp_sum((double)az) / n;
+    const double D = warp_sum((double)a2) - n * (Gx * Gx + Gy * Gy + Gz * Gz);
+    const double sc = (D > 0.0 && M.E > 0.0) ? sqrt(M.E / D) : 0.0;
+    const float rs = (float)sc, rgx = (float)Gx, rgy = (float)Gy, rgz = (float)Gz;
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const int g = lane + 32 * k;
+      if (g < ng) {
+        float4 a = sx4[g], b = sy4[g], d = sz4[g];
+        a.x = rux + rs * (a.x - rgx); a.y = rux + rs * (a.y - rgx); a.z = rux + rs * (a.z - rgx); a.w = rux + rs * (a.w - rgx);
+        b.x = ruy + rs * (b.x - rgy); b.y = ruy + rs * (b.y - rgy); b.z = ruy + rs * (b.z - rgy); b.w = ruy + rs * (b.w - rgy);
+        d.x = ruz + rs * (d.x - rgz); d.y = ruz + rs * (d.y - rgz); d.z = ruz + rs * (d.z - rgz); d.w = ruz + rs * (d.w - rgz);
+        __stcs(gx + g, a); __stcs(gy + g, b); __stcs(gz + g, d);
+      }
+    }
+  }
+  if (lane == 0) thermal_finish<float>(P, M, n, c, m_state, stats);
+  return true;
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(kThermalWarps * 32, 2)
+thermal_warp_kernel(StepParams P, const int64_t *__restrict__ offsets, int ncells, Real *vx, Real *vy,
+                    Real *vz, int32_t *m_state, double *stats, int *defer_count, int *defer_list) {
+  constexpr int CAP = ThermalCap<Real>::value;
+  constexpr int W = Vec<Real>::W;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Real *wx = reinterpret_cast<Real *>(smem) + (size_t)warp * 3 * CAP;
+  Real *wy = wx + CAP, *wz = wy + CAP;
+  const int nwarps = gridDim.x * kThermalWarps;
+  int c = blockIdx.x * kThermalWarps + warp;
+  int64_t off = c < ncells ? offsets[c] : 0, end = c < ncells ? offsets[c + 1] : 0;
+  for (; c < ncells; c += nwarps) {
+    const int n = (int)(end - off);
+    const int64_t cur_off = off;
+    // prefetch the next cell's offsets of this warp (hides one global round trip)
+    const int cn = c + nwarps;
+    if (cn < ncells) {
+      off = offsets[cn];
+      end = offsets[cn + 1];
+    }
+    bool done = false;
+    if (n > 0 && n <= CAP) {
+      const bool aligned = (cur_off % W) == 0 && (n % W) == 0 &&
+                           ((reinterpret_cast<uintptr_t>(vx) | reinterpret_cast<uintptr_t>(vy) |
+                             reinterpret_cast<uintptr_t>(vz)) & 15) == 0;
+      if constexpr (sizeof(Real) == 4) {
+        done = aligned ? thermal_cell_f32(P, vx, vy, vz, cur_off, n, c, wx, wy, wz, m_state, stats)
+                       : thermal_cell_scalar<Real>(P, vx, vy, vz, cur_off, n, c, wx, wy, wz, m_state, stats);
+      } else {
+        done = aligned ? thermal_cell_vec<Real, CAP>(P, vx, vy, vz, cur_off, n, c, wx, wy, wz, m_state, stats)
+                       : thermal_cell_scalar<Real>(P, vx, vy, vz, cur_off, n, c, wx, wy, wz, m_state, stats);
+      }
+    }
+    if (!done && lane == 0) defer_list[atomicAdd(defer_count, 1)] = c;   // general path
+    __syncwarp();
+  }
+}
+
+}  // namespace trmcr

@@ -20,6 +20,7 @@
 #include "cell_step.cuh"
 #include "ctx.cuh"
 #include "shock.cuh"
+#include "thermal.cuh"
 
 using namespace trmcr;
 
@@ -30,22 +31,26 @@ namespace {
 template <typename Real>
 __global__ void __launch_bounds__(kSmemThreads)
 cell_step_smem(StepParams P, SmemLayout Lay, const int64_t *__restrict__ offsets, int ncells,
-               Real *vx, Real *vy, Real *vz, int32_t *m_state, double *stats, QueueArgs Q) {
+               const int *list_count, const int *list, Real *vx, Real *vy, Real *vz, int32_t *m_state,
+               double *stats, QueueArgs Q) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CellShared sh;
-  const int c = blockIdx.x;
-  if (c >= ncells) return;
   CellBuf<Real> B;
   bind_smem(B, smem, Lay);
-  const int64_t off = offsets[c];
-  const int n = (int)(offsets[c + 1] - off);
-  const int rc = process_cell<Real, true, true>(P, B, sh, vx + off, vy + off, vz + off, vx + off, vy + off,
-                                          vz + off, n, P.cell_base + (uint32_t)c, m_state + c,
-                                          stats + (size_t)c * TRMCR_NSTATS, Q.log, Q.log_count,
-                                          Q.log_cap);
-  if (rc != kOk && threadIdx.x == 0) {
-    const int k = atomicAdd(Q.ovf_count, 1);
-    Q.ovf_list[k] = c;
+  const int count = list ? *list_count : ncells;
+  for (int k = blockIdx.x; k < count; k += gridDim.x) {
+    const int c = list ? list[k] : k;
+    const int64_t off = offsets[c];
+    const int n = (int)(offsets[c + 1] - off);
+    const int rc = process_cell<Real, true, true>(P, B, sh, vx + off, vy + off, vz + off, vx + off,
+                                                  vy + off, vz + off, n, P.cell_base + (uint32_t)c,
+                                                  m_state + c, stats + (size_t)c * TRMCR_NSTATS, Q.log,
+                                                  Q.log_count, Q.log_cap);
+    if (rc != kOk && threadIdx.x == 0) {
+      const int j = atomicAdd(Q.ovf_count, 1);
+      Q.ovf_list[j] = c;
+    }
+    __syncthreads();
   }
 }
 
@@ -112,25 +117,41 @@ moments_kernel(const int64_t *__restrict__ offsets, int ncells, const Real *__re
   }
 }
 
-// Global sums of the per-cell statistics rows (one CTA, fixed order).
+// Global sums of the per-cell statistics rows: kGmBlocks CTAs write partial
+// sums of contiguous cell ranges, the last CTA to finish adds the partials in
+// block order (deterministic), writes `out` and re-arms the counter.
+constexpr int kGmBlocks = 64;
 __global__ void __launch_bounds__(256) global_moments_kernel(const double *__restrict__ stats, int ncells,
-                                                             double *out) {
-  __shared__ double red[8 * 8];
-  double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int c = threadIdx.x; c < ncells; c += blockDim.x) {
+                                                             double *partial, unsigned *done, double *out) {
+  __shared__ double red[8 * 10];
+  __shared__ bool last;
+  const int per = (ncells + gridDim.x - 1) / gridDim.x;
+  const int lo = blockIdx.x * per, hi = min(ncells, lo + per);
+  double v[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int c = lo + threadIdx.x; c < hi; c += blockDim.x) {
     const double *r = stats + (size_t)c * TRMCR_NSTATS;
     v[0] += r[TRMCR_ST_N]; v[1] += r[TRMCR_ST_PX]; v[2] += r[TRMCR_ST_PY]; v[3] += r[TRMCR_ST_PZ];
     v[4] += r[TRMCR_ST_ENERGY]; v[5] += r[TRMCR_ST_N] * r[TRMCR_ST_S0];
-    v[6] += r[TRMCR_ST_PROPOSALS]; v[7] += r[TRMCR_ST_ACCEPTED];
+    v[6] += r[TRMCR_ST_PROPOSALS]; v[7] += r[TRMCR_ST_ACCEPTED]; v[8] += r[TRMCR_ST_MAXW];
   }
-  block_sum<8>(v, red);
-  double w[1] = {0};
-  for (int c = threadIdx.x; c < ncells; c += blockDim.x) w[0] += stats[(size_t)c * TRMCR_NSTATS + TRMCR_ST_MAXW];
-  block_sum<1>(w, red);
+  block_sum<10>(v, red);
   if (threadIdx.x == 0) {
-    for (int k = 0; k < 8; ++k) out[k] = v[k];
-    out[TRMCR_GM_MAXW] = w[0];
-    out[TRMCR_GM_COST] = v[6] + 0.5 * w[0];
+    for (int k = 0; k < 9; ++k) partial[blockIdx.x * 10 + k] = v[k];
+    __threadfence();
+    last = (atomicAdd(done, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x < 9) {
+    __threadfence();
+    double s = 0;
+    for (int b = 0; b < (int)gridDim.x; ++b) s += ((volatile double *)partial)[b * 10 + threadIdx.x];
+    out[threadIdx.x] = s;
+    if (threadIdx.x == 8) out[TRMCR_GM_COST] = 0.0;   // filled below
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    out[TRMCR_GM_COST] = out[TRMCR_GM_PROPOSALS] + 0.5 * out[TRMCR_GM_MAXW];
+    *done = 0u;
   }
 }
 
@@ -149,14 +170,43 @@ trmcr_status launch_collide(trmcr_ctx *c) {
   QueueArgs Q{c->d_ovf_count, c->d_ovf_list, c->d_err, c->d_log, c->d_log_count, c->log_cap};
   c->P.step = c->step;
   if (c->ncells > 0) {
+    // Counts of the last observed step (pinned async copy, read when ready):
+    // the thermal fast path runs while it handles most cells (re-tried every
+    // 16 steps); when nothing was deferred the general kernels are launched
+    // with one CTA (they still drain whatever this step queues: correct, and
+    // re-sized once the counts are seen).
+    if (c->fast_pending && cudaEventQuery(c->ev_defer) == cudaSuccess) {
+      c->fast_ok = (c->h_defer[0] <= c->ncells / 2);
+      c->last_defer = c->h_defer[0];
+      c->last_ovf = c->h_defer[1];
+      c->fast_pending = 0;
+    } else if (c->fast_pending) {
+      cudaGetLastError();   // cudaErrorNotReady is not an error here
+    }
+    const bool fast = c->fast_ok || (c->step % 16 == 0);
+    CUDA_TRY(c, cudaMemsetAsync(c->d_defer_count, 0, 2 * sizeof(int), c->stream));   // defer + ovf
+    if (fast) {
+      prof_begin(c, TRMCR_K_THERMAL);
+      thermal_warp_kernel<Real><<<c->fast_grid, kThermalWarps * 32,
+                                  kThermalWarps * 3 * ThermalCap<Real>::value * sizeof(Real), c->stream>>>(
+          c->P, c->d_offsets, c->ncells, vx, vy, vz, c->d_mstate, c->d_stats, c->d_defer_count, c->d_defer_list);
+      if (auto s = check_launch(c, "thermal_warp_kernel", TRMCR_K_THERMAL)) return s;
+    }
+    const bool idle = fast && c->fast_ok && c->last_defer == 0 && c->last_ovf == 0;
     prof_begin(c, TRMCR_K_CELL_SMEM);
-    cell_step_smem<Real><<<c->ncells, kSmemThreads, c->lay.total, c->stream>>>(
-        c->P, c->lay, c->d_offsets, c->ncells, vx, vy, vz, c->d_mstate, c->d_stats, Q);
+    cell_step_smem<Real><<<idle ? 1 : c->smem_grid, kSmemThreads, c->lay.total, c->stream>>>(
+        c->P, c->lay, c->d_offsets, c->ncells, fast ? c->d_defer_count : nullptr,
+        fast ? c->d_defer_list : nullptr, vx, vy, vz, c->d_mstate, c->d_stats, Q);
     if (auto s = check_launch(c, "cell_step_smem", TRMCR_K_CELL_SMEM)) return s;
     prof_begin(c, TRMCR_K_CELL_GMEM);
-    cell_step_gmem<Real><<<c->G, c->gmem_threads, 0, c->stream>>>(c->P, c->gs, c->d_offsets, vx, vy, vz,
-                                                               c->d_mstate, c->d_stats, Q);
+    cell_step_gmem<Real><<<idle ? 1 : c->G, c->gmem_threads, 0, c->stream>>>(c->P, c->gs, c->d_offsets, vx, vy, vz,
+                                                                            c->d_mstate, c->d_stats, Q);
     if (auto s = check_launch(c, "cell_step_gmem", TRMCR_K_CELL_GMEM)) return s;
+    if (!c->fast_pending && (c->step % 8 == 0 || !c->fast_ok)) {
+      CUDA_TRY(c, cudaMemcpyAsync(c->h_defer, c->d_defer_count, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(c, cudaEventRecord(c->ev_defer, c->stream));
+      c->fast_pending = 1;
+    }
   }
   return TRMCR_OK;
 }
@@ -172,7 +222,7 @@ trmcr_status launch_moments(trmcr_ctx *c) {
 }
 
 trmcr_status do_step(trmcr_ctx *c) {
-  CUDA_TRY(c, cudaMemsetAsync(c->d_ovf_count, 0, sizeof(int), c->stream));
+  if (c->geometry == TRMCR_SHOCK_1D) CUDA_TRY(c, cudaMemsetAsync(c->d_ovf_count, 0, sizeof(int), c->stream));
   if (c->log_cap > 0)
     CUDA_TRY(c, cudaMemsetAsync(c->d_log_count, 0, sizeof(unsigned long long), c->stream));
   trmcr_status s;
@@ -203,7 +253,8 @@ int64_t trmcr_launch_count(const trmcr_ctx *ctx) { return ctx ? ctx->launches : 
 trmcr_status trmcr_global_moments(trmcr_ctx *c, double *dev_out) {
   if (!c || !dev_out) return fail(c, TRMCR_EINVAL, "null argument");
   if (c->sticky) return TRMCR_ESTATE;
-  global_moments_kernel<<<1, 256, 0, c->stream>>>(c->d_stats, c->ncells, dev_out);
+  const int blocks = std::max(1, std::min(kGmBlocks, c->ncells));
+  global_moments_kernel<<<blocks, 256, 0, c->stream>>>(c->d_stats, c->ncells, c->d_gm_partial, c->d_gm_done, dev_out);
   return check_launch(c, "global_moments_kernel");
 }
 
@@ -237,6 +288,8 @@ void trmcr_destroy(trmcr_ctx *ctx) {
   if (!ctx) return;
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->ev_defer) cudaEventDestroy(ctx->ev_defer);
+  if (ctx->h_defer) cudaFreeHost(ctx->h_defer);
   for (void *p : ctx->allocs) cudaFree(p);
   delete ctx;
 }
@@ -326,12 +379,23 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
       dalloc(c, &c->d_mstate, sizeof(int32_t) * std::max(c->ncells, 1)) ||
       dalloc(c, &c->d_stats, sizeof(double) * TRMCR_NSTATS * std::max(c->ncells, 1)) ||
       dalloc(c, &c->d_moments, sizeof(double) * TRMCR_NMOMENTS * std::max(c->ncells, 1)) ||
-      dalloc(c, &c->d_ovf_count, sizeof(int)) ||
+
       dalloc(c, &c->d_ovf_list, sizeof(int) * std::max(c->ncells, 1)) ||
-      dalloc(c, &c->d_err, sizeof(int)) || dalloc(c, &c->d_log_count, sizeof(unsigned long long)))
+      dalloc(c, &c->d_err, sizeof(int)) || dalloc(c, &c->d_log_count, sizeof(unsigned long long)) ||
+      dalloc(c, &c->d_defer_count, 2 * sizeof(int)) || dalloc(c, &c->d_gm_partial, sizeof(double) * 10 * kGmBlocks) ||
+      dalloc(c, &c->d_gm_done, sizeof(unsigned)) || dalloc(c, &c->d_defer_list, sizeof(int) * std::max(c->ncells, 1)))
     return bail(TRMCR_ENOMEM);
+  c->d_ovf_count = c->d_defer_count + 1;
+  if (cudaMallocHost(&c->h_defer, 2 * sizeof(int)) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_defer, cudaEventDisableTiming) != cudaSuccess) {
+    fail(c, TRMCR_ENOMEM, "pinned host / event allocation failed");
+    return bail(TRMCR_ENOMEM);
+  }
+  c->h_defer[0] = c->h_defer[1] = 0;
+  c->last_defer = c->last_ovf = -1;
   c->P.err = c->d_err;
-  if (cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream) != cudaSuccess ||
+  if (cudaMemsetAsync(c->d_gm_done, 0, sizeof(unsigned), c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->d_stats, 0, sizeof(double) * TRMCR_NSTATS * std::max(c->ncells, 1), c->stream) != cudaSuccess) {
     fail(c, TRMCR_ECUDA, "memset failed");
     return bail(TRMCR_ECUDA);
@@ -400,6 +464,26 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
              ? cudaFuncSetAttribute(cell_step_smem<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)
              : cudaFuncSetAttribute(cell_step_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
   if (ea != cudaSuccess) { fail(c, TRMCR_ECUDA, "cudaFuncSetAttribute failed"); return bail(TRMCR_ECUDA); }
+  {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->dev);
+    const int tsm = kThermalWarps * 3 * (c->dtype == TRMCR_F64 ? 512 * 8 : 1024 * 4);
+    cudaError_t e2 = c->dtype == TRMCR_F64
+        ? cudaFuncSetAttribute(thermal_warp_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm)
+        : cudaFuncSetAttribute(thermal_warp_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+    if (e2 != cudaSuccess) { fail(c, TRMCR_ECUDA, "cudaFuncSetAttribute(thermal) failed"); return bail(TRMCR_ECUDA); }
+    int occ_t = 1, occ_s = 1;
+    if (c->dtype == TRMCR_F64) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, thermal_warp_kernel<double>, kThermalWarps * 32, tsm);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, cell_step_smem<double>, kSmemThreads, dyn);
+    } else {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, thermal_warp_kernel<float>, kThermalWarps * 32, tsm);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, cell_step_smem<float>, kSmemThreads, dyn);
+    }
+    c->fast_grid = std::max(1, std::min((c->ncells + kThermalWarps - 1) / kThermalWarps, nsm * std::max(occ_t, 1)));
+    c->smem_grid = std::max(1, std::min(c->ncells, nsm * std::max(occ_s, 1)));
+    if (c->geometry == TRMCR_SHOCK_1D) c->fast_ok = 0;
+  }
 
   // ---- global-memory plan scratch for large / overflowing cells ----
   int big = 0;   // cells that will not fit the smem path at all
