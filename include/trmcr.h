@@ -191,6 +191,10 @@ trmcr_status trmcr_set_profiling(trmcr_ctx *ctx, int32_t on);
  * ms and launches are host arrays of TRMCR_NKERNELS entries. */
 trmcr_status trmcr_kernel_times(trmcr_ctx *ctx, double *ms, int64_t *launches);
 
+/* Debug builds (-DTRMCR_PHASE_TIMING) only: CTA cycles spent per phase of the
+ * general kernels since the last call (16 doubles); EINVAL otherwise. */
+trmcr_status trmcr_debug_phase_cycles(double *out16);
+
 /* Last error message of ctx (or of the last failed trmcr_init when ctx is NULL). */
 const char *trmcr_last_error(const trmcr_ctx *ctx);
 

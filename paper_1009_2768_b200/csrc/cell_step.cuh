@@ -18,6 +18,20 @@
 
 namespace trmcr {
 
+// Optional per-phase cycle accounting (debug builds: -DTRMCR_PHASE_TIMING).
+#ifdef TRMCR_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[16];
+#define PHASE_MARK(var) long long var = clock64()
+#define PHASE_ADD(k, var)                                                        \
+  do {                                                                           \
+    if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[k], (unsigned long long)(clock64() - var)); \
+    var = clock64();                                                             \
+  } while (0)
+#else
+#define PHASE_MARK(var)
+#define PHASE_ADD(k, var)
+#endif
+
 enum : int { kOk = 0, kOverflow = 1, kCapacity = 2 };
 // error bits of the context's device flag (read back by sync calls)
 enum : int { kErrPlanCapacity = 1, kErrParticleCapacity = 2, kErrInternal = 16 };
@@ -51,6 +65,7 @@ struct CellBuf {
   int n_cap, K_cap, L_cap;
 };
 
+constexpr int kSplitPre = 72;
 // Scalars shared by the CTA.
 struct CellShared {
   double ux, uy, uz, S0, sigma, p, mu, S_est, E1;
@@ -59,6 +74,7 @@ struct CellShared {
   int64_t rem;
   int32_t L, Ltot, U, nT, budget, leaf_off, attempts;
   unsigned long long prop, acc, viol;
+  double usplit[kSplitPre];   // split uniforms of levels < kSplitPre, drawn in parallel
 };
 
 template <typename Real> struct RealOps;
@@ -72,11 +88,18 @@ template <> struct RealOps<float> {
 };
 
 // IR at split level d with its keyed uniform; exact 0 when y < 2^-53.
-__device__ __forceinline__ int64_t ir_split(const RngKey &K, int d, double y) {
+// Uniforms of levels < kSplitPre were drawn in parallel into `pre`.
+__device__ __forceinline__ int64_t ir_split(const RngKey &K, int d, double y, const double *pre) {
   if (y < 0x1p-53) return 0;
-  const uint4 w = K(kSplit, 0, (uint32_t)d, 0);
+  double u;
+  if (d < kSplitPre) {
+    u = pre[d];
+  } else {
+    const uint4 w = K(kSplit, 0, (uint32_t)d, 0);
+    u = u53(w.x, w.y);
+  }
   const double fl = floor(y);
-  return (int64_t)fl + ((u53(w.x, w.y) < y - fl) ? 1 : 0);
+  return (int64_t)fl + ((u < y - fl) ? 1 : 0);
 }
 
 // Alg 4.2 continued until rem == 0 or level m (thread 0 only).  Quotas above
@@ -90,7 +113,7 @@ __device__ inline void split_extend(const RngKey &K, CellShared &sh, int m, int3
       break;
     }
     sh.d++;
-    int64_t q = ir_split(K, sh.d, y);
+    int64_t q = ir_split(K, sh.d, y, sh.usplit);
     if (q > sh.rem) q = sh.rem;
     if (sh.d <= L_cap) Q[sh.d] = (int32_t)q;
     else if (q > 0) sh.flag = kOverflow;
@@ -254,11 +277,22 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
   unsigned acc = 0, viol = 0;
   const int r = sh.r;
   const int leaf_off = sh.leaf_off;
+  int pd = 0;            // last level with collisions: its histogram is still in cnt[]
   for (int d = 1; d <= top; ++d) {
     const int Cd = B.C[d], Sd = B.S[d];
     if (Cd == 0) continue;
-    // in-level stable ranks per type (one warp, 32 collisions per round)
     if (warp == 0) {
+      // fold level pd's demands into base[] and clear its histogram (cnt)
+      // (two passes through cons[], idle during execution: every read of the
+      // histogram happens before any of it is cleared)
+      if (pd > 0) {
+        for (int p = lane; p < pd; p += 32) B.cons[p] = B.base[p] + B.cnt[p] + B.cnt[pd - 1 - p];
+        __syncwarp();
+        for (int p = lane; p < pd; p += 32) { B.base[p] = B.cons[p]; B.cnt[p] = 0; }
+        __syncwarp();
+      }
+      // in-level stable ranks per type (32 collisions per round); cnt ends as
+      // this level's type histogram
       for (int j0 = 0; j0 < Cd; j0 += 32) {
         const int j = j0 + lane;
         const bool valid = j < Cd;
@@ -275,6 +309,7 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
         __syncwarp();
       }
     }
+    pd = d;
     __syncthreads();
     for (int j = tid; j < Cd; j += blockDim.x) {
       const uint32_t a = B.ctype[Sd + j], b = (uint32_t)d - 1u - a;
@@ -311,14 +346,7 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
         }
       }
     }
-    __syncthreads();
-    for (int j = tid; j < Cd; j += blockDim.x) {
-      const uint32_t a = B.ctype[Sd + j];
-      atomicAdd(&B.base[a], 1);
-      atomicAdd(&B.base[d - 1 - a], 1);
-      B.cnt[a] = 0;
-    }
-    if (tid == 0) atomicAdd(&sh.prop, (unsigned long long)Cd);
+    if (tid == 0) sh.prop += (unsigned long long)Cd;
     __syncthreads();
   }
   atomicAdd(&sh.acc, (unsigned long long)acc);
@@ -326,25 +354,19 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
   __syncthreads();
 }
 
-// RAD indicator estimate with Theta taken analytically.
+// RAD indicator estimate with Theta taken analytically:
+// S_est = [sum over the non-Theta particles + |Theta| (analytic Maxwellian
+// term)] / n.  Theta's particles are still their pre-step values, so the
+// non-Theta sum is (sum over all slots) - (sum over Theta's slots): one pass
+// over the cell plus one over Theta's slots, no membership table.
 template <typename Real>
 __device__ void rad_estimate(const StepParams &P, CellBuf<Real> &B, CellShared &sh, const Perm &pi0) {
   const int tid = threadIdx.x, n = sh.n, nT = sh.nT;
-  const int nwords = (n + 31) >> 5;
-  for (int i = tid; i < nwords; i += blockDim.x) B.mask[i] = 0u;
-  __syncthreads();
-  for (int q = tid; q < nT; q += blockDim.x) {
-    const uint32_t s = pi0((uint32_t)(sh.Ltot + q));
-    if (s >= (uint32_t)n) { atomicOr(P.err, kErrInternal); continue; }
-    atomicOr(&B.mask[s >> 5], 1u << (s & 31));
-  }
-  __syncthreads();
-  double v[4] = {0, 0, 0, 0};  // non-Theta indicator sum, Theta momentum
+  const bool pxx = P.indicator == TRMCR_IND_PXX;
+  double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // all-slot indicator sum; Theta: indicator, momentum, |v|^2
   for (int i = tid; i < n; i += blockDim.x) {
     const double x = B.vx[i], y = B.vy[i], z = B.vz[i];
-    if ((B.mask[i >> 5] >> (i & 31)) & 1u) {
-      v[1] += x; v[2] += y; v[3] += z;
-    } else if (P.indicator == TRMCR_IND_PXX) {
+    if (pxx) {
       const double dx = x - sh.ux;
       v[0] += dx * dx;
     } else {
@@ -352,22 +374,27 @@ __device__ void rad_estimate(const StepParams &P, CellBuf<Real> &B, CellShared &
       v[0] += v2 * v2;
     }
   }
-  block_sum<4>(v, B.red);
-  double tx = 0, ty = 0, tz = 0;
-  if (nT > 0) { tx = v[1] / nT; ty = v[2] / nT; tz = v[3] / nT; }
-  double e[1] = {0};
-  for (int i = tid; i < n; i += blockDim.x) {
-    if ((B.mask[i >> 5] >> (i & 31)) & 1u) {
-      const double dx = B.vx[i] - tx, dy = B.vy[i] - ty, dz = B.vz[i] - tz;
-      e[0] += dx * dx + dy * dy + dz * dz;
+  for (int q = tid; q < nT; q += blockDim.x) {
+    const uint32_t s = pi0((uint32_t)(sh.Ltot + q));
+    if (s >= (uint32_t)n) { atomicOr(P.err, kErrInternal); continue; }
+    const double x = B.vx[s], y = B.vy[s], z = B.vz[s];
+    if (pxx) {
+      const double dx = x - sh.ux;
+      v[1] += dx * dx;
+    } else {
+      const double v2 = x * x + y * y + z * z;
+      v[1] += v2 * v2;
     }
+    v[2] += x; v[3] += y; v[4] += z;
+    v[5] += x * x + y * y + z * z;
   }
-  block_sum<1>(e, B.red);
+  block_sum<6>(reinterpret_cast<double(&)[6]>(v), B.red);
   if (tid == 0) {
-    double s = v[0];
+    double s = v[0] - v[1];
     if (nT > 0) {
-      const double T = e[0] / (3.0 * nT);
-      if (P.indicator == TRMCR_IND_PXX) {
+      const double tx = v[2] / nT, ty = v[3] / nT, tz = v[4] / nT;
+      const double T = fmax(0.0, v[5] / nT - (tx * tx + ty * ty + tz * tz)) / 3.0;
+      if (pxx) {
         s += (double)nT * (T + (tx - sh.ux) * (tx - sh.ux));
       } else {
         const double u2 = tx * tx + ty * ty + tz * tz;
@@ -444,6 +471,7 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
                             trmcr_coll_rec *log, unsigned long long *log_count, int64_t log_cap) {
   const int tid = threadIdx.x;
   if (n > B.n_cap) return kOverflow;
+  PHASE_MARK(t_ph);
   const RngKey K{P.k0, P.k1, gcell, P.step};
   const int m0 = P.adaptive ? *m_state : P.m_fixed;
   if (n == 0) {
@@ -477,6 +505,10 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
     c3[1] += v2 * v2;
     c3[2] += r2;
   }
+  for (int d = tid; d < kSplitPre; d += blockDim.x) {   // split uniforms, in parallel
+    const uint4 w = K(kSplit, 0, (uint32_t)d, 0);
+    sh.usplit[d] = u53(w.x, w.y);
+  }
   block_sum<3>(c3, B.red);
   dv2 = block_max(dv2, B.red);
   if (tid == 0) {
@@ -497,7 +529,7 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
     sh.m = m0; sh.m_cur = m0; sh.flag = kOk;
     sh.prop = 0; sh.acc = 0; sh.viol = 0;
     // ---- A4: split (Alg 4.2) ----
-    const int64_t N0 = ir_split(K, 0, sh.p * (double)n);
+    const int64_t N0 = ir_split(K, 0, sh.p * (double)n, sh.usplit);
     B.Q[0] = (int32_t)N0;
     sh.rem = n - N0;
     sh.d = 0;
@@ -507,14 +539,17 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
     sh.budget = n; sh.leaf_off = 0;
   }
   __syncthreads();
+  PHASE_ADD(0, t_ph);   // moments + split
   if (sh.flag != kOk) return sh.flag;
   Perm pi0;
   pi0.init(K(kPerm, 0, 0, 0), (uint32_t)n);
   const Real sigma = (Real)sh.sigma;
   // ---- A5/A6: attempt 0 ----
   plan_counts<Real>(K, B, sh);
+  PHASE_ADD(1, t_ph);   // plan counts
   if (sh.flag != kOk) return sh.flag;
   plan_execute<Real>(P, K, B, sh, pi0, sigma, log, log_count, log_cap);
+  PHASE_ADD(2, t_ph);   // plan execute
   if (tid == 0) {
     sh.Ltot = sh.L;
     sh.U = B.Q[0] < n - sh.Ltot ? B.Q[0] : n - sh.Ltot;
@@ -527,6 +562,7 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
   if (P.adaptive) {
     for (;;) {
       rad_estimate<Real>(P, B, sh, pi0);
+      PHASE_ADD(3, t_ph);   // RAD estimate
       if (tid == 0) {
         sh.done = 1;
         if (sh.E1 > P.delta2 && sh.m_cur < P.m_cap) {
@@ -547,6 +583,7 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
       plan_counts<Real>(K, B, sh);
       if (sh.flag != kOk) return sh.flag;
       plan_execute<Real>(P, K, B, sh, pi0, sigma, log, log_count, log_cap);
+      PHASE_ADD(4, t_ph);   // RAD retries
       if (tid == 0) { sh.Ltot += sh.L; sh.nT -= sh.L; }
       __syncthreads();
       if (P.debug_stop > 0 && sh.r >= P.debug_stop) {
@@ -566,13 +603,16 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
     return kOk;
   }
   // ---- A8: Maxwellian of Theta ----
+  PHASE_ADD(5, t_ph);
   maxwellian<Real>(P, K, B, sh, pi0, c3[2]);
+  PHASE_ADD(6, t_ph);   // Maxwellian
   // ---- write back + stats ----
   if (kStore) {
     for (int i = tid; i < n; i += blockDim.x) {
       out_x[i] = B.vx[i]; out_y[i] = B.vy[i]; out_z[i] = B.vz[i];
     }
   }
+  PHASE_ADD(7, t_ph);   // store
   if (tid == 0) {
     if (P.adaptive) *m_state = sh.m_next;
     if (stats_row) {

@@ -144,6 +144,7 @@ struct trmcr_ctx {
   trmcr::GmemScratch gs{};
   int G = 1;
   int gmem_threads = trmcr::kGmemThreads;
+  int smem_threads = 128;
   trmcr::SmemLayout lay{};
   trmcr::StepParams P{};
   uint32_t step = 0;

@@ -41,7 +41,7 @@ template <> __device__ __forceinline__ float mul_rn(float a, float b) { return _
 
 // warp-aggregated atomicAdd(&counts[key], 1) for lanes with key >= 0
 __device__ __forceinline__ void count_key(int32_t *counts, int key) {
-  const unsigned act = __activemask();
+  const unsigned act = 0xffffffffu;   // called by full warps
   const unsigned peers = __match_any_sync(act, key);
   const int lane = threadIdx.x & 31;
   if (key >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(&counts[key], __popc(peers));
@@ -164,29 +164,43 @@ __global__ void ghost_gen(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, c
 }
 
 // ---- A1: free transport of the interior particles ----
+// Counts per destination cell are warp-aggregated; the max displacement and
+// the dropped count are reduced per CTA (one atomic each per CTA).
 template <typename Real>
 __global__ void __launch_bounds__(256)
 transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const Real *__restrict__ vx,
                  int32_t *dest, int32_t *counts, int *W, unsigned long long *acct) {
+  __shared__ int s_disp[8];
+  __shared__ unsigned s_drop[8];
   const int64_t n = off_old[S.C];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const Real xo = x[i];
-  const int src = cell_of(S, (double)xo);
-  const Real xn = add_rn<Real>(xo, mul_rn<Real>(vx[i], (Real)S.dt));
-  x[i] = xn;
-  const double xd = (double)xn;
-  const bool keep = xd >= S.x_min && xd < S.x_max;
-  const int d = keep ? cell_of(S, xd) : -1;
-  dest[i] = d;
+  const bool valid = i < n;
+  int d = -1, disp = 0;
+  bool dropped = false;
+  if (valid) {
+    const Real xo = x[i];
+    const int src = cell_of(S, (double)xo);
+    const Real xn = add_rn<Real>(xo, mul_rn<Real>(vx[i], (Real)S.dt));
+    x[i] = xn;
+    const double xd = (double)xn;
+    const bool keep = xd >= S.x_min && xd < S.x_max;
+    d = keep ? cell_of(S, xd) : -1;
+    dest[i] = d;
+    disp = keep ? abs(d - src) : 0;
+    dropped = !keep;
+  }
   count_key(counts, d);
-  int disp = keep ? abs(d - src) : 0;
-  const unsigned act = __activemask();
-  disp = __reduce_max_sync(act, disp);
-  const unsigned dropped = __popc(__ballot_sync(act, !keep));
-  if ((threadIdx.x & 31) == (__ffs(act) - 1)) {
-    if (disp > 0) atomicMax(W, disp);
-    if (dropped) atomicAdd(&acct[2], (unsigned long long)dropped);
+  const int wd = __reduce_max_sync(0xffffffffu, disp);
+  const unsigned wdrop = __popc(__ballot_sync(0xffffffffu, dropped));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { s_disp[warp] = wd; s_drop[warp] = wdrop; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int md = 0;
+    unsigned dr = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { md = max(md, s_disp[w]); dr += s_drop[w]; }
+    if (md > 0 && md > *((volatile int *)W)) atomicMax(W, md);
+    if (dr) atomicAdd(&acct[2], (unsigned long long)dr);
   }
 }
 
@@ -202,9 +216,13 @@ struct GatherSrc {
 
 // Stable gather of destination cell c into (bx,by,bz) [velocities] and ox
 // [positions, global] in canonical source order.  Returns the count.
+// Each round covers blockDim*8 source entries: a thread tests 8 consecutive
+// destinations (independent loads in flight), a CTA exclusive scan of the
+// per-thread match counts gives every match its stable position.
 template <typename Real>
 __device__ int gather_cell(const ShockDev &S, const GatherSrc &G, int c, Real *bx, Real *by, Real *bz,
                            Real *ox, int *wcnt) {
+  constexpr int R = 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int W = *G.W;
   int running = 0;
@@ -226,11 +244,22 @@ __device__ int gather_cell(const ShockDev &S, const GatherSrc &G, int c, Real *b
       svy = (const Real *)G.gvy[side]; svz = (const Real *)G.gvz[side];
       sd = G.gdest[side];
     }
-    for (int64_t b0 = lo; b0 < hi; b0 += blockDim.x) {
-      const int64_t i = b0 + tid;
-      const bool match = i < hi && sd[i] == c;
-      const unsigned bal = __ballot_sync(0xffffffffu, match);
-      if (lane == 0) wcnt[warp] = __popc(bal);
+    for (int64_t b0 = lo; b0 < hi; b0 += (int64_t)blockDim.x * R) {
+      const int64_t i0 = b0 + (int64_t)tid * R;
+      unsigned bits = 0;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int64_t i = i0 + k;
+        if (i < hi && sd[i] == c) bits |= 1u << k;
+      }
+      const int mine = __popc(bits);
+      int incl = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane == 31) wcnt[warp] = incl;
       __syncthreads();
       int wb = 0, tot = 0;
       for (int w = 0; w < nw; ++w) {
@@ -238,10 +267,22 @@ __device__ int gather_cell(const ShockDev &S, const GatherSrc &G, int c, Real *b
         wb += (w < warp) ? t : 0;
         tot += t;
       }
-      if (match) {
-        const int pos = running + wb + __popc(bal & ((1u << lane) - 1u));
-        bx[pos] = svx[i]; by[pos] = svy[i]; bz[pos] = svz[i];
-        ox[pos] = sx[i];
+      const int pos = running + wb + incl - mine;
+      // all loads of this thread's matches first (independent, in flight), then the stores
+      Real tx[R], tvx[R], tvy[R], tvz[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        if ((bits >> k) & 1u) {
+          const int64_t i = i0 + k;
+          tx[k] = sx[i]; tvx[k] = svx[i]; tvy[k] = svy[i]; tvz[k] = svz[i];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        if ((bits >> k) & 1u) {
+          const int q = pos + __popc(bits & ((1u << k) - 1u));
+          bx[q] = tvx[k]; by[q] = tvy[k]; bz[q] = tvz[k]; ox[q] = tx[k];
+        }
       }
       running += tot;
       __syncthreads();
@@ -250,8 +291,8 @@ __device__ int gather_cell(const ShockDev &S, const GatherSrc &G, int c, Real *b
   return running;
 }
 
-template <typename Real>
-__global__ void __launch_bounds__(kSmemThreads)
+template <typename Real, int THREADS>
+__global__ void __launch_bounds__(THREADS, 768 / THREADS)
 shock_collide_smem(StepParams P, SmemLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, QueueArgs Q) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -264,8 +305,10 @@ shock_collide_smem(StepParams P, SmemLayout Lay, ShockDev S, GatherSrc G, const 
   const int n = (int)(off_new[c + 1] - base);
   int rc = kOverflow;
   if (n <= B.n_cap) {
+    PHASE_MARK(t_g);
     gather_cell<Real>(S, G, c, B.vx, B.vy, B.vz, ox + base, wcnt);
     __syncthreads();
+    PHASE_ADD(8, t_g);   // gather
     rc = process_cell<Real, false, true>(P, B, sh, nullptr, nullptr, nullptr, ovx + base, ovy + base,
                                          ovz + base, n, P.cell_base + (uint32_t)c, m_state + c,
                                          stats + (size_t)c * TRMCR_NSTATS, Q.log, Q.log_count, Q.log_cap);
@@ -411,7 +454,9 @@ trmcr_status shock_step(trmcr_ctx *c) {
   c->P.step = c->step;
   Real *ox = (Real *)c->x[nxt], *ovx = (Real *)c->v[nxt][0], *ovy = (Real *)c->v[nxt][1], *ovz = (Real *)c->v[nxt][2];
   prof_begin(c, TRMCR_K_SHOCK_SMEM);
-  shock_collide_smem<Real><<<s.C, kSmemThreads, c->lay.total, c->stream>>>(
+  auto kern = c->smem_threads == 64 ? shock_collide_smem<Real, 64>
+              : (c->smem_threads == 128 ? shock_collide_smem<Real, 128> : shock_collide_smem<Real, 256>);
+  kern<<<s.C, c->smem_threads, c->lay.total, c->stream>>>(
       c->P, c->lay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, Q);
   if (auto e = check_launch(c, "shock_collide_smem", TRMCR_K_SHOCK_SMEM)) return e;
   prof_begin(c, TRMCR_K_SHOCK_GMEM);

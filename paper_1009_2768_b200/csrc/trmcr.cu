@@ -28,8 +28,8 @@ using namespace trmcr;
 
 namespace {
 
-template <typename Real>
-__global__ void __launch_bounds__(kSmemThreads)
+template <typename Real, int THREADS>
+__global__ void __launch_bounds__(THREADS, 768 / THREADS)
 cell_step_smem(StepParams P, SmemLayout Lay, const int64_t *__restrict__ offsets, int ncells,
                const int *list_count, const int *list, Real *vx, Real *vy, Real *vz, int32_t *m_state,
                double *stats, QueueArgs Q) {
@@ -194,7 +194,9 @@ trmcr_status launch_collide(trmcr_ctx *c) {
     }
     const bool idle = fast && c->fast_ok && c->last_defer == 0 && c->last_ovf == 0;
     prof_begin(c, TRMCR_K_CELL_SMEM);
-    cell_step_smem<Real><<<idle ? 1 : c->smem_grid, kSmemThreads, c->lay.total, c->stream>>>(
+    auto kern = c->smem_threads == 64 ? cell_step_smem<Real, 64>
+                : (c->smem_threads == 128 ? cell_step_smem<Real, 128> : cell_step_smem<Real, 256>);
+    kern<<<idle ? 1 : c->smem_grid, c->smem_threads, c->lay.total, c->stream>>>(
         c->P, c->lay, c->d_offsets, c->ncells, fast ? c->d_defer_count : nullptr,
         fast ? c->d_defer_list : nullptr, vx, vy, vz, c->d_mstate, c->d_stats, Q);
     if (auto s = check_launch(c, "cell_step_smem", TRMCR_K_CELL_SMEM)) return s;
@@ -256,6 +258,22 @@ trmcr_status trmcr_global_moments(trmcr_ctx *c, double *dev_out) {
   const int blocks = std::max(1, std::min(kGmBlocks, c->ncells));
   global_moments_kernel<<<blocks, 256, 0, c->stream>>>(c->d_stats, c->ncells, c->d_gm_partial, c->d_gm_done, dev_out);
   return check_launch(c, "global_moments_kernel");
+}
+
+// Debug builds only: per-phase CTA cycles of the general kernels (reset on read).
+trmcr_status trmcr_debug_phase_cycles(double *out16) {
+#ifdef TRMCR_PHASE_TIMING
+  unsigned long long h[16];
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(h, g_phase_cycles, sizeof(h));
+  for (int k = 0; k < 16; ++k) out16[k] = (double)h[k];
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  return TRMCR_OK;
+#else
+  (void)out16;
+  return TRMCR_EINVAL;
+#endif
 }
 
 trmcr_status trmcr_set_profiling(trmcr_ctx *c, int32_t on) {
@@ -439,14 +457,15 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
   const int budget = std::min(smem_max - 4096, 160 * 1024);
   int n_cap = 0;
   if (c->geometry == TRMCR_HOMOGENEOUS) n_cap = std::max(32, (max_cell + 31) / 32 * 32);
-  else n_cap = std::max(64, (2 * max_cell + 31) / 32 * 32);   // shock cells fluctuate
+  else n_cap = std::max(64, (max_cell + max_cell / 4 + 31) / 32 * 32);   // shock cells fluctuate; rarer giants go to gmem
   const int L_cap = 64;
   // debug knobs: TRMCR_FORCE_GMEM=1 routes every cell through the global-memory
   // path; TRMCR_SMEM_KCAP overrides the shared-memory tree capacity.
   const char *force_g = getenv("TRMCR_FORCE_GMEM");
   const char *kcap_env = getenv("TRMCR_SMEM_KCAP");
   for (;;) {
-    const int K_cap = kcap_env ? atoi(kcap_env) : std::max(256, n_cap / 2);
+    const int K_cap = kcap_env ? atoi(kcap_env)
+                               : (c->geometry == TRMCR_SHOCK_1D ? std::max(256, n_cap / 4) : std::max(256, n_cap / 2));
     c->lay.build(n_cap, K_cap, L_cap, c->rs);
     if ((int)c->lay.total <= budget || n_cap <= 32) break;
     n_cap = std::max(32, n_cap / 2 / 32 * 32);
@@ -454,15 +473,22 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
   if (force_g && atoi(force_g)) c->lay.n_cap = 0;
   if (const char *gt = getenv("TRMCR_GMEM_THREADS")) c->gmem_threads = std::max(32, std::min(1024, atoi(gt)));
   const int dyn = (int)c->lay.total;
-  cudaError_t ea;
-  if (c->geometry == TRMCR_SHOCK_1D)
-    ea = c->dtype == TRMCR_F64
-             ? cudaFuncSetAttribute(shock_collide_smem<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)
-             : cudaFuncSetAttribute(shock_collide_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-  else
-    ea = c->dtype == TRMCR_F64
-             ? cudaFuncSetAttribute(cell_step_smem<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)
-             : cudaFuncSetAttribute(cell_step_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  if (const char *st = getenv("TRMCR_SMEM_THREADS")) c->smem_threads = atoi(st);
+  if (c->smem_threads != 64 && c->smem_threads != 256) c->smem_threads = 128;
+  cudaError_t ea = cudaSuccess;
+  {
+    const void *fns[] = {
+        (const void *)shock_collide_smem<double, 64>, (const void *)shock_collide_smem<double, 128>,
+        (const void *)shock_collide_smem<double, 256>, (const void *)shock_collide_smem<float, 64>,
+        (const void *)shock_collide_smem<float, 128>, (const void *)shock_collide_smem<float, 256>,
+        (const void *)cell_step_smem<double, 64>, (const void *)cell_step_smem<double, 128>,
+        (const void *)cell_step_smem<double, 256>, (const void *)cell_step_smem<float, 64>,
+        (const void *)cell_step_smem<float, 128>, (const void *)cell_step_smem<float, 256>};
+    for (const void *f : fns) {
+      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+      if (e != cudaSuccess) ea = e;
+    }
+  }
   if (ea != cudaSuccess) { fail(c, TRMCR_ECUDA, "cudaFuncSetAttribute failed"); return bail(TRMCR_ECUDA); }
   {
     int nsm = 148;
@@ -475,10 +501,12 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
     int occ_t = 1, occ_s = 1;
     if (c->dtype == TRMCR_F64) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, thermal_warp_kernel<double>, kThermalWarps * 32, tsm);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, cell_step_smem<double>, kSmemThreads, dyn);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, cell_step_smem<double, 256>, 256, dyn);
+      occ_s = occ_s * 256 / c->smem_threads;
     } else {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, thermal_warp_kernel<float>, kThermalWarps * 32, tsm);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, cell_step_smem<float>, kSmemThreads, dyn);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, cell_step_smem<float, 256>, 256, dyn);
+      occ_s = occ_s * 256 / c->smem_threads;
     }
     c->fast_grid = std::max(1, std::min((c->ncells + kThermalWarps - 1) / kThermalWarps, nsm * std::max(occ_t, 1)));
     c->smem_grid = std::max(1, std::min(c->ncells, nsm * std::max(occ_s, 1)));
