@@ -53,8 +53,6 @@ def workload(name: str, rank: int = 0, world: int = 1, eps_override=None):
                              truncation="TRMC-R m=64", sharding="cells", global_moments="allreduce/step"),
                     global_cells=ncells)
     if name in ("c4", "c5"):
-        if world > 1:
-            raise SystemExit("shock slab decomposition across GPUs is not implemented yet (DESIGN.md §8)")
         if name == "c4":
             setup = synth.shock_setup(mach=3.0, ncells=2000, n_total=1_000_000, x_min=-20, x_max=20)
             eps = eps_override or 1.0
@@ -65,12 +63,20 @@ def workload(name: str, rank: int = 0, world: int = 1, eps_override=None):
         inv = setup["ncells"] / (setup["x_max"] - setup["x_min"])
         cell = np.clip(np.floor((x.astype(np.float64) - setup["x_min"]) * inv), 0, setup["ncells"] - 1)
         order = np.argsort(cell, kind="stable")
-        return dict(kind="shock", x=x[order], vx=vx[order], vy=vy[order], vz=vz[order], setup=setup,
+        x, vx, vy, vz = x[order], vx[order], vy[order], vz[order]
+        first, ncl = 0, setup["ncells"]
+        if world > 1:     # slabs balanced by particle count
+            from paper_1009_2768_b200 import dist as D
+            counts = np.bincount(cell.astype(np.int64), minlength=setup["ncells"])
+            first, ncl = D.slab_cuts(counts, world)[rank]
+            x, vx, vy, vz = D.slab_particles(x, vx, vy, vz, setup, first, ncl)
+        return dict(kind="shock", x=x, vx=vx, vy=vy, vz=vz, setup=setup, first=first, local_cells=ncl,
                     dtype=np.float32,
                     kw=dict(model=1, adaptive=True, m_init=2, m_cap=64, eps=eps, dt=setup["dt"], seed=1),
                     cfg=dict(workload=f"configs[{3 if name == 'c4' else 4}] 1D Mach-{setup['mach']:g} shock",
                              cells=setup["ncells"], particles=len(x), eps=eps, dt=setup["dt"],
-                             truncation="TRMC-RAD m_init=2 m_cap=64", sharding="none"),
+                             truncation="TRMC-RAD m_init=2 m_cap=64",
+                             sharding="slabs balanced by particle count, neighbour exchange over NCCL"),
                     global_cells=setup["ncells"])
     if name == "c2":
         n = 1_000_000
@@ -242,17 +248,22 @@ def run_trmcr(args, rank, world, local_rank):
                              cell_base=W["cell_base"], stream=stream.cuda_stream, **W["kw"])
         n_local = int(W["offsets"][-1])
     else:
-        sim = api.Simulation(T(W["vx"]), T(W["vy"]), T(W["vz"]), x=T(W["x"]), shock=W["setup"],
-                             stream=stream.cuda_stream, **W["kw"])
+        from paper_1009_2768_b200 import dist as D
+        slab = D.ShockSlab(api, W["setup"], W["first"], W["local_cells"], T(W["vx"]), T(W["vy"]), T(W["vz"]),
+                           x=T(W["x"]), device=dev, stream=stream.cuda_stream, **W["kw"])
+        sim = slab.sim
         n_local = sim.num_particles()
     gm = torch.zeros(len(api.GLOBAL_FIELDS), dtype=torch.float64, device=dev)
+    xchg = lambda s: D.exchange_p2p(s.send_l, s.send_r, s.recv_l, s.recv_r, rank, world)
 
     def one_step():
-        sim.step(1)
         if W["kind"] == "hom":
+            sim.step(1)
             sim.global_moments(gm)
             if world > 1:
                 dist.all_reduce(gm)
+        else:
+            slab.step(xchg)
 
     for _ in range(args.warmup):
         one_step()

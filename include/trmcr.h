@@ -75,7 +75,12 @@ typedef struct {
  *   particle; reservoir states (rho,u,T)_{L,R} from Rankine-Hugoniot
  *   (P:975-985).  offsets must be NULL.
  * cell_base: global id of local cell 0 (keys the RNG: results do not depend
- *   on how cells are split across devices). */
+ *   on how cells are split across devices).
+ * SHOCK_1D slabs: the context owns global cells [cell_base, cell_base +
+ *   n_cells) of an n_cells_global grid on the GLOBAL domain [x_min, x_max);
+ *   neighbors = bit 0 (a slab on the left), bit 1 (a slab on the right); the
+ *   reservoir of a side exists only without a neighbour there.  A slab with
+ *   neighbours steps with trmcr_shock_begin / (exchange) / trmcr_shock_finish. */
 typedef struct {
   int32_t geometry;          /* trmcr_geometry                                       */
   int32_t n_cells;
@@ -84,6 +89,8 @@ typedef struct {
   const int64_t *offsets;    /* HOMOGENEOUS: host [n_cells+1]; SHOCK_1D: NULL        */
   double x_min, x_max, weight;
   double rho_L, u_L, T_L, rho_R, u_R, T_R;
+  int32_t n_cells_global;    /* SHOCK_1D: cells of the whole domain (0: = n_cells)   */
+  int32_t neighbors;         /* SHOCK_1D: bit 0 left slab, bit 1 right slab          */
 } trmcr_cells;
 
 /* Collision kernel and truncation control. */
@@ -168,6 +175,26 @@ trmcr_status trmcr_set_velocities(trmcr_ctx *ctx, const void *vx, const void *vy
  * [n_cells * TRMCR_NMOMENTS].  Homogeneous geometry only.  Syncs. */
 trmcr_status trmcr_step_host(trmcr_ctx *ctx, const void *vx, const void *vy, const void *vz,
                              double *host_moments);
+
+/* ---- 1D shock slab decomposition (multi-GPU) ----
+ * Exchange buffer of `capacity` particles, trmcr_exchange_bytes() bytes, layout
+ * [int32 count | pad to 16 B][capacity x][vx][vy][vz][capacity int32 global dest],
+ * reals in the context dtype.  trmcr_shock_begin (reservoirs, transport, counts)
+ * packs, in canonical order, the particles that moved into the left/right slab
+ * into send_left/send_right; the caller moves send_left to the left rank's
+ * recv_right and send_right to the right rank's recv_left (e.g. NCCL
+ * send/recv on the context stream); trmcr_shock_finish merges the immigrants
+ * as virtual source segments (the global canonical order of §3.3 of DESIGN.md,
+ * so results do not depend on the partition) and runs the collision step.
+ * Buffers are caller memory (device) and must outlive the context.
+ * Errors: EINVAL (not a shock context, missing buffer for a neighbour),
+ * ECAPACITY at the next sync if more than `capacity` particles emigrate or a
+ * particle crosses a whole slab. */
+int64_t trmcr_exchange_bytes(int32_t dtype, int64_t capacity);
+trmcr_status trmcr_shock_set_exchange(trmcr_ctx *ctx, void *send_left, void *send_right,
+                                      void *recv_left, void *recv_right, int64_t capacity);
+trmcr_status trmcr_shock_begin(trmcr_ctx *ctx);
+trmcr_status trmcr_shock_finish(trmcr_ctx *ctx);
 
 /* Decision log for parity tests: capacity records (0 disables). */
 trmcr_status trmcr_set_log(trmcr_ctx *ctx, int64_t capacity);

@@ -51,7 +51,8 @@ class _Cells(C.Structure):
                 ("pad", C.c_int32), ("offsets", C.POINTER(C.c_int64)),
                 ("x_min", C.c_double), ("x_max", C.c_double), ("weight", C.c_double),
                 ("rho_L", C.c_double), ("u_L", C.c_double), ("T_L", C.c_double),
-                ("rho_R", C.c_double), ("u_R", C.c_double), ("T_R", C.c_double)]
+                ("rho_R", C.c_double), ("u_R", C.c_double), ("T_R", C.c_double),
+                ("n_cells_global", C.c_int32), ("neighbors", C.c_int32)]
 
 
 class _Kernel(C.Structure):
@@ -82,6 +83,14 @@ def lib():
         L.trmcr_step_host.argtypes = [vp, vp, vp, vp, P(C.c_double)]
         L.trmcr_set_log.argtypes = [vp, C.c_int64]
         L.trmcr_get_log.argtypes = [vp, vp, P(C.c_int64)]
+        L.trmcr_exchange_bytes.argtypes = [C.c_int32, C.c_int64]
+        L.trmcr_exchange_bytes.restype = C.c_int64
+        L.trmcr_shock_set_exchange.argtypes = [vp, vp, vp, vp, vp, C.c_int64]
+        L.trmcr_shock_set_exchange.restype = C.c_int
+        L.trmcr_shock_begin.argtypes = [vp]
+        L.trmcr_shock_begin.restype = C.c_int
+        L.trmcr_shock_finish.argtypes = [vp]
+        L.trmcr_shock_finish.restype = C.c_int
         L.trmcr_global_moments.argtypes = [vp, vp]
         L.trmcr_global_moments.restype = C.c_int
         L.trmcr_set_profiling.argtypes = [vp, C.c_int32]
@@ -145,13 +154,15 @@ class Simulation:
             self._off = off
             self.ncells = len(off) - 1
             cells = _Cells(HOMOGENEOUS, self.ncells, cell_base, 0,
-                           off.ctypes.data_as(C.POINTER(C.c_int64)), 0, 0, 0, 0, 0, 0, 0, 0, 0)
+                           off.ctypes.data_as(C.POINTER(C.c_int64)), 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0)
             self.geometry = HOMOGENEOUS
         else:
-            self.ncells = int(shock["ncells"])
+            self.ncells = int(shock.get("local_cells", shock["ncells"]))
+            self.neighbors = int(shock.get("neighbors", 0))
             cells = _Cells(SHOCK_1D, self.ncells, cell_base, 0, None, shock["x_min"], shock["x_max"],
                            shock["weight"], shock["rho_L"], shock["u_L"], shock["T_L"],
-                           shock["rho_R"], shock["u_R"], shock["T_R"])
+                           shock["rho_R"], shock["u_R"], shock["T_R"], int(shock["ncells"]),
+                           self.neighbors)
             self.geometry = SHOCK_1D
         kern = _Kernel(model, int(bool(adaptive)), m_fixed, m_init, m_cap, indicator, delta1, delta2,
                        seed & 0xFFFFFFFFFFFFFFFF)
@@ -248,6 +259,23 @@ class Simulation:
         p, host, _ = _ptr(dev_out)
         assert not host and dev_out.numel() >= len(GLOBAL_FIELDS)
         self._check(lib().trmcr_global_moments(self._h, C.c_void_p(p)))
+
+    # ---- slab decomposition of the shock (see include/trmcr.h) ----
+    def exchange_bytes(self, capacity: int) -> int:
+        return int(lib().trmcr_exchange_bytes(self.dtype, int(capacity)))
+
+    def set_exchange(self, send_left, send_right, recv_left, recv_right, capacity: int):
+        """Register caller-owned device buffers (torch uint8 tensors of exchange_bytes())."""
+        p = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None
+        self._xbufs = (send_left, send_right, recv_left, recv_right)
+        self._check(lib().trmcr_shock_set_exchange(self._h, p(send_left), p(send_right), p(recv_left),
+                                                   p(recv_right), int(capacity)))
+
+    def shock_begin(self):
+        self._check(lib().trmcr_shock_begin(self._h))
+
+    def shock_finish(self):
+        self._check(lib().trmcr_shock_finish(self._h))
 
     def set_profiling(self, on: bool = True):
         self._check(lib().trmcr_set_profiling(self._h, int(bool(on))))

@@ -92,7 +92,9 @@ struct QueueArgs {
 
 // Shock geometry state (A1, A2): see shock.cuh.
 struct ShockState {
-  int C = 0;
+  int C = 0, Cg = 0, cbase = 0, has_left = 0, has_right = 0;
+  void *xsend[2] = {nullptr, nullptr}, *xrecv[2] = {nullptr, nullptr};   // slab exchange (caller memory)
+  int xcap = 0;
   double x_min = 0, x_max = 1, inv_dx = 1, weight = 1;
   double rho[2] = {1, 1}, u[2] = {0, 0}, T[2] = {1, 1}, Lg[2] = {0, 0};
   int cap_g = 0;
@@ -103,7 +105,7 @@ struct ShockState {
   void *gv[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
   int32_t *d_counts = nullptr;              // [C] particles per destination cell
   int *d_ng = nullptr;                      // [2] ghosts generated this step
-  int *d_W = nullptr;                       // max |destination - source| cell
+  int *d_W = nullptr;                       // [2] max local displacement, emigrant scan width
   unsigned long long *d_acct = nullptr;     // [4] injected L, injected R, dropped, generated
 };
 
@@ -227,6 +229,7 @@ inline trmcr_status sync_check(trmcr_ctx *c) {
   if (err & 1) return fail(c, TRMCR_ECAPACITY, "a cell's collision tree exceeded the global-memory plan capacity");
   if (err & 2) return fail(c, TRMCR_ECAPACITY, "particle capacity exceeded (shock inflow)");
   if (err & 16) return fail(c, TRMCR_ECUDA, "internal fault: tree index out of range");
+  if (err & 32) return fail(c, TRMCR_ECAPACITY, "a particle crossed more than one slab in a step");
   return TRMCR_OK;
 }
 

@@ -20,17 +20,42 @@
 
 namespace trmcr {
 
+// Geometry seen by one rank: local cells [0, C) are global cells
+// [cbase, cbase + C) of a Cg-cell grid on the GLOBAL domain [x_min, x_max).
 struct ShockDev {
-  int C;
+  int C, Cg, cbase;
+  int has_left, has_right;     // a neighbouring slab exists (else: reservoir)
   double x_min, x_max, inv_dx, dt;
   double rho[2], u[2], T[2], Lg[2], y[2];
   int cap_g;
 };
 
+constexpr int kDropped = INT32_MIN;   // destination of a particle that left the domain
+
+// global cell of a position inside the domain, clamped (A2)
 __device__ __forceinline__ int cell_of(const ShockDev &S, double x) {
   const double f = floor((x - S.x_min) * S.inv_dx);
-  return f < 0.0 ? 0 : (f >= (double)S.C ? S.C - 1 : (int)f);
+  return f < 0.0 ? 0 : (f >= (double)S.Cg ? S.Cg - 1 : (int)f);
 }
+
+// Exchange buffer (caller memory, see trmcr_shock_set_exchange):
+// [int32 count | pad to 16 B][cap x][cap vx][cap vy][cap vz][cap int32 global dest]
+template <typename Real>
+struct XBuf {
+  int *count;
+  Real *x, *vx, *vy, *vz;
+  int32_t *dest;
+  __host__ __device__ static XBuf bind(void *base, int cap) {
+    XBuf b;
+    unsigned char *p = reinterpret_cast<unsigned char *>(base);
+    b.count = reinterpret_cast<int *>(p);
+    Real *r = reinterpret_cast<Real *>(p + 16);
+    b.x = r; b.vx = r + cap; b.vy = r + 2 * (size_t)cap; b.vz = r + 3 * (size_t)cap;
+    b.dest = reinterpret_cast<int32_t *>(r + 4 * (size_t)cap);
+    return b;
+  }
+  static size_t bytes(int cap) { return 16 + (size_t)cap * (4 * sizeof(Real) + 4); }
+};
 
 template <typename Real> __device__ __forceinline__ Real add_rn(Real a, Real b);
 template <> __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
@@ -54,8 +79,9 @@ __global__ void shock_bin_init(ShockDev S, const Real *__restrict__ x, int64_t n
   if (i >= n) return;
   const double xi = (double)x[i];
   if (!(xi >= S.x_min && xi < S.x_max)) { atomicOr(err, 4); return; }
-  const int c = cell_of(S, xi);
-  if (i > 0 && cell_of(S, (double)x[i - 1]) > c) atomicOr(err, 8);
+  const int c = cell_of(S, xi) - S.cbase;
+  if (c < 0 || c >= S.C) { atomicOr(err, 4); return; }
+  if (i > 0 && cell_of(S, (double)x[i - 1]) - S.cbase > c) atomicOr(err, 8);
   atomicAdd(&counts[c], 1);
 }
 
@@ -116,6 +142,7 @@ __global__ void __launch_bounds__(1024) scan_offsets(const int32_t *__restrict__
 __global__ void ghost_count(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, int *ng, int *err) {
   const int side = threadIdx.x;
   if (side > 1) return;
+  if (side == 0 ? S.has_left : S.has_right) { ng[side] = 0; return; }   // a neighbour, not a reservoir
   const RngKey K{k0, k1, 0xFFFFFFF0u + (uint32_t)side, step};
   const uint4 w = K(kResv, side, 0, 0);
   const double y = S.y[side];
@@ -151,63 +178,177 @@ __global__ void ghost_gen(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, c
   const Real xn = add_rn<Real>((Real)xg, mul_rn<Real>(vx, (Real)S.dt));
   const double xd = (double)xn;
   const bool keep = xd >= S.x_min && xd < S.x_max;
-  const int d = keep ? cell_of(S, xd) : -1;
+  const int d = keep ? cell_of(S, xd) - S.cbase : kDropped;   // local (may lie in a neighbour)
   Real *gx = side ? gx1 : gx0;
   Real *gvx = side ? gvx1 : gvx0, *gvy = side ? gvy1 : gvy0, *gvz = side ? gvz1 : gvz0;
   int32_t *gd = side ? gd1 : gd0;
   gx[k] = xn; gvx[k] = vx; gvy[k] = vy; gvz[k] = vz; gd[k] = d;
   if (keep) {
-    atomicAdd(&counts[d], 1);
-    atomicMax(W, side ? S.C - d : d + 1);
     atomicAdd(&acct[side], 1ull);
+    if (d >= 0 && d < S.C) {
+      atomicAdd(&counts[d], 1);
+      atomicMax(W, side ? S.C - d : d + 1);
+    } else {
+      atomicMax(W + 1, S.C + 1);   // emigrating ghost: pack kernel scans the ghosts
+    }
   }
 }
 
 // ---- A1: free transport of the interior particles ----
-// Counts per destination cell are warp-aggregated; the max displacement and
-// the dropped count are reduced per CTA (one atomic each per CTA).
+// dest = local destination cell (outside [0, C): emigrant to a neighbouring
+// slab; kDropped: left the domain).  Counts per local cell are
+// warp-aggregated; W[0] = max local displacement, W[1] = max displacement of
+// emigrants (cells the pack kernel must scan), reduced per CTA.
 template <typename Real>
 __global__ void __launch_bounds__(256)
 transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const Real *__restrict__ vx,
                  int32_t *dest, int32_t *counts, int *W, unsigned long long *acct) {
-  __shared__ int s_disp[8];
+  __shared__ int s_disp[8], s_emi[8];
   __shared__ unsigned s_drop[8];
   const int64_t n = off_old[S.C];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = i < n;
-  int d = -1, disp = 0;
+  int d = -1, disp = 0, emi = 0;
   bool dropped = false;
   if (valid) {
     const Real xo = x[i];
-    const int src = cell_of(S, (double)xo);
+    const int src = cell_of(S, (double)xo) - S.cbase;
     const Real xn = add_rn<Real>(xo, mul_rn<Real>(vx[i], (Real)S.dt));
     x[i] = xn;
     const double xd = (double)xn;
     const bool keep = xd >= S.x_min && xd < S.x_max;
-    d = keep ? cell_of(S, xd) : -1;
-    dest[i] = d;
-    disp = keep ? abs(d - src) : 0;
+    const int dl = keep ? cell_of(S, xd) - S.cbase : kDropped;
+    dest[i] = dl;
     dropped = !keep;
+    if (keep && dl >= 0 && dl < S.C) {
+      d = dl;
+      disp = abs(dl - src);
+    } else if (keep) {
+      emi = dl < 0 ? src + 1 : S.C - src;   // source cells the pack scan must cover
+    }
   }
   count_key(counts, d);
   const int wd = __reduce_max_sync(0xffffffffu, disp);
+  const int we = __reduce_max_sync(0xffffffffu, emi);
   const unsigned wdrop = __popc(__ballot_sync(0xffffffffu, dropped));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) { s_disp[warp] = wd; s_drop[warp] = wdrop; }
+  if (lane == 0) { s_disp[warp] = wd; s_emi[warp] = we; s_drop[warp] = wdrop; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int md = 0;
+    int md = 0, me = 0;
     unsigned dr = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { md = max(md, s_disp[w]); dr += s_drop[w]; }
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      md = max(md, s_disp[w]); me = max(me, s_emi[w]); dr += s_drop[w];
+    }
     if (md > 0 && md > *((volatile int *)W)) atomicMax(W, md);
+    if (me > 0 && me > *((volatile int *)(W + 1))) atomicMax(W + 1, me);
     if (dr) atomicAdd(&acct[2], (unsigned long long)dr);
   }
+}
+
+// ---- slab exchange: pack emigrants (stable, canonical order) ----
+// side 0: destination left of the slab (dest < 0), side 1: right (dest >= C).
+// Canonical source order: left ghosts, interior (array order), right ghosts.
+// One CTA per side; blockDim*8 entries per round, CTA scan for positions.
+template <typename Real>
+__global__ void __launch_bounds__(1024)
+pack_emigrants(ShockDev S, const int64_t *__restrict__ off_old, const int *ng, const int *W, const Real *x,
+               const Real *vx, const Real *vy, const Real *vz, const int32_t *dest, const Real *gx0,
+               const Real *gvx0, const Real *gvy0, const Real *gvz0, const int32_t *gd0, const Real *gx1,
+               const Real *gvx1, const Real *gvy1, const Real *gvz1, const int32_t *gd1, void *send_l,
+               void *send_r, int cap, int *err) {
+  constexpr int R = 8;
+  __shared__ int wcnt[32];
+  const int side = blockIdx.x;
+  if (side == 0 ? !S.has_left : !S.has_right) return;
+  XBuf<Real> B = XBuf<Real>::bind(side == 0 ? send_l : send_r, cap);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int We = W[1];
+  int running = 0;
+  for (int seg = 0; seg < 3; ++seg) {
+    int64_t lo, hi;
+    const Real *sx, *svx, *svy, *svz;
+    const int32_t *sd;
+    if (seg == 1) {
+      if (We <= 0) continue;
+      const int a = side == 0 ? 0 : max(S.C - We, 0), b = side == 0 ? min(We, S.C) : S.C;
+      lo = off_old[a]; hi = off_old[b];
+      sx = x; svx = vx; svy = vy; svz = vz; sd = dest;
+    } else {
+      const int g = seg == 0 ? 0 : 1;
+      lo = 0; hi = ng[g];
+      sx = g ? gx1 : gx0; svx = g ? gvx1 : gvx0; svy = g ? gvy1 : gvy0; svz = g ? gvz1 : gvz0;
+      sd = g ? gd1 : gd0;
+    }
+    for (int64_t b0 = lo; b0 < hi; b0 += (int64_t)blockDim.x * R) {
+      const int64_t i0 = b0 + (int64_t)tid * R;
+      unsigned bits = 0;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int64_t i = i0 + k;
+        if (i < hi) {
+          const int dd = sd[i];
+          const bool m = dd != kDropped && (side == 0 ? dd < 0 : dd >= S.C);
+          if (m) bits |= 1u << k;
+        }
+      }
+      const int mine = __popc(bits);
+      int incl = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane == 31) wcnt[warp] = incl;
+      __syncthreads();
+      int wb = 0, tot = 0;
+      for (int w = 0; w < nw; ++w) { const int t = wcnt[w]; wb += (w < warp) ? t : 0; tot += t; }
+      int pos = running + wb + incl - mine;
+      while (bits) {
+        const int k = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int64_t i = i0 + k;
+        if (pos < cap) {
+          B.x[pos] = sx[i]; B.vx[pos] = svx[i]; B.vy[pos] = svy[i]; B.vz[pos] = svz[i];
+          B.dest[pos] = sd[i] + S.cbase;   // global destination cell
+        }
+        ++pos;
+      }
+      running += tot;
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    if (running > cap) { atomicOr(err, 2); running = cap; }
+    *B.count = running;
+  }
+}
+
+// ---- slab exchange: immigrants (received) join the local counts ----
+// side 0: from the left neighbour (virtual source before cell 0),
+// side 1: from the right neighbour (virtual source after cell C-1).
+template <typename Real>
+__global__ void immigrant_count(ShockDev S, const void *recv_l, const void *recv_r, int cap, int32_t *counts,
+                                int *W, int *err) {
+  const int side = blockIdx.y;
+  if (side == 0 ? !S.has_left : !S.has_right) return;
+  const XBuf<Real> B = XBuf<Real>::bind(const_cast<void *>(side == 0 ? recv_l : recv_r), cap);
+  const int n = min(*B.count, cap);
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int d = B.dest[k] - S.cbase;
+  if (d < 0 || d >= S.C) { atomicOr(err, 32); return; }   // would need more than one hop
+  atomicAdd(&counts[d], 1);
+  atomicMax(W, side == 0 ? d + 1 : S.C - d);
 }
 
 struct GatherSrc {
   const int64_t *off_old;
   const int *ng;
   const int *W;
+  const void *recv[2];                // immigrants from the left / right neighbour (or null)
+  int xcap;
+  int cbase;
   const void *x, *vx, *vy, *vz;      // interior (source buffer, transported positions)
   const int32_t *dest;
   const void *gx[2], *gvx[2], *gvy[2], *gvz[2];
@@ -226,20 +367,31 @@ __device__ int gather_cell(const ShockDev &S, const GatherSrc &G, int c, Real *b
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int W = *G.W;
   int running = 0;
-  for (int seg = 0; seg < 3; ++seg) {
-    int64_t lo, hi;
+  // canonical source order: left reservoir ghosts, left immigrants, interior,
+  // right immigrants, right reservoir ghosts
+  for (int seg = 0; seg < 5; ++seg) {
+    int64_t lo = 0, hi = 0;
     const Real *sx, *svx, *svy, *svz;
     const int32_t *sd;
-    if (seg == 1) {
+    int match = c;                       // destination value to look for
+    if (seg == 2) {
       const int a = max(c - W, 0), b = min(c + W, S.C - 1);
       lo = G.off_old[a]; hi = G.off_old[b + 1];
       sx = (const Real *)G.x; svx = (const Real *)G.vx; svy = (const Real *)G.vy; svz = (const Real *)G.vz;
       sd = G.dest;
+    } else if (seg == 1 || seg == 3) {
+      const int side = seg == 1 ? 0 : 1;
+      const bool in = side == 0 ? (c - W <= -1) : (c + W >= S.C);
+      if (!in || G.recv[side] == nullptr) continue;
+      const XBuf<Real> X = XBuf<Real>::bind(const_cast<void *>(G.recv[side]), G.xcap);
+      hi = min(*X.count, G.xcap);
+      sx = X.x; svx = X.vx; svy = X.vy; svz = X.vz; sd = X.dest;
+      match = c + G.cbase;               // immigrants carry global destinations
     } else {
       const int side = seg == 0 ? 0 : 1;
       const bool in = side == 0 ? (c - W <= -1) : (c + W >= S.C);
       if (!in) continue;
-      lo = 0; hi = G.ng[side];
+      hi = G.ng[side];
       sx = (const Real *)G.gx[side]; svx = (const Real *)G.gvx[side];
       svy = (const Real *)G.gvy[side]; svz = (const Real *)G.gvz[side];
       sd = G.gdest[side];
@@ -250,7 +402,7 @@ __device__ int gather_cell(const ShockDev &S, const GatherSrc &G, int c, Real *b
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         const int64_t i = i0 + k;
-        if (i < hi && sd[i] == c) bits |= 1u << k;
+        if (i < hi && sd[i] == match) bits |= 1u << k;
       }
       const int mine = __popc(bits);
       int incl = mine;
@@ -348,7 +500,8 @@ shock_collide_gmem(StepParams P, GmemScratch GS, ShockDev S, GatherSrc G, const 
 inline ShockDev shock_dev(const trmcr_ctx *c) {
   const ShockState &s = c->shock;
   ShockDev d;
-  d.C = s.C; d.x_min = s.x_min; d.x_max = s.x_max; d.inv_dx = s.inv_dx; d.dt = c->dt;
+  d.C = s.C; d.Cg = s.Cg; d.cbase = s.cbase; d.has_left = s.has_left; d.has_right = s.has_right;
+  d.x_min = s.x_min; d.x_max = s.x_max; d.inv_dx = s.inv_dx; d.dt = c->dt;
   for (int k = 0; k < 2; ++k) {
     d.rho[k] = s.rho[k]; d.u[k] = s.u[k]; d.T[k] = s.T[k]; d.Lg[k] = s.Lg[k];
     d.y[k] = s.rho[k] * s.Lg[k] / s.weight;
@@ -357,13 +510,20 @@ inline ShockDev shock_dev(const trmcr_ctx *c) {
   return d;
 }
 
-// Allocate shock state, validate + count the initial particles (sorted by
-// cell), build offsets.  Synchronises (init only).  *max_cell: largest cell.
+// Allocate shock state, validate + count the initial particles (inside this
+// slab, sorted by cell), build offsets.  Synchronises (init only).
 inline trmcr_status shock_init(trmcr_ctx *c, const trmcr_cells *cc, int *max_cell) {
   ShockState &s = c->shock;
   s.C = cc->n_cells;
+  s.Cg = cc->n_cells_global > 0 ? cc->n_cells_global : cc->n_cells;
+  s.cbase = cc->cell_base;
+  s.has_left = (cc->neighbors & 1) ? 1 : 0;
+  s.has_right = (cc->neighbors & 2) ? 1 : 0;
+  if (s.cbase + s.C > s.Cg) return fail(c, TRMCR_EINVAL, "slab outside the global grid");
+  if (s.has_left != (s.cbase > 0) || s.has_right != (s.cbase + s.C < s.Cg))
+    return fail(c, TRMCR_EINVAL, "neighbours must be exactly the slabs next to this one");
   s.x_min = cc->x_min; s.x_max = cc->x_max; s.weight = cc->weight;
-  s.inv_dx = (double)cc->n_cells / (cc->x_max - cc->x_min);
+  s.inv_dx = (double)s.Cg / (cc->x_max - cc->x_min);
   s.rho[0] = cc->rho_L; s.u[0] = cc->u_L; s.T[0] = cc->T_L;
   s.rho[1] = cc->rho_R; s.u[1] = cc->u_R; s.T[1] = cc->T_R;
   double ymax = 0;
@@ -375,7 +535,7 @@ inline trmcr_status shock_init(trmcr_ctx *c, const trmcr_cells *cc, int *max_cel
   s.cap_g = (int)floor(ymax) + 2;   // IR(y) <= floor(y) + 1
   if (dalloc(c, &s.d_off[0], sizeof(int64_t) * (s.C + 1)) || dalloc(c, &s.d_off[1], sizeof(int64_t) * (s.C + 1)) ||
       dalloc(c, &s.d_dest, sizeof(int32_t) * (size_t)c->cap) || dalloc(c, &s.d_counts, sizeof(int32_t) * s.C) ||
-      dalloc(c, &s.d_ng, sizeof(int) * 2) || dalloc(c, &s.d_W, sizeof(int)) ||
+      dalloc(c, &s.d_ng, sizeof(int) * 2) || dalloc(c, &s.d_W, sizeof(int) * 2) ||
       dalloc(c, &s.d_acct, sizeof(unsigned long long) * 4))
     return TRMCR_ENOMEM;
   for (int k = 0; k < 2; ++k) {
@@ -385,6 +545,7 @@ inline trmcr_status shock_init(trmcr_ctx *c, const trmcr_cells *cc, int *max_cel
   }
   CUDA_TRY(c, cudaMemsetAsync(s.d_counts, 0, sizeof(int32_t) * s.C, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(s.d_acct, 0, sizeof(unsigned long long) * 4, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(s.d_ng, 0, sizeof(int) * 2, c->stream));
   const ShockDev d = shock_dev(c);
   if (c->n > 0) {
     const unsigned blocks = (unsigned)((c->n + 255) / 256);
@@ -401,7 +562,7 @@ inline trmcr_status shock_init(trmcr_ctx *c, const trmcr_cells *cc, int *max_cel
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   int err = 0;
   CUDA_TRY(c, cudaMemcpy(&err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost));
-  if (err & 4) return fail(c, TRMCR_EINVAL, "particle outside the shock domain");
+  if (err & 4) return fail(c, TRMCR_EINVAL, "particle outside this slab of the shock domain");
   if (err & 8) return fail(c, TRMCR_EINVAL, "shock particles must be sorted by cell (stable order)");
   *max_cell = 0;
   for (int32_t v : counts) *max_cell = std::max(*max_cell, (int)v);
@@ -410,14 +571,15 @@ inline trmcr_status shock_init(trmcr_ctx *c, const trmcr_cells *cc, int *max_cel
   return TRMCR_OK;
 }
 
-// One full shock step: A1 + A2 + A3..A8.
+// Phase 1 of a shock step: reservoirs, transport, counts, emigrant packing.
 template <typename Real>
-trmcr_status shock_step(trmcr_ctx *c) {
+trmcr_status shock_begin(trmcr_ctx *c) {
   ShockState &s = c->shock;
   const ShockDev d = shock_dev(c);
-  const int cur = c->cur, nxt = cur ^ 1;
+  const int cur = c->cur;
+  CUDA_TRY(c, cudaMemsetAsync(c->d_ovf_count, 0, sizeof(int), c->stream));
   CUDA_TRY(c, cudaMemsetAsync(s.d_counts, 0, sizeof(int32_t) * s.C, c->stream));
-  CUDA_TRY(c, cudaMemsetAsync(s.d_W, 0, sizeof(int), c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(s.d_W, 0, 2 * sizeof(int), c->stream));
   CUDA_TRY(c, cudaMemsetAsync(s.d_acct, 0, sizeof(unsigned long long) * 4, c->stream));
   prof_begin(c, TRMCR_K_GHOST_COUNT);
   ghost_count<<<1, 32, 0, c->stream>>>(d, c->P.k0, c->P.k1, c->step, s.d_ng, c->d_err);
@@ -439,6 +601,31 @@ trmcr_status shock_step(trmcr_ctx *c) {
                                                           s.d_W, s.d_acct);
     if (auto e = check_launch(c, "transport_kernel", TRMCR_K_TRANSPORT)) return e;
   }
+  if (s.has_left || s.has_right) {
+    if (!s.xsend[0] && !s.xsend[1]) return fail(c, TRMCR_EINVAL, "slab exchange buffers not set (trmcr_shock_set_exchange)");
+    pack_emigrants<Real><<<2, 1024, 0, c->stream>>>(
+        d, s.d_off[cur], s.d_ng, s.d_W, (const Real *)c->x[cur], (const Real *)c->v[cur][0],
+        (const Real *)c->v[cur][1], (const Real *)c->v[cur][2], s.d_dest, (const Real *)s.gx[0],
+        (const Real *)s.gv[0][0], (const Real *)s.gv[0][1], (const Real *)s.gv[0][2], s.d_gdest[0],
+        (const Real *)s.gx[1], (const Real *)s.gv[1][0], (const Real *)s.gv[1][1], (const Real *)s.gv[1][2],
+        s.d_gdest[1], s.xsend[0], s.xsend[1], s.xcap, c->d_err);
+    if (auto e = check_launch(c, "pack_emigrants")) return e;
+  }
+  return TRMCR_OK;
+}
+
+// Phase 2: immigrants (exchange buffers filled by the caller), offsets, the
+// fused stable gather + collision step, buffer swap.
+template <typename Real>
+trmcr_status shock_finish(trmcr_ctx *c) {
+  ShockState &s = c->shock;
+  const ShockDev d = shock_dev(c);
+  const int cur = c->cur, nxt = cur ^ 1;
+  if (s.has_left || s.has_right) {
+    dim3 grid((unsigned)((s.xcap + 255) / 256), 2);
+    immigrant_count<Real><<<grid, 256, 0, c->stream>>>(d, s.xrecv[0], s.xrecv[1], s.xcap, s.d_counts, s.d_W, c->d_err);
+    if (auto e = check_launch(c, "immigrant_count")) return e;
+  }
   prof_begin(c, TRMCR_K_SCAN);
   scan_offsets<<<1, 1024, 0, c->stream>>>(s.d_counts, s.C, s.d_off[nxt], c->cap, c->d_err);
   if (auto e = check_launch(c, "scan_offsets", TRMCR_K_SCAN)) return e;
@@ -450,6 +637,10 @@ trmcr_status shock_step(trmcr_ctx *c) {
     G.gx[k] = s.gx[k]; G.gvx[k] = s.gv[k][0]; G.gvy[k] = s.gv[k][1]; G.gvz[k] = s.gv[k][2];
     G.gdest[k] = s.d_gdest[k];
   }
+  G.recv[0] = s.has_left ? s.xrecv[0] : nullptr;
+  G.recv[1] = s.has_right ? s.xrecv[1] : nullptr;
+  G.xcap = s.xcap;
+  G.cbase = s.cbase;
   QueueArgs Q{c->d_ovf_count, c->d_ovf_list, c->d_err, c->d_log, c->d_log_count, c->log_cap};
   c->P.step = c->step;
   Real *ox = (Real *)c->x[nxt], *ovx = (Real *)c->v[nxt][0], *ovy = (Real *)c->v[nxt][1], *ovz = (Real *)c->v[nxt][2];
@@ -466,6 +657,12 @@ trmcr_status shock_step(trmcr_ctx *c) {
   c->cur = nxt;
   c->d_offsets = s.d_off[nxt];
   return TRMCR_OK;
+}
+
+template <typename Real>
+trmcr_status shock_step(trmcr_ctx *c) {
+  if (trmcr_status e = shock_begin<Real>(c)) return e;
+  return shock_finish<Real>(c);
 }
 
 }  // namespace trmcr

@@ -224,7 +224,8 @@ trmcr_status launch_moments(trmcr_ctx *c) {
 }
 
 trmcr_status do_step(trmcr_ctx *c) {
-  if (c->geometry == TRMCR_SHOCK_1D) CUDA_TRY(c, cudaMemsetAsync(c->d_ovf_count, 0, sizeof(int), c->stream));
+  if (c->geometry == TRMCR_SHOCK_1D && (c->shock.has_left || c->shock.has_right))
+    return fail(c, TRMCR_EINVAL, "a slab with neighbours steps with trmcr_shock_begin / exchange / trmcr_shock_finish");
   if (c->log_cap > 0)
     CUDA_TRY(c, cudaMemsetAsync(c->d_log_count, 0, sizeof(unsigned long long), c->stream));
   trmcr_status s;
@@ -384,7 +385,9 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
   P.shock = c->geometry == TRMCR_SHOCK_1D;
   P.err = nullptr;   // set once d_err exists
   P.debug_stop = getenv("TRMCR_DEBUG_STOP") ? atoi(getenv("TRMCR_DEBUG_STOP")) : 0;
-  P.w_over_dx = P.shock ? cc->weight / ((cc->x_max - cc->x_min) / cc->n_cells) : 0.0;
+  P.w_over_dx = P.shock ? cc->weight / ((cc->x_max - cc->x_min) /
+                                        (cc->n_cells_global > 0 ? cc->n_cells_global : cc->n_cells))
+                        : 0.0;
 
   // ---- buffers ----
   const int nbuf = c->geometry == TRMCR_SHOCK_1D ? 2 : 1;
@@ -534,6 +537,41 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
     return bail(TRMCR_ECUDA);
   }
   *out = c;
+  return TRMCR_OK;
+}
+
+int64_t trmcr_exchange_bytes(int32_t dtype, int64_t capacity) {
+  if (capacity < 0) return -1;
+  return dtype == TRMCR_F64 ? (int64_t)XBuf<double>::bytes((int)capacity) : (int64_t)XBuf<float>::bytes((int)capacity);
+}
+
+trmcr_status trmcr_shock_set_exchange(trmcr_ctx *c, void *send_left, void *send_right, void *recv_left,
+                                      void *recv_right, int64_t capacity) {
+  if (!c || capacity <= 0 || capacity > (1 << 28)) return fail(c, TRMCR_EINVAL, "bad argument");
+  if (c->geometry != TRMCR_SHOCK_1D) return fail(c, TRMCR_EINVAL, "not a shock context");
+  ShockState &s = c->shock;
+  if ((s.has_left && (!send_left || !recv_left)) || (s.has_right && (!send_right || !recv_right)))
+    return fail(c, TRMCR_EINVAL, "missing exchange buffer for an existing neighbour");
+  s.xsend[0] = send_left; s.xsend[1] = send_right; s.xrecv[0] = recv_left; s.xrecv[1] = recv_right;
+  s.xcap = (int)capacity;
+  return TRMCR_OK;
+}
+
+trmcr_status trmcr_shock_begin(trmcr_ctx *c) {
+  if (!c) return fail(nullptr, TRMCR_EINVAL, "null ctx");
+  if (c->sticky) return TRMCR_ESTATE;
+  if (c->geometry != TRMCR_SHOCK_1D) return fail(c, TRMCR_EINVAL, "not a shock context");
+  if (c->log_cap > 0) CUDA_TRY(c, cudaMemsetAsync(c->d_log_count, 0, sizeof(unsigned long long), c->stream));
+  return c->dtype == TRMCR_F64 ? shock_begin<double>(c) : shock_begin<float>(c);
+}
+
+trmcr_status trmcr_shock_finish(trmcr_ctx *c) {
+  if (!c) return fail(nullptr, TRMCR_EINVAL, "null ctx");
+  if (c->sticky) return TRMCR_ESTATE;
+  if (c->geometry != TRMCR_SHOCK_1D) return fail(c, TRMCR_EINVAL, "not a shock context");
+  trmcr_status s = c->dtype == TRMCR_F64 ? shock_finish<double>(c) : shock_finish<float>(c);
+  if (s) return s;
+  c->step++;
   return TRMCR_OK;
 }
 

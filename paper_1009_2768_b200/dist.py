@@ -1,0 +1,120 @@
+"""Host-side multi-GPU logic (one process per GPU, torch.distributed).
+
+* Homogeneous ensembles shard by contiguous global cell ranges; the RNG is
+  keyed by global cell id so per-cell results do not depend on the number of
+  GPUs.  The only collective is the all-reduce of the global sums.
+* The 1D shock is split into slabs of contiguous cells balanced by particle
+  count; each step every slab sends the particles that moved into a
+  neighbouring slab to rank +- 1 (fixed-capacity buffers with a count header,
+  one message per direction, no size round trip) between
+  trmcr_shock_begin and trmcr_shock_finish.  The exchange uses
+  torch.distributed point-to-point ops, so the same code runs over NCCL
+  (CUDA tensors, NVLink) and gloo (CPU tensors, tests).
+"""
+from __future__ import annotations
+
+from typing import Callable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+
+def shard_range(n: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous near-equal partition of [0, n)."""
+    return rank * n // world, (rank + 1) * n // world
+
+
+def shard_homogeneous(offsets: np.ndarray, rank: int, world: int):
+    """Local offsets (starting at 0), global id of the first local cell and the
+    particle slice of this rank."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    lo, hi = shard_range(len(offsets) - 1, rank, world)
+    local = offsets[lo:hi + 1] - offsets[lo]
+    return local, lo, slice(int(offsets[lo]), int(offsets[hi]))
+
+
+def slab_cuts(counts: Sequence[int], world: int, min_cells: int = 4) -> List[Tuple[int, int]]:
+    """(first cell, number of cells) per rank: contiguous slabs with about
+    n / world particles each (the shock's density jump makes equal-cell slabs
+    unbalanced), at least `min_cells` cells each."""
+    counts = np.asarray(counts, dtype=np.int64)
+    C = len(counts)
+    if world * min_cells > C:
+        raise ValueError("too many ranks for the grid")
+    cum = np.concatenate([[0], np.cumsum(counts)])
+    total = cum[-1]
+    cuts = [0]
+    for r in range(1, world):
+        target = total * r / world
+        c = int(np.searchsorted(cum, target))
+        c = max(c, cuts[-1] + min_cells)
+        c = min(c, C - (world - r) * min_cells)
+        cuts.append(c)
+    cuts.append(C)
+    return [(cuts[r], cuts[r + 1] - cuts[r]) for r in range(world)]
+
+
+def exchange_p2p(send_left, send_right, recv_left, recv_right, rank: int, world: int, group=None):
+    """Send send_left to rank-1 (its recv_right) and send_right to rank+1 (its
+    recv_left); receive symmetrically.  Buffers are torch tensors (CUDA over
+    NCCL, CPU over gloo); missing neighbours are skipped."""
+    import torch.distributed as dist
+    ops = []
+    if rank > 0:
+        ops.append(dist.P2POp(dist.isend, send_left, rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, recv_left, rank - 1, group))
+    if rank < world - 1:
+        ops.append(dist.P2POp(dist.isend, send_right, rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, recv_right, rank + 1, group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
+def slab_particles(x, vx, vy, vz, setup: dict, first: int, ncells: int):
+    """The (cell-sorted) particles of global cells [first, first + ncells)."""
+    inv = setup["ncells"] / (setup["x_max"] - setup["x_min"])
+    cell = np.clip(np.floor((np.asarray(x, dtype=np.float64) - setup["x_min"]) * inv), 0,
+                   setup["ncells"] - 1).astype(np.int64)
+    lo = np.searchsorted(cell, first, side="left")
+    hi = np.searchsorted(cell, first + ncells, side="left")
+    return x[lo:hi], vx[lo:hi], vy[lo:hi], vz[lo:hi]
+
+
+class ShockSlab:
+    """One rank's slab of the 1D shock: a Simulation over global cells
+    [first, first + ncells) plus its exchange buffers."""
+
+    def __init__(self, api, setup: dict, first: int, ncells: int, vx, vy, vz, *, x, device,
+                 exchange_capacity: int = 1 << 16, **kw):
+        import torch
+        self.first, self.ncells = first, ncells
+        C = setup["ncells"]
+        neighbors = (1 if first > 0 else 0) | (2 if first + ncells < C else 0)
+        sh = dict(setup)
+        sh.update(local_cells=ncells, neighbors=neighbors)
+        self.sim = api.Simulation(vx, vy, vz, x=x, shock=sh, cell_base=first, **kw)
+        nb = self.sim.exchange_bytes(exchange_capacity)
+        mk = lambda: torch.zeros(nb, dtype=torch.uint8, device=device)
+        self.send_l, self.send_r, self.recv_l, self.recv_r = mk(), mk(), mk(), mk()
+        self.sim.set_exchange(self.send_l if neighbors & 1 else None, self.send_r if neighbors & 2 else None,
+                              self.recv_l if neighbors & 1 else None, self.recv_r if neighbors & 2 else None,
+                              exchange_capacity)
+        self.neighbors = neighbors
+
+    def step(self, exchange: Callable[["ShockSlab"], None]):
+        """begin (transport, pack) -> exchange(self) -> finish (gather, collide)."""
+        if self.neighbors == 0:
+            self.sim.step(1)
+            return
+        self.sim.shock_begin()
+        exchange(self)
+        self.sim.shock_finish()
+
+
+def host_exchange(slabs: List[ShockSlab]):
+    """In-process exchange between slabs of one GPU (tests): copy each send
+    buffer into its neighbour's receive buffer (device copies on the current
+    stream; no kernel waits on another)."""
+    for a, b in zip(slabs[:-1], slabs[1:]):
+        b.recv_l.copy_(a.send_r)
+        a.recv_r.copy_(b.send_l)
