@@ -213,6 +213,9 @@ enum {
   TRMCR_NKERNELS
 };
 trmcr_status trmcr_set_profiling(trmcr_ctx *ctx, int32_t on);
+/* Same, restricted to the kernel ids whose bit is set in `mask` (fewer events
+ * in the stream: bracket only the kernel being measured). */
+trmcr_status trmcr_set_profiling_mask(trmcr_ctx *ctx, uint32_t mask);
 /* Sums, per kernel id, the device time (ms) and launch count recorded since
  * the previous call (or since profiling was enabled), then resets. Syncs.
  * ms and launches are host arrays of TRMCR_NKERNELS entries. */

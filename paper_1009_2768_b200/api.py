@@ -93,6 +93,8 @@ def lib():
         L.trmcr_shock_finish.restype = C.c_int
         L.trmcr_global_moments.argtypes = [vp, vp]
         L.trmcr_global_moments.restype = C.c_int
+        L.trmcr_set_profiling_mask.argtypes = [vp, C.c_uint32]
+        L.trmcr_set_profiling_mask.restype = C.c_int
         L.trmcr_set_profiling.argtypes = [vp, C.c_int32]
         L.trmcr_set_profiling.restype = C.c_int
         L.trmcr_kernel_times.argtypes = [vp, P(C.c_double), P(C.c_int64)]
@@ -279,6 +281,13 @@ class Simulation:
 
     def set_profiling(self, on: bool = True):
         self._check(lib().trmcr_set_profiling(self._h, int(bool(on))))
+
+    def set_profiling_kernels(self, names):
+        """Bracket only the named kernels with events (see KERNELS)."""
+        mask = 0
+        for nm in names:
+            mask |= 1 << KERNELS.index(nm)
+        self._check(lib().trmcr_set_profiling_mask(self._h, mask))
 
     def kernel_times(self) -> dict:
         """{kernel name: (total ms, launches)} since the last call (device events)."""

@@ -156,6 +156,7 @@ struct trmcr_ctx {
   int64_t launches = 0;
   // per-kernel timing (trmcr_set_profiling)
   int prof = 0;
+  uint32_t prof_mask = 0xFFFFFFFFu;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<int> ev_kid;
@@ -209,13 +210,13 @@ inline void prof_event(trmcr_ctx *c) {
   cudaEventRecord(c->ev_pool[c->ev_used++], c->stream);
 }
 inline void prof_begin(trmcr_ctx *c, int kid) {
-  if (!c->prof) return;
+  if (!c->prof || !((c->prof_mask >> kid) & 1u)) return;
   c->ev_kid.push_back(kid);
   prof_event(c);
 }
 
 inline trmcr_status check_launch(trmcr_ctx *c, const char *what, int kid = -1) {
-  if (c->prof && kid >= 0) prof_event(c);
+  if (c->prof && kid >= 0 && ((c->prof_mask >> kid) & 1u)) prof_event(c);
   c->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(c, TRMCR_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));

@@ -262,6 +262,28 @@ __device__ __forceinline__ void gauss3_fast(const RngKey &K, uint32_t slot, floa
   g0 = r1 * c2; g1 = r1 * s2; g2 = r3 * c4;
 }
 
+// Box-Muller pair from two 24-bit uniforms (fp32 statistical path).
+__device__ __forceinline__ void bm_pair(uint32_t wa, uint32_t wb, float &c, float &s) {
+  constexpr float kM2Ln2 = -1.3862943611198906f;   // -2 ln 2
+  const float a = kM2Ln2 * __log2f(u24_bits(wa));
+  const float r = a * rsqrtf(a);
+  __sincosf(6.283185307179586f * u24_bits(wb), &s, &c);
+  c *= r;
+  s *= r;
+}
+// 12 standard normals for the 4 consecutive slots of float4 group g: three
+// Philox blocks (MAXW, element 3g..3g+2) -> 6 Box-Muller pairs (fp32 mode's
+// draw definition for the fluid-regime path).
+__device__ __forceinline__ void gauss12(const RngKey &K, uint32_t g, float4 &a, float4 &b, float4 &d) {
+  const uint4 w0 = K(kMaxw, 0, 0, 3 * g), w1 = K(kMaxw, 0, 0, 3 * g + 1), w2 = K(kMaxw, 0, 0, 3 * g + 2);
+  bm_pair(w0.x, w0.y, a.x, b.x);
+  bm_pair(w0.z, w0.w, d.x, a.y);
+  bm_pair(w1.x, w1.y, b.y, d.y);
+  bm_pair(w1.z, w1.w, a.z, b.z);
+  bm_pair(w2.x, w2.y, d.z, a.w);
+  bm_pair(w2.z, w2.w, b.w, d.w);
+}
+
 __device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, float *vx, float *vy, float *vz, int64_t off,
                                                  int n, int c, float *wx, float *wy, float *wz,
                                                  int32_t *m_state, double *stats) {
@@ -330,10 +352,7 @@ __device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, float *vx,
       const int g = lane + 32 * k;
       if (g < ng) {
         float4 a, b, d;
-        gauss3_fast(K, (uint32_t)(4 * g + 0), a.x, b.x, d.x);
-        gauss3_fast(K, (uint32_t)(4 * g + 1), a.y, b.y, d.y);
-        gauss3_fast(K, (uint32_t)(4 * g + 2), a.z, b.z, d.z);
-        gauss3_fast(K, (uint32_t)(4 * g + 3), a.w, b.w, d.w);
+        gauss12(K, (uint32_t)g, a, b, d);
         sx4[g] = a; sy4[g] = b; sz4[g] = d;
         ax += (a.x + a.y) + (a.z + a.w); ay += (b.x + b.y) + (b.z + b.w); az += (d.x + d.y) + (d.z + d.w);
         a2 += ((a.x * a.x + b.x * b.x + d.x * d.x) + (a.y * a.y + b.y * b.y + d.y * d.y)) +

@@ -282,8 +282,15 @@ trmcr_status trmcr_set_profiling(trmcr_ctx *c, int32_t on) {
   if (c->sticky) return TRMCR_ESTATE;
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->prof = on ? 1 : 0;
+  c->prof_mask = 0xFFFFFFFFu;
   c->ev_used = 0;
   c->ev_kid.clear();
+  return TRMCR_OK;
+}
+
+trmcr_status trmcr_set_profiling_mask(trmcr_ctx *c, uint32_t mask) {
+  if (trmcr_status s = trmcr_set_profiling(c, mask != 0)) return s;
+  c->prof_mask = mask;
   return TRMCR_OK;
 }
 
