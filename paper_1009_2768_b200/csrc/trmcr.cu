@@ -120,7 +120,7 @@ moments_kernel(const int64_t *__restrict__ offsets, int ncells, const Real *__re
 // Global sums of the per-cell statistics rows: kGmBlocks CTAs write partial
 // sums of contiguous cell ranges, the last CTA to finish adds the partials in
 // block order (deterministic), writes `out` and re-arms the counter.
-constexpr int kGmBlocks = 64;
+constexpr int kGmBlocks = 256;
 __global__ void __launch_bounds__(256) global_moments_kernel(const double *__restrict__ stats, int ncells,
                                                              double *partial, unsigned *done, double *out) {
   __shared__ double red[8 * 10];
