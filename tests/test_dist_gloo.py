@@ -25,14 +25,21 @@ def _free_port():
 
 
 def _run(fn, world, *args):
-    port = _free_port()
-    mp.spawn(_entry, args=(fn, world, port, args), nprocs=world, join=True)
+    # a fresh port per attempt; one retry guards against a port grabbed in between
+    for attempt in range(2):
+        port = _free_port()
+        try:
+            mp.spawn(_entry, args=(fn, world, port, args), nprocs=world, join=True)
+            return
+        except mp.ProcessRaisedException as e:
+            if attempt == 1 or "address already in use" not in str(e).lower():
+                raise
 
 
 def _entry(rank, fn, world, port, args):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import datetime
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world,
+                            timeout=datetime.timedelta(seconds=120))
     try:
         fn(rank, world, *args)
     finally:
