@@ -313,11 +313,11 @@ def run_trmcr(args, rank, world, local_rank):
     # ---- roofline of the dominant kernel (algorithmic bytes) ----
     dom, (dom_ms, dom_n) = max(ktimes.items(), key=lambda kv: kv[1][0])
     rs = 4 if td == torch.float32 else 8
-    if dom in ("cell_step_smem", "cell_step_gmem", "thermal_warp_kernel"):
+    if dom in ("cell_step_smem", "cell_step_gmem", "thermal_warp_kernel", "cell_step_warp"):
         bytes_per = 2 * 3 * rs            # read v, write the changed v (f_chg = 1 here)
         if W["kind"] == "hom" and W["kw"]["eps"] > 0.05:
             bytes_per = 2 * 3 * rs        # upper bound; changed fraction < 1 (dense write-back)
-    elif dom in ("shock_collide_smem", "shock_collide_gmem"):
+    elif dom in ("shock_collide_smem", "shock_collide_gmem", "shock_collide_warp"):
         bytes_per = 2 * 4 * rs            # read (x, v), write (x, v) once
     elif dom == "transport_kernel":
         bytes_per = 3 * rs                # read x, v_x; write x

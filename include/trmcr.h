@@ -210,7 +210,7 @@ int64_t trmcr_launch_count(const trmcr_ctx *ctx);
 enum {
   TRMCR_K_CELL_SMEM = 0, TRMCR_K_CELL_GMEM, TRMCR_K_MOMENTS, TRMCR_K_GHOST_COUNT, TRMCR_K_GHOST_GEN,
   TRMCR_K_TRANSPORT, TRMCR_K_SCAN, TRMCR_K_SHOCK_SMEM, TRMCR_K_SHOCK_GMEM, TRMCR_K_THERMAL,
-  TRMCR_NKERNELS
+  TRMCR_K_CELL_WARP, TRMCR_K_SHOCK_WARP, TRMCR_NKERNELS
 };
 trmcr_status trmcr_set_profiling(trmcr_ctx *ctx, int32_t on);
 /* Same, restricted to the kernel ids whose bit is set in `mask` (fewer events

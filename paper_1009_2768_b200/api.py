@@ -29,7 +29,7 @@ GLOBAL_FIELDS = ["n", "px", "py", "pz", "energy", "nPxx", "proposals", "accepted
 MOMENT_FIELDS = ["n", "rho", "ux", "uy", "uz", "T", "E", "p", "Pxx", "M4", "M4c", "m_max"]
 KERNELS = ["cell_step_smem", "cell_step_gmem", "moments_kernel", "ghost_count", "ghost_gen",
            "transport_kernel", "scan_offsets", "shock_collide_smem", "shock_collide_gmem",
-           "thermal_warp_kernel"]
+           "thermal_warp_kernel", "cell_step_warp", "shock_collide_warp"]
 STATS_DTYPE = np.dtype([(f, "<f8") for f in STAT_FIELDS])
 COLL_DTYPE = np.dtype([("cell", "<i4"), ("attempt", "<i4"), ("level", "<i4"), ("accepted", "<i4"),
                        ("j", "<i8"), ("slot_i", "<i8"), ("slot_k", "<i8")])

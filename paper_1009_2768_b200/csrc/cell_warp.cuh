@@ -1,0 +1,432 @@
+// cell_warp.cuh — the general collision step (A3-A8, trees included) with one
+// WARP per cell: the same computation as process_cell (cell_step.cuh, one CTA
+// per cell) and the same keyed draws, but every phase is warp-synchronous
+// (__syncwarp only, no CTA barrier), so a CTA of 8 warps advances 8 cells
+// independently.  Each warp owns a shared-memory slab (velocities + plan).
+// A cell larger than the slab, or whose tree outgrows it, is left untouched
+// and queued for the CTA kernel (which in turn queues giants for the
+// global-memory kernel).
+#pragma once
+#include "cell_step.cuh"
+
+namespace trmcr {
+
+constexpr int kWarpCellWarps = 8;
+
+// Per-warp scalars (in the warp's slab, lane 0 writes, __syncwarp publishes).
+struct WarpShared {
+  double ux, uy, uz, S0, sigma, p, mu, S_est, E1;
+  double sums[4];
+  int n, m_cur, m_next, d, top, lo, hi, r, flag, done;
+  int64_t rem;
+  int32_t L, Ltot, U, nT, budget, leaf_off;
+  unsigned long long prop, acc, viol;
+};
+
+
+struct WarpSlabLayout {
+  int n_cap, K_cap, L_cap, v_smem;   // v_smem = 0: the cell's velocities live in global memory
+  size_t per_warp;   // bytes of one warp's slab incl. WarpShared (16-byte multiple)
+  size_t off_v, off_ctype, off_crank, off_cslot, off_ints, off_rk, off_u, off_red, off_sh;
+  void build(int n, int K, int L, size_t rs, int v_in_smem) {
+    n_cap = n; K_cap = K; L_cap = L; v_smem = v_in_smem;
+    size_t o = 0;
+    auto al = [&](size_t a) { o = (o + a - 1) / a * a; };
+    off_red = o; o += 8 * sizeof(double);
+    al(16); off_rk = o; o += (size_t)(L + 1) * sizeof(uint4);
+    off_u = o; o += (size_t)kSplitPre * sizeof(double);
+    al(16); off_v = o; if (v_in_smem) o += 3 * (size_t)n * rs;
+    al(16); off_ctype = o; o += (size_t)K * 4;
+    off_crank = o; o += (size_t)K * 4;
+    off_cslot = o; o += (size_t)K * 8;
+    off_ints = o; o += 6 * (size_t)(L + 1) * 4;
+    al(16); off_sh = o; o += sizeof(WarpShared);
+    al(16); per_warp = o;
+  }
+};
+
+template <typename Real>
+__device__ __forceinline__ void bind_warp_slab(CellBuf<Real> &B, unsigned char *base, const WarpSlabLayout &Lay,
+                                               double *&usplit) {
+  B.red = reinterpret_cast<double *>(base + Lay.off_red);
+  B.rk = reinterpret_cast<uint4 *>(base + Lay.off_rk);
+  usplit = reinterpret_cast<double *>(base + Lay.off_u);
+  Real *v = reinterpret_cast<Real *>(base + Lay.off_v);
+  B.vx = v; B.vy = v + Lay.n_cap; B.vz = v + 2 * Lay.n_cap;   // rebound per cell when !v_smem
+  B.ctype = reinterpret_cast<uint32_t *>(base + Lay.off_ctype);
+  B.crank = reinterpret_cast<uint32_t *>(base + Lay.off_crank);
+  B.cslot = reinterpret_cast<uint32_t *>(base + Lay.off_cslot);
+  int32_t *ints = reinterpret_cast<int32_t *>(base + Lay.off_ints);
+  const int Lp = Lay.L_cap + 1;
+  B.Q = ints; B.C = ints + Lp; B.S = ints + 2 * Lp; B.cons = ints + 3 * Lp;
+  B.base = ints + 4 * Lp; B.cnt = ints + 5 * Lp;
+  B.mask = nullptr;
+  B.n_cap = Lay.n_cap; B.K_cap = Lay.K_cap; B.L_cap = Lay.L_cap;
+}
+
+// ---- warp versions of the phases (same definitions as cell_step.cuh) ----
+
+__device__ __forceinline__ void wsplit_extend(const RngKey &K, WarpShared &sh, int m, int32_t *Q, int L_cap,
+                                              const double *usplit) {
+  while (sh.rem > 0 && sh.d < m) {
+    const double y = sh.p * (double)sh.rem;
+    if (y < 0x1p-53) {
+      for (int d = sh.d + 1; d <= m && d <= L_cap; ++d) Q[d] = 0;
+      sh.d = m;
+      break;
+    }
+    sh.d++;
+    int64_t q = ir_split(K, sh.d, y, usplit);
+    if (q > sh.rem) q = sh.rem;
+    if (sh.d <= L_cap) Q[sh.d] = (int32_t)q;
+    else if (q > 0) sh.flag = kOverflow;
+    sh.rem -= q;
+  }
+}
+
+template <typename Real>
+__device__ void wplan_counts(const RngKey &K, CellBuf<Real> &B, WarpShared &sh) {
+  const int lane = threadIdx.x & 31;
+  int top = sh.hi;
+  while (top >= sh.lo && B.Q[top] == 0) top--;
+  for (;;) {
+    if (top < sh.lo || top < 1) {
+      __syncwarp();
+      if (lane == 0) { sh.top = 0; sh.L = 0; }
+      __syncwarp();
+      return;
+    }
+    if (top > B.L_cap) {
+      __syncwarp();
+      if (lane == 0) sh.flag = kOverflow;
+      __syncwarp();
+      return;
+    }
+    for (int d = lane; d <= top; d += 32) B.cons[d] = 0;
+    __syncwarp();
+    int Sacc = 0;
+    for (int d = top; d >= 1; --d) {
+      const int Qd = (d >= sh.lo) ? B.Q[d] : 0;
+      const int Cd = (Qd + B.cons[d] + 1) >> 1;
+      if ((int64_t)Sacc + Cd > B.K_cap) {
+        __syncwarp();
+        if (lane == 0) sh.flag = kOverflow;
+        __syncwarp();
+        return;
+      }
+      __syncwarp();
+      if (lane == 0) { B.C[d] = Cd; B.S[d] = Sacc; }
+      for (int j = lane; j < Cd; j += 32) {
+        const uint32_t w = K(kType, sh.r, d, j).x;
+        const uint32_t a = __umulhi(w, (uint32_t)d);
+        B.ctype[Sacc + j] = a;
+        atomicAdd(&B.cons[a], 1);
+        atomicAdd(&B.cons[d - 1 - a], 1);
+      }
+      Sacc += Cd;
+      __syncwarp();
+    }
+    if (B.cons[0] <= sh.budget) {
+      __syncwarp();
+      if (lane == 0) { sh.L = B.cons[0]; sh.top = top; }
+      __syncwarp();
+      return;
+    }
+    int t = top - 1;                       // guard: drop the top quota level
+    while (t >= sh.lo && B.Q[t] == 0) t--;
+    top = t;
+    __syncwarp();
+  }
+}
+
+template <typename Real>
+__device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real> &B, WarpShared &sh,
+                              const Perm &pi0, Real sigma, trmcr_coll_rec *log, unsigned long long *log_count,
+                              int64_t log_cap) {
+  const int lane = threadIdx.x & 31;
+  const int top = sh.top;
+  if (top < 1) return;
+  for (int d = lane; d <= top; d += 32) {
+    B.base[d] = 0;
+    B.cnt[d] = 0;
+    if (d >= 1) B.rk[d] = K(kPerm, sh.r, d, 0);
+  }
+  __syncwarp();
+  unsigned acc = 0, viol = 0;
+  unsigned long long prop = 0;
+  const int r = sh.r, leaf_off = sh.leaf_off, n = sh.n;
+  int pd = 0;
+  for (int d = 1; d <= top; ++d) {
+    const int Cd = B.C[d], Sd = B.S[d];
+    if (Cd == 0) continue;
+    if (pd > 0) {                          // fold level pd into base[], clear its histogram
+      for (int p = lane; p < pd; p += 32) B.cons[p] = B.base[p] + B.cnt[p] + B.cnt[pd - 1 - p];
+      __syncwarp();
+      for (int p = lane; p < pd; p += 32) { B.base[p] = B.cons[p]; B.cnt[p] = 0; }
+      __syncwarp();
+    }
+    for (int j0 = 0; j0 < Cd; j0 += 32) {  // stable in-level ranks per type
+      const int j = j0 + lane;
+      const bool valid = j < Cd;
+      const uint32_t a = valid ? B.ctype[Sd + j] : 0xFFFFFFFFu;
+      const unsigned peers = __match_any_sync(0xffffffffu, a);
+      const unsigned lt = (1u << lane) - 1u;
+      int c0 = 0;
+      if (valid) c0 = B.cnt[a];
+      __syncwarp();
+      if (valid) {
+        B.crank[Sd + j] = (uint32_t)(c0 + __popc(peers & lt));
+        if ((peers & lt) == 0u) B.cnt[a] = c0 + __popc(peers);
+      }
+      __syncwarp();
+    }
+    pd = d;
+    for (int j = lane; j < Cd; j += 32) {
+      const uint32_t a = B.ctype[Sd + j], b = (uint32_t)d - 1u - a;
+      const uint32_t rank = B.crank[Sd + j];
+      const uint32_t t[2] = {(uint32_t)B.base[a] + rank, (uint32_t)(B.base[b] + B.cnt[b]) + rank};
+      const uint32_t pool[2] = {a, b};
+      uint32_t slot[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        if (pool[s] == 0) {
+          slot[s] = pi0((uint32_t)leaf_off + t[s]);
+        } else {
+          Perm pp;
+          pp.init(B.rk[pool[s]], 2u * (uint32_t)B.C[pool[s]]);
+          const uint32_t o = pp(t[s]);
+          slot[s] = o == 0xFFFFFFFFu ? o : B.cslot[2u * (uint32_t)B.S[pool[s]] + o];
+        }
+        if (slot[s] >= (uint32_t)n) { atomicOr(P.err, kErrInternal); slot[s] = 0; }
+      }
+      B.cslot[2 * (Sd + j)] = slot[0];
+      B.cslot[2 * (Sd + j) + 1] = slot[1];
+      const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, slot[0], slot[1], viol);
+      acc += ok;
+      if (P.log_on) {
+        const unsigned long long at = atomicAdd(log_count, 1ull);
+        if ((int64_t)at < log_cap) {
+          trmcr_coll_rec rec;
+          rec.cell = (int32_t)K.cell; rec.attempt = r; rec.level = d; rec.accepted = ok;
+          rec.j = j; rec.slot_i = slot[0]; rec.slot_k = slot[1];
+          log[at] = rec;
+        }
+      }
+    }
+    prop += (unsigned long long)Cd;
+    __syncwarp();
+  }
+  acc = __reduce_add_sync(0xffffffffu, acc);
+  viol = __reduce_add_sync(0xffffffffu, viol);
+  if (lane == 0) { sh.prop += prop; sh.acc += acc; sh.viol += viol; }
+  __syncwarp();
+}
+
+template <typename Real>
+__device__ void wrad_estimate(const StepParams &P, CellBuf<Real> &B, WarpShared &sh, const Perm &pi0) {
+  const int lane = threadIdx.x & 31, n = sh.n, nT = sh.nT;
+  const bool pxx = P.indicator == TRMCR_IND_PXX;
+  const double ux = sh.ux;
+  double v0 = 0, v1 = 0, tx = 0, ty = 0, tz = 0, t2 = 0;
+  for (int i = lane; i < n; i += 32) {
+    const double x = B.vx[i], y = B.vy[i], z = B.vz[i];
+    if (pxx) { const double dx = x - ux; v0 += dx * dx; }
+    else { const double v2 = x * x + y * y + z * z; v0 += v2 * v2; }
+  }
+  for (int q = lane; q < nT; q += 32) {
+    const uint32_t s = pi0((uint32_t)(sh.Ltot + q));
+    if (s >= (uint32_t)n) { atomicOr(P.err, kErrInternal); continue; }
+    const double x = B.vx[s], y = B.vy[s], z = B.vz[s];
+    if (pxx) { const double dx = x - ux; v1 += dx * dx; }
+    else { const double v2 = x * x + y * y + z * z; v1 += v2 * v2; }
+    tx += x; ty += y; tz += z; t2 += x * x + y * y + z * z;
+  }
+  v0 = warp_sum(v0); v1 = warp_sum(v1); tx = warp_sum(tx); ty = warp_sum(ty); tz = warp_sum(tz);
+  t2 = warp_sum(t2);
+  if (lane == 0) {
+    double s = v0 - v1;
+    if (nT > 0) {
+      tx /= nT; ty /= nT; tz /= nT;
+      const double T = fmax(0.0, t2 / nT - (tx * tx + ty * ty + tz * tz)) / 3.0;
+      if (pxx) {
+        s += (double)nT * (T + (tx - ux) * (tx - ux));
+      } else {
+        const double u2 = tx * tx + ty * ty + tz * tz;
+        s += (double)nT * (u2 * u2 + 10.0 * u2 * T + 15.0 * T * T);
+      }
+    }
+    sh.S_est = s / n;
+    sh.E1 = sh.S0 != 0.0 ? fabs(sh.S_est - sh.S0) / fabs(sh.S0) : (sh.S_est == 0.0 ? 0.0 : INFINITY);
+  }
+  __syncwarp();
+}
+
+template <typename Real>
+__device__ void wmaxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> &B, WarpShared &sh,
+                            const Perm &pi0, double ec_all) {
+  const int lane = threadIdx.x & 31, nT = sh.nT;
+  if (nT < 2) return;
+  const bool full = (nT == sh.n);
+  double ux, uy, uz;
+  if (full) {
+    ux = sh.ux; uy = sh.uy; uz = sh.uz;
+  } else {
+    double a = 0, b = 0, c = 0;
+    for (int q = lane; q < nT; q += 32) {
+      const uint32_t s = pi0((uint32_t)(sh.Ltot + q));
+      if (s >= (uint32_t)sh.n) { atomicOr(P.err, kErrInternal); continue; }
+      a += (double)B.vx[s]; b += (double)B.vy[s]; c += (double)B.vz[s];
+    }
+    ux = warp_sum(a) / nT; uy = warp_sum(b) / nT; uz = warp_sum(c) / nT;
+  }
+  double g0s = 0, g1s = 0, g2s = 0, gg = 0, ec = 0;
+  for (int q = lane; q < nT; q += 32) {
+    const uint32_t s = full ? (uint32_t)q : pi0((uint32_t)(sh.Ltot + q));
+    if (s >= (uint32_t)sh.n) continue;
+    if (!full) {
+      const double dx = B.vx[s] - ux, dy = B.vy[s] - uy, dz = B.vz[s] - uz;
+      ec += dx * dx + dy * dy + dz * dz;
+    }
+    Real g0, g1, g2;
+    gauss3<Real>(K, s, g0, g1, g2);
+    B.vx[s] = g0; B.vy[s] = g1; B.vz[s] = g2;
+    g0s += g0; g1s += g1; g2s += g2;
+    gg += (double)g0 * g0 + (double)g1 * g1 + (double)g2 * g2;
+  }
+  g0s = warp_sum(g0s); g1s = warp_sum(g1s); g2s = warp_sum(g2s); gg = warp_sum(gg);
+  ec = full ? ec_all : warp_sum(ec);
+  const double gx = g0s / nT, gy = g1s / nT, gz = g2s / nT;
+  const double D = gg - nT * (gx * gx + gy * gy + gz * gz);
+  const double sc = (D > 0.0 && ec > 0.0) ? sqrt(ec / D) : 0.0;
+  const Real rsc = (Real)sc, rgx = (Real)gx, rgy = (Real)gy, rgz = (Real)gz;
+  const Real rux = (Real)ux, ruy = (Real)uy, ruz = (Real)uz;
+  __syncwarp();
+  for (int q = lane; q < nT; q += 32) {
+    const uint32_t s = full ? (uint32_t)q : pi0((uint32_t)(sh.Ltot + q));
+    if (s >= (uint32_t)sh.n) continue;
+    B.vx[s] = rux + rsc * (B.vx[s] - rgx);
+    B.vy[s] = ruy + rsc * (B.vy[s] - rgy);
+    B.vz[s] = ruz + rsc * (B.vz[s] - rgz);
+  }
+  __syncwarp();
+}
+
+// The cell (already staged in B.v*, n particles, sums of the staging pass in
+// sx, sy, sz) through A3-A8.  Returns kOk or kOverflow (nothing written then
+// except B's scratch).  Writes m_state, stats, and (kStore) the velocities.
+template <typename Real>
+__device__ int process_cell_warp(const StepParams &P, CellBuf<Real> &B, WarpShared &sh, double *usplit,
+                                 double sx, double sy, double sz, Real *out_x, Real *out_y, Real *out_z, int n,
+                                 uint32_t gcell, int32_t *m_state, double *stats_row, trmcr_coll_rec *log,
+                                 unsigned long long *log_count, int64_t log_cap) {
+  const int lane = threadIdx.x & 31;
+  const RngKey K{P.k0, P.k1, gcell, P.step};
+  const int m0 = P.adaptive ? *m_state : P.m_fixed;
+  // ---- A3: moments ----
+  const double Sx = warp_sum(sx), Sy = warp_sum(sy), Sz = warp_sum(sz);
+  const double ux = Sx / n, uy = Sy / n, uz = Sz / n;
+  double c0 = 0, c1 = 0, c2 = 0, dv2 = 0;
+  for (int i = lane; i < n; i += 32) {
+    const double x = B.vx[i], y = B.vy[i], z = B.vz[i];
+    const double dx = x - ux, dy = y - uy, dz = z - uz;
+    const double r2 = dx * dx + dy * dy + dz * dz;
+    dv2 = fmax(dv2, r2);
+    c0 += dx * dx;
+    const double v2 = x * x + y * y + z * z;
+    c1 += v2 * v2;
+    c2 += r2;
+  }
+  for (int d = lane; d < kSplitPre; d += 32) {   // split uniforms, in parallel
+    const uint4 w = K(kSplit, 0, (uint32_t)d, 0);
+    usplit[d] = u53(w.x, w.y);
+  }
+  c0 = warp_sum(c0); c1 = warp_sum(c1); c2 = warp_sum(c2); dv2 = warp_max(dv2);
+  __syncwarp();
+  if (lane == 0) {
+    sh.n = n; sh.ux = ux; sh.uy = uy; sh.uz = uz;
+    sh.sums[0] = Sx; sh.sums[1] = Sy; sh.sums[2] = Sz; sh.sums[3] = c2 + n * (ux * ux + uy * uy + uz * uz);
+    sh.S0 = (P.indicator == TRMCR_IND_PXX ? c0 : c1) / n;
+    const double rho_c = P.shock ? n * P.w_over_dx : 1.0;
+    if (P.model == TRMCR_HARD_SPHERE) { sh.sigma = 2.0 * sqrt(dv2); sh.mu = rho_c * sh.sigma; }
+    else { sh.sigma = 0.0; sh.mu = rho_c; }
+    sh.p = exp(-(sh.mu * P.dt / P.eps));
+    sh.m_cur = m0; sh.flag = kOk;
+    sh.prop = 0; sh.acc = 0; sh.viol = 0;
+    // ---- A4: split ----
+    const int64_t N0 = ir_split(K, 0, sh.p * (double)n, usplit);
+    B.Q[0] = (int32_t)N0;
+    sh.rem = n - N0;
+    sh.d = 0;
+    wsplit_extend(K, sh, m0, B.Q, B.L_cap, usplit);
+    sh.r = 0; sh.lo = 1; sh.hi = sh.d < B.L_cap ? sh.d : B.L_cap;
+    sh.budget = n; sh.leaf_off = 0;
+  }
+  __syncwarp();
+  if (sh.flag != kOk) return sh.flag;
+  Perm pi0;
+  pi0.init(K(kPerm, 0, 0, 0), (uint32_t)n);
+  const Real sigma = (Real)sh.sigma;
+  // ---- A5/A6: attempt 0 ----
+  wplan_counts<Real>(K, B, sh);
+  if (sh.flag != kOk) return sh.flag;
+  wplan_execute<Real>(P, K, B, sh, pi0, sigma, log, log_count, log_cap);
+  if (lane == 0) {
+    sh.Ltot = sh.L;
+    sh.U = B.Q[0] < n - sh.Ltot ? B.Q[0] : n - sh.Ltot;
+    sh.nT = n - sh.Ltot - sh.U;
+    sh.m_next = sh.m_cur;
+    sh.S_est = sh.S0; sh.E1 = 0.0;
+  }
+  __syncwarp();
+  // ---- A7: TRMC-RAD ----
+  if (P.adaptive) {
+    for (;;) {
+      wrad_estimate<Real>(P, B, sh, pi0);
+      if (lane == 0) {
+        sh.done = 1;
+        if (sh.E1 > P.delta2 && sh.m_cur < P.m_cap) {
+          const int m_new = 2 * sh.m_cur < P.m_cap ? 2 * sh.m_cur : P.m_cap;
+          wsplit_extend(K, sh, m_new, B.Q, B.L_cap, usplit);
+          sh.r += 1;
+          sh.lo = sh.m_cur + 1;
+          sh.hi = sh.d < B.L_cap ? sh.d : B.L_cap;
+          sh.budget = sh.nT;
+          sh.leaf_off = sh.Ltot;
+          sh.m_cur = m_new;
+          sh.done = 0;
+        }
+      }
+      __syncwarp();
+      if (sh.flag != kOk) return sh.flag;
+      if (sh.done) break;
+      wplan_counts<Real>(K, B, sh);
+      if (sh.flag != kOk) return sh.flag;
+      wplan_execute<Real>(P, K, B, sh, pi0, sigma, log, log_count, log_cap);
+      if (lane == 0) { sh.Ltot += sh.L; sh.nT -= sh.L; }
+      __syncwarp();
+    }
+    if (lane == 0) sh.m_next = (sh.E1 < P.delta1) ? (sh.m_cur / 2 > 1 ? sh.m_cur / 2 : 1) : sh.m_cur;
+    __syncwarp();
+  }
+  // ---- A8 ----
+  wmaxwellian<Real>(P, K, B, sh, pi0, c2);
+  if (out_x != B.vx)
+    for (int i = lane; i < n; i += 32) { out_x[i] = B.vx[i]; out_y[i] = B.vy[i]; out_z[i] = B.vz[i]; }
+  if (lane == 0) {
+    if (P.adaptive) *m_state = sh.m_next;
+    double *s = stats_row;
+    s[TRMCR_ST_N] = n; s[TRMCR_ST_P] = sh.p; s[TRMCR_ST_MU] = sh.mu; s[TRMCR_ST_SIGMA] = sh.sigma;
+    s[TRMCR_ST_S0] = sh.S0; s[TRMCR_ST_SEST] = sh.S_est; s[TRMCR_ST_E1] = sh.E1;
+    s[TRMCR_ST_MUSED] = sh.m_cur; s[TRMCR_ST_MNEXT] = sh.m_next; s[TRMCR_ST_DEPTH] = sh.d;
+    s[TRMCR_ST_ATTEMPTS] = sh.r + 1; s[TRMCR_ST_LEAVES] = sh.Ltot; s[TRMCR_ST_UNTOUCHED] = sh.U;
+    s[TRMCR_ST_THERMALISED] = sh.nT; s[TRMCR_ST_PROPOSALS] = (double)sh.prop;
+    s[TRMCR_ST_ACCEPTED] = (double)sh.acc; s[TRMCR_ST_VIOLATIONS] = (double)sh.viol;
+    s[TRMCR_ST_MAXW] = sh.nT >= 2 ? sh.nT : 0;
+    s[TRMCR_ST_PX] = sh.sums[0]; s[TRMCR_ST_PY] = sh.sums[1]; s[TRMCR_ST_PZ] = sh.sums[2];
+    s[TRMCR_ST_ENERGY] = sh.sums[3];
+  }
+  __syncwarp();
+  return kOk;
+}
+
+}  // namespace trmcr

@@ -8,6 +8,7 @@
 
 #include "../../include/trmcr.h"
 #include "cell_step.cuh"
+#include "cell_warp.cuh"
 
 namespace trmcr {
 
@@ -137,6 +138,9 @@ struct trmcr_ctx {
   int *d_ovf_count = nullptr, *d_ovf_list = nullptr, *d_err = nullptr;
   // thermal fast path (thermal.cuh): cells it defers go to the general kernel
   int *d_defer_count = nullptr, *d_defer_list = nullptr;
+  int *d_defer2_count = nullptr, *d_defer2_list = nullptr;   // warp kernel -> CTA kernel
+  trmcr::WarpSlabLayout wlay{};
+  int warp_smem = 0, warp_grid = 1, warp_wpc = 1;
   int *h_defer = nullptr;          // pinned copy of the last defer count
   double *d_gm_partial = nullptr;  // global-moments partial sums
   unsigned *d_gm_done = nullptr;

@@ -17,6 +17,7 @@
 //                             to the other buffer.
 #pragma once
 #include "ctx.cuh"
+#include "cell_warp.cuh"
 
 namespace trmcr {
 
@@ -443,16 +444,140 @@ __device__ int gather_cell(const ShockDev &S, const GatherSrc &G, int c, Real *b
   return running;
 }
 
+// Warp-level stable gather of destination cell c (same canonical order as
+// gather_cell): each lane tests 8 consecutive source entries per round, a warp
+// scan gives the positions.  Velocities -> (bx,by,bz) (the warp's slab),
+// positions -> ox (global).  Returns the count; sums of the velocities in s*.
+template <typename Real>
+__device__ int gather_cell_warp(const ShockDev &S, const GatherSrc &G, int c, Real *bx, Real *by, Real *bz,
+                                Real *ox, int cap, double &sxo, double &syo, double &szo) {
+  constexpr int R = 8;
+  const int lane = threadIdx.x & 31;
+  const int W = *G.W;
+  int running = 0;
+  double sx = 0, sy = 0, sz = 0;
+  for (int seg = 0; seg < 5; ++seg) {
+    int64_t lo = 0, hi = 0;
+    const Real *px, *pvx, *pvy, *pvz;
+    const int32_t *pd;
+    int match = c;
+    if (seg == 2) {
+      const int a = max(c - W, 0), b = min(c + W, S.C - 1);
+      lo = G.off_old[a]; hi = G.off_old[b + 1];
+      px = (const Real *)G.x; pvx = (const Real *)G.vx; pvy = (const Real *)G.vy; pvz = (const Real *)G.vz;
+      pd = G.dest;
+    } else if (seg == 1 || seg == 3) {
+      const int side = seg == 1 ? 0 : 1;
+      const bool in = side == 0 ? (c - W <= -1) : (c + W >= S.C);
+      if (!in || G.recv[side] == nullptr) continue;
+      const XBuf<Real> X = XBuf<Real>::bind(const_cast<void *>(G.recv[side]), G.xcap);
+      hi = min(*X.count, G.xcap);
+      px = X.x; pvx = X.vx; pvy = X.vy; pvz = X.vz; pd = X.dest;
+      match = c + G.cbase;
+    } else {
+      const int side = seg == 0 ? 0 : 1;
+      const bool in = side == 0 ? (c - W <= -1) : (c + W >= S.C);
+      if (!in) continue;
+      hi = G.ng[side];
+      px = (const Real *)G.gx[side]; pvx = (const Real *)G.gvx[side];
+      pvy = (const Real *)G.gvy[side]; pvz = (const Real *)G.gvz[side];
+      pd = G.gdest[side];
+    }
+    for (int64_t b0 = lo; b0 < hi; b0 += 32 * R) {
+      const int64_t i0 = b0 + (int64_t)lane * R;
+      unsigned bits = 0;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int64_t i = i0 + k;
+        if (i < hi && pd[i] == match) bits |= 1u << k;
+      }
+      const int mine = __popc(bits);
+      int incl = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      const int pos = running + incl - mine;
+      Real tx[R], tvx[R], tvy[R], tvz[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        if ((bits >> k) & 1u) {
+          const int64_t i = i0 + k;
+          tx[k] = px[i]; tvx[k] = pvx[i]; tvy[k] = pvy[i]; tvz[k] = pvz[i];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        if ((bits >> k) & 1u) {
+          const int q = pos + __popc(bits & ((1u << k) - 1u));
+          if (q < cap) { bx[q] = tvx[k]; by[q] = tvy[k]; bz[q] = tvz[k]; }
+          ox[q] = tx[k];
+          sx += tvx[k]; sy += tvy[k]; sz += tvz[k];
+        }
+      }
+      running += tot;
+    }
+  }
+  sxo = sx; syo = sy; szo = sz;
+  __syncwarp();
+  return running;
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(kWarpCellWarps * 32)
+shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
+                   Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, int *defer_count,
+                   int *defer_list, QueueArgs Q) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char *slab = smem + (size_t)warp * Lay.per_warp;
+  WarpShared &sh = *reinterpret_cast<WarpShared *>(slab + Lay.off_sh);
+  CellBuf<Real> B;
+  double *usplit;
+  bind_warp_slab(B, slab, Lay, usplit);
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  for (int c = blockIdx.x * (blockDim.x >> 5) + warp; c < S.C; c += nw) {
+    const int64_t base = off_new[c];
+    const int n = (int)(off_new[c + 1] - base);
+    int rc = kOverflow;
+    if (n <= Lay.n_cap) {
+      double sx, sy, sz;
+      if (!Lay.v_smem) { B.vx = ovx + base; B.vy = ovy + base; B.vz = ovz + base; }   // work in place (L1)
+      gather_cell_warp<Real>(S, G, c, B.vx, B.vy, B.vz, ox + base, Lay.n_cap, sx, sy, sz);
+      if (n == 0) {
+        if (lane == 0) {
+          double *s = stats + (size_t)c * TRMCR_NSTATS;
+          for (int k = 0; k < TRMCR_NSTATS; ++k) s[k] = 0.0;
+          const int m = P.adaptive ? m_state[c] : P.m_fixed;
+          s[TRMCR_ST_MUSED] = m; s[TRMCR_ST_MNEXT] = m;
+        }
+        rc = kOk;
+      } else {
+        rc = process_cell_warp<Real>(P, B, sh, usplit, sx, sy, sz, ovx + base, ovy + base, ovz + base, n,
+                                     P.cell_base + (uint32_t)c, m_state + c, stats + (size_t)c * TRMCR_NSTATS,
+                                     Q.log, Q.log_count, Q.log_cap);
+      }
+    }
+    if (rc != kOk && lane == 0) defer_list[atomicAdd(defer_count, 1)] = c;
+    __syncwarp();
+  }
+}
+
 template <typename Real, int THREADS>
 __global__ void __launch_bounds__(THREADS, 768 / THREADS)
 shock_collide_smem(StepParams P, SmemLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
-                   Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, QueueArgs Q) {
+                   Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats,
+                   const int *list_count, const int *list, QueueArgs Q) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CellShared sh;
   __shared__ int wcnt[32];
-  const int c = blockIdx.x;
+  const int count = list ? *list_count : S.C;
   CellBuf<Real> B;
   bind_smem(B, smem, Lay);
+  for (int k = blockIdx.x; k < count; k += gridDim.x) {
+  const int c = list ? list[k] : k;
   const int64_t base = off_new[c];
   const int n = (int)(off_new[c + 1] - base);
   int rc = kOverflow;
@@ -466,8 +591,10 @@ shock_collide_smem(StepParams P, SmemLayout Lay, ShockDev S, GatherSrc G, const 
                                          stats + (size_t)c * TRMCR_NSTATS, Q.log, Q.log_count, Q.log_cap);
   }
   if (rc != kOk && threadIdx.x == 0) {
-    const int k = atomicAdd(Q.ovf_count, 1);
-    Q.ovf_list[k] = c;
+    const int j = atomicAdd(Q.ovf_count, 1);
+    Q.ovf_list[j] = c;
+  }
+  __syncthreads();
   }
 }
 
@@ -644,11 +771,21 @@ trmcr_status shock_finish(trmcr_ctx *c) {
   QueueArgs Q{c->d_ovf_count, c->d_ovf_list, c->d_err, c->d_log, c->d_log_count, c->log_cap};
   c->P.step = c->step;
   Real *ox = (Real *)c->x[nxt], *ovx = (Real *)c->v[nxt][0], *ovy = (Real *)c->v[nxt][1], *ovz = (Real *)c->v[nxt][2];
+  const bool use_warp = c->wlay.n_cap > 0;
+  if (use_warp) {
+    CUDA_TRY(c, cudaMemsetAsync(c->d_defer_count, 0, sizeof(int), c->stream));
+    prof_begin(c, TRMCR_K_SHOCK_WARP);
+    shock_collide_warp<Real><<<c->warp_grid, c->warp_wpc * 32, c->warp_smem, c->stream>>>(
+        c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
+        c->d_defer_list, Q);
+    if (auto e = check_launch(c, "shock_collide_warp", TRMCR_K_SHOCK_WARP)) return e;
+  }
   prof_begin(c, TRMCR_K_SHOCK_SMEM);
   auto kern = c->smem_threads == 64 ? shock_collide_smem<Real, 64>
               : (c->smem_threads == 128 ? shock_collide_smem<Real, 128> : shock_collide_smem<Real, 256>);
-  kern<<<s.C, c->smem_threads, c->lay.total, c->stream>>>(
-      c->P, c->lay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, Q);
+  kern<<<use_warp ? c->smem_grid : s.C, c->smem_threads, c->lay.total, c->stream>>>(
+      c->P, c->lay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats,
+      use_warp ? c->d_defer_count : nullptr, use_warp ? c->d_defer_list : nullptr, Q);
   if (auto e = check_launch(c, "shock_collide_smem", TRMCR_K_SHOCK_SMEM)) return e;
   prof_begin(c, TRMCR_K_SHOCK_GMEM);
   shock_collide_gmem<Real><<<c->G, c->gmem_threads, 0, c->stream>>>(c->P, c->gs, d, G, s.d_off[nxt], ox, ovx, ovy,

@@ -77,6 +77,44 @@ cell_step_gmem(StepParams P, GmemScratch G, const int64_t *__restrict__ offsets,
   }
 }
 
+// General cells, one warp each (cell_warp.cuh), over the thermal kernel's
+// defer list (or every cell); cells that do not fit go to list2 (CTA kernel).
+template <typename Real>
+__global__ void __launch_bounds__(kWarpCellWarps * 32)
+cell_step_warp(StepParams P, WarpSlabLayout Lay, const int64_t *__restrict__ offsets, int ncells,
+               const int *list_count, const int *list, Real *vx, Real *vy, Real *vz, int32_t *m_state,
+               double *stats, int *list2_count, int *list2, QueueArgs Q) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char *slab = smem + (size_t)warp * Lay.per_warp;
+  WarpShared &sh = *reinterpret_cast<WarpShared *>(slab + Lay.off_sh);
+  CellBuf<Real> B;
+  double *usplit;
+  bind_warp_slab(B, slab, Lay, usplit);
+  const int count = list ? *list_count : ncells;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  for (int k = blockIdx.x * (blockDim.x >> 5) + warp; k < count; k += nw) {
+    const int c = list ? list[k] : k;
+    const int64_t off = offsets[c];
+    const int n = (int)(offsets[c + 1] - off);
+    int rc = kOverflow;
+    if (n > 0 && n <= Lay.n_cap) {
+      double sx = 0, sy = 0, sz = 0;
+      for (int i = lane; i < n; i += 32) {
+        const Real a = vx[off + i], b = vy[off + i], d = vz[off + i];
+        B.vx[i] = a; B.vy[i] = b; B.vz[i] = d;
+        sx += a; sy += b; sz += d;
+      }
+      __syncwarp();
+      rc = process_cell_warp<Real>(P, B, sh, usplit, sx, sy, sz, vx + off, vy + off, vz + off, n,
+                                   P.cell_base + (uint32_t)c, m_state + c, stats + (size_t)c * TRMCR_NSTATS,
+                                   Q.log, Q.log_count, Q.log_cap);
+    }
+    if (rc != kOk && lane == 0) list2[atomicAdd(list2_count, 1)] = c;
+    __syncwarp();
+  }
+}
+
 // A9: per-cell moments, one CTA per cell (two passes).
 template <typename Real>
 __global__ void __launch_bounds__(256)
@@ -193,12 +231,23 @@ trmcr_status launch_collide(trmcr_ctx *c) {
       if (auto s = check_launch(c, "thermal_warp_kernel", TRMCR_K_THERMAL)) return s;
     }
     const bool idle = fast && c->fast_ok && c->last_defer == 0 && c->last_ovf == 0;
+    const bool use_warp = c->wlay.n_cap > 0;
+    const int *l1c = fast ? c->d_defer_count : nullptr, *l1 = fast ? c->d_defer_list : nullptr;
+    if (use_warp) {
+      CUDA_TRY(c, cudaMemsetAsync(c->d_defer2_count, 0, sizeof(int), c->stream));
+      prof_begin(c, TRMCR_K_CELL_WARP);
+      cell_step_warp<Real><<<idle ? 1 : c->warp_grid, c->warp_wpc * 32, c->warp_smem, c->stream>>>(
+          c->P, c->wlay, c->d_offsets, c->ncells, l1c, l1, vx, vy, vz, c->d_mstate, c->d_stats,
+          c->d_defer2_count, c->d_defer2_list, Q);
+      if (auto s = check_launch(c, "cell_step_warp", TRMCR_K_CELL_WARP)) return s;
+      l1c = c->d_defer2_count;
+      l1 = c->d_defer2_list;
+    }
     prof_begin(c, TRMCR_K_CELL_SMEM);
     auto kern = c->smem_threads == 64 ? cell_step_smem<Real, 64>
                 : (c->smem_threads == 128 ? cell_step_smem<Real, 128> : cell_step_smem<Real, 256>);
     kern<<<idle ? 1 : c->smem_grid, c->smem_threads, c->lay.total, c->stream>>>(
-        c->P, c->lay, c->d_offsets, c->ncells, fast ? c->d_defer_count : nullptr,
-        fast ? c->d_defer_list : nullptr, vx, vy, vz, c->d_mstate, c->d_stats, Q);
+        c->P, c->lay, c->d_offsets, c->ncells, l1c, l1, vx, vy, vz, c->d_mstate, c->d_stats, Q);
     if (auto s = check_launch(c, "cell_step_smem", TRMCR_K_CELL_SMEM)) return s;
     prof_begin(c, TRMCR_K_CELL_GMEM);
     cell_step_gmem<Real><<<idle ? 1 : c->G, c->gmem_threads, 0, c->stream>>>(c->P, c->gs, c->d_offsets, vx, vy, vz,
@@ -221,6 +270,15 @@ trmcr_status launch_moments(trmcr_ctx *c) {
       c->d_offsets, c->ncells, (const Real *)c->v[c->cur][0], (const Real *)c->v[c->cur][1],
       (const Real *)c->v[c->cur][2], c->d_mstate, c->P.shock, c->P.w_over_dx, c->d_moments);
   return check_launch(c, "moments_kernel", TRMCR_K_MOMENTS);
+}
+
+// Allow the device maximum of dynamic shared memory (minus the kernel's static
+// shared memory): the attribute is per function and process-wide.
+cudaError_t allow_max_dyn_smem(const void *f, int smem_optin) {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, f);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin - (int)a.sharedSizeBytes);
 }
 
 trmcr_status do_step(trmcr_ctx *c) {
@@ -410,7 +468,8 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
 
       dalloc(c, &c->d_ovf_list, sizeof(int) * std::max(c->ncells, 1)) ||
       dalloc(c, &c->d_err, sizeof(int)) || dalloc(c, &c->d_log_count, sizeof(unsigned long long)) ||
-      dalloc(c, &c->d_defer_count, 2 * sizeof(int)) || dalloc(c, &c->d_gm_partial, sizeof(double) * 10 * kGmBlocks) ||
+      dalloc(c, &c->d_defer_count, 2 * sizeof(int)) || dalloc(c, &c->d_defer2_count, sizeof(int)) ||
+      dalloc(c, &c->d_defer2_list, sizeof(int) * std::max(c->ncells, 1)) || dalloc(c, &c->d_gm_partial, sizeof(double) * 10 * kGmBlocks) ||
       dalloc(c, &c->d_gm_done, sizeof(unsigned)) || dalloc(c, &c->d_defer_list, sizeof(int) * std::max(c->ncells, 1)))
     return bail(TRMCR_ENOMEM);
   c->d_ovf_count = c->d_defer_count + 1;
@@ -494,10 +553,13 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
         (const void *)cell_step_smem<double, 64>, (const void *)cell_step_smem<double, 128>,
         (const void *)cell_step_smem<double, 256>, (const void *)cell_step_smem<float, 64>,
         (const void *)cell_step_smem<float, 128>, (const void *)cell_step_smem<float, 256>};
+    // the attribute is per function (process-wide): set the device maximum so
+    // that contexts with different layouts can coexist
     for (const void *f : fns) {
-      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+      cudaError_t e = allow_max_dyn_smem(f, smem_max);
       if (e != cudaSuccess) ea = e;
     }
+    (void)dyn;
   }
   if (ea != cudaSuccess) { fail(c, TRMCR_ECUDA, "cudaFuncSetAttribute failed"); return bail(TRMCR_ECUDA); }
   {
@@ -505,8 +567,8 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->dev);
     const int tsm = kThermalWarps * 3 * (c->dtype == TRMCR_F64 ? 512 * 8 : 1024 * 4);
     cudaError_t e2 = c->dtype == TRMCR_F64
-        ? cudaFuncSetAttribute(thermal_warp_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm)
-        : cudaFuncSetAttribute(thermal_warp_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        ? allow_max_dyn_smem((const void *)thermal_warp_kernel<double>, smem_max)
+        : allow_max_dyn_smem((const void *)thermal_warp_kernel<float>, smem_max);
     if (e2 != cudaSuccess) { fail(c, TRMCR_ECUDA, "cudaFuncSetAttribute(thermal) failed"); return bail(TRMCR_ECUDA); }
     int occ_t = 1, occ_s = 1;
     if (c->dtype == TRMCR_F64) {
@@ -521,6 +583,42 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
     c->fast_grid = std::max(1, std::min((c->ncells + kThermalWarps - 1) / kThermalWarps, nsm * std::max(occ_t, 1)));
     c->smem_grid = std::max(1, std::min(c->ncells, nsm * std::max(occ_s, 1)));
     if (c->geometry == TRMCR_SHOCK_1D) c->fast_ok = 0;
+  }
+
+  // ---- warp-per-cell general kernel slab (0 disables) ----
+  {
+    const char *wenv = getenv("TRMCR_WARP_PATH");
+    const bool want = !(wenv && atoi(wenv) == 0);
+    int wn = c->geometry == TRMCR_SHOCK_1D ? std::max(64, (2 * max_cell + 31) / 32 * 32)
+                                           : std::max(32, (max_cell + 31) / 32 * 32);
+    const int wK = c->geometry == TRMCR_SHOCK_1D ? std::max(256, wn / 4) : std::max(256, wn / 2);
+    // shock: velocities are gathered into the output buffer and processed in
+    // place (a deferred cell is re-gathered); homogeneous: staged in the slab
+    // (in place would corrupt the input of a deferred cell)
+    const int v_smem = c->geometry == TRMCR_SHOCK_1D ? 0 : 1;
+    if (!v_smem) wn = std::max(wn, 4096);
+    c->wlay.build(wn, wK, 64, c->rs, v_smem);
+    const size_t slab = c->wlay.per_warp;
+    c->warp_wpc = (int)std::max<size_t>(1, std::min<size_t>(kWarpCellWarps, (64 * 1024) / slab));
+    c->warp_smem = (int)(slab * c->warp_wpc);
+    if (!want || c->warp_smem > smem_max - 2048) {
+      c->wlay.n_cap = 0;     // disabled: the CTA kernel takes every general cell
+    } else {
+      const void *fns[] = {(const void *)cell_step_warp<float>, (const void *)cell_step_warp<double>,
+                           (const void *)shock_collide_warp<float>, (const void *)shock_collide_warp<double>};
+      for (const void *f : fns)
+        if (allow_max_dyn_smem(f, smem_max) != cudaSuccess) {
+          fail(c, TRMCR_ECUDA, "cudaFuncSetAttribute(warp) failed");
+          return bail(TRMCR_ECUDA);
+        }
+      int occ = 1, nsm = 148;
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->dev);
+      if (c->dtype == TRMCR_F64)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, shock_collide_warp<double>, c->warp_wpc * 32, c->warp_smem);
+      else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, shock_collide_warp<float>, c->warp_wpc * 32, c->warp_smem);
+      c->warp_grid = std::max(1, std::min((c->ncells + c->warp_wpc - 1) / c->warp_wpc, nsm * std::max(occ, 1)));
+    }
   }
 
   // ---- global-memory plan scratch for large / overflowing cells ----

@@ -11,10 +11,13 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
-@pytest.mark.parametrize("seed", [1, 2, 3])
-def test_random_configs(orc, seed):
+@pytest.mark.parametrize("seed,warp_path", [(1, "1"), (2, "1"), (3, "1"), (4, "0")])
+def test_random_configs(orc, seed, warp_path, monkeypatch):
+    """warp_path "0" routes the general cells through the CTA kernel instead of
+    the warp-per-cell kernel (TRMCR_WARP_PATH, read at init)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+    monkeypatch.setenv("TRMCR_WARP_PATH", warp_path)
     from paper_1009_2768_b200 import api
     rng = np.random.default_rng(seed)
     for it in range(20):
