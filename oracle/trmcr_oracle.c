@@ -143,7 +143,7 @@ int32_t orc_split(double p, int64_t n, int32_t m, uint64_t seed, uint32_t gcell,
 }
 
 /* ===================================================================== */
-/* Keyed permutation: 4-round balanced Feistel with cycle walking.        */
+/* Keyed permutation: 4-round (unbalanced) Feistel with cycle walking.    */
 /* Realises "a random choice" of f_0 particles and of stored particles     */
 /* as uniform draws without replacement [R17].                */
 /* ===================================================================== */
@@ -154,21 +154,25 @@ static uint32_t mix32(uint32_t x) {
   return x;
 }
 
+/* Domain 2^b with b = ceil(log2 N); the state splits into L (a = floor(b/2)
+ * bits, high) and R (c = b - a bits, low).  Round i: (L, R) <- (R, L ^ (F(R,
+ * k_i) mod 2^width(L))), so the widths alternate and return after 4 rounds. */
 int64_t orc_feistel(uint64_t x, uint64_t N, const uint32_t rk[4]) {
   if (N <= 1) return (int64_t)x;
-  int bits = 0;
-  while ((1ull << bits) < N) bits++;
-  int half = (bits + 1) / 2;
-  uint64_t mask = (1ull << half) - 1ull;
+  int b = 0;
+  while ((1ull << b) < N) b++;
+  const int a = b / 2, c = b - a;
   uint64_t y = x;
   do {
-    uint64_t L = y >> half, R = y & mask;
+    uint64_t L = y >> c, R = y & ((1ull << c) - 1ull);
+    int wl = a, wr = c;
     for (int i = 0; i < 4; i++) {
-      uint64_t t = L ^ ((uint64_t)mix32((uint32_t)R ^ rk[i]) & mask);
+      uint64_t t = L ^ ((uint64_t)mix32((uint32_t)R ^ rk[i]) & ((1ull << wl) - 1ull));
       L = R;
       R = t;
+      int w = wl; wl = wr; wr = w;
     }
-    y = (L << half) | R;
+    y = (L << c) | R;
   } while (y >= N);
   return (int64_t)y;
 }

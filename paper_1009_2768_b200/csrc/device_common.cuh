@@ -56,26 +56,32 @@ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
   return x;
 }
 
+// Domain 2^b, b = ceil(log2 N) (< 2N, so cycle walking takes < 2 rounds on
+// average); L = high a = floor(b/2) bits, R = low c = b - a bits; round i:
+// (L, R) <- (R, L ^ (mix32(R ^ k_i) mod 2^width(L))): widths alternate and are
+// back to (a, c) after 4 rounds.
 struct Perm {
   uint4 rk;
-  uint32_t N, half, mask;
+  uint32_t N, c, mask_a, mask_c;
   __device__ __forceinline__ void init(uint4 key, uint32_t n) {
     rk = key;
     N = n;
-    const uint32_t bits = n > 1 ? 32u - __clz(n - 1u) : 1u;
-    half = (bits + 1u) >> 1;
-    mask = (half >= 32u) ? 0xFFFFFFFFu : ((1u << half) - 1u);
+    const uint32_t b = n > 1 ? 32u - __clz(n - 1u) : 1u;
+    const uint32_t a = b >> 1;
+    c = b - a;
+    mask_a = (1u << a) - 1u;
+    mask_c = (c >= 32u) ? 0xFFFFFFFFu : ((1u << c) - 1u);
   }
   __device__ __forceinline__ uint32_t round4(uint32_t y) const {
-    uint32_t L = y >> half, R = y & mask, t;
-    t = L ^ (mix32(R ^ rk.x) & mask); L = R; R = t;
-    t = L ^ (mix32(R ^ rk.y) & mask); L = R; R = t;
-    t = L ^ (mix32(R ^ rk.z) & mask); L = R; R = t;
-    t = L ^ (mix32(R ^ rk.w) & mask); L = R; R = t;
-    return (L << half) | R;
+    uint32_t L = y >> c, R = y & mask_c, t;
+    t = L ^ (mix32(R ^ rk.x) & mask_a); L = R; R = t;   // widths (a,c) -> (c,a)
+    t = L ^ (mix32(R ^ rk.y) & mask_c); L = R; R = t;   // (c,a) -> (a,c)
+    t = L ^ (mix32(R ^ rk.z) & mask_a); L = R; R = t;
+    t = L ^ (mix32(R ^ rk.w) & mask_c); L = R; R = t;
+    return (L << c) | R;
   }
-  // Cycle walking: expected < 4 rounds (domain < 4N).  Out-of-range input or
-  // a walk longer than 4096 (impossible for x < N) returns 0xFFFFFFFF.
+  // Cycle walking.  Out-of-range input or a walk longer than 4096 (impossible
+  // for x < N) returns 0xFFFFFFFF.
   __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
     if (N <= 1u) return x < N || N == 0u ? x : 0xFFFFFFFFu;
     if (x >= N) return 0xFFFFFFFFu;
