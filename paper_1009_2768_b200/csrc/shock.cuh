@@ -451,7 +451,7 @@ __device__ int gather_cell(const ShockDev &S, const GatherSrc &G, int c, Real *b
 template <typename Real>
 __device__ int gather_cell_warp(const ShockDev &S, const GatherSrc &G, int c, Real *bx, Real *by, Real *bz,
                                 Real *ox, int cap, double &sxo, double &syo, double &szo) {
-  constexpr int R = 8;
+  constexpr int R = 4;
   const int lane = threadIdx.x & 31;
   const int W = *G.W;
   int running = 0;
@@ -526,7 +526,7 @@ __device__ int gather_cell_warp(const ShockDev &S, const GatherSrc &G, int c, Re
 }
 
 template <typename Real>
-__global__ void __launch_bounds__(kWarpCellWarps * 32)
+__global__ void __launch_bounds__(kWarpCellWarps * 32, 3)
 shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, int *defer_count,
                    int *defer_list, QueueArgs Q) {

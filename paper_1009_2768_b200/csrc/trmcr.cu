@@ -80,7 +80,7 @@ cell_step_gmem(StepParams P, GmemScratch G, const int64_t *__restrict__ offsets,
 // General cells, one warp each (cell_warp.cuh), over the thermal kernel's
 // defer list (or every cell); cells that do not fit go to list2 (CTA kernel).
 template <typename Real>
-__global__ void __launch_bounds__(kWarpCellWarps * 32)
+__global__ void __launch_bounds__(kWarpCellWarps * 32, 3)
 cell_step_warp(StepParams P, WarpSlabLayout Lay, const int64_t *__restrict__ offsets, int ncells,
                const int *list_count, const int *list, Real *vx, Real *vy, Real *vz, int32_t *m_state,
                double *stats, int *list2_count, int *list2, QueueArgs Q) {
@@ -179,17 +179,17 @@ __global__ void __launch_bounds__(256) global_moments_kernel(const double *__res
     last = (atomicAdd(done, 1u) == gridDim.x - 1);
   }
   __syncthreads();
-  if (last && threadIdx.x < 9) {
+  if (last) {                      // uniform per CTA: the last CTA adds the partials
     __threadfence();
-    double s = 0;
-    for (int b = 0; b < (int)gridDim.x; ++b) s += ((volatile double *)partial)[b * 10 + threadIdx.x];
-    out[threadIdx.x] = s;
-    if (threadIdx.x == 8) out[TRMCR_GM_COST] = 0.0;   // filled below
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    out[TRMCR_GM_COST] = out[TRMCR_GM_PROPOSALS] + 0.5 * out[TRMCR_GM_MAXW];
-    *done = 0u;
+    double w[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+      for (int k = 0; k < 9; ++k) w[k] += ((volatile double *)partial)[b * 10 + k];
+    block_sum<10>(w, red);
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < 9; ++k) out[k] = w[k];
+      out[TRMCR_GM_COST] = w[TRMCR_GM_PROPOSALS] + 0.5 * w[TRMCR_GM_MAXW];
+      *done = 0u;
+    }
   }
 }
 
@@ -231,7 +231,9 @@ trmcr_status launch_collide(trmcr_ctx *c) {
       if (auto s = check_launch(c, "thermal_warp_kernel", TRMCR_K_THERMAL)) return s;
     }
     const bool idle = fast && c->fast_ok && c->last_defer == 0 && c->last_ovf == 0;
-    const bool use_warp = c->wlay.n_cap > 0;
+    // idle (nothing deferred lately): skip the warp kernel, the CTA kernel
+    // (one CTA) drains whatever this step defers
+    const bool use_warp = c->wlay.n_cap > 0 && !idle;
     const int *l1c = fast ? c->d_defer_count : nullptr, *l1 = fast ? c->d_defer_list : nullptr;
     if (use_warp) {
       CUDA_TRY(c, cudaMemsetAsync(c->d_defer2_count, 0, sizeof(int), c->stream));
@@ -591,7 +593,7 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
     const bool want = !(wenv && atoi(wenv) == 0);
     int wn = c->geometry == TRMCR_SHOCK_1D ? std::max(64, (2 * max_cell + 31) / 32 * 32)
                                            : std::max(32, (max_cell + 31) / 32 * 32);
-    const int wK = c->geometry == TRMCR_SHOCK_1D ? std::max(256, wn / 4) : std::max(256, wn / 2);
+    const int wK = c->geometry == TRMCR_SHOCK_1D ? std::max(256, std::min(512, wn / 4)) : std::max(256, wn / 2);
     // shock: velocities are gathered into the output buffer and processed in
     // place (a deferred cell is re-gathered); homogeneous: staged in the slab
     // (in place would corrupt the input of a deferred cell)
