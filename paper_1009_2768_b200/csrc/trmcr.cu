@@ -32,7 +32,7 @@ template <typename Real, int THREADS>
 __global__ void __launch_bounds__(THREADS, 768 / THREADS)
 cell_step_smem(StepParams P, SmemLayout Lay, const int64_t *__restrict__ offsets, int ncells,
                const int *list_count, const int *list, Real *vx, Real *vy, Real *vz, int32_t *m_state,
-               double *stats, QueueArgs Q) {
+               double *stats, QueueArgs Q, GmemScratch GS, int inline_gmem) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CellShared sh;
   CellBuf<Real> B;
@@ -46,7 +46,19 @@ cell_step_smem(StepParams P, SmemLayout Lay, const int64_t *__restrict__ offsets
                                                   vy + off, vz + off, n, P.cell_base + (uint32_t)c,
                                                   m_state + c, stats + (size_t)c * TRMCR_NSTATS, Q.log,
                                                   Q.log_count, Q.log_cap);
-    if (rc != kOk && threadIdx.x == 0) {
+    if (rc != kOk && inline_gmem) {
+      // single-CTA (idle) launch: redo the cell here with the global-memory
+      // plan of scratch slab 0 (no separate global-memory kernel launch)
+      __syncthreads();
+      CellBuf<Real> BG;
+      bind_gmem(BG, GS, B.red);
+      BG.vx = vx + off; BG.vy = vy + off; BG.vz = vz + off;
+      const int rg = process_cell<Real, false, false>(P, BG, sh, vx + off, vy + off, vz + off, vx + off,
+                                                      vy + off, vz + off, n, P.cell_base + (uint32_t)c,
+                                                      m_state + c, stats + (size_t)c * TRMCR_NSTATS, Q.log,
+                                                      Q.log_count, Q.log_cap);
+      if (rg != kOk && threadIdx.x == 0) atomicOr(Q.err, 1);
+    } else if (rc != kOk && threadIdx.x == 0) {
       const int j = atomicAdd(Q.ovf_count, 1);
       Q.ovf_list[j] = c;
     }
@@ -249,12 +261,14 @@ trmcr_status launch_collide(trmcr_ctx *c) {
     auto kern = c->smem_threads == 64 ? cell_step_smem<Real, 64>
                 : (c->smem_threads == 128 ? cell_step_smem<Real, 128> : cell_step_smem<Real, 256>);
     kern<<<idle ? 1 : c->smem_grid, c->smem_threads, c->lay.total, c->stream>>>(
-        c->P, c->lay, c->d_offsets, c->ncells, l1c, l1, vx, vy, vz, c->d_mstate, c->d_stats, Q);
+        c->P, c->lay, c->d_offsets, c->ncells, l1c, l1, vx, vy, vz, c->d_mstate, c->d_stats, Q, c->gs, idle ? 1 : 0);
     if (auto s = check_launch(c, "cell_step_smem", TRMCR_K_CELL_SMEM)) return s;
-    prof_begin(c, TRMCR_K_CELL_GMEM);
-    cell_step_gmem<Real><<<idle ? 1 : c->G, c->gmem_threads, 0, c->stream>>>(c->P, c->gs, c->d_offsets, vx, vy, vz,
-                                                                            c->d_mstate, c->d_stats, Q);
-    if (auto s = check_launch(c, "cell_step_gmem", TRMCR_K_CELL_GMEM)) return s;
+    if (!idle) {   // idle: the single CTA above handled overflowing cells itself
+      prof_begin(c, TRMCR_K_CELL_GMEM);
+      cell_step_gmem<Real><<<c->G, c->gmem_threads, 0, c->stream>>>(c->P, c->gs, c->d_offsets, vx, vy, vz,
+                                                                    c->d_mstate, c->d_stats, Q);
+      if (auto s = check_launch(c, "cell_step_gmem", TRMCR_K_CELL_GMEM)) return s;
+    }
     if (!c->fast_pending && (c->step % 8 == 0 || !c->fast_ok)) {
       CUDA_TRY(c, cudaMemcpyAsync(c->h_defer, c->d_defer_count, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
       CUDA_TRY(c, cudaEventRecord(c->ev_defer, c->stream));
