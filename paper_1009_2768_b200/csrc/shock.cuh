@@ -18,6 +18,7 @@
 #pragma once
 #include "ctx.cuh"
 #include "cell_warp.cuh"
+#include "thermal.cuh"
 
 namespace trmcr {
 
@@ -197,54 +198,100 @@ __global__ void ghost_gen(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, c
 
 // ---- A1: free transport of the interior particles ----
 // dest = local destination cell (outside [0, C): emigrant to a neighbouring
-// slab; kDropped: left the domain).  Counts per local cell are
-// warp-aggregated; W[0] = max local displacement, W[1] = max displacement of
-// emigrants (cells the pack kernel must scan), reduced per CTA.
+// slab; kDropped: left the domain).  The particles of one CTA are sorted by
+// source cell and move less than a cell or two, so their destinations fall in
+// a small window: counts are accumulated in a shared-memory histogram over
+// [dmin, dmin + kHist) and flushed with one global atomic per touched cell
+// (a destination outside the window falls back to a global atomic).
+// W[0] = max local displacement, W[1] = emigrant scan width, acct[2] = dropped.
+constexpr int kTransportThreads = 256, kTransportPer = 4, kHist = 64;
+
 template <typename Real>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kTransportThreads)
 transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const Real *__restrict__ vx,
                  int32_t *dest, int32_t *counts, int *W, unsigned long long *acct) {
-  __shared__ int s_disp[8], s_emi[8];
-  __shared__ unsigned s_drop[8];
+  __shared__ int s_hist[kHist];
+  __shared__ int s_red[3][kTransportThreads / 32];
+  __shared__ int s_dmin;
   const int64_t n = off_old[S.C];
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = i < n;
-  int d = -1, disp = 0, emi = 0;
-  bool dropped = false;
-  if (valid) {
-    const Real xo = x[i];
-    const int src = cell_of(S, (double)xo) - S.cbase;
-    const Real xn = add_rn<Real>(xo, mul_rn<Real>(vx[i], (Real)S.dt));
-    x[i] = xn;
+  const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kTransportPer;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int d[kTransportPer];
+  int disp = 0, emi = 0, dropped = 0, dmin = INT32_MAX;
+  Real xs[kTransportPer], vs[kTransportPer];
+  const bool vec = (i0 + kTransportPer <= n) && (sizeof(Real) * kTransportPer == 16);
+  if (vec) {
+    using V = typename Vec<Real>::T;
+    const V xv = *reinterpret_cast<const V *>(x + i0), vv = *reinterpret_cast<const V *>(vx + i0);
+#pragma unroll
+    for (int k = 0; k < kTransportPer; ++k) { xs[k] = vget<V, Real>(xv, k); vs[k] = vget<V, Real>(vv, k); }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kTransportPer; ++k) {
+      xs[k] = (i0 + k < n) ? x[i0 + k] : Real(0);
+      vs[k] = (i0 + k < n) ? vx[i0 + k] : Real(0);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kTransportPer; ++k) {
+    d[k] = -1;
+    if (i0 + k >= n) continue;
+    const int src = cell_of(S, (double)xs[k]) - S.cbase;
+    const Real xn = add_rn<Real>(xs[k], mul_rn<Real>(vs[k], (Real)S.dt));
+    xs[k] = xn;
     const double xd = (double)xn;
     const bool keep = xd >= S.x_min && xd < S.x_max;
     const int dl = keep ? cell_of(S, xd) - S.cbase : kDropped;
-    dest[i] = dl;
-    dropped = !keep;
-    if (keep && dl >= 0 && dl < S.C) {
-      d = dl;
-      disp = abs(dl - src);
-    } else if (keep) {
-      emi = dl < 0 ? src + 1 : S.C - src;   // source cells the pack scan must cover
+    if (!keep) {
+      ++dropped;
+    } else if (dl >= 0 && dl < S.C) {
+      d[k] = dl;
+      disp = max(disp, abs(dl - src));
+      dmin = min(dmin, dl);
+    } else {
+      emi = max(emi, dl < 0 ? src + 1 : S.C - src);
     }
+    if (!vec) { x[i0 + k] = xn; dest[i0 + k] = dl; }
+    else d[k] = dl;   // written below as one int4; non-local ones reset to -1 after
   }
-  count_key(counts, d);
-  const int wd = __reduce_max_sync(0xffffffffu, disp);
-  const int we = __reduce_max_sync(0xffffffffu, emi);
-  const unsigned wdrop = __popc(__ballot_sync(0xffffffffu, dropped));
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) { s_disp[warp] = wd; s_emi[warp] = we; s_drop[warp] = wdrop; }
+  if (vec) {
+    using V = typename Vec<Real>::T;
+    V xv;
+#pragma unroll
+    for (int k = 0; k < kTransportPer; ++k) vset<V, Real>(xv, k, xs[k]);
+    *reinterpret_cast<V *>(x + i0) = xv;
+    *reinterpret_cast<int4 *>(dest + i0) = make_int4(d[0], d[1], d[2], d[3]);
+#pragma unroll
+    for (int k = 0; k < kTransportPer; ++k) if (d[k] < 0 || d[k] >= S.C) d[k] = -1;   // not counted here
+  }
+  // CTA reductions: window base, max displacement, emigrant width, dropped
+  dmin = __reduce_min_sync(0xffffffffu, dmin);
+  const int wd = __reduce_max_sync(0xffffffffu, disp), we = __reduce_max_sync(0xffffffffu, emi);
+  const int wdr = __reduce_add_sync(0xffffffffu, dropped);
+  if (threadIdx.x < kHist) s_hist[threadIdx.x] = 0;
+  if (lane == 0) { s_red[0][warp] = dmin; s_red[1][warp] = wd; s_red[2][warp] = we; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int md = 0, me = 0;
-    unsigned dr = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      md = max(md, s_disp[w]); me = max(me, s_emi[w]); dr += s_drop[w];
+    int m = INT32_MAX, md = 0, me = 0;
+    for (int w = 0; w < kTransportThreads / 32; ++w) {
+      m = min(m, s_red[0][w]); md = max(md, s_red[1][w]); me = max(me, s_red[2][w]);
     }
+    s_dmin = m;
     if (md > 0 && md > *((volatile int *)W)) atomicMax(W, md);
     if (me > 0 && me > *((volatile int *)(W + 1))) atomicMax(W + 1, me);
-    if (dr) atomicAdd(&acct[2], (unsigned long long)dr);
   }
+  if (lane == 0 && wdr) atomicAdd(&acct[2], (unsigned long long)wdr);
+  __syncthreads();
+  const int base = s_dmin;
+#pragma unroll
+  for (int k = 0; k < kTransportPer; ++k) {
+    if (d[k] < 0) continue;
+    const int h = d[k] - base;
+    if (h < kHist) atomicAdd(&s_hist[h], 1);
+    else atomicAdd(&counts[d[k]], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < kHist && s_hist[threadIdx.x] > 0) atomicAdd(&counts[base + threadIdx.x], s_hist[threadIdx.x]);
 }
 
 // ---- slab exchange: pack emigrants (stable, canonical order) ----
@@ -721,9 +768,10 @@ trmcr_status shock_begin(trmcr_ctx *c) {
     if (auto e = check_launch(c, "ghost_gen", TRMCR_K_GHOST_GEN)) return e;
   }
   {
-    const unsigned blocks = (unsigned)((c->cap + 255) / 256);
+    const int per_block = kTransportThreads * kTransportPer;
+    const unsigned blocks = (unsigned)((c->cap + per_block - 1) / per_block);
     prof_begin(c, TRMCR_K_TRANSPORT);
-    transport_kernel<Real><<<blocks, 256, 0, c->stream>>>(d, s.d_off[cur], (Real *)c->x[cur],
+    transport_kernel<Real><<<blocks, kTransportThreads, 0, c->stream>>>(d, s.d_off[cur], (Real *)c->x[cur],
                                                           (const Real *)c->v[cur][0], s.d_dest, s.d_counts,
                                                           s.d_W, s.d_acct);
     if (auto e = check_launch(c, "transport_kernel", TRMCR_K_TRANSPORT)) return e;
