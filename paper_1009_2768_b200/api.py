@@ -14,7 +14,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtrmcr.so")
+LIB_PATH = os.environ.get("TRMCR_LIB") or os.path.join(HERE, "libtrmcr.so")   # override: experiments
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ECAPACITY, ESTATE = range(7)
 MAXWELL, HARD_SPHERE = 0, 1

@@ -89,7 +89,27 @@ struct QueueArgs {
   trmcr_coll_rec *log;
   unsigned long long *log_count;
   int64_t log_cap;
+  int *zero_next;          // step-parity counter set of the next step: zeroed by block 0 (nullable)
 };
+
+// Last statement of every step kernel (late-trigger variant).
+// Triggering at the end (not the start) measured faster on C3: an early
+// trigger lets the successor's CTAs take SM slots while this kernel runs.
+__device__ __forceinline__ void step_kernel_epilogue() {
+#ifndef TRMCR_PDL_EARLY
+  trmcr::pdl_trigger();
+#endif
+}
+
+// First statements of every step kernel: wait for the predecessor (PDL), let
+// the successor be scheduled, re-arm the next step's counters.
+__device__ __forceinline__ void step_kernel_prologue(int *zero_next) {
+  trmcr::pdl_wait();
+#ifdef TRMCR_PDL_EARLY
+  trmcr::pdl_trigger();
+#endif
+  if (zero_next && blockIdx.x == 0 && threadIdx.x < 4) zero_next[threadIdx.x] = 0;
+}
 
 // Shock geometry state (A1, A2): see shock.cuh.
 struct ShockState {
@@ -137,6 +157,8 @@ struct trmcr_ctx {
   double *d_stats = nullptr, *d_moments = nullptr;
   int *d_ovf_count = nullptr, *d_ovf_list = nullptr, *d_err = nullptr;
   // thermal fast path (thermal.cuh): cells it defers go to the general kernel
+  int *d_cnt = nullptr;            // [2][4] step-parity counter sets {defer, ovf, defer2, -}
+  int use_pdl = 1;                 // programmatic dependent launch (TRMCR_PDL=0 disables)
   int *d_defer_count = nullptr, *d_defer_list = nullptr;
   int *d_defer2_count = nullptr, *d_defer2_list = nullptr;   // warp kernel -> CTA kernel
   trmcr::WarpSlabLayout wlay{};
@@ -145,6 +167,7 @@ struct trmcr_ctx {
   double *d_gm_partial = nullptr;  // global-moments partial sums
   unsigned *d_gm_done = nullptr;
   cudaEvent_t ev_defer = nullptr;
+  int thermal_prefetch = 1;   // L2 prefetch of each warp's next cell (TRMCR_THERMAL_PREFETCH=0 disables)
   int fast_ok = 1, fast_pending = 0, fast_grid = 0, smem_grid = 0, last_defer = -1, last_ovf = -1;
   unsigned char *d_scratch = nullptr;
   trmcr::GmemScratch gs{};

@@ -94,6 +94,15 @@ struct Perm {
   }
 };
 
+// ---- programmatic dependent launch (PDL) ----
+// Every kernel of the step starts with pdl_wait(): it returns once the
+// preceding kernel in the stream has completed and its writes are visible
+// (a no-op when the kernel was launched without the PDL attribute), so the
+// data dependencies are those of plain stream order.  pdl_trigger() lets the
+// next kernel be scheduled (its launch latency overlaps this kernel).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- CTA reductions (fixed order: reproducible run to run) ----
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -262,20 +262,65 @@ __device__ __forceinline__ void gauss3_fast(const RngKey &K, uint32_t slot, floa
   g0 = r1 * c2; g1 = r1 * s2; g2 = r3 * c4;
 }
 
-// Box-Muller pair from two 24-bit uniforms (fp32 statistical path).
-__device__ __forceinline__ void bm_pair(uint32_t wa, uint32_t wb, float &c, float &s) {
-  constexpr float kM2Ln2 = -1.3862943611198906f;   // -2 ln 2
-  const float a = kM2Ln2 * __log2f(u24_bits(wa));
-  const float r = a * rsqrtf(a);
-  __sincosf(6.283185307179586f * u24_bits(wb), &s, &c);
-  c *= r;
-  s *= r;
+// Raw MUFU approximations (flush-to-zero, no special-case fix-ups): every
+// operand below is a normal number (u in [2^-24, 1), a in [1.2e-7, 23.1],
+// 2 pi u in (0, 2 pi)), so the fix-up code the compiler adds around
+// __log2f / rsqrtf would never fire.
+__device__ __forceinline__ float lg2_ftz(float x) {
+  float y; asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y;
 }
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float y; asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y;
+}
+__device__ __forceinline__ float sin_ftz(float x) {
+  float y; asm("sin.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y;
+}
+__device__ __forceinline__ float cos_ftz(float x) {
+  float y; asm("cos.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y;
+}
+
+// Box-Muller pair from two 24-bit uniforms (fp32 statistical path), scaled by
+// the constant 1/sqrt(2 ln 2): r = sqrt(-log2 u) instead of sqrt(-2 ln u).
+// The Maxwellian is built by shift-and-rescale to the cell's own energy
+// (v' = u + s (g - G), s = sqrt(E / sum|g - G|^2)), so a common scale of all
+// g cancels exactly (up to rounding) and its multiply is dropped.
+// 2 pi u2 = 2 pi (b - (1 - 2^-24)) is one FFMA from the mantissa word b.
+__device__ __forceinline__ void bm_pair(uint32_t wa, uint32_t wb, float &c, float &s) {
+  constexpr float k2Pi = 6.283185307179586f;
+  const float l = lg2_ftz(u24_bits(wa));           // log2 u < 0
+  const float r = -l * rsqrt_ftz(-l);
+  const float b = __uint_as_float(0x3F800000u | (wb >> 9));
+  const float t = fmaf(b, k2Pi, -k2Pi * (1.0f - 0x1p-24f));
+  s = r * sin_ftz(t);
+  c = r * cos_ftz(t);
+}
+
+// Philox4x32-10 with the key schedule precomputed on the host (kernel
+// parameter, i.e. constant bank: the key XORs cost no extra instruction) and
+// counter words 1..3 fixed per cell: the same bijection as philox10().
+struct KeySched {
+  uint32_t k0[10], k1[10];
+};
+__device__ __forceinline__ uint4 philox10_ks(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                             const KeySched &ks) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ ks.k0[r], n2 = hi0 ^ c3 ^ ks.k1[r];
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
+  return make_uint4(c0, c1, c2, c3);
+}
+
 // 12 standard normals for the 4 consecutive slots of float4 group g: three
 // Philox blocks (MAXW, element 3g..3g+2) -> 6 Box-Muller pairs (fp32 mode's
 // draw definition for the fluid-regime path).
-__device__ __forceinline__ void gauss12(const RngKey &K, uint32_t g, float4 &a, float4 &b, float4 &d) {
-  const uint4 w0 = K(kMaxw, 0, 0, 3 * g), w1 = K(kMaxw, 0, 0, 3 * g + 1), w2 = K(kMaxw, 0, 0, 3 * g + 2);
+__device__ __forceinline__ void gauss12(const KeySched &ks, uint32_t cell, uint32_t step, uint32_t g, float4 &a,
+                                        float4 &b, float4 &d) {
+  const uint32_t c1 = kMaxw << 24;
+  const uint4 w0 = philox10_ks(3 * g, c1, cell, step, ks), w1 = philox10_ks(3 * g + 1, c1, cell, step, ks),
+              w2 = philox10_ks(3 * g + 2, c1, cell, step, ks);
   bm_pair(w0.x, w0.y, a.x, b.x);
   bm_pair(w0.z, w0.w, d.x, a.y);
   bm_pair(w1.x, w1.y, b.y, d.y);
@@ -284,9 +329,10 @@ __device__ __forceinline__ void gauss12(const RngKey &K, uint32_t g, float4 &a, 
   bm_pair(w2.z, w2.w, b.w, d.w);
 }
 
-__device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, float *vx, float *vy, float *vz, int64_t off,
-                                                 int n, int c, float *wx, float *wy, float *wz,
-                                                 int32_t *m_state, double *stats) {
+__device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, const KeySched &ks, float *vx, float *vy,
+                                                 float *vz, int64_t off, int n, int c, float *wx, float *wy,
+                                                 float *wz, int32_t *m_state, double *stats, int64_t next_off,
+                                                 int next_n) {
   constexpr int CAP = ThermalCap<float>::value;
   constexpr int G = CAP / 4 / 32;                 // float4 groups per lane at n = CAP
   const int lane = threadIdx.x & 31;
@@ -303,6 +349,11 @@ __device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, float *vx,
   }
   cp_async_wait_all();
   __syncwarp();
+  // the warp's next cell: HBM -> L2 while this one is computed
+  if (next_n > 0 && lane < 3 && ((next_off | next_n) & 3) == 0) {
+    const float *base = lane == 0 ? vx : (lane == 1 ? vy : vz);
+    prefetch_l2(base + next_off, (unsigned)next_n * 4u);
+  }
   float sx = 0, sy = 0, sz = 0;
 #pragma unroll
   for (int k = 0; k < G; ++k) {
@@ -344,7 +395,7 @@ __device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, float *vx,
   M.E = warp_sum((double)e);
   thermal_decide(P, M, n, warp_sum((double)pxx), warp_sum((double)m4), warp_max((double)mx));
   if (!(M.p * (double)n < 0x1p-53)) return false;
-  const RngKey K{P.k0, P.k1, P.cell_base + (uint32_t)c, P.step};
+  const uint32_t gcell = P.cell_base + (uint32_t)c;
   if (n >= 2) {
     float ax = 0, ay = 0, az = 0, a2 = 0;
 #pragma unroll 2
@@ -352,7 +403,7 @@ __device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, float *vx,
       const int g = lane + 32 * k;
       if (g < ng) {
         float4 a, b, d;
-        gauss12(K, (uint32_t)g, a, b, d);
+        gauss12(ks, gcell, P.step, (uint32_t)g, a, b, d);
         sx4[g] = a; sy4[g] = b; sz4[g] = d;
         ax += (a.x + a.y) + (a.z + a.w); ay += (b.x + b.y) + (b.z + b.w); az += (d.x + d.y) + (d.z + d.w);
         a2 += ((a.x * a.x + b.x * b.x + d.x * d.x) + (a.y * a.y + b.y * b.y + d.y * d.y)) +
@@ -362,16 +413,18 @@ __device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, float *vx,
     const double Gx = warp_sum((double)ax) / n, Gy = warp_sum((double)ay) / n, Gz = warp_sum((double)az) / n;
     const double D = warp_sum((double)a2) - n * (Gx * Gx + Gy * Gy + Gz * Gz);
     const double sc = (D > 0.0 && M.E > 0.0) ? sqrt(M.E / D) : 0.0;
-    const float rs = (float)sc, rgx = (float)Gx, rgy = (float)Gy, rgz = (float)Gz;
+    // v' = u + s (g - G) = s g + (u - s G): one FFMA per component
+    const float rs = (float)sc;
+    const float bx = (float)(M.ux - sc * Gx), by = (float)(M.uy - sc * Gy), bz = (float)(M.uz - sc * Gz);
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < G; ++k) {
       const int g = lane + 32 * k;
       if (g < ng) {
         float4 a = sx4[g], b = sy4[g], d = sz4[g];
-        a.x = rux + rs * (a.x - rgx); a.y = rux + rs * (a.y - rgx); a.z = rux + rs * (a.z - rgx); a.w = rux + rs * (a.w - rgx);
-        b.x = ruy + rs * (b.x - rgy); b.y = ruy + rs * (b.y - rgy); b.z = ruy + rs * (b.z - rgy); b.w = ruy + rs * (b.w - rgy);
-        d.x = ruz + rs * (d.x - rgz); d.y = ruz + rs * (d.y - rgz); d.z = ruz + rs * (d.z - rgz); d.w = ruz + rs * (d.w - rgz);
+        a.x = fmaf(rs, a.x, bx); a.y = fmaf(rs, a.y, bx); a.z = fmaf(rs, a.z, bx); a.w = fmaf(rs, a.w, bx);
+        b.x = fmaf(rs, b.x, by); b.y = fmaf(rs, b.y, by); b.z = fmaf(rs, b.z, by); b.w = fmaf(rs, b.w, by);
+        d.x = fmaf(rs, d.x, bz); d.y = fmaf(rs, d.y, bz); d.z = fmaf(rs, d.z, bz); d.w = fmaf(rs, d.w, bz);
         __stcs(gx + g, a); __stcs(gy + g, b); __stcs(gz + g, d);
       }
     }
@@ -382,8 +435,10 @@ __device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, float *vx,
 
 template <typename Real>
 __global__ void __launch_bounds__(kThermalWarps * 32, 2)
-thermal_warp_kernel(StepParams P, const int64_t *__restrict__ offsets, int ncells, Real *vx, Real *vy,
-                    Real *vz, int32_t *m_state, double *stats, int *defer_count, int *defer_list) {
+thermal_warp_kernel(StepParams P, KeySched ks, const int64_t *__restrict__ offsets, int ncells, Real *vx,
+                    Real *vy, Real *vz, int32_t *m_state, double *stats, int *defer_count, int *defer_list,
+                    int prefetch, int *zero_next) {
+  step_kernel_prologue(zero_next);
   constexpr int CAP = ThermalCap<Real>::value;
   constexpr int W = Vec<Real>::W;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -393,6 +448,8 @@ thermal_warp_kernel(StepParams P, const int64_t *__restrict__ offsets, int ncell
   const int nwarps = gridDim.x * kThermalWarps;
   int c = blockIdx.x * kThermalWarps + warp;
   int64_t off = c < ncells ? offsets[c] : 0, end = c < ncells ? offsets[c + 1] : 0;
+  const bool base_al = ((reinterpret_cast<uintptr_t>(vx) | reinterpret_cast<uintptr_t>(vy) |
+                         reinterpret_cast<uintptr_t>(vz)) & 15) == 0;
   for (; c < ncells; c += nwarps) {
     const int n = (int)(end - off);
     const int64_t cur_off = off;
@@ -404,11 +461,10 @@ thermal_warp_kernel(StepParams P, const int64_t *__restrict__ offsets, int ncell
     }
     bool done = false;
     if (n > 0 && n <= CAP) {
-      const bool aligned = (cur_off % W) == 0 && (n % W) == 0 &&
-                           ((reinterpret_cast<uintptr_t>(vx) | reinterpret_cast<uintptr_t>(vy) |
-                             reinterpret_cast<uintptr_t>(vz)) & 15) == 0;
+      const bool aligned = (cur_off % W) == 0 && (n % W) == 0 && base_al;
       if constexpr (sizeof(Real) == 4) {
-        done = aligned ? thermal_cell_f32(P, vx, vy, vz, cur_off, n, c, wx, wy, wz, m_state, stats)
+        const int nn = (prefetch && cn < ncells) ? (int)(end - off) : 0;
+        done = aligned ? thermal_cell_f32(P, ks, vx, vy, vz, cur_off, n, c, wx, wy, wz, m_state, stats, off, nn)
                        : thermal_cell_scalar<Real>(P, vx, vy, vz, cur_off, n, c, wx, wy, wz, m_state, stats);
       } else {
         done = aligned ? thermal_cell_vec<Real, CAP>(P, vx, vy, vz, cur_off, n, c, wx, wy, wz, m_state, stats)
@@ -418,6 +474,7 @@ thermal_warp_kernel(StepParams P, const int64_t *__restrict__ offsets, int ncell
     if (!done && lane == 0) defer_list[atomicAdd(defer_count, 1)] = c;   // general path
     __syncwarp();
   }
+  step_kernel_epilogue();
 }
 
 }  // namespace trmcr

@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS)
 cell_step_smem(StepParams P, SmemLayout Lay, const int64_t *__restrict__ offsets, int ncells,
                const int *list_count, const int *list, Real *vx, Real *vy, Real *vz, int32_t *m_state,
                double *stats, QueueArgs Q, GmemScratch GS, int inline_gmem) {
+  step_kernel_prologue(Q.zero_next);
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CellShared sh;
   CellBuf<Real> B;
@@ -64,12 +65,14 @@ cell_step_smem(StepParams P, SmemLayout Lay, const int64_t *__restrict__ offsets
     }
     __syncthreads();
   }
+  step_kernel_epilogue();
 }
 
 template <typename Real>
 __global__ void __launch_bounds__(kGmemThreads)
 cell_step_gmem(StepParams P, GmemScratch G, const int64_t *__restrict__ offsets, Real *vx, Real *vy,
                Real *vz, int32_t *m_state, double *stats, QueueArgs Q) {
+  step_kernel_prologue(Q.zero_next);
   __shared__ CellShared sh;
   __shared__ double red[32 * 8];
   const int count = *Q.ovf_count;
@@ -87,6 +90,7 @@ cell_step_gmem(StepParams P, GmemScratch G, const int64_t *__restrict__ offsets,
     if (rc != kOk && threadIdx.x == 0) atomicOr(Q.err, 1);
     __syncthreads();
   }
+  step_kernel_epilogue();
 }
 
 // General cells, one warp each (cell_warp.cuh), over the thermal kernel's
@@ -96,6 +100,7 @@ __global__ void __launch_bounds__(kWarpCellWarps * 32, 3)
 cell_step_warp(StepParams P, WarpSlabLayout Lay, const int64_t *__restrict__ offsets, int ncells,
                const int *list_count, const int *list, Real *vx, Real *vy, Real *vz, int32_t *m_state,
                double *stats, int *list2_count, int *list2, QueueArgs Q) {
+  step_kernel_prologue(Q.zero_next);
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char *slab = smem + (size_t)warp * Lay.per_warp;
@@ -125,6 +130,7 @@ cell_step_warp(StepParams P, WarpSlabLayout Lay, const int64_t *__restrict__ off
     if (rc != kOk && lane == 0) list2[atomicAdd(list2_count, 1)] = c;
     __syncwarp();
   }
+  step_kernel_epilogue();
 }
 
 // A9: per-cell moments, one CTA per cell (two passes).
@@ -173,6 +179,7 @@ moments_kernel(const int64_t *__restrict__ offsets, int ncells, const Real *__re
 constexpr int kGmBlocks = 256;
 __global__ void __launch_bounds__(256) global_moments_kernel(const double *__restrict__ stats, int ncells,
                                                              double *partial, unsigned *done, double *out) {
+  step_kernel_prologue(nullptr);
   __shared__ double red[8 * 10];
   __shared__ bool last;
   const int per = (ncells + gridDim.x - 1) / gridDim.x;
@@ -203,6 +210,7 @@ __global__ void __launch_bounds__(256) global_moments_kernel(const double *__res
       *done = 0u;
     }
   }
+  step_kernel_epilogue();
 }
 
 __global__ void fill_i32(int32_t *a, int n, int32_t v) {
@@ -214,10 +222,31 @@ __global__ void fill_i32(int32_t *a, int n, int32_t v) {
 
 namespace {
 
+// Kernel launch, with the programmatic-stream-serialization attribute when
+// PDL is on (the kernel must begin with step_kernel_prologue / pdl_wait).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(const trmcr_ctx *c, void (*k)(KArgs...), int grid, int block, size_t smem, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = c->use_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 template <typename Real>
 trmcr_status launch_collide(trmcr_ctx *c) {
   Real *vx = (Real *)c->v[c->cur][0], *vy = (Real *)c->v[c->cur][1], *vz = (Real *)c->v[c->cur][2];
-  QueueArgs Q{c->d_ovf_count, c->d_ovf_list, c->d_err, c->d_log, c->d_log_count, c->log_cap};
+  // step-parity counter sets: this step's are zero (re-armed by the previous
+  // step's kernels, or at init); this step's kernels re-arm the other set
+  int *cnt = c->d_cnt + 4 * (c->step & 1), *nxt = c->d_cnt + 4 * ((c->step + 1) & 1);
+  c->d_defer_count = cnt; c->d_ovf_count = cnt + 1; c->d_defer2_count = cnt + 2;
+  QueueArgs Q{c->d_ovf_count, c->d_ovf_list, c->d_err, c->d_log, c->d_log_count, c->log_cap, nxt};
   c->P.step = c->step;
   if (c->ncells > 0) {
     // Counts of the last observed step (pinned async copy, read when ready):
@@ -234,12 +263,17 @@ trmcr_status launch_collide(trmcr_ctx *c) {
       cudaGetLastError();   // cudaErrorNotReady is not an error here
     }
     const bool fast = c->fast_ok || (c->step % 16 == 0);
-    CUDA_TRY(c, cudaMemsetAsync(c->d_defer_count, 0, 2 * sizeof(int), c->stream));   // defer + ovf
     if (fast) {
       prof_begin(c, TRMCR_K_THERMAL);
-      thermal_warp_kernel<Real><<<c->fast_grid, kThermalWarps * 32,
-                                  kThermalWarps * 3 * ThermalCap<Real>::value * sizeof(Real), c->stream>>>(
-          c->P, c->d_offsets, c->ncells, vx, vy, vz, c->d_mstate, c->d_stats, c->d_defer_count, c->d_defer_list);
+      KeySched ks;
+      for (int r = 0; r < 10; ++r) {
+        ks.k0[r] = c->P.k0 + (uint32_t)r * 0x9E3779B9u;
+        ks.k1[r] = c->P.k1 + (uint32_t)r * 0xBB67AE85u;
+      }
+      launch_k(c, thermal_warp_kernel<Real>, c->fast_grid, kThermalWarps * 32,
+               kThermalWarps * 3 * ThermalCap<Real>::value * sizeof(Real), c->P, ks, (const int64_t *)c->d_offsets,
+               c->ncells, vx, vy, vz, c->d_mstate, c->d_stats, c->d_defer_count, c->d_defer_list,
+               c->thermal_prefetch, nxt);
       if (auto s = check_launch(c, "thermal_warp_kernel", TRMCR_K_THERMAL)) return s;
     }
     const bool idle = fast && c->fast_ok && c->last_defer == 0 && c->last_ovf == 0;
@@ -248,11 +282,10 @@ trmcr_status launch_collide(trmcr_ctx *c) {
     const bool use_warp = c->wlay.n_cap > 0 && !idle;
     const int *l1c = fast ? c->d_defer_count : nullptr, *l1 = fast ? c->d_defer_list : nullptr;
     if (use_warp) {
-      CUDA_TRY(c, cudaMemsetAsync(c->d_defer2_count, 0, sizeof(int), c->stream));
       prof_begin(c, TRMCR_K_CELL_WARP);
-      cell_step_warp<Real><<<idle ? 1 : c->warp_grid, c->warp_wpc * 32, c->warp_smem, c->stream>>>(
-          c->P, c->wlay, c->d_offsets, c->ncells, l1c, l1, vx, vy, vz, c->d_mstate, c->d_stats,
-          c->d_defer2_count, c->d_defer2_list, Q);
+      launch_k(c, cell_step_warp<Real>, idle ? 1 : c->warp_grid, c->warp_wpc * 32, (size_t)c->warp_smem, c->P,
+               c->wlay, (const int64_t *)c->d_offsets, c->ncells, l1c, l1, vx, vy, vz, c->d_mstate, c->d_stats,
+               c->d_defer2_count, c->d_defer2_list, Q);
       if (auto s = check_launch(c, "cell_step_warp", TRMCR_K_CELL_WARP)) return s;
       l1c = c->d_defer2_count;
       l1 = c->d_defer2_list;
@@ -260,13 +293,14 @@ trmcr_status launch_collide(trmcr_ctx *c) {
     prof_begin(c, TRMCR_K_CELL_SMEM);
     auto kern = c->smem_threads == 64 ? cell_step_smem<Real, 64>
                 : (c->smem_threads == 128 ? cell_step_smem<Real, 128> : cell_step_smem<Real, 256>);
-    kern<<<idle ? 1 : c->smem_grid, c->smem_threads, c->lay.total, c->stream>>>(
-        c->P, c->lay, c->d_offsets, c->ncells, l1c, l1, vx, vy, vz, c->d_mstate, c->d_stats, Q, c->gs, idle ? 1 : 0);
+    launch_k(c, kern, idle ? 1 : c->smem_grid, c->smem_threads, (size_t)c->lay.total, c->P, c->lay,
+             (const int64_t *)c->d_offsets, c->ncells, l1c, l1, vx, vy, vz, c->d_mstate, c->d_stats, Q, c->gs,
+             idle ? 1 : 0);
     if (auto s = check_launch(c, "cell_step_smem", TRMCR_K_CELL_SMEM)) return s;
     if (!idle) {   // idle: the single CTA above handled overflowing cells itself
       prof_begin(c, TRMCR_K_CELL_GMEM);
-      cell_step_gmem<Real><<<c->G, c->gmem_threads, 0, c->stream>>>(c->P, c->gs, c->d_offsets, vx, vy, vz,
-                                                                    c->d_mstate, c->d_stats, Q);
+      launch_k(c, cell_step_gmem<Real>, c->G, c->gmem_threads, 0, c->P, c->gs, (const int64_t *)c->d_offsets, vx,
+               vy, vz, c->d_mstate, c->d_stats, Q);
       if (auto s = check_launch(c, "cell_step_gmem", TRMCR_K_CELL_GMEM)) return s;
     }
     if (!c->fast_pending && (c->step % 8 == 0 || !c->fast_ok)) {
@@ -331,7 +365,8 @@ trmcr_status trmcr_global_moments(trmcr_ctx *c, double *dev_out) {
   if (!c || !dev_out) return fail(c, TRMCR_EINVAL, "null argument");
   if (c->sticky) return TRMCR_ESTATE;
   const int blocks = std::max(1, std::min(kGmBlocks, c->ncells));
-  global_moments_kernel<<<blocks, 256, 0, c->stream>>>(c->d_stats, c->ncells, c->d_gm_partial, c->d_gm_done, dev_out);
+  launch_k(c, global_moments_kernel, blocks, 256, 0, (const double *)c->d_stats, c->ncells, c->d_gm_partial,
+           c->d_gm_done, dev_out);
   return check_launch(c, "global_moments_kernel");
 }
 
@@ -484,11 +519,12 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
 
       dalloc(c, &c->d_ovf_list, sizeof(int) * std::max(c->ncells, 1)) ||
       dalloc(c, &c->d_err, sizeof(int)) || dalloc(c, &c->d_log_count, sizeof(unsigned long long)) ||
-      dalloc(c, &c->d_defer_count, 2 * sizeof(int)) || dalloc(c, &c->d_defer2_count, sizeof(int)) ||
+      dalloc(c, &c->d_cnt, 8 * sizeof(int)) ||
       dalloc(c, &c->d_defer2_list, sizeof(int) * std::max(c->ncells, 1)) || dalloc(c, &c->d_gm_partial, sizeof(double) * 10 * kGmBlocks) ||
       dalloc(c, &c->d_gm_done, sizeof(unsigned)) || dalloc(c, &c->d_defer_list, sizeof(int) * std::max(c->ncells, 1)))
     return bail(TRMCR_ENOMEM);
-  c->d_ovf_count = c->d_defer_count + 1;
+  c->d_defer_count = c->d_cnt; c->d_ovf_count = c->d_cnt + 1; c->d_defer2_count = c->d_cnt + 2;
+  if (const char *pe = getenv("TRMCR_PDL")) c->use_pdl = atoi(pe) != 0;
   if (cudaMallocHost(&c->h_defer, 2 * sizeof(int)) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_defer, cudaEventDisableTiming) != cudaSuccess) {
     fail(c, TRMCR_ENOMEM, "pinned host / event allocation failed");
@@ -499,6 +535,7 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
   c->P.err = c->d_err;
   if (cudaMemsetAsync(c->d_gm_done, 0, sizeof(unsigned), c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->d_cnt, 0, 8 * sizeof(int), c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->d_stats, 0, sizeof(double) * TRMCR_NSTATS * std::max(c->ncells, 1), c->stream) != cudaSuccess) {
     fail(c, TRMCR_ECUDA, "memset failed");
     return bail(TRMCR_ECUDA);
@@ -596,6 +633,7 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, cell_step_smem<float, 256>, 256, dyn);
       occ_s = occ_s * 256 / c->smem_threads;
     }
+    if (const char *pe = getenv("TRMCR_THERMAL_PREFETCH")) c->thermal_prefetch = atoi(pe);
     c->fast_grid = std::max(1, std::min((c->ncells + kThermalWarps - 1) / kThermalWarps, nsm * std::max(occ_t, 1)));
     c->smem_grid = std::max(1, std::min(c->ncells, nsm * std::max(occ_s, 1)));
     if (c->geometry == TRMCR_SHOCK_1D) c->fast_ok = 0;
