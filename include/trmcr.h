@@ -191,6 +191,14 @@ trmcr_status trmcr_step_host(trmcr_ctx *ctx, const void *vx, const void *vy, con
  * ECAPACITY at the next sync if more than `capacity` particles emigrate or a
  * particle crosses a whole slab. */
 int64_t trmcr_exchange_bytes(int32_t dtype, int64_t capacity);
+/* Sort diagnostics of the last shock step (syncs): out[0] = max cell
+ * displacement W of a local particle, out[1] = emigrant scan width, out[2] = 1
+ * when the scatter sort could not be used and the collision
+ * kernels gathered instead (a tile's destinations spanned more than 64 cells
+ * or an edge particle landed more than 4096 cells from its edge), out[3] = 1
+ * when the scatter sort is enabled for this context.  EINVAL for a
+ * homogeneous context. */
+trmcr_status trmcr_shock_sort_info(trmcr_ctx *ctx, int64_t *out4);
 trmcr_status trmcr_shock_set_exchange(trmcr_ctx *ctx, void *send_left, void *send_right,
                                       void *recv_left, void *recv_right, int64_t capacity);
 trmcr_status trmcr_shock_begin(trmcr_ctx *ctx);
@@ -210,7 +218,7 @@ int64_t trmcr_launch_count(const trmcr_ctx *ctx);
 enum {
   TRMCR_K_CELL_SMEM = 0, TRMCR_K_CELL_GMEM, TRMCR_K_MOMENTS, TRMCR_K_GHOST_COUNT, TRMCR_K_GHOST_GEN,
   TRMCR_K_TRANSPORT, TRMCR_K_SCAN, TRMCR_K_SHOCK_SMEM, TRMCR_K_SHOCK_GMEM, TRMCR_K_THERMAL,
-  TRMCR_K_CELL_WARP, TRMCR_K_SHOCK_WARP, TRMCR_NKERNELS
+  TRMCR_K_CELL_WARP, TRMCR_K_SHOCK_WARP, TRMCR_K_SCATTER, TRMCR_NKERNELS
 };
 trmcr_status trmcr_set_profiling(trmcr_ctx *ctx, int32_t on);
 /* Same, restricted to the kernel ids whose bit is set in `mask` (fewer events

@@ -29,7 +29,7 @@ GLOBAL_FIELDS = ["n", "px", "py", "pz", "energy", "nPxx", "proposals", "accepted
 MOMENT_FIELDS = ["n", "rho", "ux", "uy", "uz", "T", "E", "p", "Pxx", "M4", "M4c", "m_max"]
 KERNELS = ["cell_step_smem", "cell_step_gmem", "moments_kernel", "ghost_count", "ghost_gen",
            "transport_kernel", "scan_offsets", "shock_collide_smem", "shock_collide_gmem",
-           "thermal_warp_kernel", "cell_step_warp", "shock_collide_warp"]
+           "thermal_warp_kernel", "cell_step_warp", "shock_collide_warp", "scatter_sorted"]
 STATS_DTYPE = np.dtype([(f, "<f8") for f in STAT_FIELDS])
 COLL_DTYPE = np.dtype([("cell", "<i4"), ("attempt", "<i4"), ("level", "<i4"), ("accepted", "<i4"),
                        ("j", "<i8"), ("slot_i", "<i8"), ("slot_k", "<i8")])
@@ -83,6 +83,8 @@ def lib():
         L.trmcr_step_host.argtypes = [vp, vp, vp, vp, P(C.c_double)]
         L.trmcr_set_log.argtypes = [vp, C.c_int64]
         L.trmcr_get_log.argtypes = [vp, vp, P(C.c_int64)]
+        L.trmcr_shock_sort_info.argtypes = [C.c_void_p, C.c_void_p]
+        L.trmcr_shock_sort_info.restype = C.c_int
         L.trmcr_exchange_bytes.argtypes = [C.c_int32, C.c_int64]
         L.trmcr_exchange_bytes.restype = C.c_int64
         L.trmcr_shock_set_exchange.argtypes = [vp, vp, vp, vp, vp, C.c_int64]
@@ -263,6 +265,13 @@ class Simulation:
         self._check(lib().trmcr_global_moments(self._h, C.c_void_p(p)))
 
     # ---- slab decomposition of the shock (see include/trmcr.h) ----
+    def sort_info(self) -> dict:
+        """Scatter-sort diagnostics of the last shock step (trmcr_shock_sort_info)."""
+        out = np.zeros(4, dtype=np.int64)
+        self._check(lib().trmcr_shock_sort_info(self._h, out.ctypes.data))
+        return {"W": int(out[0]), "emigrant_width": int(out[1]), "gathered": bool(out[2]),
+                "scatter_enabled": bool(out[3])}
+
     def exchange_bytes(self, capacity: int) -> int:
         return int(lib().trmcr_exchange_bytes(self.dtype, int(capacity)))
 

@@ -126,7 +126,12 @@ struct ShockState {
   void *gv[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
   int32_t *d_counts = nullptr;              // [C] particles per destination cell
   int *d_ng = nullptr;                      // [2] ghosts generated this step
-  int *d_W = nullptr;                       // [2] max local displacement, emigrant scan width
+  int *d_W = nullptr;                       // [3] max local displacement, emigrant scan width, scatter overflow
+  int32_t *d_tileH = nullptr;               // [ntiles][kHist] destination histogram of each transport tile
+  int2 *d_tile_meta = nullptr;              // [ntiles] (first histogram cell dmin, last source cell)
+  int32_t *d_lcnt = nullptr;                // [kEdgeBins] left-edge (ghost + immigrant) particles per cell
+  int ntiles = 0;
+  int scatter = 1;                          // sort by scatter (TRMCR_SHOCK_SCATTER=0: gather in the collide kernel)
   unsigned long long *d_acct = nullptr;     // [4] injected L, injected R, dropped, generated
 };
 

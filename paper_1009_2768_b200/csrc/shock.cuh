@@ -9,7 +9,13 @@
 //   transport_kernel          x <- x + v_x dt (splitting); destination
 //                             cell; per-cell counts; max displacement W
 //   scan_offsets              exclusive scan -> new offsets (capacity check)
-//   shock_collide_smem/gmem   per destination cell: stable gather of its
+//   edge_place                ghosts + immigrants (few) placed at their stable
+//                             positions at the ends of their cells
+//   scatter_sorted            interior particles placed at their stable
+//                             positions: tile histograms from transport_kernel,
+//                             look-back over earlier tiles, in-tile ranks
+//   shock_collide_warp        per cell, in place on the sorted arrays
+//   shock_collide_smem/gmem   deferred cells: stable gather of their
 //                             particles from the source window [c-W, c+W] in
 //                             canonical order (left ghosts, interior in array
 //                             order, right ghosts), then the collision step
@@ -205,19 +211,21 @@ __global__ void ghost_gen(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, c
 // (a destination outside the window falls back to a global atomic).
 // W[0] = max local displacement, W[1] = emigrant scan width, acct[2] = dropped.
 constexpr int kTransportThreads = 256, kTransportPer = 4, kHist = 64;
+constexpr int kTile = kTransportThreads * kTransportPer;   // particles per transport tile
+constexpr int kEdgeBins = 4096;   // cells from a domain / slab edge that ghosts and immigrants may reach
 
 template <typename Real>
 __global__ void __launch_bounds__(kTransportThreads)
 transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const Real *__restrict__ vx,
-                 int32_t *dest, int32_t *counts, int *W, unsigned long long *acct) {
+                 int32_t *dest, int32_t *counts, int *W, unsigned long long *acct, int32_t *tileH, int2 *tile_meta) {
   __shared__ int s_hist[kHist];
-  __shared__ int s_red[3][kTransportThreads / 32];
+  __shared__ int s_red[4][kTransportThreads / 32];
   __shared__ int s_dmin;
   const int64_t n = off_old[S.C];
   const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kTransportPer;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int d[kTransportPer];
-  int disp = 0, emi = 0, dropped = 0, dmin = INT32_MAX;
+  int disp = 0, emi = 0, dropped = 0, dmin = INT32_MAX, smax = -1;
   Real xs[kTransportPer], vs[kTransportPer];
   const bool vec = (i0 + kTransportPer <= n) && (sizeof(Real) * kTransportPer == 16);
   if (vec) {
@@ -237,6 +245,7 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
     d[k] = -1;
     if (i0 + k >= n) continue;
     const int src = cell_of(S, (double)xs[k]) - S.cbase;
+    smax = max(smax, src);
     const Real xn = add_rn<Real>(xs[k], mul_rn<Real>(vs[k], (Real)S.dt));
     xs[k] = xn;
     const double xd = (double)xn;
@@ -268,15 +277,17 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
   dmin = __reduce_min_sync(0xffffffffu, dmin);
   const int wd = __reduce_max_sync(0xffffffffu, disp), we = __reduce_max_sync(0xffffffffu, emi);
   const int wdr = __reduce_add_sync(0xffffffffu, dropped);
+  const int wsm = __reduce_max_sync(0xffffffffu, smax);
   if (threadIdx.x < kHist) s_hist[threadIdx.x] = 0;
-  if (lane == 0) { s_red[0][warp] = dmin; s_red[1][warp] = wd; s_red[2][warp] = we; }
+  if (lane == 0) { s_red[0][warp] = dmin; s_red[1][warp] = wd; s_red[2][warp] = we; s_red[3][warp] = wsm; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int m = INT32_MAX, md = 0, me = 0;
+    int m = INT32_MAX, md = 0, me = 0, ms = -1;
     for (int w = 0; w < kTransportThreads / 32; ++w) {
-      m = min(m, s_red[0][w]); md = max(md, s_red[1][w]); me = max(me, s_red[2][w]);
+      m = min(m, s_red[0][w]); md = max(md, s_red[1][w]); me = max(me, s_red[2][w]); ms = max(ms, s_red[3][w]);
     }
     s_dmin = m;
+    if (tile_meta) tile_meta[blockIdx.x] = make_int2(m, ms);
     if (md > 0 && md > *((volatile int *)W)) atomicMax(W, md);
     if (me > 0 && me > *((volatile int *)(W + 1))) atomicMax(W + 1, me);
   }
@@ -288,10 +299,14 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
     if (d[k] < 0) continue;
     const int h = d[k] - base;
     if (h < kHist) atomicAdd(&s_hist[h], 1);
-    else atomicAdd(&counts[d[k]], 1);
+    else { atomicAdd(&counts[d[k]], 1); if (tileH) W[2] = 1; }   // scatter sort not possible this step
   }
   __syncthreads();
-  if (threadIdx.x < kHist && s_hist[threadIdx.x] > 0) atomicAdd(&counts[base + threadIdx.x], s_hist[threadIdx.x]);
+  if (threadIdx.x < kHist) {
+    const int h = s_hist[threadIdx.x];
+    if (h > 0) atomicAdd(&counts[base + threadIdx.x], h);
+    if (tileH) tileH[(size_t)blockIdx.x * kHist + threadIdx.x] = h;
+  }
 }
 
 // ---- slab exchange: pack emigrants (stable, canonical order) ----
@@ -390,6 +405,170 @@ __global__ void immigrant_count(ShockDev S, const void *recv_l, const void *recv
   atomicMax(W, side == 0 ? d + 1 : S.C - d);
 }
 
+// ---- A2 by scatter: ghosts and immigrants (canonical order) ----
+// side 0: left reservoir ghosts, then left immigrants: the first particles of
+// their cells, pos = off_new[d] + running count; lcnt[d] = how many (read by
+// scatter_sorted).  side 1: right immigrants, then right reservoir ghosts: the
+// last particles of their cells, pos = off_new[d + 1] - total[d] + running.
+// One warp per side (these segments hold a few hundred particles).
+template <typename Real>
+__global__ void __launch_bounds__(32)
+edge_place(ShockDev S, const int64_t *__restrict__ off_new, const int *ng, const void *recv_l, const void *recv_r,
+           int xcap, const Real *gx0, const Real *gvx0, const Real *gvy0, const Real *gvz0, const int32_t *gd0,
+           const Real *gx1, const Real *gvx1, const Real *gvy1, const Real *gvz1, const int32_t *gd1,
+           int32_t *lcnt, Real *ox, Real *ovx, Real *ovy, Real *ovz, int *W) {
+  __shared__ int run[kEdgeBins];
+  __shared__ int tot[kEdgeBins];
+  const int side = blockIdx.x, lane = threadIdx.x;
+  for (int b = lane; b < kEdgeBins; b += 32) { run[b] = 0; tot[b] = 0; }
+  __syncwarp();
+  // segment order for this side: side 0: ghosts(0), immigrants(0); side 1: immigrants(1), ghosts(1)
+  for (int pass = side == 0 ? 1 : 0; pass < 2; ++pass) {    // side 1: pass 0 counts, pass 1 places
+    for (int seg = 0; seg < 2; ++seg) {
+      const bool ghosts = (side == 0) == (seg == 0);
+      int cnt = 0, shift = 0;
+      const Real *px, *pvx, *pvy, *pvz;
+      const int32_t *pd;
+      if (ghosts) {
+        if (side == 0 ? S.has_left : S.has_right) continue;
+        cnt = ng[side];
+        px = side ? gx1 : gx0; pvx = side ? gvx1 : gvx0; pvy = side ? gvy1 : gvy0; pvz = side ? gvz1 : gvz0;
+        pd = side ? gd1 : gd0;
+      } else {
+        const void *rb = side == 0 ? recv_l : recv_r;
+        if (rb == nullptr) continue;
+        const XBuf<Real> X = XBuf<Real>::bind(const_cast<void *>(rb), xcap);
+        cnt = min(*X.count, xcap);
+        px = X.x; pvx = X.vx; pvy = X.vy; pvz = X.vz; pd = X.dest;
+        shift = S.cbase;                      // immigrants carry global destinations
+      }
+      for (int k0 = 0; k0 < cnt; k0 += 32) {
+        const int k = k0 + lane;
+        int d = -1;
+        if (k < cnt) {
+          const int dd = pd[k];
+          if (dd != kDropped && dd - shift >= 0 && dd - shift < S.C) d = dd - shift;
+        }
+        const int bin = d < 0 ? -1 : (side == 0 ? d : S.C - 1 - d);
+        if (bin >= kEdgeBins) W[2] = 1;     // out of reach of the edge bins: gather this step
+        const bool ok = bin >= 0 && bin < kEdgeBins;
+        const unsigned peers = __match_any_sync(0xffffffffu, ok ? bin : -1 - lane);
+        const int leader = __ffs(peers) - 1;
+        if (side == 1 && pass == 0) {
+          if (ok && leader == lane) tot[bin] += __popc(peers);
+        } else {
+          int rank = 0;
+          if (ok) rank = run[bin] + __popc(peers & ((1u << lane) - 1u));
+          __syncwarp();
+          if (ok && leader == lane) run[bin] += __popc(peers);
+          if (ok) {
+            const int64_t pos = side == 0 ? off_new[d] + rank : off_new[d + 1] - tot[bin] + rank;
+            ox[pos] = px[k]; ovx[pos] = pvx[k]; ovy[pos] = pvy[k]; ovz[pos] = pvz[k];
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+  if (side == 0)
+    for (int b = lane; b < kEdgeBins; b += 32) lcnt[b] = run[b];
+}
+
+// ---- A2 by scatter: interior particles ----
+// Tile t = transport tile t (kTile consecutive particles of the cell-sorted
+// source array).  A particle's stable position in its destination cell d is
+// off_new[d] + lcnt[d] + (particles of earlier tiles with destination d) +
+// (its rank among the tile's particles with destination d, in index order).
+// Earlier tiles are looked back over until one whose last source cell is more
+// than W cells before the tile's first destination (none of its particles, nor
+// any earlier one, can reach it); transport_kernel stored each tile's
+// destination histogram over [dmin, dmin + kHist).
+constexpr int kScatterThreads = 256;
+template <typename Real>
+__global__ void __launch_bounds__(kScatterThreads)
+scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *__restrict__ off_new,
+               const Real *__restrict__ x, const Real *__restrict__ vx, const Real *__restrict__ vy,
+               const Real *__restrict__ vz, const int32_t *__restrict__ dest, const int32_t *__restrict__ tileH,
+               const int2 *__restrict__ tile_meta, const int32_t *__restrict__ lcnt, const int *W, Real *ox,
+               Real *ovx, Real *ovy, Real *ovz) {
+  constexpr int NW = kScatterThreads / 32, PARTS = kScatterThreads / kHist;
+  __shared__ int s_pre[kHist], s_run[kHist];
+  __shared__ int s_part[PARTS][kHist];
+  __shared__ int s_wc[NW][kHist];
+  __shared__ int2 s_meta[32];
+  __shared__ int s_nb, s_more;
+  const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (W[2]) return;                                   // gather fallback this step
+  const int64_t n = off_old[S.C];
+  const int64_t i_begin = (int64_t)t * kTile;
+  if (i_begin >= n) return;
+  const int dmin = tile_meta[t].x;
+  if (dmin == INT32_MAX) return;                     // no local destination in this tile
+  const int Wd = W[0];
+  // ---- prefix per bin: lcnt + look-back over earlier tiles, 32 at a time ----
+  const int b = tid & (kHist - 1), part = tid / kHist;
+  int acc = 0;
+  for (int t0 = t - 1;; t0 -= 32) {
+    if (warp == 0) {
+      const int tp = t0 - lane;
+      int2 m = make_int2(INT32_MAX, -1);
+      bool stop = tp < 0;
+      if (!stop) { m = tile_meta[tp]; stop = m.y + Wd < dmin; }
+      const unsigned st = __ballot_sync(0xffffffffu, stop);
+      const int nb = st ? __ffs(st) - 1 : 32;
+      s_meta[lane] = m;
+      if (lane == 0) { s_nb = nb; s_more = st == 0u; }
+    }
+    __syncthreads();
+    const int nb = s_nb;
+    for (int j = part; j < nb; j += PARTS) {
+      const int2 m = s_meta[j];
+      const int bb = dmin + b - m.x;
+      if (m.x != INT32_MAX && bb >= 0 && bb < kHist) acc += tileH[(size_t)(t0 - j) * kHist + bb];
+    }
+    const int more = s_more;
+    __syncthreads();
+    if (!more) break;
+  }
+  s_part[part][b] = acc;
+  if (tid < kHist) s_run[tid] = 0;
+  __syncthreads();
+  if (tid < kHist) {
+    int p = 0;
+#pragma unroll
+    for (int q = 0; q < PARTS; ++q) p += s_part[q][tid];
+    const int d = dmin + tid;
+    if (d < kEdgeBins && d < S.C) p += lcnt[d];
+    s_pre[tid] = p;
+  }
+  // ---- in-tile stable ranks, kScatterThreads particles per round in index order ----
+  for (int64_t r0 = i_begin; r0 < i_begin + kTile && r0 < n; r0 += kScatterThreads) {
+    const int64_t i = r0 + tid;
+    int d = -1;
+    if (i < n) d = dest[i];
+    const bool loc = d >= 0 && d < S.C && d - dmin < kHist;
+    const int bin = loc ? d - dmin : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, loc ? bin : -1 - lane);
+    for (int q = tid; q < NW * kHist; q += kScatterThreads) (&s_wc[0][0])[q] = 0;
+    __syncthreads();
+    if (loc && __ffs(peers) - 1 == lane) s_wc[warp][bin] = __popc(peers);
+    __syncthreads();
+    if (loc) {
+      int rank = s_run[bin] + __popc(peers & ((1u << lane) - 1u));
+      for (int w = 0; w < warp; ++w) rank += s_wc[w][bin];
+      const int64_t pos = off_new[d] + s_pre[bin] + rank;
+      ox[pos] = x[i]; ovx[pos] = vx[i]; ovy[pos] = vy[i]; ovz[pos] = vz[i];
+    }
+    __syncthreads();
+    if (tid < kHist) {
+      int a = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) a += s_wc[w][tid];
+      s_run[tid] += a;
+    }
+  }
+}
+
 struct GatherSrc {
   const int64_t *off_old;
   const int *ng;
@@ -401,6 +580,7 @@ struct GatherSrc {
   const int32_t *dest;
   const void *gx[2], *gvx[2], *gvy[2], *gvz[2];
   const int32_t *gdest[2];
+  int scatter;                        // 1: scatter_sorted placed the particles (unless W[2] is set)
 };
 
 // Stable gather of destination cell c into (bx,by,bz) [velocities] and ox
@@ -585,6 +765,7 @@ shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
   double *usplit;
   bind_warp_slab(B, slab, Lay, usplit);
   const int nw = gridDim.x * (blockDim.x >> 5);
+  const bool sorted = G.scatter && !Lay.v_smem && G.W[2] == 0;
   for (int c = blockIdx.x * (blockDim.x >> 5) + warp; c < S.C; c += nw) {
     const int64_t base = off_new[c];
     const int n = (int)(off_new[c + 1] - base);
@@ -592,7 +773,12 @@ shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
     if (n <= Lay.n_cap) {
       double sx, sy, sz;
       if (!Lay.v_smem) { B.vx = ovx + base; B.vy = ovy + base; B.vz = ovz + base; }   // work in place (L1)
-      gather_cell_warp<Real>(S, G, c, B.vx, B.vy, B.vz, ox + base, Lay.n_cap, sx, sy, sz);
+      if (sorted) {                        // already in place: sums of the cell
+        sx = 0; sy = 0; sz = 0;
+        for (int i = lane; i < n; i += 32) { sx += B.vx[i]; sy += B.vy[i]; sz += B.vz[i]; }
+      } else {
+        gather_cell_warp<Real>(S, G, c, B.vx, B.vy, B.vz, ox + base, Lay.n_cap, sx, sy, sz);
+      }
       if (n == 0) {
         if (lane == 0) {
           double *s = stats + (size_t)c * TRMCR_NSTATS;
@@ -709,7 +895,7 @@ inline trmcr_status shock_init(trmcr_ctx *c, const trmcr_cells *cc, int *max_cel
   s.cap_g = (int)floor(ymax) + 2;   // IR(y) <= floor(y) + 1
   if (dalloc(c, &s.d_off[0], sizeof(int64_t) * (s.C + 1)) || dalloc(c, &s.d_off[1], sizeof(int64_t) * (s.C + 1)) ||
       dalloc(c, &s.d_dest, sizeof(int32_t) * (size_t)c->cap) || dalloc(c, &s.d_counts, sizeof(int32_t) * s.C) ||
-      dalloc(c, &s.d_ng, sizeof(int) * 2) || dalloc(c, &s.d_W, sizeof(int) * 2) ||
+      dalloc(c, &s.d_ng, sizeof(int) * 2) || dalloc(c, &s.d_W, sizeof(int) * 3) ||
       dalloc(c, &s.d_acct, sizeof(unsigned long long) * 4))
     return TRMCR_ENOMEM;
   for (int k = 0; k < 2; ++k) {
@@ -717,6 +903,12 @@ inline trmcr_status shock_init(trmcr_ctx *c, const trmcr_cells *cc, int *max_cel
     for (int j = 0; j < 3; ++j)
       if (dalloc(c, &s.gv[k][j], c->rs * s.cap_g)) return TRMCR_ENOMEM;
   }
+  if (const char *se = getenv("TRMCR_SHOCK_SCATTER")) s.scatter = atoi(se) != 0;
+  s.ntiles = (int)((c->cap + kTile - 1) / kTile);
+  if (s.scatter && (dalloc(c, &s.d_tileH, sizeof(int32_t) * kHist * (size_t)std::max(s.ntiles, 1)) ||
+                    dalloc(c, &s.d_tile_meta, sizeof(int2) * (size_t)std::max(s.ntiles, 1)) ||
+                    dalloc(c, &s.d_lcnt, sizeof(int32_t) * kEdgeBins)))
+    return TRMCR_ENOMEM;
   CUDA_TRY(c, cudaMemsetAsync(s.d_counts, 0, sizeof(int32_t) * s.C, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(s.d_acct, 0, sizeof(unsigned long long) * 4, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(s.d_ng, 0, sizeof(int) * 2, c->stream));
@@ -753,7 +945,7 @@ trmcr_status shock_begin(trmcr_ctx *c) {
   const int cur = c->cur;
   CUDA_TRY(c, cudaMemsetAsync(c->d_ovf_count, 0, sizeof(int), c->stream));
   CUDA_TRY(c, cudaMemsetAsync(s.d_counts, 0, sizeof(int32_t) * s.C, c->stream));
-  CUDA_TRY(c, cudaMemsetAsync(s.d_W, 0, 2 * sizeof(int), c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(s.d_W, 0, 3 * sizeof(int), c->stream));
   CUDA_TRY(c, cudaMemsetAsync(s.d_acct, 0, sizeof(unsigned long long) * 4, c->stream));
   prof_begin(c, TRMCR_K_GHOST_COUNT);
   ghost_count<<<1, 32, 0, c->stream>>>(d, c->P.k0, c->P.k1, c->step, s.d_ng, c->d_err);
@@ -771,9 +963,10 @@ trmcr_status shock_begin(trmcr_ctx *c) {
     const int per_block = kTransportThreads * kTransportPer;
     const unsigned blocks = (unsigned)((c->cap + per_block - 1) / per_block);
     prof_begin(c, TRMCR_K_TRANSPORT);
-    transport_kernel<Real><<<blocks, kTransportThreads, 0, c->stream>>>(d, s.d_off[cur], (Real *)c->x[cur],
-                                                          (const Real *)c->v[cur][0], s.d_dest, s.d_counts,
-                                                          s.d_W, s.d_acct);
+    const bool sc = s.scatter && c->wlay.n_cap > 0 && !c->wlay.v_smem;
+    transport_kernel<Real><<<blocks, kTransportThreads, 0, c->stream>>>(
+        d, s.d_off[cur], (Real *)c->x[cur], (const Real *)c->v[cur][0], s.d_dest, s.d_counts, s.d_W, s.d_acct,
+        sc ? s.d_tileH : nullptr, sc ? s.d_tile_meta : nullptr);
     if (auto e = check_launch(c, "transport_kernel", TRMCR_K_TRANSPORT)) return e;
   }
   if (s.has_left || s.has_right) {
@@ -820,6 +1013,21 @@ trmcr_status shock_finish(trmcr_ctx *c) {
   c->P.step = c->step;
   Real *ox = (Real *)c->x[nxt], *ovx = (Real *)c->v[nxt][0], *ovy = (Real *)c->v[nxt][1], *ovz = (Real *)c->v[nxt][2];
   const bool use_warp = c->wlay.n_cap > 0;
+  G.scatter = s.scatter && use_warp && !c->wlay.v_smem;
+  if (G.scatter) {
+    prof_begin(c, TRMCR_K_SCATTER);
+    edge_place<Real><<<2, 32, 0, c->stream>>>(
+        d, s.d_off[nxt], s.d_ng, G.recv[0], G.recv[1], s.xcap, (const Real *)s.gx[0], (const Real *)s.gv[0][0],
+        (const Real *)s.gv[0][1], (const Real *)s.gv[0][2], s.d_gdest[0], (const Real *)s.gx[1],
+        (const Real *)s.gv[1][0], (const Real *)s.gv[1][1], (const Real *)s.gv[1][2], s.d_gdest[1], s.d_lcnt, ox,
+        ovx, ovy, ovz, s.d_W);
+    if (auto e = check_launch(c, "edge_place")) return e;
+    scatter_sorted<Real><<<std::max(s.ntiles, 1), kScatterThreads, 0, c->stream>>>(
+        d, s.d_off[cur], s.d_off[nxt], (const Real *)c->x[cur], (const Real *)c->v[cur][0],
+        (const Real *)c->v[cur][1], (const Real *)c->v[cur][2], s.d_dest, s.d_tileH, s.d_tile_meta, s.d_lcnt,
+        s.d_W, ox, ovx, ovy, ovz);
+    if (auto e = check_launch(c, "scatter_sorted", TRMCR_K_SCATTER)) return e;
+  }
   if (use_warp) {
     CUDA_TRY(c, cudaMemsetAsync(c->d_defer_count, 0, sizeof(int), c->stream));
     prof_begin(c, TRMCR_K_SHOCK_WARP);

@@ -704,6 +704,17 @@ int64_t trmcr_exchange_bytes(int32_t dtype, int64_t capacity) {
   return dtype == TRMCR_F64 ? (int64_t)XBuf<double>::bytes((int)capacity) : (int64_t)XBuf<float>::bytes((int)capacity);
 }
 
+trmcr_status trmcr_shock_sort_info(trmcr_ctx *c, int64_t *out4) {
+  if (!c || !out4) return fail(c, TRMCR_EINVAL, "null argument");
+  if (c->geometry != TRMCR_SHOCK_1D) return fail(c, TRMCR_EINVAL, "not a shock context");
+  int w[3] = {0, 0, 0};
+  CUDA_TRY(c, cudaMemcpyAsync(w, c->shock.d_W, sizeof(w), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  out4[0] = w[0]; out4[1] = w[1]; out4[2] = w[2];
+  out4[3] = c->shock.scatter && c->wlay.n_cap > 0 && !c->wlay.v_smem;
+  return TRMCR_OK;
+}
+
 trmcr_status trmcr_shock_set_exchange(trmcr_ctx *c, void *send_left, void *send_right, void *recv_left,
                                       void *recv_right, int64_t capacity) {
   if (!c || capacity <= 0 || capacity > (1 << 28)) return fail(c, TRMCR_EINVAL, "bad argument");
