@@ -143,9 +143,9 @@ int32_t orc_split(double p, int64_t n, int32_t m, uint64_t seed, uint32_t gcell,
 }
 
 /* ===================================================================== */
-/* Keyed permutation: 4-round (unbalanced) Feistel with cycle walking.    */
-/* Realises "a random choice" of f_0 particles and of stored particles     */
-/* as uniform draws without replacement [R17].                */
+/* Keyed permutation: Feistel on a mixed-radix domain with cycle walking.  */
+/* walking.  Realises "a random choice" of f_0 particles and of stored     */
+/* particles as uniform draws without replacement [R17].      */
 /* ===================================================================== */
 static uint32_t mix32(uint32_t x) {
   x ^= x >> 16; x *= 0x7feb352du;
@@ -154,25 +154,35 @@ static uint32_t mix32(uint32_t x) {
   return x;
 }
 
-/* Domain 2^b with b = ceil(log2 N); the state splits into L (a = floor(b/2)
- * bits, high) and R (c = b - a bits, low).  Round i: (L, R) <- (R, L ^ (F(R,
- * k_i) mod 2^width(L))), so the widths alternate and return after 4 rounds. */
+/* Domain Z_A x Z_C with A = ceil(sqrt(N)), C = ceil(N / A), so that
+ * N <= A C < N + A (cycle walking rejects less than 1/sqrt(N) of the points).
+ * x = L C + R with L in Z_A, R in Z_C.  Round i (i = 0..R-1):
+ *   (L, R) <- (R, (L + f_i(R)) mod |L|),  f_i(R) = floor(mix32(R ^ k_i) |L| / 2^32),
+ * |L| the size of the half being replaced (sizes alternate; R is even, so they
+ * are back to (A, C) at the end), k_i = key[i mod 4] + floor(i / 4) 0x9E3779B9
+ * (mod 2^32), y = L C + R; the walk repeats the rounds until y < N.  Each
+ * round is a bijection Z_A x Z_C -> Z_C x Z_A.  Rounds: R = 16 for N <= 64,
+ * else 8 — fewer rounds leave a measurable pair bias (adjacent images over-
+ * represented; R17, tests/test_oracle_primitives.py). */
 int64_t orc_feistel(uint64_t x, uint64_t N, const uint32_t rk[4]) {
   if (N <= 1) return (int64_t)x;
-  int b = 0;
-  while ((1ull << b) < N) b++;
-  const int a = b / 2, c = b - a;
-  uint64_t y = x;
+  uint64_t A = 1;
+  while (A * A < N) A++;
+  const uint64_t C = (N + A - 1) / A;
+  const int rounds = N <= 64 ? 16 : 8;
+  uint64_t L = x / C, R = x % C, y;
   do {
-    uint64_t L = y >> c, R = y & ((1ull << c) - 1ull);
-    int wl = a, wr = c;
-    for (int i = 0; i < 4; i++) {
-      uint64_t t = L ^ ((uint64_t)mix32((uint32_t)R ^ rk[i]) & ((1ull << wl) - 1ull));
+    uint64_t wl = A, wr = C;
+    for (int i = 0; i < rounds; i++) {
+      const uint32_t k = rk[i & 3] + (uint32_t)(i >> 2) * 0x9E3779B9u;
+      const uint64_t f = ((uint64_t)mix32((uint32_t)R ^ k) * wl) >> 32;
+      uint64_t t = L + f;
+      if (t >= wl) t -= wl;
       L = R;
       R = t;
-      int w = wl; wl = wr; wr = w;
+      const uint64_t w = wl; wl = wr; wr = w;
     }
-    y = (L << c) | R;
+    y = L * C + R;
   } while (y >= N);
   return (int64_t)y;
 }

@@ -61,6 +61,7 @@ struct CellBuf {
   int32_t *cnt;            // [L_cap+1] per-type counter of the current level
   uint4 *rk;               // [L_cap+1] permutation keys of pools
   uint32_t *mask;          // [ceil(n_cap/32)] Theta membership
+  PermDom *pdom;           // [L_cap+1] warp kernel: domain of pool p's permutation (or null)
   double *red;             // [32*8] reduction scratch
   int n_cap, K_cap, L_cap;
 };

@@ -27,13 +27,14 @@ struct WarpShared {
 struct WarpSlabLayout {
   int n_cap, K_cap, L_cap, v_smem;   // v_smem = 0: the cell's velocities live in global memory
   size_t per_warp;   // bytes of one warp's slab incl. WarpShared (16-byte multiple)
-  size_t off_v, off_ctype, off_crank, off_cslot, off_ints, off_rk, off_u, off_red, off_sh;
+  size_t off_v, off_ctype, off_crank, off_cslot, off_ints, off_rk, off_pdom, off_u, off_red, off_sh;
   void build(int n, int K, int L, size_t rs, int v_in_smem) {
     n_cap = n; K_cap = K; L_cap = L; v_smem = v_in_smem;
     size_t o = 0;
     auto al = [&](size_t a) { o = (o + a - 1) / a * a; };
     off_red = o; o += 8 * sizeof(double);
     al(16); off_rk = o; o += (size_t)(L + 1) * sizeof(uint4);
+    off_pdom = o; o += (size_t)(L + 1) * sizeof(PermDom);
     off_u = o; o += (size_t)kSplitPre * sizeof(double);
     al(16); off_v = o; if (v_in_smem) o += 3 * (size_t)n * rs;
     al(16); off_ctype = o; o += (size_t)K * 4;
@@ -60,6 +61,7 @@ __device__ __forceinline__ void bind_warp_slab(CellBuf<Real> &B, unsigned char *
   const int Lp = Lay.L_cap + 1;
   B.Q = ints; B.C = ints + Lp; B.S = ints + 2 * Lp; B.cons = ints + 3 * Lp;
   B.base = ints + 4 * Lp; B.cnt = ints + 5 * Lp;
+  B.pdom = reinterpret_cast<PermDom *>(base + Lay.off_pdom);
   B.mask = nullptr;
   B.n_cap = Lay.n_cap; B.K_cap = Lay.K_cap; B.L_cap = Lay.L_cap;
 }
@@ -149,7 +151,10 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
   for (int d = lane; d <= top; d += 32) {
     B.base[d] = 0;
     B.cnt[d] = 0;
-    if (d >= 1) B.rk[d] = K(kPerm, sh.r, d, 0);
+    if (d >= 1) {
+      B.rk[d] = K(kPerm, sh.r, d, 0);
+      B.pdom[d] = perm_dom(2u * (uint32_t)B.C[d]);
+    }
   }
   __syncwarp();
   unsigned acc = 0, viol = 0;
@@ -186,17 +191,16 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
       const uint32_t rank = B.crank[Sd + j];
       const uint32_t t[2] = {(uint32_t)B.base[a] + rank, (uint32_t)(B.base[b] + B.cnt[b]) + rank};
       const uint32_t pool[2] = {a, b};
+      // one code path for both sides (pool 0: pi0 at leaf_off + t; pool p:
+      // pi_p at t, then its output slot), cycle walks interleaved
+      uint32_t y[2];
+      perm_eval2(a == 0 ? (uint32_t)leaf_off + t[0] : t[0], a == 0 ? pi0.rk : B.rk[a], a == 0 ? pi0.D : B.pdom[a],
+                 b == 0 ? (uint32_t)leaf_off + t[1] : t[1], b == 0 ? pi0.rk : B.rk[b], b == 0 ? pi0.D : B.pdom[b],
+                 y[0], y[1]);
       uint32_t slot[2];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        if (pool[s] == 0) {
-          slot[s] = pi0((uint32_t)leaf_off + t[s]);
-        } else {
-          Perm pp;
-          pp.init(B.rk[pool[s]], 2u * (uint32_t)B.C[pool[s]]);
-          const uint32_t o = pp(t[s]);
-          slot[s] = o == 0xFFFFFFFFu ? o : B.cslot[2u * (uint32_t)B.S[pool[s]] + o];
-        }
+        slot[s] = (pool[s] == 0 || y[s] == 0xFFFFFFFFu) ? y[s] : B.cslot[2u * (uint32_t)B.S[pool[s]] + y[s]];
         if (slot[s] >= (uint32_t)n) { atomicOr(P.err, kErrInternal); slot[s] = 0; }
       }
       B.cslot[2 * (Sd + j)] = slot[0];

@@ -50,6 +50,7 @@ __device__ __forceinline__ void bind_smem(CellBuf<Real> &B, unsigned char *base,
   B.Q = ints; B.C = ints + Lp; B.S = ints + 2 * Lp; B.cons = ints + 3 * Lp;
   B.base = ints + 4 * Lp; B.cnt = ints + 5 * Lp;
   B.mask = reinterpret_cast<uint32_t *>(base + Lay.off_mask);
+  B.pdom = nullptr;
   B.n_cap = Lay.n_cap; B.K_cap = Lay.K_cap; B.L_cap = Lay.L_cap;
 }
 
@@ -73,6 +74,7 @@ __device__ __forceinline__ void bind_gmem(CellBuf<Real> &B, const GmemScratch &G
   B.Q = ints; B.C = ints + Lp; B.S = ints + 2 * Lp; B.cons = ints + 3 * Lp;
   B.base = ints + 4 * Lp; B.cnt = ints + 5 * Lp;
   B.mask = reinterpret_cast<uint32_t *>(p);
+  B.pdom = nullptr;
   B.n_cap = G.n_cap; B.K_cap = G.K_cap; B.L_cap = G.L_cap;
 }
 

@@ -48,7 +48,7 @@ __device__ __forceinline__ float u24(uint32_t w) {
   return (static_cast<float>(w >> 9) + 0.5f) * 0x1p-23f;
 }
 
-// ---- keyed bijection of [0, N): 4-round balanced Feistel + cycle walking ----
+// ---- keyed bijection of [0, N): Feistel on Z_A x Z_C + cycle walking ----
 __device__ __forceinline__ uint32_t mix32(uint32_t x) {
   x ^= x >> 16; x *= 0x7feb352du;
   x ^= x >> 15; x *= 0x846ca68bu;
@@ -56,43 +56,90 @@ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
   return x;
 }
 
-// Domain 2^b, b = ceil(log2 N) (< 2N, so cycle walking takes < 2 rounds on
-// average); L = high a = floor(b/2) bits, R = low c = b - a bits; round i:
-// (L, R) <- (R, L ^ (mix32(R ^ k_i) mod 2^width(L))): widths alternate and are
-// back to (a, c) after 4 rounds.
+// Domain A C with A = ceil(sqrt N), C = ceil(N / A) (N <= A C < N + A, so the
+// walk rarely repeats); x = L C + R.  Round i: (L, R) <- (R, (L + f_i(R)) mod
+// |L|), f_i(R) = umulhi(mix32(R ^ k_i), |L|), k_i = key[i & 3] + (i >> 2)
+// 0x9E3779B9; 16 rounds for N <= 64, else 8 (R17).  The state stays
+// split (L, R) through the walk, so only the first split divides (by
+// multiply-high with one correction step, exact for every 32-bit x).
+struct PermDom {
+  uint32_t N, A, C, m;   // m = floor(2^32 / C) (0 when C == 1)
+};
+__device__ __forceinline__ PermDom perm_dom(uint32_t n) {
+  PermDom D;
+  D.N = n;
+  if (n <= 1u) { D.A = 1u; D.C = 1u; D.m = 0u; return D; }
+  uint32_t a = (uint32_t)sqrtf((float)n);
+  while ((uint64_t)a * a < n) ++a;
+  while (a > 1u && (uint64_t)(a - 1u) * (a - 1u) >= n) --a;
+  D.A = a;
+  D.C = (n + a - 1u) / a;
+  D.m = D.C == 1u ? 0u : (uint32_t)((1ull << 32) / D.C);
+  return D;
+}
+// One round on (L in Z_wl, R): (L, R) <- (R, (L + f(R)) mod wl).  The
+// reduction is min(t, t - wl) (t < 2 wl: t - wl wraps above t when t < wl).
+__device__ __forceinline__ void perm_round(uint32_t &L, uint32_t &R, uint32_t k, uint32_t wl) {
+  const uint32_t t = L + __umulhi(mix32(R ^ k), wl);
+  L = R;
+  R = min(t, t - wl);
+}
+__device__ __forceinline__ void perm_rounds(uint32_t &L, uint32_t &R, const uint4 &rk, const PermDom &D) {
+  const int groups = D.N <= 64u ? 4 : 2;             // 16 or 8 rounds
+  uint32_t kadd = 0u;
+  for (int g = 0; g < groups; ++g, kadd += 0x9E3779B9u) {
+    perm_round(L, R, rk.x + kadd, D.A);
+    perm_round(L, R, rk.y + kadd, D.C);
+    perm_round(L, R, rk.z + kadd, D.A);
+    perm_round(L, R, rk.w + kadd, D.C);
+  }
+}
+__device__ __forceinline__ void perm_split(uint32_t x, const PermDom &D, uint32_t &L, uint32_t &R) {
+  if (D.C == 1u) { L = x; R = 0u; return; }
+  uint32_t q = __umulhi(x, D.m);
+  uint32_t r = x - q * D.C;
+  if (r >= D.C) { ++q; r -= D.C; }
+  L = q; R = r;
+}
+
 struct Perm {
   uint4 rk;
-  uint32_t N, c, mask_a, mask_c;
-  __device__ __forceinline__ void init(uint4 key, uint32_t n) {
-    rk = key;
-    N = n;
-    const uint32_t b = n > 1 ? 32u - __clz(n - 1u) : 1u;
-    const uint32_t a = b >> 1;
-    c = b - a;
-    mask_a = (1u << a) - 1u;
-    mask_c = (c >= 32u) ? 0xFFFFFFFFu : ((1u << c) - 1u);
-  }
-  __device__ __forceinline__ uint32_t round4(uint32_t y) const {
-    uint32_t L = y >> c, R = y & mask_c, t;
-    t = L ^ (mix32(R ^ rk.x) & mask_a); L = R; R = t;   // widths (a,c) -> (c,a)
-    t = L ^ (mix32(R ^ rk.y) & mask_c); L = R; R = t;   // (c,a) -> (a,c)
-    t = L ^ (mix32(R ^ rk.z) & mask_a); L = R; R = t;
-    t = L ^ (mix32(R ^ rk.w) & mask_c); L = R; R = t;
-    return (L << c) | R;
-  }
+  PermDom D;
+  __device__ __forceinline__ void init(uint4 key, uint32_t n) { rk = key; D = perm_dom(n); }
   // Cycle walking.  Out-of-range input or a walk longer than 4096 (impossible
   // for x < N) returns 0xFFFFFFFF.
   __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
-    if (N <= 1u) return x < N || N == 0u ? x : 0xFFFFFFFFu;
-    if (x >= N) return 0xFFFFFFFFu;
-    uint32_t y = round4(x);
-    for (int it = 0; y >= N; ++it) {
+    if (D.N <= 1u) return x < D.N || D.N == 0u ? x : 0xFFFFFFFFu;
+    if (x >= D.N) return 0xFFFFFFFFu;
+    uint32_t L, R;
+    perm_split(x, D, L, R);
+    for (int it = 0;; ++it) {
       if (it > 4096) return 0xFFFFFFFFu;
-      y = round4(y);
+      perm_rounds(L, R, rk, D);
+      const uint32_t y = L * D.C + R;
+      if (y < D.N) return y;
     }
-    return y;
   }
 };
+
+// Two evaluations (x_s under key k_s on domain D_s) with their cycle walks
+// interleaved: the warp pays max(walk_0, walk_1) passes, not the sum, and the
+// two chains are independent work for the scheduler.  Results as Perm().
+__device__ __forceinline__ void perm_eval2(uint32_t x0, const uint4 &k0, const PermDom &D0, uint32_t x1,
+                                           const uint4 &k1, const PermDom &D1, uint32_t &y0, uint32_t &y1) {
+  const bool t0 = D0.N <= 1u || x0 >= D0.N, t1 = D1.N <= 1u || x1 >= D1.N;   // trivial / invalid
+  bool w0 = !t0, w1 = !t1;
+  y0 = t0 ? (x0 < D0.N ? x0 : 0xFFFFFFFFu) : 0u;
+  y1 = t1 ? (x1 < D1.N ? x1 : 0xFFFFFFFFu) : 0u;
+  uint32_t L0 = 0, R0 = 0, L1 = 0, R1 = 0;
+  if (w0) perm_split(x0, D0, L0, R0);
+  if (w1) perm_split(x1, D1, L1, R1);
+  for (int it = 0; w0 || w1; ++it) {
+    if (it > 4096) { if (w0) y0 = 0xFFFFFFFFu; if (w1) y1 = 0xFFFFFFFFu; break; }
+    if (w0) { perm_rounds(L0, R0, k0, D0); y0 = L0 * D0.C + R0; w0 = y0 >= D0.N; }
+    if (w1) { perm_rounds(L1, R1, k1, D1); y1 = L1 * D1.C + R1; w1 = y1 >= D1.N; }
+  }
+}
 
 // ---- programmatic dependent launch (PDL) ----
 // Every kernel of the step starts with pdl_wait(): it returns once the

@@ -753,7 +753,7 @@ __device__ int gather_cell_warp(const ShockDev &S, const GatherSrc &G, int c, Re
 }
 
 template <typename Real>
-__global__ void __launch_bounds__(kWarpCellWarps * 32, 3)
+__global__ void __launch_bounds__(kWarpCellWarps * 32, 2)
 shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, int *defer_count,
                    int *defer_list, QueueArgs Q) {

@@ -96,7 +96,7 @@ cell_step_gmem(StepParams P, GmemScratch G, const int64_t *__restrict__ offsets,
 // General cells, one warp each (cell_warp.cuh), over the thermal kernel's
 // defer list (or every cell); cells that do not fit go to list2 (CTA kernel).
 template <typename Real>
-__global__ void __launch_bounds__(kWarpCellWarps * 32, 3)
+__global__ void __launch_bounds__(kWarpCellWarps * 32, 2)
 cell_step_warp(StepParams P, WarpSlabLayout Lay, const int64_t *__restrict__ offsets, int ncells,
                const int *list_count, const int *list, Real *vx, Real *vy, Real *vz, int32_t *m_state,
                double *stats, int *list2_count, int *list2, QueueArgs Q) {

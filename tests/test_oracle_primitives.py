@@ -75,9 +75,41 @@ def test_ir_two_point_law(orc):
 
 def test_feistel_is_bijection(orc):
     rk = [0x12345678, 0x9ABCDEF0, 0x0F1E2D3C, 0x4B5A6978]
-    for N in [1, 2, 3, 5, 16, 17, 100, 1000, 4097]:
+    # includes C = 1 (N = 2), perfect squares, A C = N exactly, A C - N = A - 1
+    for N in [1, 2, 3, 4, 5, 7, 9, 16, 17, 40, 42, 100, 1000, 1023, 1025, 4097]:
         img = [orc.feistel(x, N, rk) for x in range(N)]
         assert sorted(img) == list(range(N))
+
+
+def test_feistel_adjacent_images_not_favoured(orc):
+    """P(|pi(x) - pi(x+1)| = 1) over 20000 keys equals 2/N for N = 100 and 1000
+    (z < 4.5).  A 4-round Feistel fails this (z ~ 70 at N = 100 with 2M keys:
+    the two outputs of one collision would be re-paired too often)."""
+    rng = np.random.default_rng(11)
+    for N in (100, 1000):
+        K = 20000
+        hit = 0
+        for _ in range(K):
+            rk = rng.integers(0, 2**32, size=4, dtype=np.uint64)
+            hit += abs(orc.feistel(N // 3, N, rk) - orc.feistel(N // 3 + 1, N, rk)) == 1
+        p0 = 2 / N
+        z = (hit / K - p0) / np.sqrt(p0 * (1 - p0) / K)
+        assert abs(z) < 4.5, (N, z)
+
+
+def test_feistel_pairs_uniform_over_keys(orc):
+    """Ordered pair (pi(0), pi(1)) over 9000 keys is uniform on the 90 pairs of
+    distinct values of [0, 10) (chi^2, 89 dof): a uniform draw without
+    replacement, not just uniform marginals."""
+    rng = np.random.default_rng(5)
+    hits = np.zeros((10, 10))
+    for _ in range(9000):
+        rk = rng.integers(0, 2**32, size=4, dtype=np.uint64)
+        hits[orc.feistel(0, 10, rk), orc.feistel(1, 10, rk)] += 1
+    assert np.trace(hits) == 0
+    off = hits[~np.eye(10, dtype=bool)]
+    chi2 = ((off - 100) ** 2 / 100).sum()
+    assert chi2 < 135.0     # p ~ 0.001 for 89 dof
 
 
 def test_feistel_uniform_over_keys(orc):
