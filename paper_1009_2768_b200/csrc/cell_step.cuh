@@ -53,6 +53,9 @@ struct CellBuf {
   uint32_t *ctype;         // [K_cap] type a of collision (level d, j) at S[d]+j
   uint32_t *crank;         // [K_cap] rank among same-type collisions of its level
   uint32_t *cslot;         // [2 K_cap] input/output slots (side 0, side 1)
+  uint8_t *ctype8;         // warp kernel: compact copies of the three above (types < 256,
+  uint16_t *crank16;       //   ranks and slots < 65536), so more warps fit an SM
+  uint16_t *cslot16;
   int32_t *Q;              // [L_cap+1] split quotas N_d
   int32_t *C;              // [L_cap+1] collisions per level
   int32_t *S;              // [L_cap+1] first collision index of level

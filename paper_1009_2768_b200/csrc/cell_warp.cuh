@@ -11,7 +11,10 @@
 
 namespace trmcr {
 
-constexpr int kWarpCellWarps = 8;
+constexpr int kWarpCellWarps = 4;
+#ifndef TRMCR_WARP_MINB
+#define TRMCR_WARP_MINB 5        // CTAs of kWarpCellWarps warps per SM the register budget allows
+#endif
 
 // Per-warp scalars (in the warp's slab, lane 0 writes, __syncwarp publishes).
 struct WarpShared {
@@ -37,9 +40,9 @@ struct WarpSlabLayout {
     off_pdom = o; o += (size_t)(L + 1) * sizeof(PermDom);
     off_u = o; o += (size_t)kSplitPre * sizeof(double);
     al(16); off_v = o; if (v_in_smem) o += 3 * (size_t)n * rs;
-    al(16); off_ctype = o; o += (size_t)K * 4;
-    off_crank = o; o += (size_t)K * 4;
-    off_cslot = o; o += (size_t)K * 8;
+    al(16); off_cslot = o; o += (size_t)K * 4;     // 2 K uint16
+    off_crank = o; o += (size_t)K * 2;             // K uint16
+    off_ctype = o; o += (size_t)K;                 // K uint8
     off_ints = o; o += 6 * (size_t)(L + 1) * 4;
     al(16); off_sh = o; o += sizeof(WarpShared);
     al(16); per_warp = o;
@@ -54,9 +57,10 @@ __device__ __forceinline__ void bind_warp_slab(CellBuf<Real> &B, unsigned char *
   usplit = reinterpret_cast<double *>(base + Lay.off_u);
   Real *v = reinterpret_cast<Real *>(base + Lay.off_v);
   B.vx = v; B.vy = v + Lay.n_cap; B.vz = v + 2 * Lay.n_cap;   // rebound per cell when !v_smem
-  B.ctype = reinterpret_cast<uint32_t *>(base + Lay.off_ctype);
-  B.crank = reinterpret_cast<uint32_t *>(base + Lay.off_crank);
-  B.cslot = reinterpret_cast<uint32_t *>(base + Lay.off_cslot);
+  B.ctype = nullptr; B.crank = nullptr; B.cslot = nullptr;
+  B.ctype8 = reinterpret_cast<uint8_t *>(base + Lay.off_ctype);
+  B.crank16 = reinterpret_cast<uint16_t *>(base + Lay.off_crank);
+  B.cslot16 = reinterpret_cast<uint16_t *>(base + Lay.off_cslot);
   int32_t *ints = reinterpret_cast<int32_t *>(base + Lay.off_ints);
   const int Lp = Lay.L_cap + 1;
   B.Q = ints; B.C = ints + Lp; B.S = ints + 2 * Lp; B.cons = ints + 3 * Lp;
@@ -121,7 +125,7 @@ __device__ void wplan_counts(const RngKey &K, CellBuf<Real> &B, WarpShared &sh) 
       for (int j = lane; j < Cd; j += 32) {
         const uint32_t w = K(kType, sh.r, d, j).x;
         const uint32_t a = __umulhi(w, (uint32_t)d);
-        B.ctype[Sacc + j] = a;
+        B.ctype8[Sacc + j] = (uint8_t)a;
         atomicAdd(&B.cons[a], 1);
         atomicAdd(&B.cons[d - 1 - a], 1);
       }
@@ -173,22 +177,22 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
     for (int j0 = 0; j0 < Cd; j0 += 32) {  // stable in-level ranks per type
       const int j = j0 + lane;
       const bool valid = j < Cd;
-      const uint32_t a = valid ? B.ctype[Sd + j] : 0xFFFFFFFFu;
+      const uint32_t a = valid ? (uint32_t)B.ctype8[Sd + j] : 0xFFFFFFFFu;
       const unsigned peers = __match_any_sync(0xffffffffu, a);
       const unsigned lt = (1u << lane) - 1u;
       int c0 = 0;
       if (valid) c0 = B.cnt[a];
       __syncwarp();
       if (valid) {
-        B.crank[Sd + j] = (uint32_t)(c0 + __popc(peers & lt));
+        B.crank16[Sd + j] = (uint16_t)(c0 + __popc(peers & lt));
         if ((peers & lt) == 0u) B.cnt[a] = c0 + __popc(peers);
       }
       __syncwarp();
     }
     pd = d;
     for (int j = lane; j < Cd; j += 32) {
-      const uint32_t a = B.ctype[Sd + j], b = (uint32_t)d - 1u - a;
-      const uint32_t rank = B.crank[Sd + j];
+      const uint32_t a = B.ctype8[Sd + j], b = (uint32_t)d - 1u - a;
+      const uint32_t rank = B.crank16[Sd + j];
       const uint32_t t[2] = {(uint32_t)B.base[a] + rank, (uint32_t)(B.base[b] + B.cnt[b]) + rank};
       const uint32_t pool[2] = {a, b};
       // one code path for both sides (pool 0: pi0 at leaf_off + t; pool p:
@@ -200,11 +204,11 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
       uint32_t slot[2];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        slot[s] = (pool[s] == 0 || y[s] == 0xFFFFFFFFu) ? y[s] : B.cslot[2u * (uint32_t)B.S[pool[s]] + y[s]];
+        slot[s] = (pool[s] == 0 || y[s] == 0xFFFFFFFFu) ? y[s] : (uint32_t)B.cslot16[2u * (uint32_t)B.S[pool[s]] + y[s]];
         if (slot[s] >= (uint32_t)n) { atomicOr(P.err, kErrInternal); slot[s] = 0; }
       }
-      B.cslot[2 * (Sd + j)] = slot[0];
-      B.cslot[2 * (Sd + j) + 1] = slot[1];
+      B.cslot16[2 * (Sd + j)] = (uint16_t)slot[0];
+      B.cslot16[2 * (Sd + j) + 1] = (uint16_t)slot[1];
       const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, slot[0], slot[1], viol);
       acc += ok;
       if (P.log_on) {
@@ -245,8 +249,8 @@ __device__ void wrad_estimate(const StepParams &P, CellBuf<Real> &B, WarpShared 
     else { const double v2 = x * x + y * y + z * z; v1 += v2 * v2; }
     tx += x; ty += y; tz += z; t2 += x * x + y * y + z * z;
   }
-  v0 = warp_sum(v0); v1 = warp_sum(v1); tx = warp_sum(tx); ty = warp_sum(ty); tz = warp_sum(tz);
-  t2 = warp_sum(t2);
+  v0 = warp_sum_call(v0); v1 = warp_sum_call(v1); tx = warp_sum_call(tx); ty = warp_sum_call(ty); tz = warp_sum_call(tz);
+  t2 = warp_sum_call(t2);
   if (lane == 0) {
     double s = v0 - v1;
     if (nT > 0) {
@@ -281,7 +285,7 @@ __device__ void wmaxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> 
       if (s >= (uint32_t)sh.n) { atomicOr(P.err, kErrInternal); continue; }
       a += (double)B.vx[s]; b += (double)B.vy[s]; c += (double)B.vz[s];
     }
-    ux = warp_sum(a) / nT; uy = warp_sum(b) / nT; uz = warp_sum(c) / nT;
+    ux = warp_sum_call(a) / nT; uy = warp_sum_call(b) / nT; uz = warp_sum_call(c) / nT;
   }
   double g0s = 0, g1s = 0, g2s = 0, gg = 0, ec = 0;
   for (int q = lane; q < nT; q += 32) {
@@ -297,8 +301,8 @@ __device__ void wmaxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> 
     g0s += g0; g1s += g1; g2s += g2;
     gg += (double)g0 * g0 + (double)g1 * g1 + (double)g2 * g2;
   }
-  g0s = warp_sum(g0s); g1s = warp_sum(g1s); g2s = warp_sum(g2s); gg = warp_sum(gg);
-  ec = full ? ec_all : warp_sum(ec);
+  g0s = warp_sum_call(g0s); g1s = warp_sum_call(g1s); g2s = warp_sum_call(g2s); gg = warp_sum_call(gg);
+  ec = full ? ec_all : warp_sum_call(ec);
   const double gx = g0s / nT, gy = g1s / nT, gz = g2s / nT;
   const double D = gg - nT * (gx * gx + gy * gy + gz * gz);
   const double sc = (D > 0.0 && ec > 0.0) ? sqrt(ec / D) : 0.0;
@@ -327,7 +331,7 @@ __device__ int process_cell_warp(const StepParams &P, CellBuf<Real> &B, WarpShar
   const RngKey K{P.k0, P.k1, gcell, P.step};
   const int m0 = P.adaptive ? *m_state : P.m_fixed;
   // ---- A3: moments ----
-  const double Sx = warp_sum(sx), Sy = warp_sum(sy), Sz = warp_sum(sz);
+  const double Sx = warp_sum_call(sx), Sy = warp_sum_call(sy), Sz = warp_sum_call(sz);
   const double ux = Sx / n, uy = Sy / n, uz = Sz / n;
   double c0 = 0, c1 = 0, c2 = 0, dv2 = 0;
   for (int i = lane; i < n; i += 32) {
@@ -344,7 +348,7 @@ __device__ int process_cell_warp(const StepParams &P, CellBuf<Real> &B, WarpShar
     const uint4 w = K(kSplit, 0, (uint32_t)d, 0);
     usplit[d] = u53(w.x, w.y);
   }
-  c0 = warp_sum(c0); c1 = warp_sum(c1); c2 = warp_sum(c2); dv2 = warp_max(dv2);
+  c0 = warp_sum_call(c0); c1 = warp_sum_call(c1); c2 = warp_sum_call(c2); dv2 = warp_max_call(dv2);
   __syncwarp();
   if (lane == 0) {
     sh.n = n; sh.ux = ux; sh.uy = uy; sh.uz = uz;
@@ -370,47 +374,45 @@ __device__ int process_cell_warp(const StepParams &P, CellBuf<Real> &B, WarpShar
   Perm pi0;
   pi0.init(K(kPerm, 0, 0, 0), (uint32_t)n);
   const Real sigma = (Real)sh.sigma;
-  // ---- A5/A6: attempt 0 ----
-  wplan_counts<Real>(K, B, sh);
-  if (sh.flag != kOk) return sh.flag;
-  wplan_execute<Real>(P, K, B, sh, pi0, sigma, log, log_count, log_cap);
-  if (lane == 0) {
-    sh.Ltot = sh.L;
-    sh.U = B.Q[0] < n - sh.Ltot ? B.Q[0] : n - sh.Ltot;
-    sh.nT = n - sh.Ltot - sh.U;
-    sh.m_next = sh.m_cur;
-    sh.S_est = sh.S0; sh.E1 = 0.0;
-  }
-  __syncwarp();
-  // ---- A7: TRMC-RAD ----
-  if (P.adaptive) {
-    for (;;) {
-      wrad_estimate<Real>(P, B, sh, pi0);
-      if (lane == 0) {
-        sh.done = 1;
-        if (sh.E1 > P.delta2 && sh.m_cur < P.m_cap) {
-          const int m_new = 2 * sh.m_cur < P.m_cap ? 2 * sh.m_cur : P.m_cap;
-          wsplit_extend(K, sh, m_new, B.Q, B.L_cap, usplit);
-          sh.r += 1;
-          sh.lo = sh.m_cur + 1;
-          sh.hi = sh.d < B.L_cap ? sh.d : B.L_cap;
-          sh.budget = sh.nT;
-          sh.leaf_off = sh.Ltot;
-          sh.m_cur = m_new;
-          sh.done = 0;
-        }
+  // ---- A5/A6 (attempt 0), then A7 (TRMC-RAD) retries: one loop, so every
+  // phase has a single inlined copy (instruction-cache footprint) ----
+  for (int attempt = 0;; ++attempt) {
+    wplan_counts<Real>(K, B, sh);
+    if (sh.flag != kOk) return sh.flag;
+    wplan_execute<Real>(P, K, B, sh, pi0, sigma, log, log_count, log_cap);
+    if (lane == 0) {
+      if (attempt == 0) {
+        sh.Ltot = sh.L;
+        sh.U = B.Q[0] < n - sh.Ltot ? B.Q[0] : n - sh.Ltot;
+        sh.nT = n - sh.Ltot - sh.U;
+        sh.m_next = sh.m_cur;
+        sh.S_est = sh.S0; sh.E1 = 0.0;
+      } else {
+        sh.Ltot += sh.L; sh.nT -= sh.L;
       }
-      __syncwarp();
-      if (sh.flag != kOk) return sh.flag;
-      if (sh.done) break;
-      wplan_counts<Real>(K, B, sh);
-      if (sh.flag != kOk) return sh.flag;
-      wplan_execute<Real>(P, K, B, sh, pi0, sigma, log, log_count, log_cap);
-      if (lane == 0) { sh.Ltot += sh.L; sh.nT -= sh.L; }
-      __syncwarp();
     }
-    if (lane == 0) sh.m_next = (sh.E1 < P.delta1) ? (sh.m_cur / 2 > 1 ? sh.m_cur / 2 : 1) : sh.m_cur;
     __syncwarp();
+    if (!P.adaptive) break;
+    wrad_estimate<Real>(P, B, sh, pi0);
+    if (lane == 0) {
+      sh.done = 1;
+      if (sh.E1 > P.delta2 && sh.m_cur < P.m_cap) {
+        const int m_new = 2 * sh.m_cur < P.m_cap ? 2 * sh.m_cur : P.m_cap;
+        wsplit_extend(K, sh, m_new, B.Q, B.L_cap, usplit);
+        sh.r += 1;
+        sh.lo = sh.m_cur + 1;
+        sh.hi = sh.d < B.L_cap ? sh.d : B.L_cap;
+        sh.budget = sh.nT;
+        sh.leaf_off = sh.Ltot;
+        sh.m_cur = m_new;
+        sh.done = 0;
+      } else {
+        sh.m_next = (sh.E1 < P.delta1) ? (sh.m_cur / 2 > 1 ? sh.m_cur / 2 : 1) : sh.m_cur;
+      }
+    }
+    __syncwarp();
+    if (sh.flag != kOk) return sh.flag;
+    if (sh.done) break;
   }
   // ---- A8 ----
   wmaxwellian<Real>(P, K, B, sh, pi0, c2);

@@ -30,11 +30,17 @@ __device__ __forceinline__ uint4 philox10(uint32_t c0, uint32_t c1, uint32_t c2,
 
 // Stream identity of one cell at one step: key = seed, counter words 2,3 =
 // (global cell, step); word 1 = purpose<<24 | attempt<<20 | level; word 0 = element.
+// Out-of-line copy for the general kernels: one body instead of one per call
+// site keeps those kernels inside the instruction cache.
+__device__ __noinline__ uint4 philox10_call(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                            uint32_t k1) {
+  return philox10(c0, c1, c2, c3, k0, k1);
+}
 struct RngKey {
   uint32_t k0, k1, cell, step;
   __device__ __forceinline__ uint4 operator()(uint32_t purpose, uint32_t attempt, uint32_t level,
                                               uint32_t elem) const {
-    return philox10(elem, (purpose << 24) | (attempt << 20) | level, cell, step, k0, k1);
+    return philox10_call(elem, (purpose << 24) | (attempt << 20) | level, cell, step, k0, k1);
   }
 };
 
@@ -161,6 +167,9 @@ __device__ __forceinline__ double warp_max(double v) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
+// out-of-line versions (general warp kernel: code size)
+__device__ __noinline__ double warp_sum_call(double v) { return warp_sum(v); }
+__device__ __noinline__ double warp_max_call(double v) { return warp_max(v); }
 
 // Sums NV doubles over the CTA; every thread receives the totals.
 // `red` must hold (blockDim.x/32)*NV doubles of shared memory.

@@ -210,68 +210,74 @@ __global__ void ghost_gen(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, c
 // [dmin, dmin + kHist) and flushed with one global atomic per touched cell
 // (a destination outside the window falls back to a global atomic).
 // W[0] = max local displacement, W[1] = emigrant scan width, acct[2] = dropped.
-constexpr int kTransportThreads = 256, kTransportPer = 4, kHist = 64;
-constexpr int kTile = kTransportThreads * kTransportPer;   // particles per transport tile
+constexpr int kTransportThreads = 256, kTransportPer = 4, kTransportGroups = 4, kHist = 256;
+// particles per transport tile: thread t of the CTA owns the 4-particle groups
+// t, t + 256, t + 512, t + 768 of the tile (16-byte coalesced I/O)
+constexpr int kTile = kTransportThreads * kTransportPer * kTransportGroups;
 constexpr int kEdgeBins = 4096;   // cells from a domain / slab edge that ghosts and immigrants may reach
 
 template <typename Real>
 __global__ void __launch_bounds__(kTransportThreads)
 transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const Real *__restrict__ vx,
                  int32_t *dest, int32_t *counts, int *W, unsigned long long *acct, int32_t *tileH, int2 *tile_meta) {
+  constexpr int P4 = kTransportPer, NG = kTransportGroups;
   __shared__ int s_hist[kHist];
   __shared__ int s_red[4][kTransportThreads / 32];
   __shared__ int s_dmin;
   const int64_t n = off_old[S.C];
-  const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kTransportPer;
+  const int64_t tile0 = (int64_t)blockIdx.x * kTile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int d[kTransportPer];
+  int d[NG][P4];
   int disp = 0, emi = 0, dropped = 0, dmin = INT32_MAX, smax = -1;
-  Real xs[kTransportPer], vs[kTransportPer];
-  const bool vec = (i0 + kTransportPer <= n) && (sizeof(Real) * kTransportPer == 16);
-  if (vec) {
-    using V = typename Vec<Real>::T;
-    const V xv = *reinterpret_cast<const V *>(x + i0), vv = *reinterpret_cast<const V *>(vx + i0);
 #pragma unroll
-    for (int k = 0; k < kTransportPer; ++k) { xs[k] = vget<V, Real>(xv, k); vs[k] = vget<V, Real>(vv, k); }
-  } else {
+  for (int g = 0; g < NG; ++g) {
+    const int64_t i0 = tile0 + ((int64_t)g * kTransportThreads + threadIdx.x) * P4;
+    Real xs[P4], vs[P4];
+    const bool vec = (i0 + P4 <= n) && (sizeof(Real) * P4 == 16);
+    if (vec) {
+      using V = typename Vec<Real>::T;
+      const V xv = *reinterpret_cast<const V *>(x + i0), vv = *reinterpret_cast<const V *>(vx + i0);
 #pragma unroll
-    for (int k = 0; k < kTransportPer; ++k) {
-      xs[k] = (i0 + k < n) ? x[i0 + k] : Real(0);
-      vs[k] = (i0 + k < n) ? vx[i0 + k] : Real(0);
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < kTransportPer; ++k) {
-    d[k] = -1;
-    if (i0 + k >= n) continue;
-    const int src = cell_of(S, (double)xs[k]) - S.cbase;
-    smax = max(smax, src);
-    const Real xn = add_rn<Real>(xs[k], mul_rn<Real>(vs[k], (Real)S.dt));
-    xs[k] = xn;
-    const double xd = (double)xn;
-    const bool keep = xd >= S.x_min && xd < S.x_max;
-    const int dl = keep ? cell_of(S, xd) - S.cbase : kDropped;
-    if (!keep) {
-      ++dropped;
-    } else if (dl >= 0 && dl < S.C) {
-      d[k] = dl;
-      disp = max(disp, abs(dl - src));
-      dmin = min(dmin, dl);
+      for (int k = 0; k < P4; ++k) { xs[k] = vget<V, Real>(xv, k); vs[k] = vget<V, Real>(vv, k); }
     } else {
-      emi = max(emi, dl < 0 ? src + 1 : S.C - src);
+#pragma unroll
+      for (int k = 0; k < P4; ++k) {
+        xs[k] = (i0 + k < n) ? x[i0 + k] : Real(0);
+        vs[k] = (i0 + k < n) ? vx[i0 + k] : Real(0);
+      }
     }
-    if (!vec) { x[i0 + k] = xn; dest[i0 + k] = dl; }
-    else d[k] = dl;   // written below as one int4; non-local ones reset to -1 after
-  }
-  if (vec) {
-    using V = typename Vec<Real>::T;
-    V xv;
 #pragma unroll
-    for (int k = 0; k < kTransportPer; ++k) vset<V, Real>(xv, k, xs[k]);
-    *reinterpret_cast<V *>(x + i0) = xv;
-    *reinterpret_cast<int4 *>(dest + i0) = make_int4(d[0], d[1], d[2], d[3]);
+    for (int k = 0; k < P4; ++k) {
+      d[g][k] = -1;
+      if (i0 + k >= n) continue;
+      const int src = cell_of(S, (double)xs[k]) - S.cbase;
+      smax = max(smax, src);
+      const Real xn = add_rn<Real>(xs[k], mul_rn<Real>(vs[k], (Real)S.dt));
+      xs[k] = xn;
+      const double xd = (double)xn;
+      const bool keep = xd >= S.x_min && xd < S.x_max;
+      const int dl = keep ? cell_of(S, xd) - S.cbase : kDropped;
+      if (!keep) {
+        ++dropped;
+      } else if (dl >= 0 && dl < S.C) {
+        disp = max(disp, abs(dl - src));
+        dmin = min(dmin, dl);
+      } else {
+        emi = max(emi, dl < 0 ? src + 1 : S.C - src);
+      }
+      if (!vec) { x[i0 + k] = xn; dest[i0 + k] = dl; }
+      d[g][k] = dl;
+    }
+    if (vec) {
+      using V = typename Vec<Real>::T;
+      V xv;
 #pragma unroll
-    for (int k = 0; k < kTransportPer; ++k) if (d[k] < 0 || d[k] >= S.C) d[k] = -1;   // not counted here
+      for (int k = 0; k < P4; ++k) vset<V, Real>(xv, k, xs[k]);
+      *reinterpret_cast<V *>(x + i0) = xv;
+      *reinterpret_cast<int4 *>(dest + i0) = make_int4(d[g][0], d[g][1], d[g][2], d[g][3]);
+    }
+#pragma unroll
+    for (int k = 0; k < P4; ++k) if (d[g][k] < 0 || d[g][k] >= S.C) d[g][k] = -1;   // counted below: local only
   }
   // CTA reductions: window base, max displacement, emigrant width, dropped
   dmin = __reduce_min_sync(0xffffffffu, dmin);
@@ -295,12 +301,14 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
   __syncthreads();
   const int base = s_dmin;
 #pragma unroll
-  for (int k = 0; k < kTransportPer; ++k) {
-    if (d[k] < 0) continue;
-    const int h = d[k] - base;
-    if (h < kHist) atomicAdd(&s_hist[h], 1);
-    else { atomicAdd(&counts[d[k]], 1); if (tileH) W[2] = 1; }   // scatter sort not possible this step
-  }
+  for (int g = 0; g < NG; ++g)
+#pragma unroll
+    for (int k = 0; k < P4; ++k) {
+      if (d[g][k] < 0) continue;
+      const int h = d[g][k] - base;
+      if (h < kHist) atomicAdd(&s_hist[h], 1);
+      else { atomicAdd(&counts[d[g][k]], 1); if (tileH) W[2] = 1; }   // scatter sort not possible this step
+    }
   __syncthreads();
   if (threadIdx.x < kHist) {
     const int h = s_hist[threadIdx.x];
@@ -489,12 +497,13 @@ __global__ void __launch_bounds__(kScatterThreads)
 scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *__restrict__ off_new,
                const Real *__restrict__ x, const Real *__restrict__ vx, const Real *__restrict__ vy,
                const Real *__restrict__ vz, const int32_t *__restrict__ dest, const int32_t *__restrict__ tileH,
-               const int2 *__restrict__ tile_meta, const int32_t *__restrict__ lcnt, const int *W, Real *ox,
-               Real *ovx, Real *ovy, Real *ovz) {
+               const int2 *__restrict__ tile_meta, const int32_t *__restrict__ lcnt, const int *W,
+               Real *__restrict__ ox, Real *__restrict__ ovx, Real *__restrict__ ovy, Real *__restrict__ ovz) {
   constexpr int NW = kScatterThreads / 32, PARTS = kScatterThreads / kHist;
-  __shared__ int s_pre[kHist], s_run[kHist];
+  constexpr int CHUNK = kTile / NW, ROUNDS = CHUNK / 32;   // each warp: CHUNK consecutive particles
   __shared__ int s_part[PARTS][kHist];
-  __shared__ int s_wc[NW][kHist];
+  __shared__ int s_wc[NW][kHist];                          // per-warp counts, then running positions
+  __shared__ int64_t s_off[kHist];                         // off_new of the tile's destination cells
   __shared__ int2 s_meta[32];
   __shared__ int s_nb, s_more;
   const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -505,6 +514,27 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
   const int dmin = tile_meta[t].x;
   if (dmin == INT32_MAX) return;                     // no local destination in this tile
   const int Wd = W[0];
+  // ---- pass 1: this warp's destinations (kept in registers) and bin counts ----
+  for (int q = tid; q < NW * kHist; q += kScatterThreads) (&s_wc[0][0])[q] = 0;
+  __syncwarp();
+  __syncthreads();
+  const int64_t c0 = i_begin + (int64_t)warp * CHUNK;
+  int bins[ROUNDS];
+#pragma unroll
+  for (int r = 0; r < ROUNDS; ++r) {                  // all destination loads in flight at once
+    const int64_t i = c0 + r * 32 + lane;
+    bins[r] = i < n ? dest[i] : -1;
+  }
+  if (tid < kHist) s_off[tid] = dmin + tid <= S.C ? off_new[dmin + tid] : 0;
+#pragma unroll
+  for (int r = 0; r < ROUNDS; ++r) {
+    const int d = bins[r];
+    const bool loc = d >= 0 && d < S.C && d - dmin < kHist;
+    bins[r] = loc ? d - dmin : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, loc ? bins[r] : -1 - lane);
+    if (loc && __ffs(peers) - 1 == lane) s_wc[warp][bins[r]] += __popc(peers);
+    __syncwarp();
+  }
   // ---- prefix per bin: lcnt + look-back over earlier tiles, 32 at a time ----
   const int b = tid & (kHist - 1), part = tid / kHist;
   int acc = 0;
@@ -531,7 +561,6 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
     if (!more) break;
   }
   s_part[part][b] = acc;
-  if (tid < kHist) s_run[tid] = 0;
   __syncthreads();
   if (tid < kHist) {
     int p = 0;
@@ -539,32 +568,39 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
     for (int q = 0; q < PARTS; ++q) p += s_part[q][tid];
     const int d = dmin + tid;
     if (d < kEdgeBins && d < S.C) p += lcnt[d];
-    s_pre[tid] = p;
+    // running start of each warp's chunk in this bin (exclusive prefix over warps)
+    for (int w = 0; w < NW; ++w) { const int cw = s_wc[w][tid]; s_wc[w][tid] = p; p += cw; }
   }
-  // ---- in-tile stable ranks, kScatterThreads particles per round in index order ----
-  for (int64_t r0 = i_begin; r0 < i_begin + kTile && r0 < n; r0 += kScatterThreads) {
-    const int64_t i = r0 + tid;
-    int d = -1;
-    if (i < n) d = dest[i];
-    const bool loc = d >= 0 && d < S.C && d - dmin < kHist;
-    const int bin = loc ? d - dmin : -1;
-    const unsigned peers = __match_any_sync(0xffffffffu, loc ? bin : -1 - lane);
-    for (int q = tid; q < NW * kHist; q += kScatterThreads) (&s_wc[0][0])[q] = 0;
-    __syncthreads();
-    if (loc && __ffs(peers) - 1 == lane) s_wc[warp][bin] = __popc(peers);
-    __syncthreads();
-    if (loc) {
-      int rank = s_run[bin] + __popc(peers & ((1u << lane) - 1u));
-      for (int w = 0; w < warp; ++w) rank += s_wc[w][bin];
-      const int64_t pos = off_new[d] + s_pre[bin] + rank;
-      ox[pos] = x[i]; ovx[pos] = vx[i]; ovy[pos] = vy[i]; ovz[pos] = vz[i];
-    }
-    __syncthreads();
-    if (tid < kHist) {
-      int a = 0;
+  __syncthreads();
+  // ---- pass 2: stable positions, in index order within the warp's chunk ----
+  int rk[ROUNDS];
 #pragma unroll
-      for (int w = 0; w < NW; ++w) a += s_wc[w][tid];
-      s_run[tid] += a;
+  for (int r = 0; r < ROUNDS; ++r) {
+    const int bin = bins[r];
+    const unsigned peers = __match_any_sync(0xffffffffu, bin >= 0 ? bin : -1 - lane);
+    rk[r] = 0;
+    if (bin >= 0) rk[r] = s_wc[warp][bin] + __popc(peers & ((1u << lane) - 1u));
+    __syncwarp();
+    if (bin >= 0 && __ffs(peers) - 1 == lane) s_wc[warp][bin] += __popc(peers);
+    __syncwarp();
+  }
+  // ---- data movement: independent 4-round batches of loads, then the stores ----
+  constexpr int BATCH = 4;
+#pragma unroll
+  for (int r0 = 0; r0 < ROUNDS; r0 += BATCH) {
+    Real a[BATCH], bx[BATCH], by[BATCH], bz[BATCH];
+#pragma unroll
+    for (int q = 0; q < BATCH; ++q) {
+      const int64_t i = c0 + (r0 + q) * 32 + lane;
+      if (bins[r0 + q] >= 0) { a[q] = x[i]; bx[q] = vx[i]; by[q] = vy[i]; bz[q] = vz[i]; }
+    }
+#pragma unroll
+    for (int q = 0; q < BATCH; ++q) {
+      const int bin = bins[r0 + q];
+      if (bin >= 0) {
+        const int64_t pos = s_off[bin] + rk[r0 + q];
+        ox[pos] = a[q]; ovx[pos] = bx[q]; ovy[pos] = by[q]; ovz[pos] = bz[q];
+      }
     }
   }
 }
@@ -676,7 +712,7 @@ __device__ int gather_cell(const ShockDev &S, const GatherSrc &G, int c, Real *b
 // scan gives the positions.  Velocities -> (bx,by,bz) (the warp's slab),
 // positions -> ox (global).  Returns the count; sums of the velocities in s*.
 template <typename Real>
-__device__ int gather_cell_warp(const ShockDev &S, const GatherSrc &G, int c, Real *bx, Real *by, Real *bz,
+__device__ __noinline__ int gather_cell_warp(const ShockDev &S, const GatherSrc &G, int c, Real *bx, Real *by, Real *bz,
                                 Real *ox, int cap, double &sxo, double &syo, double &szo) {
   constexpr int R = 4;
   const int lane = threadIdx.x & 31;
@@ -753,7 +789,7 @@ __device__ int gather_cell_warp(const ShockDev &S, const GatherSrc &G, int c, Re
 }
 
 template <typename Real>
-__global__ void __launch_bounds__(kWarpCellWarps * 32, 2)
+__global__ void __launch_bounds__(kWarpCellWarps * 32, TRMCR_WARP_MINB)
 shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, int *defer_count,
                    int *defer_list, QueueArgs Q) {
@@ -960,7 +996,7 @@ trmcr_status shock_begin(trmcr_ctx *c) {
     if (auto e = check_launch(c, "ghost_gen", TRMCR_K_GHOST_GEN)) return e;
   }
   {
-    const int per_block = kTransportThreads * kTransportPer;
+    const int per_block = kTile;
     const unsigned blocks = (unsigned)((c->cap + per_block - 1) / per_block);
     prof_begin(c, TRMCR_K_TRANSPORT);
     const bool sc = s.scatter && c->wlay.n_cap > 0 && !c->wlay.v_smem;

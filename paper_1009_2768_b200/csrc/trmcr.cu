@@ -96,7 +96,7 @@ cell_step_gmem(StepParams P, GmemScratch G, const int64_t *__restrict__ offsets,
 // General cells, one warp each (cell_warp.cuh), over the thermal kernel's
 // defer list (or every cell); cells that do not fit go to list2 (CTA kernel).
 template <typename Real>
-__global__ void __launch_bounds__(kWarpCellWarps * 32, 2)
+__global__ void __launch_bounds__(kWarpCellWarps * 32, TRMCR_WARP_MINB)
 cell_step_warp(StepParams P, WarpSlabLayout Lay, const int64_t *__restrict__ offsets, int ncells,
                const int *list_count, const int *list, Real *vx, Real *vy, Real *vz, int32_t *m_state,
                double *stats, int *list2_count, int *list2, QueueArgs Q) {
@@ -651,9 +651,10 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
     // (in place would corrupt the input of a deferred cell)
     const int v_smem = c->geometry == TRMCR_SHOCK_1D ? 0 : 1;
     if (!v_smem) wn = std::max(wn, 4096);
+    wn = std::min(wn, 65504);   // slots are 16-bit in the warp plan; larger cells take the CTA path
     c->wlay.build(wn, wK, 64, c->rs, v_smem);
     const size_t slab = c->wlay.per_warp;
-    c->warp_wpc = (int)std::max<size_t>(1, std::min<size_t>(kWarpCellWarps, (64 * 1024) / slab));
+    c->warp_wpc = (int)std::max<size_t>(1, std::min<size_t>(kWarpCellWarps, (48 * 1024) / slab));
     c->warp_smem = (int)(slab * c->warp_wpc);
     if (!want || c->warp_smem > smem_max - 2048) {
       c->wlay.n_cap = 0;     // disabled: the CTA kernel takes every general cell

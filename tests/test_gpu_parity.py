@@ -206,11 +206,17 @@ def _shock_pair(orc, api, mach, ncells, ntot, steps, eps, dtype, seed=1, x_min=-
     return setup, sim, o
 
 
-def test_shock_fp64_parity(orc, api):
+@pytest.mark.parametrize("scatter", ["1", "0"])
+def test_shock_fp64_parity(orc, api, monkeypatch, scatter):
+    """Both sort paths: scatter_sorted + edge_place (default) and the gather
+    inside the collision kernels (TRMCR_SHOCK_SCATTER=0)."""
+    monkeypatch.setenv("TRMCR_SHOCK_SCATTER", scatter)
     setup, sim, o = _shock_pair(orc, api, 3.0, 40, 8000, 0, 0.2, np.float64)
     for s in range(8):
         sim.step(1)
         o.step(1)
+        info = sim.sort_info()
+        assert info["scatter_enabled"] == (scatter == "1") and not info["gathered"]
         g = sim.particles()
         np.testing.assert_array_equal(g["offsets"], o.offsets)
         n = o.n

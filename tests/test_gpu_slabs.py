@@ -45,6 +45,9 @@ def test_slabs_match_single_domain(world, dtype):
         dist.host_exchange(slabs)
         for s in slabs:
             s.sim.shock_finish()
+        for sim in [full] + [s.sim for s in slabs]:     # the scatter sort ran (no gather fallback)
+            info = sim.sort_info()
+            assert info["scatter_enabled"] and not info["gathered"]
     g = full.particles()
     parts = [s.sim.particles() for s in slabs]
     for k in ("x", "vx", "vy", "vz"):
