@@ -322,7 +322,13 @@ def run_trmcr(args, rank, world, local_rank):
         if W["kind"] == "hom" and W["kw"]["eps"] > 0.05:
             bytes_per = 2 * 3 * rs        # upper bound; changed fraction < 1 (dense write-back)
     elif dom in ("shock_collide_smem", "shock_collide_gmem", "shock_collide_warp"):
-        bytes_per = 2 * 4 * rs            # read (x, v), write (x, v) once
+        # SURVEY 8(d) D3, collision step: read every v, write the changed ones:
+        # 3 rs (1 + f_chg), f_chg = 1 - untouched / n of this run's last step
+        st = sim.stats()
+        f_chg = 1.0 - float(st["untouched"].sum()) / max(float(st["n"].sum()), 1.0)
+        bytes_per = 3 * rs * (1.0 + f_chg)
+    elif dom == "scatter_sorted":
+        bytes_per = 2 * 4 * rs            # the sort: read (x, v), write (x, v)
     elif dom == "transport_kernel":
         bytes_per = 3 * rs                # read x, v_x; write x
     else:
@@ -332,7 +338,7 @@ def run_trmcr(args, rank, world, local_rank):
     traffic = ncu_traffic(args.workload)
     roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
             "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-            "traffic": traffic, "algorithmic_bytes_per_particle": bytes_per,
+            "traffic": traffic, "algorithmic_bytes_per_particle": round(bytes_per, 3),
             "kernel_share_of_step": round(dom_ms / ms_local, 4),
             "kernel_ms_probe": kernel_ms_probe}
 

@@ -13,7 +13,7 @@ namespace trmcr {
 
 constexpr int kWarpCellWarps = 4;
 #ifndef TRMCR_WARP_MINB
-#define TRMCR_WARP_MINB 5        // CTAs of kWarpCellWarps warps per SM the register budget allows
+#define TRMCR_WARP_MINB 4        // CTAs of kWarpCellWarps warps per SM the register budget allows (128 regs)
 #endif
 
 // Per-warp scalars (in the warp's slab, lane 0 writes, __syncwarp publishes).

@@ -262,6 +262,10 @@ __device__ __forceinline__ void gauss3_fast(const RngKey &K, uint32_t slot, floa
   g0 = r1 * c2; g1 = r1 * s2; g2 = r3 * c4;
 }
 
+__device__ __forceinline__ float2 lo2(const float4 &a) { return make_float2(a.x, a.y); }
+__device__ __forceinline__ float2 hi2(const float4 &a) { return make_float2(a.z, a.w); }
+__device__ __forceinline__ float4 f4(const float2 &l, const float2 &h) { return make_float4(l.x, l.y, h.x, h.y); }
+
 // Raw MUFU approximations (flush-to-zero, no special-case fix-ups): every
 // operand below is a normal number (u in [2^-24, 1), a in [1.2e-7, 23.1],
 // 2 pi u in (0, 2 pi)), so the fix-up code the compiler adds around
@@ -291,8 +295,9 @@ __device__ __forceinline__ void bm_pair(uint32_t wa, uint32_t wb, float &c, floa
   const float r = -l * rsqrt_ftz(-l);
   const float b = __uint_as_float(0x3F800000u | (wb >> 9));
   const float t = fmaf(b, k2Pi, -k2Pi * (1.0f - 0x1p-24f));
-  s = r * sin_ftz(t);
-  c = r * cos_ftz(t);
+  const float2 cs = __fmul2_rn(make_float2(cos_ftz(t), sin_ftz(t)), make_float2(r, r));
+  c = cs.x;
+  s = cs.y;
 }
 
 // Philox4x32-10 with the key schedule precomputed on the host (kernel
@@ -354,78 +359,92 @@ __device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, const KeyS
     const float *base = lane == 0 ? vx : (lane == 1 ? vy : vz);
     prefetch_l2(base + next_off, (unsigned)next_n * 4u);
   }
-  float sx = 0, sy = 0, sz = 0;
+  // fp32 math below in packed pairs (FADD2 / FMUL2 / FFMA2: two lanes of
+  // IEEE fp32 per instruction, sm_100)
+  float2 s2x = make_float2(0.f, 0.f), s2y = s2x, s2z = s2x;
 #pragma unroll
   for (int k = 0; k < G; ++k) {
     const int g = lane + 32 * k;
     if (g < ng) {
       const float4 a = sx4[g], b = sy4[g], d = sz4[g];
-      sx += (a.x + a.y) + (a.z + a.w); sy += (b.x + b.y) + (b.z + b.w); sz += (d.x + d.y) + (d.z + d.w);
+      s2x = __fadd2_rn(__fadd2_rn(s2x, lo2(a)), hi2(a));
+      s2y = __fadd2_rn(__fadd2_rn(s2y, lo2(b)), hi2(b));
+      s2z = __fadd2_rn(__fadd2_rn(s2z, lo2(d)), hi2(d));
     }
   }
   ThermalMoments M;
-  M.Sx = warp_sum((double)sx); M.Sy = warp_sum((double)sy); M.Sz = warp_sum((double)sz);
+  M.Sx = warp_sum((double)(s2x.x + s2x.y)); M.Sy = warp_sum((double)(s2y.x + s2y.y));
+  M.Sz = warp_sum((double)(s2z.x + s2z.y));
   M.ux = M.Sx / n; M.uy = M.Sy / n; M.uz = M.Sz / n;
   const float rux = (float)M.ux, ruy = (float)M.uy, ruz = (float)M.uz;
-  float e = 0, pxx = 0, m4 = 0, mx = 0;
+  const float2 nux = make_float2(-rux, -rux), nuy = make_float2(-ruy, -ruy), nuz = make_float2(-ruz, -ruz);
+  float2 e2 = make_float2(0.f, 0.f), p2 = e2, q2 = e2;
+  float mx = 0;
   const bool want_m4 = P.indicator == TRMCR_IND_M4;
 #pragma unroll
   for (int k = 0; k < G; ++k) {
     const int g = lane + 32 * k;
     if (g < ng) {
       const float4 a = sx4[g], b = sy4[g], d = sz4[g];
-      const float xs[4] = {a.x, a.y, a.z, a.w}, ys[4] = {b.x, b.y, b.z, b.w}, zs[4] = {d.x, d.y, d.z, d.w};
-      float eg = 0, pg = 0, mg = 0;
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const float dx = xs[w] - rux, dy = ys[w] - ruy, dz = zs[w] - ruz;
-        const float px = dx * dx;
-        const float r2 = px + dy * dy + dz * dz;
-        eg += r2;
-        mx = fmaxf(mx, r2);
-        pg += px;
+      for (int h = 0; h < 2; ++h) {
+        const float2 xh = h ? hi2(a) : lo2(a), yh = h ? hi2(b) : lo2(b), zh = h ? hi2(d) : lo2(d);
+        const float2 dx = __fadd2_rn(xh, nux), dy = __fadd2_rn(yh, nuy), dz = __fadd2_rn(zh, nuz);
+        const float2 px = __fmul2_rn(dx, dx);
+        const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, px));
+        e2 = __fadd2_rn(e2, r2);
+        p2 = __fadd2_rn(p2, px);
+        mx = fmaxf(mx, fmaxf(r2.x, r2.y));
         if (want_m4) {
-          const float v2 = xs[w] * xs[w] + ys[w] * ys[w] + zs[w] * zs[w];
-          mg += v2 * v2;
+          const float2 v2 = __ffma2_rn(zh, zh, __ffma2_rn(yh, yh, __fmul2_rn(xh, xh)));
+          q2 = __ffma2_rn(v2, v2, q2);
         }
       }
-      e += eg; pxx += pg; m4 += mg;
     }
   }
-  M.E = warp_sum((double)e);
-  thermal_decide(P, M, n, warp_sum((double)pxx), warp_sum((double)m4), warp_max((double)mx));
+  M.E = warp_sum((double)(e2.x + e2.y));
+  thermal_decide(P, M, n, warp_sum((double)(p2.x + p2.y)), warp_sum((double)(q2.x + q2.y)), warp_max((double)mx));
   if (!(M.p * (double)n < 0x1p-53)) return false;
   const uint32_t gcell = P.cell_base + (uint32_t)c;
   if (n >= 2) {
-    float ax = 0, ay = 0, az = 0, a2 = 0;
+    float2 ax = make_float2(0.f, 0.f), ay = ax, az = ax, a2 = ax;
 #pragma unroll 2
     for (int k = 0; k < G; ++k) {
       const int g = lane + 32 * k;
       if (g < ng) {
         float4 a, b, d;
+#ifdef TRMCR_THERMAL_NOGAUSS   // roofline experiment only: no draws
+        a = make_float4(g, 1, 2, 3); b = a; d = a;
+#else
         gauss12(ks, gcell, P.step, (uint32_t)g, a, b, d);
+#endif
         sx4[g] = a; sy4[g] = b; sz4[g] = d;
-        ax += (a.x + a.y) + (a.z + a.w); ay += (b.x + b.y) + (b.z + b.w); az += (d.x + d.y) + (d.z + d.w);
-        a2 += ((a.x * a.x + b.x * b.x + d.x * d.x) + (a.y * a.y + b.y * b.y + d.y * d.y)) +
-              ((a.z * a.z + b.z * b.z + d.z * d.z) + (a.w * a.w + b.w * b.w + d.w * d.w));
+        ax = __fadd2_rn(__fadd2_rn(ax, lo2(a)), hi2(a));
+        ay = __fadd2_rn(__fadd2_rn(ay, lo2(b)), hi2(b));
+        az = __fadd2_rn(__fadd2_rn(az, lo2(d)), hi2(d));
+        a2 = __ffma2_rn(lo2(a), lo2(a), a2); a2 = __ffma2_rn(hi2(a), hi2(a), a2);
+        a2 = __ffma2_rn(lo2(b), lo2(b), a2); a2 = __ffma2_rn(hi2(b), hi2(b), a2);
+        a2 = __ffma2_rn(lo2(d), lo2(d), a2); a2 = __ffma2_rn(hi2(d), hi2(d), a2);
       }
     }
-    const double Gx = warp_sum((double)ax) / n, Gy = warp_sum((double)ay) / n, Gz = warp_sum((double)az) / n;
-    const double D = warp_sum((double)a2) - n * (Gx * Gx + Gy * Gy + Gz * Gz);
+    const double Gx = warp_sum((double)(ax.x + ax.y)) / n, Gy = warp_sum((double)(ay.x + ay.y)) / n;
+    const double Gz = warp_sum((double)(az.x + az.y)) / n;
+    const double D = warp_sum((double)(a2.x + a2.y)) - n * (Gx * Gx + Gy * Gy + Gz * Gz);
     const double sc = (D > 0.0 && M.E > 0.0) ? sqrt(M.E / D) : 0.0;
     // v' = u + s (g - G) = s g + (u - s G): one FFMA per component
     const float rs = (float)sc;
     const float bx = (float)(M.ux - sc * Gx), by = (float)(M.uy - sc * Gy), bz = (float)(M.uz - sc * Gz);
+    const float2 rs2 = make_float2(rs, rs), bx2 = make_float2(bx, bx), by2 = make_float2(by, by);
+    const float2 bz2 = make_float2(bz, bz);
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < G; ++k) {
       const int g = lane + 32 * k;
       if (g < ng) {
-        float4 a = sx4[g], b = sy4[g], d = sz4[g];
-        a.x = fmaf(rs, a.x, bx); a.y = fmaf(rs, a.y, bx); a.z = fmaf(rs, a.z, bx); a.w = fmaf(rs, a.w, bx);
-        b.x = fmaf(rs, b.x, by); b.y = fmaf(rs, b.y, by); b.z = fmaf(rs, b.z, by); b.w = fmaf(rs, b.w, by);
-        d.x = fmaf(rs, d.x, bz); d.y = fmaf(rs, d.y, bz); d.z = fmaf(rs, d.z, bz); d.w = fmaf(rs, d.w, bz);
-        __stcs(gx + g, a); __stcs(gy + g, b); __stcs(gz + g, d);
+        const float4 a = sx4[g], b = sy4[g], d = sz4[g];
+        __stcs(gx + g, f4(__ffma2_rn(rs2, lo2(a), bx2), __ffma2_rn(rs2, hi2(a), bx2)));
+        __stcs(gy + g, f4(__ffma2_rn(rs2, lo2(b), by2), __ffma2_rn(rs2, hi2(b), by2)));
+        __stcs(gz + g, f4(__ffma2_rn(rs2, lo2(d), bz2), __ffma2_rn(rs2, hi2(d), bz2)));
       }
     }
   }
