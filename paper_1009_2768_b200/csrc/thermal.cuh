@@ -334,10 +334,13 @@ __device__ __forceinline__ void gauss12(const KeySched &ks, uint32_t cell, uint3
   bm_pair(w2.z, w2.w, b.w, d.w);
 }
 
-__device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, const KeySched &ks, float *vx, float *vy,
-                                                 float *vz, int64_t off, int n, int c, float *wx, float *wy,
-                                                 float *wz, int32_t *m_state, double *stats, int64_t next_off,
-                                                 int next_n) {
+// The fluid-regime step of one fp32 cell already staged (and visible to the
+// whole warp) in the slab (wx, wy, wz): moments, decision, Gaussians (into
+// the slab), conservative rescale, stores.  Returns false (nothing written)
+// when the cell is not in the fluid regime.
+__device__ __forceinline__ bool thermal_f32_compute(const StepParams &P, const KeySched &ks, float *vx, float *vy,
+                                                    float *vz, int64_t off, int n, int c, float *wx, float *wy,
+                                                    float *wz, int32_t *m_state, double *stats) {
   constexpr int CAP = ThermalCap<float>::value;
   constexpr int G = CAP / 4 / 32;                 // float4 groups per lane at n = CAP
   const int lane = threadIdx.x & 31;
@@ -346,19 +349,6 @@ __device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, const KeyS
   float4 *gz = reinterpret_cast<float4 *>(vz + off);
   float4 *sx4 = reinterpret_cast<float4 *>(wx), *sy4 = reinterpret_cast<float4 *>(wy);
   float4 *sz4 = reinterpret_cast<float4 *>(wz);
-  // pass 1: every 16-byte load of the cell in flight at once (global -> shared)
-#pragma unroll
-  for (int k = 0; k < G; ++k) {
-    const int g = lane + 32 * k;
-    if (g < ng) { cp_async16(sx4 + g, gx + g); cp_async16(sy4 + g, gy + g); cp_async16(sz4 + g, gz + g); }
-  }
-  cp_async_wait_all();
-  __syncwarp();
-  // the warp's next cell: HBM -> L2 while this one is computed
-  if (next_n > 0 && lane < 3 && ((next_off | next_n) & 3) == 0) {
-    const float *base = lane == 0 ? vx : (lane == 1 ? vy : vz);
-    prefetch_l2(base + next_off, (unsigned)next_n * 4u);
-  }
   // fp32 math below in packed pairs (FADD2 / FMUL2 / FFMA2: two lanes of
   // IEEE fp32 per instruction, sm_100)
   float2 s2x = make_float2(0.f, 0.f), s2y = s2x, s2z = s2x;
@@ -450,6 +440,41 @@ __device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, const KeyS
   }
   if (lane == 0) thermal_finish<float>(P, M, n, c, m_state, stats);
   return true;
+}
+
+// cp.async staging of one aligned fp32 cell into the slab (one commit group).
+__device__ __forceinline__ void thermal_stage_f32(const float *vx, const float *vy, const float *vz, int64_t off,
+                                                  int n, float *wx, float *wy, float *wz) {
+  constexpr int G = ThermalCap<float>::value / 4 / 32;
+  const int lane = threadIdx.x & 31;
+  const int ng = n >> 2;
+  const float4 *gx = reinterpret_cast<const float4 *>(vx + off), *gy = reinterpret_cast<const float4 *>(vy + off);
+  const float4 *gz = reinterpret_cast<const float4 *>(vz + off);
+  float4 *sx4 = reinterpret_cast<float4 *>(wx), *sy4 = reinterpret_cast<float4 *>(wy);
+  float4 *sz4 = reinterpret_cast<float4 *>(wz);
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    const int g = lane + 32 * k;
+    if (g < ng) { cp_async16(sx4 + g, gx + g); cp_async16(sy4 + g, gy + g); cp_async16(sz4 + g, gz + g); }
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+// Stage (all 16-byte loads in flight at once), wait, L2-prefetch the warp's
+// next cell, compute.
+__device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, const KeySched &ks, float *vx, float *vy,
+                                                 float *vz, int64_t off, int n, int c, float *wx, float *wy,
+                                                 float *wz, int32_t *m_state, double *stats, int64_t next_off,
+                                                 int next_n) {
+  const int lane = threadIdx.x & 31;
+  thermal_stage_f32(vx, vy, vz, off, n, wx, wy, wz);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncwarp();
+  if (next_n > 0 && lane < 3 && ((next_off | next_n) & 3) == 0) {
+    const float *base = lane == 0 ? vx : (lane == 1 ? vy : vz);
+    prefetch_l2(base + next_off, (unsigned)next_n * 4u);
+  }
+  return thermal_f32_compute(P, ks, vx, vy, vz, off, n, c, wx, wy, wz, m_state, stats);
 }
 
 template <typename Real>
