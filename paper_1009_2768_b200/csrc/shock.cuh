@@ -93,7 +93,9 @@ __global__ void shock_bin_init(ShockDev S, const Real *__restrict__ x, int64_t n
   atomicAdd(&counts[c], 1);
 }
 
-// exclusive scan of counts[0..C) into off[0..C], off[C] = total (one CTA)
+// exclusive scan of counts[0..C) into off[0..C], off[C] = total (one CTA).
+// Each thread owns 16 consecutive counts: 4 int4 loads and 8 longlong2 stores
+// (16-byte I/O) on full rounds, scalar on the ragged last one.
 __global__ void __launch_bounds__(1024) scan_offsets(const int32_t *__restrict__ counts, int C, int64_t *off,
                                                      int64_t cap, int *err) {
   __shared__ int64_t wsum[32];
@@ -102,15 +104,24 @@ __global__ void __launch_bounds__(1024) scan_offsets(const int32_t *__restrict__
   constexpr int ITEMS = 16;
   if (tid == 0) carry = 0;
   __syncthreads();
+  const bool al = ((reinterpret_cast<uintptr_t>(counts) | reinterpret_cast<uintptr_t>(off)) & 15) == 0;
   for (int base = 0; base < C; base += 1024 * ITEMS) {
-    int64_t v[ITEMS];
+    const int i0 = base + tid * ITEMS;
+    const bool vec = al && i0 + ITEMS <= C;
+    int v[ITEMS];
+    if (vec) {
+#pragma unroll
+      for (int q = 0; q < ITEMS / 4; ++q) {
+        const int4 w = *reinterpret_cast<const int4 *>(counts + i0 + 4 * q);
+        v[4 * q] = w.x; v[4 * q + 1] = w.y; v[4 * q + 2] = w.z; v[4 * q + 3] = w.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) v[k] = i0 + k < C ? counts[i0 + k] : 0;
+    }
     int64_t s = 0;
 #pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      const int i = base + tid * ITEMS + k;
-      v[k] = i < C ? counts[i] : 0;
-      s += v[k];
-    }
+    for (int k = 0; k < ITEMS; ++k) s += v[k];
     int64_t incl = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -130,11 +141,21 @@ __global__ void __launch_bounds__(1024) scan_offsets(const int32_t *__restrict__
     }
     __syncthreads();
     int64_t run = carry + (warp > 0 ? wsum[warp - 1] : 0) + incl - s;
+    if (vec) {
 #pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-      const int i = base + tid * ITEMS + k;
-      if (i < C) off[i] = run;
-      run += v[k];
+      for (int q = 0; q < ITEMS / 2; ++q) {
+        const int64_t a = run;
+        run += v[2 * q];
+        const int64_t b = run;
+        run += v[2 * q + 1];
+        *reinterpret_cast<longlong2 *>(off + i0 + 2 * q) = make_longlong2(a, b);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < ITEMS; ++k) {
+        if (i0 + k < C) off[i0 + k] = run;
+        run += v[k];
+      }
     }
     __syncthreads();
     if (tid == 0) carry += wsum[31];
