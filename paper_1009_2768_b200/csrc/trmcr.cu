@@ -656,6 +656,7 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
     const size_t slab = c->wlay.per_warp;
     c->warp_wpc = (int)std::max<size_t>(1, std::min<size_t>(kWarpCellWarps, (48 * 1024) / slab));
     c->warp_smem = (int)(slab * c->warp_wpc);
+    if (const char *pe = getenv("TRMCR_WARP_SMEM_PAD")) c->warp_smem += std::max(0, atoi(pe));   // occupancy experiments
     if (!want || c->warp_smem > smem_max - 2048) {
       c->wlay.n_cap = 0;     // disabled: the CTA kernel takes every general cell
     } else {
