@@ -18,7 +18,8 @@ constexpr int kWarpCellWarps = 4;
 
 // Per-warp scalars (in the warp's slab, lane 0 writes, __syncwarp publishes).
 struct WarpShared {
-  double ux, uy, uz, S0, sigma, p, mu, S_est, E1;
+  double ux, uy, uz, S0, sigma, p, mu, S_est, E1, c2;
+  uint4 pk;                // key of pi0
   double sums[4];
   int n, m_cur, m_next, d, top, lo, hi, r, flag, done;
   int64_t rem;
@@ -319,14 +320,17 @@ __device__ void wmaxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> 
   __syncwarp();
 }
 
-// The cell (already staged in B.v*, n particles, sums of the staging pass in
-// sx, sy, sz) through A3-A8.  Returns kOk or kOverflow (nothing written then
-// except B's scratch).  Writes m_state, stats, and (kStore) the velocities.
+// The general step of one cell in three phases that communicate through the
+// warp's WarpShared (so a CTA can run its warps' cells phase by phase in lock
+// step, keeping one phase's code in the instruction cache):
+//   wphase_begin    A3 moments, A4 split, pi0 key
+//   wphase_attempt  A5/A6 plan + collisions of one attempt, then A7's estimate
+//                   and decision (sh.done = 1 when no retry follows)
+//   wphase_end      A8 Maxwellian, m_state, statistics row
+// Each returns kOk or an overflow flag (the cell is then left for the CTA path).
 template <typename Real>
-__device__ int process_cell_warp(const StepParams &P, CellBuf<Real> &B, WarpShared &sh, double *usplit,
-                                 double sx, double sy, double sz, Real *out_x, Real *out_y, Real *out_z, int n,
-                                 uint32_t gcell, int32_t *m_state, double *stats_row, trmcr_coll_rec *log,
-                                 unsigned long long *log_count, int64_t log_cap) {
+__device__ int wphase_begin(const StepParams &P, CellBuf<Real> &B, WarpShared &sh, double *usplit, double sx,
+                            double sy, double sz, int n, uint32_t gcell, const int32_t *m_state) {
   const int lane = threadIdx.x & 31;
   const RngKey K{P.k0, P.k1, gcell, P.step};
   const int m0 = P.adaptive ? *m_state : P.m_fixed;
@@ -348,10 +352,11 @@ __device__ int process_cell_warp(const StepParams &P, CellBuf<Real> &B, WarpShar
     const uint4 w = K(kSplit, 0, (uint32_t)d, 0);
     usplit[d] = u53(w.x, w.y);
   }
+  const uint4 pk = K(kPerm, 0, 0, 0);
   c0 = warp_sum_call(c0); c1 = warp_sum_call(c1); c2 = warp_sum_call(c2); dv2 = warp_max_call(dv2);
   __syncwarp();
   if (lane == 0) {
-    sh.n = n; sh.ux = ux; sh.uy = uy; sh.uz = uz;
+    sh.n = n; sh.ux = ux; sh.uy = uy; sh.uz = uz; sh.c2 = c2; sh.pk = pk;
     sh.sums[0] = Sx; sh.sums[1] = Sy; sh.sums[2] = Sz; sh.sums[3] = c2 + n * (ux * ux + uy * uy + uz * uz);
     sh.S0 = (P.indicator == TRMCR_IND_PXX ? c0 : c1) / n;
     const double rho_c = P.shock ? n * P.w_over_dx : 1.0;
@@ -368,54 +373,69 @@ __device__ int process_cell_warp(const StepParams &P, CellBuf<Real> &B, WarpShar
     wsplit_extend(K, sh, m0, B.Q, B.L_cap, usplit);
     sh.r = 0; sh.lo = 1; sh.hi = sh.d < B.L_cap ? sh.d : B.L_cap;
     sh.budget = n; sh.leaf_off = 0;
+    sh.done = 0;
   }
   __syncwarp();
-  if (sh.flag != kOk) return sh.flag;
+  return sh.flag;
+}
+
+template <typename Real>
+__device__ int wphase_attempt(const StepParams &P, CellBuf<Real> &B, WarpShared &sh, double *usplit,
+                              uint32_t gcell, trmcr_coll_rec *log, unsigned long long *log_count,
+                              int64_t log_cap) {
+  const int lane = threadIdx.x & 31;
+  const RngKey K{P.k0, P.k1, gcell, P.step};
+  const int n = sh.n;
   Perm pi0;
-  pi0.init(K(kPerm, 0, 0, 0), (uint32_t)n);
-  const Real sigma = (Real)sh.sigma;
-  // ---- A5/A6 (attempt 0), then A7 (TRMC-RAD) retries: one loop, so every
-  // phase has a single inlined copy (instruction-cache footprint) ----
-  for (int attempt = 0;; ++attempt) {
-    wplan_counts<Real>(K, B, sh);
-    if (sh.flag != kOk) return sh.flag;
-    wplan_execute<Real>(P, K, B, sh, pi0, sigma, log, log_count, log_cap);
-    if (lane == 0) {
-      if (attempt == 0) {
-        sh.Ltot = sh.L;
-        sh.U = B.Q[0] < n - sh.Ltot ? B.Q[0] : n - sh.Ltot;
-        sh.nT = n - sh.Ltot - sh.U;
-        sh.m_next = sh.m_cur;
-        sh.S_est = sh.S0; sh.E1 = 0.0;
-      } else {
-        sh.Ltot += sh.L; sh.nT -= sh.L;
-      }
+  pi0.init(sh.pk, (uint32_t)n);
+  const int attempt = sh.r;
+  wplan_counts<Real>(K, B, sh);
+  if (sh.flag != kOk) return sh.flag;
+  wplan_execute<Real>(P, K, B, sh, pi0, (Real)sh.sigma, log, log_count, log_cap);
+  if (lane == 0) {
+    if (attempt == 0) {
+      sh.Ltot = sh.L;
+      sh.U = B.Q[0] < n - sh.Ltot ? B.Q[0] : n - sh.Ltot;
+      sh.nT = n - sh.Ltot - sh.U;
+      sh.m_next = sh.m_cur;
+      sh.S_est = sh.S0; sh.E1 = 0.0;
+    } else {
+      sh.Ltot += sh.L; sh.nT -= sh.L;
     }
-    __syncwarp();
-    if (!P.adaptive) break;
-    wrad_estimate<Real>(P, B, sh, pi0);
-    if (lane == 0) {
-      sh.done = 1;
-      if (sh.E1 > P.delta2 && sh.m_cur < P.m_cap) {
-        const int m_new = 2 * sh.m_cur < P.m_cap ? 2 * sh.m_cur : P.m_cap;
-        wsplit_extend(K, sh, m_new, B.Q, B.L_cap, usplit);
-        sh.r += 1;
-        sh.lo = sh.m_cur + 1;
-        sh.hi = sh.d < B.L_cap ? sh.d : B.L_cap;
-        sh.budget = sh.nT;
-        sh.leaf_off = sh.Ltot;
-        sh.m_cur = m_new;
-        sh.done = 0;
-      } else {
-        sh.m_next = (sh.E1 < P.delta1) ? (sh.m_cur / 2 > 1 ? sh.m_cur / 2 : 1) : sh.m_cur;
-      }
-    }
-    __syncwarp();
-    if (sh.flag != kOk) return sh.flag;
-    if (sh.done) break;
+    sh.done = 1;
   }
+  __syncwarp();
+  if (!P.adaptive) return kOk;
+  wrad_estimate<Real>(P, B, sh, pi0);
+  if (lane == 0) {
+    if (sh.E1 > P.delta2 && sh.m_cur < P.m_cap) {
+      const int m_new = 2 * sh.m_cur < P.m_cap ? 2 * sh.m_cur : P.m_cap;
+      wsplit_extend(K, sh, m_new, B.Q, B.L_cap, usplit);
+      sh.r += 1;
+      sh.lo = sh.m_cur + 1;
+      sh.hi = sh.d < B.L_cap ? sh.d : B.L_cap;
+      sh.budget = sh.nT;
+      sh.leaf_off = sh.Ltot;
+      sh.m_cur = m_new;
+      sh.done = 0;
+    } else {
+      sh.m_next = (sh.E1 < P.delta1) ? (sh.m_cur / 2 > 1 ? sh.m_cur / 2 : 1) : sh.m_cur;
+    }
+  }
+  __syncwarp();
+  return sh.flag;
+}
+
+template <typename Real>
+__device__ void wphase_end(const StepParams &P, CellBuf<Real> &B, WarpShared &sh, Real *out_x, Real *out_y,
+                           Real *out_z, uint32_t gcell, int32_t *m_state, double *stats_row) {
+  const int lane = threadIdx.x & 31;
+  const RngKey K{P.k0, P.k1, gcell, P.step};
+  const int n = sh.n;
+  Perm pi0;
+  pi0.init(sh.pk, (uint32_t)n);
   // ---- A8 ----
-  wmaxwellian<Real>(P, K, B, sh, pi0, c2);
+  wmaxwellian<Real>(P, K, B, sh, pi0, sh.c2);
   if (out_x != B.vx)
     for (int i = lane; i < n; i += 32) { out_x[i] = B.vx[i]; out_y[i] = B.vy[i]; out_z[i] = B.vz[i]; }
   if (lane == 0) {
@@ -432,6 +452,25 @@ __device__ int process_cell_warp(const StepParams &P, CellBuf<Real> &B, WarpShar
     s[TRMCR_ST_ENERGY] = sh.sums[3];
   }
   __syncwarp();
+}
+
+// The cell (already staged in B.v*, n particles, sums of the staging pass in
+// sx, sy, sz) through A3-A8, phases back to back.  Returns kOk or kOverflow
+// (nothing written then except B's scratch).  Writes m_state, stats, and the
+// velocities (out_* unless they alias the slab).
+template <typename Real>
+__device__ int process_cell_warp(const StepParams &P, CellBuf<Real> &B, WarpShared &sh, double *usplit,
+                                 double sx, double sy, double sz, Real *out_x, Real *out_y, Real *out_z, int n,
+                                 uint32_t gcell, int32_t *m_state, double *stats_row, trmcr_coll_rec *log,
+                                 unsigned long long *log_count, int64_t log_cap) {
+  int rc = wphase_begin<Real>(P, B, sh, usplit, sx, sy, sz, n, gcell, m_state);
+  if (rc != kOk) return rc;
+  for (;;) {
+    rc = wphase_attempt<Real>(P, B, sh, usplit, gcell, log, log_count, log_cap);
+    if (rc != kOk) return rc;
+    if (sh.done) break;
+  }
+  wphase_end<Real>(P, B, sh, out_x, out_y, out_z, gcell, m_state, stats_row);
   return kOk;
 }
 

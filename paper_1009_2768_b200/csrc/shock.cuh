@@ -855,6 +855,67 @@ shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
   }
 }
 
+// Lock-step variant of shock_collide_warp: CTAs of kLockWarps warps take
+// kLockWarps neighbouring cells (similar cost) per round and run the phases of
+// the general step (cell_warp.cuh: begin, attempts, end) with a CTA barrier
+// between phases, so the warps of a group execute the same phase's code (the
+// ~90 KB kernel body exceeds the 32 KB instruction cache; free-running warps
+// stall on instruction fetch: 5.3 cycles per issue, 0.2 in lock step).  Small
+// groups bound the barrier idle of unequal cells.  Sorted cells only (no
+// gather); results identical to the free-running kernel.
+constexpr int kLockWarps = 4;   // measured: 16 -> 2.02 ms, 8 -> 1.80, 4 -> 1.66 (C5), free-running 1.75
+template <typename Real>
+__global__ void __launch_bounds__(kLockWarps * 32, 16 / kLockWarps)
+shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
+                   Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, int *defer_count,
+                   int *defer_list, QueueArgs Q) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char *slab = smem + (size_t)warp * Lay.per_warp;
+  WarpShared &sh = *reinterpret_cast<WarpShared *>(slab + Lay.off_sh);
+  CellBuf<Real> B;
+  double *usplit;
+  bind_warp_slab(B, slab, Lay, usplit);
+  for (int base = blockIdx.x * kLockWarps; base < S.C; base += gridDim.x * kLockWarps) {
+    const int c = base + warp;
+    int64_t b0 = 0;
+    int n = 0, rc = kOk;
+    bool run = false;                         // this warp's cell still has phases to run
+    if (c < S.C) {
+      b0 = off_new[c];
+      n = (int)(off_new[c + 1] - b0);
+      B.vx = ovx + b0; B.vy = ovy + b0; B.vz = ovz + b0;
+      if (n > Lay.n_cap) {
+        rc = kOverflow;
+      } else if (n == 0) {
+        if (lane == 0) {
+          double *st = stats + (size_t)c * TRMCR_NSTATS;
+          for (int k = 0; k < TRMCR_NSTATS; ++k) st[k] = 0.0;
+          const int m = P.adaptive ? m_state[c] : P.m_fixed;
+          st[TRMCR_ST_MUSED] = m; st[TRMCR_ST_MNEXT] = m;
+        }
+      } else {
+        double sx = 0, sy = 0, sz = 0;
+        for (int i = lane; i < n; i += 32) { sx += B.vx[i]; sy += B.vy[i]; sz += B.vz[i]; }
+        rc = wphase_begin<Real>(P, B, sh, usplit, sx, sy, sz, n, P.cell_base + (uint32_t)c, m_state + c);
+        run = rc == kOk;
+      }
+    }
+    const bool work = run;
+    while (__syncthreads_or(run)) {
+      if (run) {
+        rc = wphase_attempt<Real>(P, B, sh, usplit, P.cell_base + (uint32_t)c, Q.log, Q.log_count, Q.log_cap);
+        run = rc == kOk && !sh.done;
+      }
+    }
+    if (work && rc == kOk)
+      wphase_end<Real>(P, B, sh, B.vx, B.vy, B.vz, P.cell_base + (uint32_t)c, m_state + c,
+                       stats + (size_t)c * TRMCR_NSTATS);
+    if (c < S.C && rc != kOk && lane == 0) defer_list[atomicAdd(defer_count, 1)] = c;
+    __syncthreads();
+  }
+}
+
 template <typename Real, int THREADS>
 __global__ void __launch_bounds__(THREADS, 768 / THREADS)
 shock_collide_smem(StepParams P, SmemLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
@@ -1088,9 +1149,14 @@ trmcr_status shock_finish(trmcr_ctx *c) {
   if (use_warp) {
     CUDA_TRY(c, cudaMemsetAsync(c->d_defer_count, 0, sizeof(int), c->stream));
     prof_begin(c, TRMCR_K_SHOCK_WARP);
-    shock_collide_warp<Real><<<c->warp_grid, c->warp_wpc * 32, c->warp_smem, c->stream>>>(
-        c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
-        c->d_defer_list, Q);
+    if (G.scatter && c->lock_grid > 0)
+      shock_collide_lock<Real><<<c->lock_grid, kLockWarps * 32, c->lock_smem, c->stream>>>(
+          c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
+          c->d_defer_list, Q);
+    else
+      shock_collide_warp<Real><<<c->warp_grid, c->warp_wpc * 32, c->warp_smem, c->stream>>>(
+          c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
+          c->d_defer_list, Q);
     if (auto e = check_launch(c, "shock_collide_warp", TRMCR_K_SHOCK_WARP)) return e;
   }
   prof_begin(c, TRMCR_K_SHOCK_SMEM);

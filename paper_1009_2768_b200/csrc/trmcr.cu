@@ -674,6 +674,22 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
       else
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, shock_collide_warp<float>, c->warp_wpc * 32, c->warp_smem);
       c->warp_grid = std::max(1, std::min((c->ncells + c->warp_wpc - 1) / c->warp_wpc, nsm * std::max(occ, 1)));
+      // shock: lock-step kernel (TRMCR_SHOCK_LOCKSTEP=0 disables)
+      const char *le = getenv("TRMCR_SHOCK_LOCKSTEP");
+      const size_t lsm = slab * kLockWarps;
+      if (c->geometry == TRMCR_SHOCK_1D && !v_smem && !(le && atoi(le) == 0) && lsm <= (size_t)smem_max - 1024) {
+        const void *lf = c->dtype == TRMCR_F64 ? (const void *)shock_collide_lock<double>
+                                               : (const void *)shock_collide_lock<float>;
+        int occ_l = 0;
+        if (allow_max_dyn_smem(lf, smem_max) == cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_l, lf, kLockWarps * 32, lsm) == cudaSuccess &&
+            occ_l > 0) {
+          c->lock_smem = (int)lsm;
+          c->lock_grid = std::max(1, std::min((c->ncells + kLockWarps - 1) / kLockWarps, nsm * occ_l));
+        } else {
+          cudaGetLastError();
+        }
+      }
     }
   }
 
