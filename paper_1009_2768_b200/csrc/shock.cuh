@@ -512,7 +512,7 @@ edge_place(ShockDev S, const int64_t *__restrict__ off_new, const int *ng, const
 // than W cells before the tile's first destination (none of its particles, nor
 // any earlier one, can reach it); transport_kernel stored each tile's
 // destination histogram over [dmin, dmin + kHist).
-constexpr int kScatterThreads = 256;
+constexpr int kScatterThreads = 512;
 template <typename Real>
 __global__ void __launch_bounds__(kScatterThreads)
 scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *__restrict__ off_new,
