@@ -250,23 +250,31 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int d[NG][P4];
   int disp = 0, emi = 0, dropped = 0, dmin = INT32_MAX, smax = -1;
+  // every load of the tile first (x is rewritten below: the compiler may not
+  // move later loads above those stores), then the arithmetic
+  Real xa[NG][P4], va[NG][P4];
 #pragma unroll
   for (int g = 0; g < NG; ++g) {
     const int64_t i0 = tile0 + ((int64_t)g * kTransportThreads + threadIdx.x) * P4;
-    Real xs[P4], vs[P4];
-    const bool vec = (i0 + P4 <= n) && (sizeof(Real) * P4 == 16);
-    if (vec) {
+    if ((i0 + P4 <= n) && (sizeof(Real) * P4 == 16)) {
       using V = typename Vec<Real>::T;
       const V xv = *reinterpret_cast<const V *>(x + i0), vv = *reinterpret_cast<const V *>(vx + i0);
 #pragma unroll
-      for (int k = 0; k < P4; ++k) { xs[k] = vget<V, Real>(xv, k); vs[k] = vget<V, Real>(vv, k); }
+      for (int k = 0; k < P4; ++k) { xa[g][k] = vget<V, Real>(xv, k); va[g][k] = vget<V, Real>(vv, k); }
     } else {
 #pragma unroll
       for (int k = 0; k < P4; ++k) {
-        xs[k] = (i0 + k < n) ? x[i0 + k] : Real(0);
-        vs[k] = (i0 + k < n) ? vx[i0 + k] : Real(0);
+        xa[g][k] = (i0 + k < n) ? x[i0 + k] : Real(0);
+        va[g][k] = (i0 + k < n) ? vx[i0 + k] : Real(0);
       }
     }
+  }
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    const int64_t i0 = tile0 + ((int64_t)g * kTransportThreads + threadIdx.x) * P4;
+    Real *xs = xa[g];
+    const Real *vs = va[g];
+    const bool vec = (i0 + P4 <= n) && (sizeof(Real) * P4 == 16);
 #pragma unroll
     for (int k = 0; k < P4; ++k) {
       d[g][k] = -1;
