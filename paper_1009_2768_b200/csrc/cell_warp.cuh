@@ -237,10 +237,25 @@ __device__ void wrad_estimate(const StepParams &P, CellBuf<Real> &B, WarpShared 
   const bool pxx = P.indicator == TRMCR_IND_PXX;
   const double ux = sh.ux;
   double v0 = 0, v1 = 0, tx = 0, ty = 0, tz = 0, t2 = 0;
-  for (int i = lane; i < n; i += 32) {
-    const double x = B.vx[i], y = B.vy[i], z = B.vz[i];
-    if (pxx) { const double dx = x - ux; v0 += dx * dx; }
-    else { const double v2 = x * x + y * y + z * z; v0 += v2 * v2; }
+  if constexpr (sizeof(Real) == 4) {            // fp32 lane partials (statistical mode)
+    const float fux = (float)ux;
+    float f0 = 0;
+    if (pxx) {
+      for (int i = lane; i < n; i += 32) { const float dx = B.vx[i] - fux; f0 += dx * dx; }
+    } else {
+      for (int i = lane; i < n; i += 32) {
+        const float x = B.vx[i], y = B.vy[i], z = B.vz[i];
+        const float v2 = x * x + y * y + z * z;
+        f0 += v2 * v2;
+      }
+    }
+    v0 = f0;
+  } else {
+    for (int i = lane; i < n; i += 32) {
+      const double x = B.vx[i], y = B.vy[i], z = B.vz[i];
+      if (pxx) { const double dx = x - ux; v0 += dx * dx; }
+      else { const double v2 = x * x + y * y + z * z; v0 += v2 * v2; }
+    }
   }
   for (int q = lane; q < nT; q += 32) {
     const uint32_t s = pi0((uint32_t)(sh.Ltot + q));
@@ -338,15 +353,32 @@ __device__ int wphase_begin(const StepParams &P, CellBuf<Real> &B, WarpShared &s
   const double Sx = warp_sum_call(sx), Sy = warp_sum_call(sy), Sz = warp_sum_call(sz);
   const double ux = Sx / n, uy = Sy / n, uz = Sz / n;
   double c0 = 0, c1 = 0, c2 = 0, dv2 = 0;
-  for (int i = lane; i < n; i += 32) {
-    const double x = B.vx[i], y = B.vy[i], z = B.vz[i];
-    const double dx = x - ux, dy = y - uy, dz = z - uz;
-    const double r2 = dx * dx + dy * dy + dz * dz;
-    dv2 = fmax(dv2, r2);
-    c0 += dx * dx;
-    const double v2 = x * x + y * y + z * z;
-    c1 += v2 * v2;
-    c2 += r2;
+  if constexpr (sizeof(Real) == 4) {
+    // fp32 statistical mode: fp32 lane partials (~n/32 terms), fp64 warp sums
+    const float fux = (float)ux, fuy = (float)uy, fuz = (float)uz;
+    float f0 = 0, f1 = 0, f2 = 0, fm = 0;
+    for (int i = lane; i < n; i += 32) {
+      const float x = B.vx[i], y = B.vy[i], z = B.vz[i];
+      const float dx = x - fux, dy = y - fuy, dz = z - fuz;
+      const float r2 = dx * dx + dy * dy + dz * dz;
+      fm = fmaxf(fm, r2);
+      f0 += dx * dx;
+      const float v2 = x * x + y * y + z * z;
+      f1 += v2 * v2;
+      f2 += r2;
+    }
+    c0 = f0; c1 = f1; c2 = f2; dv2 = fm;
+  } else {
+    for (int i = lane; i < n; i += 32) {
+      const double x = B.vx[i], y = B.vy[i], z = B.vz[i];
+      const double dx = x - ux, dy = y - uy, dz = z - uz;
+      const double r2 = dx * dx + dy * dy + dz * dz;
+      dv2 = fmax(dv2, r2);
+      c0 += dx * dx;
+      const double v2 = x * x + y * y + z * z;
+      c1 += v2 * v2;
+      c2 += r2;
+    }
   }
   for (int d = lane; d < kSplitPre; d += 32) {   // split uniforms, in parallel
     const uint4 w = K(kSplit, 0, (uint32_t)d, 0);

@@ -904,7 +904,13 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
         }
       } else {
         double sx = 0, sy = 0, sz = 0;
-        for (int i = lane; i < n; i += 32) { sx += B.vx[i]; sy += B.vy[i]; sz += B.vz[i]; }
+        if constexpr (sizeof(Real) == 4) {
+          float fx = 0, fy = 0, fz = 0;
+          for (int i = lane; i < n; i += 32) { fx += B.vx[i]; fy += B.vy[i]; fz += B.vz[i]; }
+          sx = fx; sy = fy; sz = fz;
+        } else {
+          for (int i = lane; i < n; i += 32) { sx += B.vx[i]; sy += B.vy[i]; sz += B.vz[i]; }
+        }
         rc = wphase_begin<Real>(P, B, sh, usplit, sx, sy, sz, n, P.cell_base + (uint32_t)c, m_state + c);
         run = rc == kOk;
       }
