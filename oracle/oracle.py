@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "trmcr_oracle.c")
 LIB = os.path.join(HERE, "liborc.so")
 
-MAXWELL, HARD_SPHERE = 0, 1
+MAXWELL, HARD_SPHERE, VHS = 0, 1, 2
 IND_PXX, IND_M4 = 0, 1
 P_SPLIT, P_TYPE, P_PERM, P_COLL, P_COLL2, P_MAXW, P_MAXW2, P_RESV, P_RESV2, P_LITERAL = range(1, 11)
 
@@ -42,7 +42,7 @@ class Params(C.Structure):
         ("model", C.c_int32), ("adaptive", C.c_int32), ("m_fixed", C.c_int32),
         ("m_init", C.c_int32), ("m_cap", C.c_int32), ("indicator", C.c_int32),
         ("delta1", C.c_double), ("delta2", C.c_double), ("eps", C.c_double), ("dt", C.c_double),
-        ("seed", C.c_uint64), ("literal", C.c_int32), ("pad", C.c_int32),
+        ("seed", C.c_uint64), ("literal", C.c_int32), ("pad", C.c_int32), ("alpha", C.c_double),
     ]
 
 
@@ -186,11 +186,12 @@ class Config:
     dt: float = 0.1
     seed: int = 1
     literal: int = 0
+    alpha: float = 1.0          # VHS exponent (model = VHS)
 
     def c(self) -> Params:
         return Params(self.model, self.adaptive, self.m_fixed, self.m_init, self.m_cap,
                       self.indicator, self.delta1, self.delta2, self.eps, self.dt, self.seed,
-                      self.literal, 0)
+                      self.literal, 0, self.alpha)
 
 
 class HomogeneousState:

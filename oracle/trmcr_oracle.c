@@ -278,6 +278,24 @@ typedef struct {
   double *vx, *vy, *vz; orc_cell_stats *st; logger *lg;
 } cellctx;
 
+/* Acceptance-rejection of a dummy collision (sec. VHS): accept iff
+ * xi Sigma < sigma_ij with sigma_ij = K|q|^alpha and Sigma = K (2 dv)^alpha
+ * (K cancels [R7]); Sigma here is Sigma' = (2 dv)^alpha.  HS (alpha = 1)
+ * compares |q| itself; Maxwell (alpha = 0) always accepts.  A violation is
+ * a pair above the bound (|q|^alpha > Sigma'). */
+static int vhs_accept(const orc_params *P, double sigma, double q, double xa, double *viol) {
+  if (P->model == ORC_HARD_SPHERE) {
+    if (q > sigma) *viol += 1;
+    return xa * sigma < q;
+  }
+  if (P->model == ORC_VHS) {
+    const double qa = pow(q, P->alpha);
+    if (qa > sigma) *viol += 1;
+    return xa * sigma < qa;
+  }
+  return 1;
+}
+
 static void tree_collision(cellctx *X, int r, int d, int64_t j, int64_t si, int64_t sk) {
   uint32_t w[4], w2[4];
   draw(&X->K, ORC_P_COLL, r, d, (uint32_t)j, w);
@@ -287,11 +305,10 @@ static void tree_collision(cellctx *X, int r, int d, int64_t j, int64_t si, int6
   double vk[3] = {X->vx[sk], X->vy[sk], X->vz[sk]};
   int acc = 1;
   X->st->proposals += 1;
-  if (X->P->model == ORC_HARD_SPHERE) {
+  if (X->P->model != ORC_MAXWELL) {
     double qx = vi[0] - vk[0], qy = vi[1] - vk[1], qz = vi[2] - vk[2];
     double q = sqrt(qx * qx + qy * qy + qz * qz);
-    if (q > X->sigma) X->st->violations += 1;
-    acc = (xa * X->sigma < q);
+    acc = vhs_accept(X->P, X->sigma, q, xa, &X->st->violations);
   }
   if (acc) {
     orc_collide_pair(vi, vk, xi1, xi2);
@@ -458,11 +475,10 @@ static void lit_sample(literal_t *T, int lev, int64_t *oi, int64_t *oj) {
   int acc = 1;
   double xa = lit_uniform(T), xi1 = lit_uniform(T), xi2 = lit_uniform(T);
   X->st->proposals += 1;
-  if (X->P->model == ORC_HARD_SPHERE) {
+  if (X->P->model != ORC_MAXWELL) {
     double qx = vi[0] - vj[0], qy = vi[1] - vj[1], qz = vi[2] - vj[2];
     double q = sqrt(qx * qx + qy * qy + qz * qz);
-    if (q > X->sigma) X->st->violations += 1;
-    acc = (xa * X->sigma < q);
+    acc = vhs_accept(X->P, X->sigma, q, xa, &X->st->violations);
   }
   if (acc) {
     orc_collide_pair(vi, vj, xi1, xi2);
@@ -543,6 +559,9 @@ static int collide_cell(const orc_params *P, keyctx K, double rho_c, int64_t n, 
   if (P->model == ORC_HARD_SPHERE) {
     sigma = 2.0 * sqrt(dv2);                    /* Sigma' = 2 dv; K = 1/(4 pi) [R4] */
     mu = rho_c * sigma;                         /* mu = 4 pi rho Sigma [R5]         */
+  } else if (P->model == ORC_VHS) {
+    sigma = pow(2.0 * sqrt(dv2), P->alpha);     /* Sigma' = sigma(2 dv) / K */
+    mu = rho_c * sigma;
   } else {
     mu = rho_c;                                 /* Maxwell: mu = 4 pi rho K          */
   }

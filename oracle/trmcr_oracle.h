@@ -13,7 +13,7 @@
 extern "C" {
 #endif
 
-enum { ORC_MAXWELL = 0, ORC_HARD_SPHERE = 1 };
+enum { ORC_MAXWELL = 0, ORC_HARD_SPHERE = 1, ORC_VHS = 2 };   /* B = K|q|^alpha, alpha = 0, 1, or in (0,1) */
 enum { ORC_IND_PXX = 0, ORC_IND_M4 = 1 };
 
 /* Philox purposes. */
@@ -34,6 +34,7 @@ typedef struct {
   uint64_t seed;
   int32_t literal;     /* 1: literal recursive Alg 4.3/4.4 (statistical checks) */
   int32_t pad;
+  double alpha;        /* ORC_VHS exponent                          */
 } orc_params;
 
 /* Per-cell result of one collision step (all counts as doubles for ctypes). */

@@ -256,3 +256,48 @@ def test_rad_decision_rule(orc):
     st.step(1)
     s = st.stats[0]
     assert s["E1"] > 0.01 and s["m_used"] == 32 and s["m_next"] == 32   # forced accept at cap
+
+
+def test_vhs_limits_are_hs_and_maxwell(orc):
+    """VHS (B = K|q|^alpha; dummy collisions): alpha = 1 is
+    the hard-sphere step bit for bit; alpha = 0 accepts every pair, as Maxwell
+    molecules do, with the same mu = rho (Sigma' = 1)."""
+    vx, vy, vz, off = synth.ragged_cells(12, 400, seed=8)
+    kw = dict(m_fixed=8, eps=0.5, dt=0.2, seed=8)
+    for alpha, ref_model in ((1.0, 1), (0.0, 0)):
+        a = orc.HomogeneousState(orc.Config(model=orc.VHS, alpha=alpha, **kw), vx, vy, vz, off)
+        b = orc.HomogeneousState(orc.Config(model=ref_model, **kw), vx, vy, vz, off)
+        a.step(2)
+        b.step(2)
+        for k in ("vx", "vy", "vz"):
+            np.testing.assert_array_equal(getattr(a, k), getattr(b, k))
+        for f in ("p", "mu", "proposals", "accepted", "violations", "leaves", "thermalised"):
+            np.testing.assert_array_equal(a.stats[f], b.stats[f], err_msg=f)
+    np.testing.assert_array_equal(a.stats["sigma"][a.stats["n"] > 0], 1.0)   # alpha = 0: (2 dv)^0
+
+
+@pytest.mark.parametrize("alpha", [0.3, 0.7])
+def test_vhs_acceptance_fraction(orc, alpha):
+    """accepted/proposed = E[|q|^alpha] / Sigma' over the proposed level-1 pairs
+    (original particles), Sigma' = (2 max|v - u|)^alpha; and
+    E|q|^alpha of two independent unit-temperature Maxwellian velocities is
+    2^alpha Gamma((3 + alpha)/2) / Gamma(3/2) (|q| = sqrt(2) chi_3)."""
+    n = 20_000
+    v = synth.maxwellian(n, seed=9)
+    st = _hom(orc, orc.Config(model=orc.VHS, alpha=alpha, eps=1.0, dt=0.05, seed=9), v, [0, n],
+              log_cap=200_000)
+    V = np.stack(v, 1).copy()
+    u = V.mean(0)
+    st.step(1)
+    sig = st.stats["sigma"][0]
+    assert sig == pytest.approx((2 * np.sqrt(((V - u) ** 2).sum(1).max())) ** alpha, rel=1e-12)
+    log = st.collisions()
+    lvl1 = log[log["level"] == 1]
+    q = np.linalg.norm(V[lvl1["slot_i"]] - V[lvl1["slot_k"]], axis=1)
+    p_acc = q ** alpha / sig
+    acc = lvl1["accepted"]
+    se = math.sqrt((p_acc * (1 - p_acc)).sum()) / len(acc)
+    assert abs(acc.mean() - p_acc.mean()) < 4 * se + 1e-4
+    qa = q ** alpha
+    closed = 2 ** alpha * math.gamma((3 + alpha) / 2) / math.gamma(1.5)
+    assert abs(qa.mean() - closed) < 4 * qa.std() / math.sqrt(len(qa))
