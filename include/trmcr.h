@@ -48,7 +48,10 @@ typedef enum {
   TRMCR_ESTATE = 6      /* context unusable after an earlier sticky error          */
 } trmcr_status;
 
-typedef enum { TRMCR_MAXWELL = 0, TRMCR_HARD_SPHERE = 1 } trmcr_model;   /* alpha = 0 / 1 */
+/* B(|q|, .) = K |q|^alpha, K = 1/(4 pi): Maxwell alpha = 0, hard spheres
+ * alpha = 1, VHS any alpha in [0, 1] (trmcr_kernel.alpha; dummy collisions with
+ * Sigma = sigma(2 dv), sec. VHS). */
+typedef enum { TRMCR_MAXWELL = 0, TRMCR_HARD_SPHERE = 1, TRMCR_VHS = 2 } trmcr_model;
 typedef enum { TRMCR_F32 = 0, TRMCR_F64 = 1 } trmcr_dtype;
 typedef enum { TRMCR_HOMOGENEOUS = 0, TRMCR_SHOCK_1D = 1 } trmcr_geometry;
 typedef enum { TRMCR_IND_PXX = 0, TRMCR_IND_M4 = 1 } trmcr_indicator;  /* RAD indicator S */
@@ -103,6 +106,7 @@ typedef struct {
   int32_t indicator;         /* trmcr_indicator                                       */
   double delta1, delta2;     /* RAD interval, 0 < delta1 < delta2 (paper 0.005, 0.01) */
   uint64_t seed;             /* Philox4x32-10 key                                     */
+  double alpha;              /* TRMCR_VHS exponent in [0, 1] (ignored otherwise)      */
 } trmcr_kernel;
 
 /* Per-cell statistics row (doubles), trmcr_stats(): */

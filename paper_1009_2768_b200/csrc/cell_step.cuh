@@ -38,6 +38,7 @@ enum : int { kErrPlanCapacity = 1, kErrParticleCapacity = 2, kErrInternal = 16 }
 
 struct StepParams {
   int model, adaptive, m_fixed, m_cap, indicator, log_on;
+  double alpha;            // VHS exponent
   double delta1, delta2, dt, eps;
   uint32_t k0, k1, step, cell_base;
   int shock;               // rho_c = n w / dx when 1, else 1
@@ -85,11 +86,16 @@ template <typename Real> struct RealOps;
 template <> struct RealOps<double> {
   __device__ static __forceinline__ double sqrt_(double x) { return sqrt(x); }
   __device__ static __forceinline__ void sincospi_(double x, double *s, double *c) { sincospi(x, s, c); }
+  __device__ static __forceinline__ double pow_(double x, double a) { return pow(x, a); }
 };
 template <> struct RealOps<float> {
   __device__ static __forceinline__ float sqrt_(float x) { return sqrtf(x); }
   __device__ static __forceinline__ void sincospi_(float x, float *s, float *c) { sincospif(x, s, c); }
+  __device__ static __forceinline__ float pow_(float x, float a) { return powf(x, a); }
 };
+
+// VHS majorant Sigma' = (2 sqrt(dv2))^alpha (Sigma = sigma(2 dv); K cancels).
+__device__ __forceinline__ double vhs_majorant(double dv2, double alpha) { return pow(2.0 * sqrt(dv2), alpha); }
 
 // IR at split level d with its keyed uniform; exact 0 when y < 2^-53.
 // Uniforms of levels < kSplitPre were drawn in parallel into `pre`.
@@ -154,6 +160,10 @@ __device__ __forceinline__ int tree_collision(const StepParams &P, const RngKey 
   if (P.model == TRMCR_HARD_SPHERE) {       // accept iff xi Sigma' < |q|  [R7]
     viol += (q > sigma) ? 1u : 0u;
     acc = (xa * sigma < q);
+  } else if (P.model == TRMCR_VHS) {        // accept iff xi Sigma' < |q|^alpha (sec. VHS)
+    const Real qa = O::pow_(q, (Real)P.alpha);
+    viol += (qa > sigma) ? 1u : 0u;
+    acc = (xa * sigma < qa);
   }
   if (acc) {
     const Real c = Real(2) * xi1 - Real(1);
@@ -524,6 +534,9 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
     if (P.model == TRMCR_HARD_SPHERE) {
       sh.sigma = 2.0 * sqrt(dv2);            // Sigma' = 2 dv  [R4]
       sh.mu = rho_c * sh.sigma;              // mu = 4 pi rho Sigma  [R5]
+    } else if (P.model == TRMCR_VHS) {
+      sh.sigma = vhs_majorant(dv2, P.alpha); // Sigma' = sigma(2 dv) / K
+      sh.mu = rho_c * sh.sigma;
     } else {
       sh.sigma = 0.0;
       sh.mu = rho_c;

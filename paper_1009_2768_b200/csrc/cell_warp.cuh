@@ -393,6 +393,7 @@ __device__ int wphase_begin(const StepParams &P, CellBuf<Real> &B, WarpShared &s
     sh.S0 = (P.indicator == TRMCR_IND_PXX ? c0 : c1) / n;
     const double rho_c = P.shock ? n * P.w_over_dx : 1.0;
     if (P.model == TRMCR_HARD_SPHERE) { sh.sigma = 2.0 * sqrt(dv2); sh.mu = rho_c * sh.sigma; }
+    else if (P.model == TRMCR_VHS) { sh.sigma = vhs_majorant(dv2, P.alpha); sh.mu = rho_c * sh.sigma; }
     else { sh.sigma = 0.0; sh.mu = rho_c; }
     sh.p = exp(-(sh.mu * P.dt / P.eps));
     sh.m_cur = m0; sh.flag = kOk;

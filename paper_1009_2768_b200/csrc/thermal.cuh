@@ -84,6 +84,7 @@ __device__ __forceinline__ void thermal_decide(const StepParams &P, ThermalMomen
   M.sigma = 0.0;
   M.mu = 1.0;
   if (P.model == TRMCR_HARD_SPHERE) { M.sigma = 2.0 * sqrt(dv2); M.mu = M.sigma; }
+  else if (P.model == TRMCR_VHS) { M.sigma = vhs_majorant(dv2, P.alpha); M.mu = M.sigma; }
   M.p = exp(-(M.mu * P.dt / P.eps));
 }
 

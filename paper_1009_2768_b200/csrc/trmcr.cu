@@ -437,7 +437,10 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
   if (pp->dtype != TRMCR_F32 && pp->dtype != TRMCR_F64) return fail(nullptr, TRMCR_EINVAL, "bad dtype");
   if (pp->n < 0 || pp->n > 0x7FFFFFFFLL) return fail(nullptr, TRMCR_EINVAL, "bad particle count");
   if (pp->n > 0 && (!pp->vx || !pp->vy || !pp->vz)) return fail(nullptr, TRMCR_EINVAL, "null velocity pointer");
-  if (kk->model != TRMCR_MAXWELL && kk->model != TRMCR_HARD_SPHERE) return fail(nullptr, TRMCR_EINVAL, "bad model");
+  if (kk->model != TRMCR_MAXWELL && kk->model != TRMCR_HARD_SPHERE && kk->model != TRMCR_VHS)
+    return fail(nullptr, TRMCR_EINVAL, "bad model");
+  if (kk->model == TRMCR_VHS && !(kk->alpha >= 0.0 && kk->alpha <= 1.0))
+    return fail(nullptr, TRMCR_EINVAL, "VHS alpha must lie in [0, 1]");
   if (kk->indicator != TRMCR_IND_PXX && kk->indicator != TRMCR_IND_M4) return fail(nullptr, TRMCR_EINVAL, "bad indicator");
   if (kk->adaptive) {
     if (kk->m_init < 1 || kk->m_cap < kk->m_init || kk->m_cap > 16384)
@@ -493,7 +496,8 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
 
   // ---- parameters ----
   StepParams &P = c->P;
-  P.model = kk->model; P.adaptive = kk->adaptive; P.m_fixed = kk->m_fixed; P.m_cap = kk->m_cap;
+  P.model = kk->model; P.alpha = kk->model == TRMCR_VHS ? kk->alpha : (kk->model == TRMCR_HARD_SPHERE ? 1.0 : 0.0);
+  P.adaptive = kk->adaptive; P.m_fixed = kk->m_fixed; P.m_cap = kk->m_cap;
   P.indicator = kk->indicator; P.log_on = 0;
   P.delta1 = kk->delta1; P.delta2 = kk->delta2; P.dt = dt; P.eps = eps;
   P.k0 = (uint32_t)kk->seed; P.k1 = (uint32_t)(kk->seed >> 32);

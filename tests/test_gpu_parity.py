@@ -107,6 +107,15 @@ def test_homogeneous_fp64_hs_rad_ragged(orc, api):
     _parity(orc, api, v[:3], v[3], 6, model=1, adaptive=1, m_init=2, m_cap=64, eps=0.5, dt=0.1, seed=6)
 
 
+@pytest.mark.parametrize("alpha", [0.35, 0.8])
+def test_homogeneous_fp64_vhs_rad_ragged(orc, api, alpha):
+    """VHS molecules, B = K|q|^alpha (sec. VHS): Sigma' = (2 dv)^alpha, accept iff
+    xi Sigma' < |q|^alpha; every decision and velocity as the oracle's."""
+    v = synth.ragged_cells(50, 400, seed=12)
+    _parity(orc, api, v[:3], v[3], 5, model=2, alpha=alpha, adaptive=1, m_init=2, m_cap=64, eps=0.5, dt=0.1,
+            seed=13)
+
+
 def test_homogeneous_fp64_hs_m4_indicator(orc, api):
     v = synth.ragged_cells(30, 500, seed=9)
     _parity(orc, api, v[:3], v[3], 4, model=1, adaptive=1, m_init=4, m_cap=32, indicator=1, eps=0.2,
