@@ -43,6 +43,7 @@ class Params(C.Structure):
         ("m_init", C.c_int32), ("m_cap", C.c_int32), ("indicator", C.c_int32),
         ("delta1", C.c_double), ("delta2", C.c_double), ("eps", C.c_double), ("dt", C.c_double),
         ("seed", C.c_uint64), ("literal", C.c_int32), ("pad", C.c_int32), ("alpha", C.c_double),
+        ("wb", C.c_int32), ("wb_max", C.c_int32),
     ]
 
 
@@ -111,6 +112,8 @@ def lib():
         L.orc_rankine_hugoniot.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double,
                                            P(C.c_double)]
         L.orc_rankine_hugoniot.restype = C.c_int32
+        L.orc_tree_length.argtypes = [P(C.c_int32), C.c_int64, C.c_int32, P(C.c_int64)]
+        L.orc_tree_length.restype = C.c_double
         _lib = L
     return _lib
 
@@ -139,6 +142,17 @@ def ir(y, u):
 def feistel(x, N, rk):
     r = np.ascontiguousarray(rk, dtype=np.uint32)
     return lib().orc_feistel(int(x), int(N), _p(r, C.c_uint32))
+
+
+def tree_length(path, definition):
+    """Alg 4.5 length of the tree given by its path list; definition 1 = 1 + min
+    (eq. def:2), 2 = 1 + mean (eq. def:3), 3 = the coefficient k (eq. def:1)."""
+    a = np.ascontiguousarray(path, dtype=np.int32)
+    used = C.c_int64(0)
+    L = lib().orc_tree_length(_p(a, C.c_int32), len(a), int(definition), C.byref(used))
+    if used.value != len(a):
+        raise ValueError("malformed path list")
+    return L
 
 
 def collide_pair(vi, vj, xi1, xi2):
@@ -187,11 +201,13 @@ class Config:
     seed: int = 1
     literal: int = 0
     alpha: float = 1.0          # VHS exponent (model = VHS)
+    wb: int = 0                 # TRMC-WB length: 0 off, 1 min (def:2), 2 mean (def:3), 3 level (def:1)
+    wb_max: int = 0             # TRMC-WB threshold m_max
 
     def c(self) -> Params:
         return Params(self.model, self.adaptive, self.m_fixed, self.m_init, self.m_cap,
                       self.indicator, self.delta1, self.delta2, self.eps, self.dt, self.seed,
-                      self.literal, 0, self.alpha)
+                      self.literal, 0, self.alpha, self.wb, self.wb_max)
 
 
 class HomogeneousState:

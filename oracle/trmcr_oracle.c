@@ -327,7 +327,40 @@ static void tree_collision(cellctx *X, int r, int d, int64_t j, int64_t si, int6
 /* f_0 are original particles, samples of f_k, k>=1, are outputs   */
 /* of level-k collisions ("stored particles").                  */
 /* ===================================================================== */
-typedef struct { int64_t C; int32_t *type; int64_t *slot; } level_t;
+typedef struct {
+  int64_t C; int32_t *type; int64_t *slot;
+  double *len;            /* TRMC-WB: tree length of each collision's outputs        */
+  unsigned char *used;    /* TRMC-WB: output o consumed by a higher level (2C flags) */
+} level_t;
+
+/* TRMC-WB (sec. 4.4, eqs def:1-3): length of a sample of f_k made by a
+ * collision of samples of f_j and f_h (k = h + j + 1) with lengths a, b. */
+static double wb_combine(int32_t def, int32_t k, double a, double b) {
+  if (def == 1) return 1.0 + (a < b ? a : b);        /* eq. (def:2) */
+  if (def == 2) return 1.0 + 0.5 * (a + b);          /* eq. (def:3) */
+  return (double)k;                                  /* eq. (def:1) */
+}
+
+/* Alg 4.5 on an explicit path list (the pin of Table 1). */
+static double tree_len_rec(const int32_t *path, int64_t len, int64_t *pos, int32_t k, int32_t def,
+                           int *bad) {
+  if (k == 0) return 0.0;
+  if (*pos + 2 > len) { *bad = 1; return 0.0; }
+  const int32_t j = path[(*pos)++], h = path[(*pos)++];
+  if (j < 0 || h < 0 || j + h + 1 != k) { *bad = 1; return 0.0; }
+  const double a = tree_len_rec(path, len, pos, j, def, bad);
+  const double b = tree_len_rec(path, len, pos, h, def, bad);
+  return wb_combine(def, k, a, b);
+}
+
+double orc_tree_length(const int32_t *path, int64_t len, int32_t def, int64_t *used) {
+  if (len < 1) { if (used) *used = -1; return 0.0; }
+  int64_t pos = 1;
+  int bad = 0;
+  const double L = tree_len_rec(path, len, &pos, path[0], def, &bad);
+  if (used) *used = bad ? -1 : pos;
+  return L;
+}
 
 typedef struct {
   int32_t top;      /* highest level planned (0: nothing) */
@@ -338,7 +371,9 @@ typedef struct {
 
 static void plan_free(plan_t *pl) {
   if (!pl->lv) return;
-  for (int d = 0; d < pl->nlv; d++) { free(pl->lv[d].type); free(pl->lv[d].slot); }
+  for (int d = 0; d < pl->nlv; d++) {
+    free(pl->lv[d].type); free(pl->lv[d].slot); free(pl->lv[d].len); free(pl->lv[d].used);
+  }
   free(pl->lv);
   pl->lv = NULL;
 }
@@ -398,10 +433,13 @@ static void plan_execute(cellctx *X, int r, plan_t *pl, const uint32_t rk0[4], i
     int64_t *rank = (int64_t *)malloc(sizeof(int64_t) * (size_t)C);
     for (int64_t j = 0; j < C; j++) rank[j] = cnt[L->type[j]]++;
     L->slot = (int64_t *)malloc(sizeof(int64_t) * 2 * (size_t)C);
+    L->len = (double *)calloc((size_t)C, sizeof(double));
+    L->used = (unsigned char *)calloc(2 * (size_t)C, 1);
     for (int64_t j = 0; j < C; j++) {
       int32_t a = L->type[j], b = d - 1 - a;
       int64_t t[2] = {base[a] + rank[j], base[b] + cnt[b] + rank[j]};
       int32_t pool[2] = {a, b};
+      double in_len[2] = {0.0, 0.0};            /* samples of f_0 have length 0 */
       for (int s = 0; s < 2; s++) {
         if (pool[s] == 0) {
           L->slot[2 * j + s] = orc_feistel((uint64_t)(leaf_off + t[s]), (uint64_t)n, rk0);
@@ -409,8 +447,11 @@ static void plan_execute(cellctx *X, int r, plan_t *pl, const uint32_t rk0[4], i
           level_t *Lp = &pl->lv[pool[s]];
           int64_t o = orc_feistel((uint64_t)t[s], (uint64_t)(2 * Lp->C), rk[pool[s]]);
           L->slot[2 * j + s] = Lp->slot[o];
+          Lp->used[o] = 1;
+          in_len[s] = Lp->len[o / 2];
         }
       }
+      L->len[j] = wb_combine(X->P->wb, d, in_len[0], in_len[1]);
     }
     for (int p = 0; p < d; p++) base[p] += cnt[p] + cnt[d - 1 - p];
     for (int64_t j = 0; j < C; j++) cnt[L->type[j]] = 0;
@@ -620,6 +661,18 @@ static int collide_cell(const orc_params *P, keyctx K, double rho_c, int64_t n, 
   plan_t pl = {0};
   plan_counts(&K, r, 1, sp.d, N, n, &pl);
   plan_execute(&X, r, &pl, rk0, n, 0);
+  /* TRMC-WB (Alg 4.6): final samples of f_d (outputs no higher
+   * level consumed) whose tree is longer than wb_max join the Maxwellian set */
+  int64_t nwb = 0;
+  int64_t *wbs = NULL;
+  if (P->wb && pl.top >= 1) {
+    int64_t cap = 0;
+    for (int d = 1; d <= pl.top; d++) cap += 2 * pl.lv[d].C;
+    wbs = (int64_t *)malloc(sizeof(int64_t) * (size_t)(cap > 0 ? cap : 1));
+    for (int d = 1; d <= pl.top; d++)
+      for (int64_t o = 0; o < 2 * pl.lv[d].C; o++)
+        if (!pl.lv[d].used[o] && pl.lv[d].len[o / 2] > (double)P->wb_max) wbs[nwb++] = pl.lv[d].slot[o];
+  }
   plan_free(&pl);
   int64_t Ltot = pl.L;
   int64_t U = N[0] < n - Ltot ? N[0] : n - Ltot;
@@ -662,15 +715,19 @@ static int collide_cell(const orc_params *P, keyctx K, double rho_c, int64_t n, 
   }
   st->depth = sp.d;
 
-  /* A8: thermalised set Theta = pi_0 positions [Ltot, Ltot + nT), ascending slots */
+  /* A8: thermalised set Theta = pi_0 positions [Ltot, Ltot + nT) (plus the
+   * TRMC-WB rejections), ascending slots */
+  if (nwb > 0) theta = (int64_t *)realloc(theta, sizeof(int64_t) * (size_t)(n + nwb));
   for (int64_t q = 0; q < nT; q++) theta[q] = orc_feistel((uint64_t)(Ltot + q), (uint64_t)n, rk0);
-  qsort(theta, (size_t)nT, sizeof(int64_t), cmp_i64);
-  orc_maxwellian(nT, theta, vx, vy, vz, K.seed, K.gcell, K.step);
+  for (int64_t q = 0; q < nwb; q++) theta[nT + q] = wbs[q];
+  qsort(theta, (size_t)(nT + nwb), sizeof(int64_t), cmp_i64);
+  orc_maxwellian(nT + nwb, theta, vx, vy, vz, K.seed, K.gcell, K.step);
+  free(wbs);
 
   st->S_est = S_est; st->E1 = E1;
   st->m_used = m_cur; st->m_next = m_next; st->attempts = r + 1;
   st->leaves = (double)Ltot; st->untouched = (double)U; st->thermalised = (double)nT;
-  st->maxw = nT >= 2 ? (double)nT : 0;
+  st->maxw = nT + nwb >= 2 ? (double)(nT + nwb) : 0;
   free(inTheta); free(theta); free(N);
   return rc;
 }

@@ -35,7 +35,18 @@ typedef struct {
   int32_t literal;     /* 1: literal recursive Alg 4.3/4.4 (statistical checks) */
   int32_t pad;
   double alpha;        /* ORC_VHS exponent                          */
+  int32_t wb;          /* TRMC-WB tree length (sec. 4.4): 0 off, 1 eq.(def:2)   */
+                       /* 1 + min, 2 eq.(def:3) 1 + mean, 3 eq.(def:1) = level  */
+  int32_t wb_max;      /* m_max of Alg 4.6: final samples with L > wb_max are   */
+                       /* resampled from the local Maxwellian                   */
 } orc_params;
+
+/* Length of one collision tree given as the path list of Alg 4.5:
+ * path[0] = k; for k > 0 the list continues j, h, then the sub-list of f_j,
+ * then the sub-list of f_h (each sub-list without its own leading k).
+ * def = 1 (1 + min), 2 (1 + mean), 3 (the coefficient k, eq. def:1).
+ * Returns the length; *used = entries read (negative on a malformed list). */
+double orc_tree_length(const int32_t *path, int64_t len, int32_t def, int64_t *used);
 
 /* Per-cell result of one collision step (all counts as doubles for ctypes). */
 typedef struct {

@@ -263,3 +263,20 @@ def test_rankine_hugoniot_states(orc):
         assert uL * (EL + rL * TL) == pytest.approx(uR * (ER + rR * TR), rel=1e-13)
     with pytest.raises(ValueError):
         orc.rankine_hugoniot(1.0)
+
+
+def test_tree_lengths_table1(orc):
+    """Alg 4.5 lengths of the two trees of Table 1 under eqs.
+    (def:1)-(def:3): tests/golden/table1_tree_lengths.txt."""
+    from fractions import Fraction
+    import pathlib
+    rows = [l for l in (pathlib.Path(__file__).parent / "golden" / "table1_tree_lengths.txt").read_text()
+            .splitlines() if l.strip() and not l.startswith("#")]
+    assert len(rows) == 2
+    for row in rows:
+        name, path, d1, d2, d3 = [f.strip() for f in row.split("|")]
+        path = [int(t) for t in path.split()]
+        for definition, want in ((3, d1), (1, d2), (2, d3)):   # oracle codes: 3 = def:1, 1 = def:2, 2 = def:3
+            assert orc.tree_length(path, definition) == float(Fraction(want)), (name, definition)
+    with pytest.raises(ValueError):
+        orc.tree_length([3, 1, 0, 0, 0], 1)                    # j + h + 1 != k

@@ -301,3 +301,33 @@ def test_vhs_acceptance_fraction(orc, alpha):
     qa = q ** alpha
     closed = 2 ** alpha * math.gamma((3 + alpha) / 2) / math.gamma(1.5)
     assert abs(qa.mean() - closed) < 4 * qa.std() / math.sqrt(len(qa))
+
+
+def test_trmc_wb_limits_nesting_conservation(orc):
+    """TRMC-WB (Alg 4.6): wb_max >= m keeps every tree (L <= level <= m),
+    i.e. TRMC-R bit for bit; for a smaller threshold the final samples rejected
+    under 1 + min (def:2) are a subset of those under 1 + mean (def:3), which are a
+    subset of those under L = level (def:1) - the plan and collisions are the same,
+    only the Maxwellian set grows; mass, momentum and energy are conserved."""
+    vx, vy, vz, off = synth.ragged_cells(30, 600, seed=14)
+    kw = dict(model=1, m_fixed=10, eps=2.0, dt=0.3, seed=15)
+    ref = orc.HomogeneousState(orc.Config(**kw), vx, vy, vz, off)
+    ref.step(1)
+    full = orc.HomogeneousState(orc.Config(wb=1, wb_max=10, **kw), vx, vy, vz, off)
+    full.step(1)
+    for k in ("vx", "vy", "vz"):
+        np.testing.assert_array_equal(getattr(full, k), getattr(ref, k))
+    maxw = {}
+    for wb in (1, 2, 3):
+        st = orc.HomogeneousState(orc.Config(wb=wb, wb_max=2, **kw), vx, vy, vz, off)
+        m0 = st.moments()
+        st.step(1)
+        m1 = st.moments()
+        np.testing.assert_array_equal(m1[:, 0], m0[:, 0])
+        scale = np.sqrt(2 * np.maximum(m0[:, 6], 1e-300))
+        assert np.all(np.abs(m1[:, 2:5] - m0[:, 2:5]).max(1) <= 1e-12 * scale + 1e-300)
+        assert np.allclose(m1[:, 6], m0[:, 6], rtol=1e-12)
+        np.testing.assert_array_equal(st.stats["proposals"], ref.stats["proposals"])
+        maxw[wb] = st.stats["maxw"]
+    assert np.all(maxw[1] <= maxw[2]) and np.all(maxw[2] <= maxw[3])
+    assert maxw[3].sum() > maxw[1].sum() > ref.stats["maxw"].sum()
