@@ -107,6 +107,11 @@ typedef struct {
   double delta1, delta2;     /* RAD interval, 0 < delta1 < delta2 (paper 0.005, 0.01) */
   uint64_t seed;             /* Philox4x32-10 key                                     */
   double alpha;              /* TRMCR_VHS exponent in [0, 1] (ignored otherwise)      */
+  int32_t wb;                /* TRMC-WB (sec. 4.4, Alg 4.6): 0 off; tree length 1 = 1 + min
+                                (eq. def:2), 2 = 1 + mean (eq. def:3), 3 = level (def:1);
+                                requires adaptive = 0                                  */
+  int32_t wb_max;            /* TRMC-WB m_max: final samples with longer trees are
+                                resampled from the local Maxwellian                   */
 } trmcr_kernel;
 
 /* Per-cell statistics row (doubles), trmcr_stats(): */

@@ -39,6 +39,7 @@ enum : int { kErrPlanCapacity = 1, kErrParticleCapacity = 2, kErrInternal = 16 }
 struct StepParams {
   int model, adaptive, m_fixed, m_cap, indicator, log_on;
   double alpha;            // VHS exponent
+  int wb, wb_max;          // TRMC-WB definition (0 off) and threshold
   double delta1, delta2, dt, eps;
   uint32_t k0, k1, step, cell_base;
   int shock;               // rho_c = n w / dx when 1, else 1
@@ -66,6 +67,8 @@ struct CellBuf {
   uint4 *rk;               // [L_cap+1] permutation keys of pools
   uint32_t *mask;          // [ceil(n_cap/32)] Theta membership
   PermDom *pdom;           // [L_cap+1] warp kernel: domain of pool p's permutation (or null)
+  double *wlen;            // [K_cap] TRMC-WB: tree length of collision k's outputs (or null)
+  uint8_t *wused;          // [2 K_cap] TRMC-WB: output o consumed by a higher level
   double *red;             // [32*8] reduction scratch
   int n_cap, K_cap, L_cap;
 };
@@ -77,7 +80,7 @@ struct CellShared {
   double sums[8];
   int n, m, m_cur, m_next, d, top, lo, hi, r, planned, flag, done;
   int64_t rem;
-  int32_t L, Ltot, U, nT, budget, leaf_off, attempts;
+  int32_t L, Ltot, U, nT, budget, leaf_off, attempts, ktot, nwb;
   unsigned long long prop, acc, viol;
   double usplit[kSplitPre];   // split uniforms of levels < kSplitPre, drawn in parallel
 };
@@ -96,6 +99,15 @@ template <> struct RealOps<float> {
 
 // VHS majorant Sigma' = (2 sqrt(dv2))^alpha (Sigma = sigma(2 dv); K cancels).
 __device__ __forceinline__ double vhs_majorant(double dv2, double alpha) { return pow(2.0 * sqrt(dv2), alpha); }
+
+// TRMC-WB tree length of a level-d collision's outputs from its inputs'
+// lengths a, b (samples of f_0: 0): eq. def:2 (1 + min), def:3 (1 + mean),
+// def:1 (d).  Same arithmetic as the oracle (exact dyadic sums in fp64).
+__device__ __forceinline__ double wb_combine(int def, int d, double a, double b) {
+  if (def == 1) return 1.0 + (a < b ? a : b);
+  if (def == 2) return 1.0 + 0.5 * (a + b);
+  return (double)d;
+}
 
 // IR at split level d with its keyed uniform; exact 0 when y < 2^-53.
 // Uniforms of levels < kSplitPre were drawn in parallel into `pre`.
@@ -287,6 +299,9 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
     B.cnt[d] = 0;
     if (d >= 1) B.rk[d] = K(kPerm, sh.r, d, 0);
   }
+  const int ktot = B.S[1] + B.C[1];                // collisions of the plan (levels top..1 stored from 0)
+  if (P.wb) for (int o = tid; o < 2 * ktot; o += blockDim.x) B.wused[o] = 0;
+  if (tid == 0) sh.ktot = ktot;
   __syncthreads();
   unsigned acc = 0, viol = 0;
   const int r = sh.r;
@@ -331,6 +346,7 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
       const uint32_t t[2] = {(uint32_t)B.base[a] + rank, (uint32_t)(B.base[b] + B.cnt[b]) + rank};
       const uint32_t pool[2] = {a, b};
       uint32_t slot[2];
+      double ln[2] = {0.0, 0.0};             // TRMC-WB input lengths (samples of f_0: 0)
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         if (pool[s] == 0) {
@@ -340,6 +356,11 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
           pp.init(B.rk[pool[s]], 2u * (uint32_t)B.C[pool[s]]);
           const uint32_t o = pp(t[s]);
           slot[s] = o == 0xFFFFFFFFu ? o : B.cslot[2u * (uint32_t)B.S[pool[s]] + o];
+          if (P.wb && o != 0xFFFFFFFFu) {
+            const uint32_t og = 2u * (uint32_t)B.S[pool[s]] + o;
+            B.wused[og] = 1;
+            ln[s] = B.wlen[og >> 1];
+          }
         }
         if (slot[s] >= (uint32_t)sh.n) {   // cannot happen: internal fault, never hang
           atomicOr(P.err, kErrInternal);
@@ -348,6 +369,7 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
       }
       B.cslot[2 * (Sd + j)] = slot[0];
       B.cslot[2 * (Sd + j) + 1] = slot[1];
+      if (P.wb) B.wlen[Sd + j] = wb_combine(P.wb, d, ln[0], ln[1]);
       const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, slot[0], slot[1], viol);
       acc += ok;
       if (P.log_on) {
@@ -422,30 +444,52 @@ __device__ void rad_estimate(const StepParams &P, CellBuf<Real> &B, CellShared &
   __syncthreads();
 }
 
-// Conservative Maxwellian (A8) over Theta = pi0 positions [Ltot, Ltot+nT).
+// Conservative Maxwellian (A8) over Theta = pi0 positions [Ltot, Ltot+nT)
+// plus, under TRMC-WB, the final outputs whose tree is longer than wb_max
+// (index q < nT: pi0(Ltot + q); q >= nT: output q - nT of the plan).
 template <typename Real>
 __device__ void maxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> &B, CellShared &sh,
                            const Perm &pi0, double ec_all) {
   const int tid = threadIdx.x, nT = sh.nT;
-  if (nT < 2) return;
+  const int nq = nT + (P.wb ? 2 * sh.ktot : 0);
+  auto member = [&](int q, uint32_t &s) -> bool {
+    if (q < nT) { s = pi0((uint32_t)(sh.Ltot + q)); return true; }
+    const int o = q - nT;
+    if (B.wused[o] || !(B.wlen[o >> 1] > (double)P.wb_max)) return false;
+    s = B.cslot[o];
+    return true;
+  };
+  int nwb = 0;
+  if (P.wb) {
+    double c1[1] = {0.0};
+    for (int o = tid; o < 2 * sh.ktot; o += blockDim.x)
+      c1[0] += (!B.wused[o] && B.wlen[o >> 1] > (double)P.wb_max) ? 1.0 : 0.0;
+    block_sum<1>(c1, B.red);
+    nwb = (int)c1[0];
+  }
+  if (tid == 0) sh.nwb = nwb;
+  const int nTT = nT + nwb;
+  if (nTT < 2) { __syncthreads(); return; }
   const bool full = (nT == sh.n);          // Theta = every slot: skip the permutation
   double ux, uy, uz, ec;
   if (full) {
     ux = sh.ux; uy = sh.uy; uz = sh.uz; ec = ec_all;
   } else {
     double v[3] = {0, 0, 0};
-    for (int q = tid; q < nT; q += blockDim.x) {
-      const uint32_t s = pi0((uint32_t)(sh.Ltot + q));
+    for (int q = tid; q < nq; q += blockDim.x) {
+      uint32_t s;
+      if (!member(q, s)) continue;
       if (s >= (uint32_t)sh.n) { atomicOr(P.err, kErrInternal); continue; }
       v[0] += (double)B.vx[s]; v[1] += (double)B.vy[s]; v[2] += (double)B.vz[s];
     }
     block_sum<3>(v, B.red);
-    ux = v[0] / nT; uy = v[1] / nT; uz = v[2] / nT;
+    ux = v[0] / nTT; uy = v[1] / nTT; uz = v[2] / nTT;
     ec = 0;
   }
   double g[5] = {0, 0, 0, 0, 0};   // sum g (3), sum |g|^2, centred energy of Theta
-  for (int q = tid; q < nT; q += blockDim.x) {
-    const uint32_t s = full ? (uint32_t)q : pi0((uint32_t)(sh.Ltot + q));
+  for (int q = tid; q < nq; q += blockDim.x) {
+    uint32_t s = (uint32_t)q;
+    if (!full && !member(q, s)) continue;
     if (s >= (uint32_t)sh.n) { atomicOr(P.err, kErrInternal); continue; }
     if (!full) {
       const double dx = B.vx[s] - ux, dy = B.vy[s] - uy, dz = B.vz[s] - uz;
@@ -459,13 +503,14 @@ __device__ void maxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> &
   }
   block_sum<5>(g, B.red);
   if (!full) ec = g[4];
-  const double gx = g[0] / nT, gy = g[1] / nT, gz = g[2] / nT;
-  const double D = g[3] - nT * (gx * gx + gy * gy + gz * gz);
+  const double gx = g[0] / nTT, gy = g[1] / nTT, gz = g[2] / nTT;
+  const double D = g[3] - nTT * (gx * gx + gy * gy + gz * gz);
   const double sc = (D > 0.0 && ec > 0.0) ? sqrt(ec / D) : 0.0;
   const Real rsc = (Real)sc, rgx = (Real)gx, rgy = (Real)gy, rgz = (Real)gz;
   const Real rux = (Real)ux, ruy = (Real)uy, ruz = (Real)uz;
-  for (int q = tid; q < nT; q += blockDim.x) {
-    const uint32_t s = full ? (uint32_t)q : pi0((uint32_t)(sh.Ltot + q));
+  for (int q = tid; q < nq; q += blockDim.x) {
+    uint32_t s = (uint32_t)q;
+    if (!full && !member(q, s)) continue;
     if (s >= (uint32_t)sh.n) continue;
     B.vx[s] = rux + rsc * (B.vx[s] - rgx);
     B.vy[s] = ruy + rsc * (B.vy[s] - rgy);
@@ -553,7 +598,7 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
     split_extend(K, sh, m0, B.Q, B.L_cap);
     // quotas above L_cap are zero (else split_extend flagged overflow)
     sh.r = 0; sh.lo = 1; sh.hi = sh.d < B.L_cap ? sh.d : B.L_cap;
-    sh.budget = n; sh.leaf_off = 0;
+    sh.budget = n; sh.leaf_off = 0; sh.ktot = 0; sh.nwb = 0;
   }
   __syncthreads();
   PHASE_ADD(0, t_ph);   // moments + split
@@ -640,7 +685,7 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
       s[TRMCR_ST_ATTEMPTS] = sh.r + 1; s[TRMCR_ST_LEAVES] = sh.Ltot; s[TRMCR_ST_UNTOUCHED] = sh.U;
       s[TRMCR_ST_THERMALISED] = sh.nT; s[TRMCR_ST_PROPOSALS] = (double)sh.prop;
       s[TRMCR_ST_ACCEPTED] = (double)sh.acc; s[TRMCR_ST_VIOLATIONS] = (double)sh.viol;
-      s[TRMCR_ST_MAXW] = sh.nT >= 2 ? sh.nT : 0;
+      s[TRMCR_ST_MAXW] = sh.nT + sh.nwb >= 2 ? sh.nT + sh.nwb : 0;
       s[TRMCR_ST_PX] = sh.sums[0]; s[TRMCR_ST_PY] = sh.sums[1]; s[TRMCR_ST_PZ] = sh.sums[2];
       s[TRMCR_ST_ENERGY] = sh.sums[3];
     }

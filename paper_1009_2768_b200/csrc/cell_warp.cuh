@@ -23,7 +23,7 @@ struct WarpShared {
   double sums[4];
   int n, m_cur, m_next, d, top, lo, hi, r, flag, done;
   int64_t rem;
-  int32_t L, Ltot, U, nT, budget, leaf_off;
+  int32_t L, Ltot, U, nT, budget, leaf_off, ktot, nwb;
   unsigned long long prop, acc, viol;
 };
 
@@ -31,9 +31,11 @@ struct WarpShared {
 struct WarpSlabLayout {
   int n_cap, K_cap, L_cap, v_smem;   // v_smem = 0: the cell's velocities live in global memory
   size_t per_warp;   // bytes of one warp's slab incl. WarpShared (16-byte multiple)
-  size_t off_v, off_ctype, off_crank, off_cslot, off_ints, off_rk, off_pdom, off_u, off_red, off_sh;
-  void build(int n, int K, int L, size_t rs, int v_in_smem) {
-    n_cap = n; K_cap = K; L_cap = L; v_smem = v_in_smem;
+  int wb;
+  size_t off_v, off_ctype, off_crank, off_cslot, off_ints, off_rk, off_pdom, off_u, off_red, off_sh, off_wlen,
+      off_wused;
+  void build(int n, int K, int L, size_t rs, int v_in_smem, int wb_on = 0) {
+    n_cap = n; K_cap = K; L_cap = L; v_smem = v_in_smem; wb = wb_on;
     size_t o = 0;
     auto al = [&](size_t a) { o = (o + a - 1) / a * a; };
     off_red = o; o += 8 * sizeof(double);
@@ -45,6 +47,8 @@ struct WarpSlabLayout {
     off_crank = o; o += (size_t)K * 2;             // K uint16
     off_ctype = o; o += (size_t)K;                 // K uint8
     off_ints = o; o += 6 * (size_t)(L + 1) * 4;
+    al(16); off_wlen = o; if (wb) o += (size_t)K * 8;
+    off_wused = o; if (wb) o += (size_t)K * 2;
     al(16); off_sh = o; o += sizeof(WarpShared);
     al(16); per_warp = o;
   }
@@ -67,6 +71,8 @@ __device__ __forceinline__ void bind_warp_slab(CellBuf<Real> &B, unsigned char *
   B.Q = ints; B.C = ints + Lp; B.S = ints + 2 * Lp; B.cons = ints + 3 * Lp;
   B.base = ints + 4 * Lp; B.cnt = ints + 5 * Lp;
   B.pdom = reinterpret_cast<PermDom *>(base + Lay.off_pdom);
+  B.wlen = Lay.wb ? reinterpret_cast<double *>(base + Lay.off_wlen) : nullptr;
+  B.wused = Lay.wb ? reinterpret_cast<uint8_t *>(base + Lay.off_wused) : nullptr;
   B.mask = nullptr;
   B.n_cap = Lay.n_cap; B.K_cap = Lay.K_cap; B.L_cap = Lay.L_cap;
 }
@@ -161,6 +167,9 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
       B.pdom[d] = perm_dom(2u * (uint32_t)B.C[d]);
     }
   }
+  const int ktot = B.S[1] + B.C[1];                // collisions of the plan (levels top..1 stored from 0)
+  if (P.wb) for (int o = lane; o < 2 * ktot; o += 32) B.wused[o] = 0;
+  if (lane == 0) sh.ktot = ktot;
   __syncwarp();
   unsigned acc = 0, viol = 0;
   unsigned long long prop = 0;
@@ -207,6 +216,17 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
       for (int s = 0; s < 2; ++s) {
         slot[s] = (pool[s] == 0 || y[s] == 0xFFFFFFFFu) ? y[s] : (uint32_t)B.cslot16[2u * (uint32_t)B.S[pool[s]] + y[s]];
         if (slot[s] >= (uint32_t)n) { atomicOr(P.err, kErrInternal); slot[s] = 0; }
+      }
+      if (P.wb) {                            // TRMC-WB: lengths, consumed outputs
+        double ln[2] = {0.0, 0.0};
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+          if (pool[s] != 0 && y[s] != 0xFFFFFFFFu) {
+            const uint32_t o = 2u * (uint32_t)B.S[pool[s]] + y[s];
+            B.wused[o] = 1;
+            ln[s] = B.wlen[o >> 1];
+          }
+        B.wlen[Sd + j] = wb_combine(P.wb, d, ln[0], ln[1]);
       }
       B.cslot16[2 * (Sd + j)] = (uint16_t)slot[0];
       B.cslot16[2 * (Sd + j) + 1] = (uint16_t)slot[1];
@@ -285,27 +305,47 @@ __device__ void wrad_estimate(const StepParams &P, CellBuf<Real> &B, WarpShared 
   __syncwarp();
 }
 
+// Conservative Maxwellian (A8) over Theta = pi0 positions [Ltot, Ltot + nT)
+// plus, under TRMC-WB, the final outputs whose tree is longer than wb_max:
+// index q < nT is pi0(Ltot + q); q >= nT is output q - nT of the plan.
 template <typename Real>
 __device__ void wmaxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> &B, WarpShared &sh,
                             const Perm &pi0, double ec_all) {
   const int lane = threadIdx.x & 31, nT = sh.nT;
-  if (nT < 2) return;
+  const int nq = nT + (P.wb ? 2 * sh.ktot : 0);
+  auto member = [&](int q, uint32_t &s) -> bool {
+    if (q < nT) { s = pi0((uint32_t)(sh.Ltot + q)); return true; }
+    const int o = q - nT;
+    if (B.wused[o] || !(B.wlen[o >> 1] > (double)P.wb_max)) return false;
+    s = B.cslot16[o];
+    return true;
+  };
+  int nwb = 0;
+  if (P.wb) {
+    for (int o = lane; o < 2 * sh.ktot; o += 32) nwb += (!B.wused[o] && B.wlen[o >> 1] > (double)P.wb_max) ? 1 : 0;
+    nwb = __reduce_add_sync(0xffffffffu, nwb);
+  }
+  if (lane == 0) sh.nwb = nwb;
+  const int nTT = nT + nwb;
+  if (nTT < 2) return;
   const bool full = (nT == sh.n);
   double ux, uy, uz;
   if (full) {
     ux = sh.ux; uy = sh.uy; uz = sh.uz;
   } else {
     double a = 0, b = 0, c = 0;
-    for (int q = lane; q < nT; q += 32) {
-      const uint32_t s = pi0((uint32_t)(sh.Ltot + q));
+    for (int q = lane; q < nq; q += 32) {
+      uint32_t s;
+      if (!member(q, s)) continue;
       if (s >= (uint32_t)sh.n) { atomicOr(P.err, kErrInternal); continue; }
       a += (double)B.vx[s]; b += (double)B.vy[s]; c += (double)B.vz[s];
     }
-    ux = warp_sum_call(a) / nT; uy = warp_sum_call(b) / nT; uz = warp_sum_call(c) / nT;
+    ux = warp_sum_call(a) / nTT; uy = warp_sum_call(b) / nTT; uz = warp_sum_call(c) / nTT;
   }
   double g0s = 0, g1s = 0, g2s = 0, gg = 0, ec = 0;
-  for (int q = lane; q < nT; q += 32) {
-    const uint32_t s = full ? (uint32_t)q : pi0((uint32_t)(sh.Ltot + q));
+  for (int q = lane; q < nq; q += 32) {
+    uint32_t s = (uint32_t)q;
+    if (!full && !member(q, s)) continue;
     if (s >= (uint32_t)sh.n) continue;
     if (!full) {
       const double dx = B.vx[s] - ux, dy = B.vy[s] - uy, dz = B.vz[s] - uz;
@@ -319,14 +359,15 @@ __device__ void wmaxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> 
   }
   g0s = warp_sum_call(g0s); g1s = warp_sum_call(g1s); g2s = warp_sum_call(g2s); gg = warp_sum_call(gg);
   ec = full ? ec_all : warp_sum_call(ec);
-  const double gx = g0s / nT, gy = g1s / nT, gz = g2s / nT;
-  const double D = gg - nT * (gx * gx + gy * gy + gz * gz);
+  const double gx = g0s / nTT, gy = g1s / nTT, gz = g2s / nTT;
+  const double D = gg - nTT * (gx * gx + gy * gy + gz * gz);
   const double sc = (D > 0.0 && ec > 0.0) ? sqrt(ec / D) : 0.0;
   const Real rsc = (Real)sc, rgx = (Real)gx, rgy = (Real)gy, rgz = (Real)gz;
   const Real rux = (Real)ux, ruy = (Real)uy, ruz = (Real)uz;
   __syncwarp();
-  for (int q = lane; q < nT; q += 32) {
-    const uint32_t s = full ? (uint32_t)q : pi0((uint32_t)(sh.Ltot + q));
+  for (int q = lane; q < nq; q += 32) {
+    uint32_t s = (uint32_t)q;
+    if (!full && !member(q, s)) continue;
     if (s >= (uint32_t)sh.n) continue;
     B.vx[s] = rux + rsc * (B.vx[s] - rgx);
     B.vy[s] = ruy + rsc * (B.vy[s] - rgy);
@@ -406,7 +447,7 @@ __device__ int wphase_begin(const StepParams &P, CellBuf<Real> &B, WarpShared &s
     wsplit_extend(K, sh, m0, B.Q, B.L_cap, usplit);
     sh.r = 0; sh.lo = 1; sh.hi = sh.d < B.L_cap ? sh.d : B.L_cap;
     sh.budget = n; sh.leaf_off = 0;
-    sh.done = 0;
+    sh.done = 0; sh.ktot = 0; sh.nwb = 0;
   }
   __syncwarp();
   return sh.flag;
@@ -480,7 +521,7 @@ __device__ void wphase_end(const StepParams &P, CellBuf<Real> &B, WarpShared &sh
     s[TRMCR_ST_ATTEMPTS] = sh.r + 1; s[TRMCR_ST_LEAVES] = sh.Ltot; s[TRMCR_ST_UNTOUCHED] = sh.U;
     s[TRMCR_ST_THERMALISED] = sh.nT; s[TRMCR_ST_PROPOSALS] = (double)sh.prop;
     s[TRMCR_ST_ACCEPTED] = (double)sh.acc; s[TRMCR_ST_VIOLATIONS] = (double)sh.viol;
-    s[TRMCR_ST_MAXW] = sh.nT >= 2 ? sh.nT : 0;
+    s[TRMCR_ST_MAXW] = sh.nT + sh.nwb >= 2 ? sh.nT + sh.nwb : 0;
     s[TRMCR_ST_PX] = sh.sums[0]; s[TRMCR_ST_PY] = sh.sums[1]; s[TRMCR_ST_PZ] = sh.sums[2];
     s[TRMCR_ST_ENERGY] = sh.sums[3];
   }

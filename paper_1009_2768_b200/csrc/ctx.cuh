@@ -17,11 +17,11 @@ constexpr int kGmemThreads = 1024;
 
 // ---- shared-memory layout of cell_step_smem ----
 struct SmemLayout {
-  int n_cap, K_cap, L_cap;
+  int n_cap, K_cap, L_cap, wb;
   size_t real_size;
-  size_t off_v, off_ctype, off_crank, off_cslot, off_ints, off_rk, off_mask, off_red, total;
-  void build(int n, int K, int L, size_t rs) {
-    n_cap = n; K_cap = K; L_cap = L; real_size = rs;
+  size_t off_v, off_ctype, off_crank, off_cslot, off_ints, off_rk, off_mask, off_red, off_wlen, off_wused, total;
+  void build(int n, int K, int L, size_t rs, int wb_on = 0) {
+    n_cap = n; K_cap = K; L_cap = L; real_size = rs; wb = wb_on;
     size_t o = 0;
     auto al = [&](size_t a) { o = (o + a - 1) / a * a; };
     off_red = o; o += 32 * 8 * sizeof(double);
@@ -32,6 +32,8 @@ struct SmemLayout {
     off_cslot = o; o += (size_t)K * 8;
     off_ints = o; o += 6 * (size_t)(L + 1) * 4;
     off_mask = o; o += (size_t)((n + 31) / 32) * 4;
+    al(16); off_wlen = o; if (wb) o += (size_t)K * 8;
+    off_wused = o; if (wb) o += (size_t)K * 2;
     al(16); total = o;
   }
 };
@@ -51,13 +53,15 @@ __device__ __forceinline__ void bind_smem(CellBuf<Real> &B, unsigned char *base,
   B.base = ints + 4 * Lp; B.cnt = ints + 5 * Lp;
   B.mask = reinterpret_cast<uint32_t *>(base + Lay.off_mask);
   B.pdom = nullptr;
+  B.wlen = Lay.wb ? reinterpret_cast<double *>(base + Lay.off_wlen) : nullptr;
+  B.wused = Lay.wb ? reinterpret_cast<uint8_t *>(base + Lay.off_wused) : nullptr;
   B.n_cap = Lay.n_cap; B.K_cap = Lay.K_cap; B.L_cap = Lay.L_cap;
 }
 
 struct GmemScratch {
   unsigned char *base;
   size_t stride;
-  int n_cap, K_cap, L_cap;
+  int n_cap, K_cap, L_cap, wb;
 };
 
 // Bind the plan arrays of CTA blockIdx.x to its slab of global scratch.
@@ -73,14 +77,17 @@ __device__ __forceinline__ void bind_gmem(CellBuf<Real> &B, const GmemScratch &G
   int32_t *ints = reinterpret_cast<int32_t *>(p); p += 6 * (size_t)Lp * 4;
   B.Q = ints; B.C = ints + Lp; B.S = ints + 2 * Lp; B.cons = ints + 3 * Lp;
   B.base = ints + 4 * Lp; B.cnt = ints + 5 * Lp;
-  B.mask = reinterpret_cast<uint32_t *>(p);
+  B.mask = reinterpret_cast<uint32_t *>(p); p += (size_t)((G.n_cap + 31) / 32) * 4;
   B.pdom = nullptr;
+  p = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+  B.wlen = G.wb ? reinterpret_cast<double *>(p) : nullptr;
+  B.wused = G.wb ? reinterpret_cast<uint8_t *>(p + (size_t)G.K_cap * 8) : nullptr;
   B.n_cap = G.n_cap; B.K_cap = G.K_cap; B.L_cap = G.L_cap;
 }
 
-inline size_t gmem_stride(int n_cap, int64_t K_cap, int L_cap) {
+inline size_t gmem_stride(int n_cap, int64_t K_cap, int L_cap, int wb = 0) {
   size_t s = (size_t)(L_cap + 1) * 16 + (size_t)K_cap * 16 + 6 * (size_t)(L_cap + 1) * 4 +
-             (size_t)((n_cap + 31) / 32) * 4 + 256;
+             (size_t)((n_cap + 31) / 32) * 4 + 256 + (wb ? (size_t)K_cap * 10 + 16 : 0);
   return (s + 255) / 256 * 256;
 }
 

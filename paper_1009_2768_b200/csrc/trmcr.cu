@@ -441,6 +441,8 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
     return fail(nullptr, TRMCR_EINVAL, "bad model");
   if (kk->model == TRMCR_VHS && !(kk->alpha >= 0.0 && kk->alpha <= 1.0))
     return fail(nullptr, TRMCR_EINVAL, "VHS alpha must lie in [0, 1]");
+  if (kk->wb < 0 || kk->wb > 3 || (kk->wb && (kk->adaptive || kk->wb_max < 0)))
+    return fail(nullptr, TRMCR_EINVAL, "TRMC-WB: wb in 0..3, wb_max >= 0, not with adaptive (RAD)");
   if (kk->indicator != TRMCR_IND_PXX && kk->indicator != TRMCR_IND_M4) return fail(nullptr, TRMCR_EINVAL, "bad indicator");
   if (kk->adaptive) {
     if (kk->m_init < 1 || kk->m_cap < kk->m_init || kk->m_cap > 16384)
@@ -497,7 +499,8 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
   // ---- parameters ----
   StepParams &P = c->P;
   P.model = kk->model; P.alpha = kk->model == TRMCR_VHS ? kk->alpha : (kk->model == TRMCR_HARD_SPHERE ? 1.0 : 0.0);
-  P.adaptive = kk->adaptive; P.m_fixed = kk->m_fixed; P.m_cap = kk->m_cap;
+  P.adaptive = kk->adaptive;
+  P.wb = kk->wb; P.wb_max = kk->wb_max; P.m_fixed = kk->m_fixed; P.m_cap = kk->m_cap;
   P.indicator = kk->indicator; P.log_on = 0;
   P.delta1 = kk->delta1; P.delta2 = kk->delta2; P.dt = dt; P.eps = eps;
   P.k0 = (uint32_t)kk->seed; P.k1 = (uint32_t)(kk->seed >> 32);
@@ -592,7 +595,7 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
   for (;;) {
     const int K_cap = kcap_env ? atoi(kcap_env)
                                : (c->geometry == TRMCR_SHOCK_1D ? std::max(256, n_cap / 4) : std::max(256, n_cap / 2));
-    c->lay.build(n_cap, K_cap, L_cap, c->rs);
+    c->lay.build(n_cap, K_cap, L_cap, c->rs, c->P.wb != 0);
     if ((int)c->lay.total <= budget || n_cap <= 32) break;
     n_cap = std::max(32, n_cap / 2 / 32 * 32);
   }
@@ -656,7 +659,7 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
     const int v_smem = c->geometry == TRMCR_SHOCK_1D ? 0 : 1;
     if (!v_smem) wn = std::max(wn, 4096);
     wn = std::min(wn, 65504);   // slots are 16-bit in the warp plan; larger cells take the CTA path
-    c->wlay.build(wn, wK, 64, c->rs, v_smem);
+    c->wlay.build(wn, wK, 64, c->rs, v_smem, c->P.wb != 0);
     const size_t slab = c->wlay.per_warp;
     c->warp_wpc = (int)std::max<size_t>(1, std::min<size_t>(kWarpCellWarps, (48 * 1024) / slab));
     c->warp_smem = (int)(slab * c->warp_wpc);
@@ -706,12 +709,12 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
                           : (int)std::min<int64_t>(c->cap, std::max(16 * max_cell, 65536));
   const int L_cap_g = std::max(kk->adaptive ? kk->m_cap : kk->m_fixed, 64) + 1;
   const int64_t K_cap_g = std::min<int64_t>(4LL * n_cap_g + 65536, 0x3FFFFFFFLL);
-  const size_t stride = gmem_stride(n_cap_g, K_cap_g, L_cap_g);
+  const size_t stride = gmem_stride(n_cap_g, K_cap_g, L_cap_g, c->P.wb != 0);
   int G = std::max(1, std::min(c->ncells, big > 0 ? 148 : (c->geometry == TRMCR_SHOCK_1D ? 16 : 8)));
   while (G > 1 && (double)G * stride > 4e9) G /= 2;
   c->G = G;
   if (dalloc(c, &c->d_scratch, stride * G)) return bail(TRMCR_ENOMEM);
-  c->gs = GmemScratch{c->d_scratch, stride, n_cap_g, (int)K_cap_g, L_cap_g};
+  c->gs = GmemScratch{c->d_scratch, stride, n_cap_g, (int)K_cap_g, L_cap_g, c->P.wb != 0 ? 1 : 0};
 
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
     fail(c, TRMCR_ECUDA, "init synchronisation failed");

@@ -116,6 +116,15 @@ def test_homogeneous_fp64_vhs_rad_ragged(orc, api, alpha):
             seed=13)
 
 
+@pytest.mark.parametrize("wb,warp_path", [(1, "1"), (2, "1"), (3, "1"), (1, "0")])
+def test_homogeneous_fp64_trmc_wb(orc, api, monkeypatch, wb, warp_path):
+    """TRMC-WB (Alg 4.6): tree lengths under eqs. def:2, def:3, def:1 in the
+    LS plan, rejected final samples join the Maxwellian; warp and CTA kernels."""
+    monkeypatch.setenv("TRMCR_WARP_PATH", warp_path)
+    v = synth.ragged_cells(40, 500, seed=16)
+    _parity(orc, api, v[:3], v[3], 3, model=1, m_fixed=10, wb=wb, wb_max=2, eps=2.0, dt=0.3, seed=17)
+
+
 def test_homogeneous_fp64_hs_m4_indicator(orc, api):
     v = synth.ragged_cells(30, 500, seed=9)
     _parity(orc, api, v[:3], v[3], 4, model=1, adaptive=1, m_init=4, m_cap=32, indicator=1, eps=0.2,
