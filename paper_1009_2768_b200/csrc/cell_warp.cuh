@@ -152,7 +152,7 @@ __device__ void wplan_counts(const RngKey &K, CellBuf<Real> &B, WarpShared &sh) 
   }
 }
 
-template <typename Real>
+template <typename Real, bool WB>
 __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real> &B, WarpShared &sh,
                               const Perm &pi0, Real sigma, trmcr_coll_rec *log, unsigned long long *log_count,
                               int64_t log_cap) {
@@ -168,7 +168,7 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
     }
   }
   const int ktot = B.S[1] + B.C[1];                // collisions of the plan (levels top..1 stored from 0)
-  if (P.wb) for (int o = lane; o < 2 * ktot; o += 32) B.wused[o] = 0;
+  if (WB && P.wb) for (int o = lane; o < 2 * ktot; o += 32) B.wused[o] = 0;
   if (lane == 0) sh.ktot = ktot;
   __syncwarp();
   unsigned acc = 0, viol = 0;
@@ -217,7 +217,7 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
         slot[s] = (pool[s] == 0 || y[s] == 0xFFFFFFFFu) ? y[s] : (uint32_t)B.cslot16[2u * (uint32_t)B.S[pool[s]] + y[s]];
         if (slot[s] >= (uint32_t)n) { atomicOr(P.err, kErrInternal); slot[s] = 0; }
       }
-      if (P.wb) {                            // TRMC-WB: lengths, consumed outputs
+      if (WB && P.wb) {                      // TRMC-WB: lengths, consumed outputs
         double ln[2] = {0.0, 0.0};
 #pragma unroll
         for (int s = 0; s < 2; ++s)
@@ -308,20 +308,20 @@ __device__ void wrad_estimate(const StepParams &P, CellBuf<Real> &B, WarpShared 
 // Conservative Maxwellian (A8) over Theta = pi0 positions [Ltot, Ltot + nT)
 // plus, under TRMC-WB, the final outputs whose tree is longer than wb_max:
 // index q < nT is pi0(Ltot + q); q >= nT is output q - nT of the plan.
-template <typename Real>
+template <typename Real, bool WB>
 __device__ void wmaxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> &B, WarpShared &sh,
                             const Perm &pi0, double ec_all) {
   const int lane = threadIdx.x & 31, nT = sh.nT;
-  const int nq = nT + (P.wb ? 2 * sh.ktot : 0);
+  const int nq = nT + ((WB && P.wb) ? 2 * sh.ktot : 0);
   auto member = [&](int q, uint32_t &s) -> bool {
-    if (q < nT) { s = pi0((uint32_t)(sh.Ltot + q)); return true; }
+    if (!WB || q < nT) { s = pi0((uint32_t)(sh.Ltot + q)); return true; }
     const int o = q - nT;
     if (B.wused[o] || !(B.wlen[o >> 1] > (double)P.wb_max)) return false;
     s = B.cslot16[o];
     return true;
   };
   int nwb = 0;
-  if (P.wb) {
+  if (WB && P.wb) {
     for (int o = lane; o < 2 * sh.ktot; o += 32) nwb += (!B.wused[o] && B.wlen[o >> 1] > (double)P.wb_max) ? 1 : 0;
     nwb = __reduce_add_sync(0xffffffffu, nwb);
   }
@@ -376,6 +376,8 @@ __device__ void wmaxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> 
   __syncwarp();
 }
 
+// WB: compile the TRMC-WB bookkeeping in (the kernels are instantiated with and
+// without it; the hot path without carries no extra code or registers).
 // The general step of one cell in three phases that communicate through the
 // warp's WarpShared (so a CTA can run its warps' cells phase by phase in lock
 // step, keeping one phase's code in the instruction cache):
@@ -453,7 +455,7 @@ __device__ int wphase_begin(const StepParams &P, CellBuf<Real> &B, WarpShared &s
   return sh.flag;
 }
 
-template <typename Real>
+template <typename Real, bool WB>
 __device__ int wphase_attempt(const StepParams &P, CellBuf<Real> &B, WarpShared &sh, double *usplit,
                               uint32_t gcell, trmcr_coll_rec *log, unsigned long long *log_count,
                               int64_t log_cap) {
@@ -465,7 +467,7 @@ __device__ int wphase_attempt(const StepParams &P, CellBuf<Real> &B, WarpShared 
   const int attempt = sh.r;
   wplan_counts<Real>(K, B, sh);
   if (sh.flag != kOk) return sh.flag;
-  wplan_execute<Real>(P, K, B, sh, pi0, (Real)sh.sigma, log, log_count, log_cap);
+  wplan_execute<Real, WB>(P, K, B, sh, pi0, (Real)sh.sigma, log, log_count, log_cap);
   if (lane == 0) {
     if (attempt == 0) {
       sh.Ltot = sh.L;
@@ -500,7 +502,7 @@ __device__ int wphase_attempt(const StepParams &P, CellBuf<Real> &B, WarpShared 
   return sh.flag;
 }
 
-template <typename Real>
+template <typename Real, bool WB>
 __device__ void wphase_end(const StepParams &P, CellBuf<Real> &B, WarpShared &sh, Real *out_x, Real *out_y,
                            Real *out_z, uint32_t gcell, int32_t *m_state, double *stats_row) {
   const int lane = threadIdx.x & 31;
@@ -509,7 +511,7 @@ __device__ void wphase_end(const StepParams &P, CellBuf<Real> &B, WarpShared &sh
   Perm pi0;
   pi0.init(sh.pk, (uint32_t)n);
   // ---- A8 ----
-  wmaxwellian<Real>(P, K, B, sh, pi0, sh.c2);
+  wmaxwellian<Real, WB>(P, K, B, sh, pi0, sh.c2);
   if (out_x != B.vx)
     for (int i = lane; i < n; i += 32) { out_x[i] = B.vx[i]; out_y[i] = B.vy[i]; out_z[i] = B.vz[i]; }
   if (lane == 0) {
@@ -532,7 +534,7 @@ __device__ void wphase_end(const StepParams &P, CellBuf<Real> &B, WarpShared &sh
 // sx, sy, sz) through A3-A8, phases back to back.  Returns kOk or kOverflow
 // (nothing written then except B's scratch).  Writes m_state, stats, and the
 // velocities (out_* unless they alias the slab).
-template <typename Real>
+template <typename Real, bool WB>
 __device__ int process_cell_warp(const StepParams &P, CellBuf<Real> &B, WarpShared &sh, double *usplit,
                                  double sx, double sy, double sz, Real *out_x, Real *out_y, Real *out_z, int n,
                                  uint32_t gcell, int32_t *m_state, double *stats_row, trmcr_coll_rec *log,
@@ -540,11 +542,11 @@ __device__ int process_cell_warp(const StepParams &P, CellBuf<Real> &B, WarpShar
   int rc = wphase_begin<Real>(P, B, sh, usplit, sx, sy, sz, n, gcell, m_state);
   if (rc != kOk) return rc;
   for (;;) {
-    rc = wphase_attempt<Real>(P, B, sh, usplit, gcell, log, log_count, log_cap);
+    rc = wphase_attempt<Real, WB>(P, B, sh, usplit, gcell, log, log_count, log_cap);
     if (rc != kOk) return rc;
     if (sh.done) break;
   }
-  wphase_end<Real>(P, B, sh, out_x, out_y, out_z, gcell, m_state, stats_row);
+  wphase_end<Real, WB>(P, B, sh, out_x, out_y, out_z, gcell, m_state, stats_row);
   return kOk;
 }
 

@@ -817,7 +817,7 @@ __device__ __noinline__ int gather_cell_warp(const ShockDev &S, const GatherSrc 
   return running;
 }
 
-template <typename Real>
+template <typename Real, bool WB>
 __global__ void __launch_bounds__(kWarpCellWarps * 32, TRMCR_WARP_MINB)
 shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, int *defer_count,
@@ -853,7 +853,7 @@ shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
         }
         rc = kOk;
       } else {
-        rc = process_cell_warp<Real>(P, B, sh, usplit, sx, sy, sz, ovx + base, ovy + base, ovz + base, n,
+        rc = process_cell_warp<Real, WB>(P, B, sh, usplit, sx, sy, sz, ovx + base, ovy + base, ovz + base, n,
                                      P.cell_base + (uint32_t)c, m_state + c, stats + (size_t)c * TRMCR_NSTATS,
                                      Q.log, Q.log_count, Q.log_cap);
       }
@@ -872,7 +872,7 @@ shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
 // groups bound the barrier idle of unequal cells.  Sorted cells only (no
 // gather); results identical to the free-running kernel.
 constexpr int kLockWarps = 4;   // measured: 16 -> 2.02 ms, 8 -> 1.80, 4 -> 1.66 (C5), free-running 1.75
-template <typename Real>
+template <typename Real, bool WB>
 __global__ void __launch_bounds__(kLockWarps * 32, 16 / kLockWarps)
 shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, int *defer_count,
@@ -918,12 +918,12 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
     const bool work = run;
     while (__syncthreads_or(run)) {
       if (run) {
-        rc = wphase_attempt<Real>(P, B, sh, usplit, P.cell_base + (uint32_t)c, Q.log, Q.log_count, Q.log_cap);
+        rc = wphase_attempt<Real, WB>(P, B, sh, usplit, P.cell_base + (uint32_t)c, Q.log, Q.log_count, Q.log_cap);
         run = rc == kOk && !sh.done;
       }
     }
     if (work && rc == kOk)
-      wphase_end<Real>(P, B, sh, B.vx, B.vy, B.vz, P.cell_base + (uint32_t)c, m_state + c,
+      wphase_end<Real, WB>(P, B, sh, B.vx, B.vy, B.vz, P.cell_base + (uint32_t)c, m_state + c,
                        stats + (size_t)c * TRMCR_NSTATS);
     if (c < S.C && rc != kOk && lane == 0) defer_list[atomicAdd(defer_count, 1)] = c;
     __syncthreads();
@@ -1163,14 +1163,17 @@ trmcr_status shock_finish(trmcr_ctx *c) {
   if (use_warp) {
     CUDA_TRY(c, cudaMemsetAsync(c->d_defer_count, 0, sizeof(int), c->stream));
     prof_begin(c, TRMCR_K_SHOCK_WARP);
+    const bool wb = c->P.wb != 0;
     if (G.scatter && c->lock_grid > 0)
-      shock_collide_lock<Real><<<c->lock_grid, kLockWarps * 32, c->lock_smem, c->stream>>>(
-          c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
-          c->d_defer_list, Q);
+      (wb ? shock_collide_lock<Real, true> : shock_collide_lock<Real, false>)
+          <<<c->lock_grid, kLockWarps * 32, c->lock_smem, c->stream>>>(
+              c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
+              c->d_defer_list, Q);
     else
-      shock_collide_warp<Real><<<c->warp_grid, c->warp_wpc * 32, c->warp_smem, c->stream>>>(
-          c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
-          c->d_defer_list, Q);
+      (wb ? shock_collide_warp<Real, true> : shock_collide_warp<Real, false>)
+          <<<c->warp_grid, c->warp_wpc * 32, c->warp_smem, c->stream>>>(
+              c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
+              c->d_defer_list, Q);
     if (auto e = check_launch(c, "shock_collide_warp", TRMCR_K_SHOCK_WARP)) return e;
   }
   prof_begin(c, TRMCR_K_SHOCK_SMEM);

@@ -95,7 +95,7 @@ cell_step_gmem(StepParams P, GmemScratch G, const int64_t *__restrict__ offsets,
 
 // General cells, one warp each (cell_warp.cuh), over the thermal kernel's
 // defer list (or every cell); cells that do not fit go to list2 (CTA kernel).
-template <typename Real>
+template <typename Real, bool WB>
 __global__ void __launch_bounds__(kWarpCellWarps * 32, TRMCR_WARP_MINB)
 cell_step_warp(StepParams P, WarpSlabLayout Lay, const int64_t *__restrict__ offsets, int ncells,
                const int *list_count, const int *list, Real *vx, Real *vy, Real *vz, int32_t *m_state,
@@ -123,7 +123,7 @@ cell_step_warp(StepParams P, WarpSlabLayout Lay, const int64_t *__restrict__ off
         sx += a; sy += b; sz += d;
       }
       __syncwarp();
-      rc = process_cell_warp<Real>(P, B, sh, usplit, sx, sy, sz, vx + off, vy + off, vz + off, n,
+      rc = process_cell_warp<Real, WB>(P, B, sh, usplit, sx, sy, sz, vx + off, vy + off, vz + off, n,
                                    P.cell_base + (uint32_t)c, m_state + c, stats + (size_t)c * TRMCR_NSTATS,
                                    Q.log, Q.log_count, Q.log_cap);
     }
@@ -283,7 +283,7 @@ trmcr_status launch_collide(trmcr_ctx *c) {
     const int *l1c = fast ? c->d_defer_count : nullptr, *l1 = fast ? c->d_defer_list : nullptr;
     if (use_warp) {
       prof_begin(c, TRMCR_K_CELL_WARP);
-      launch_k(c, cell_step_warp<Real>, idle ? 1 : c->warp_grid, c->warp_wpc * 32, (size_t)c->warp_smem, c->P,
+      launch_k(c, c->P.wb ? cell_step_warp<Real, true> : cell_step_warp<Real, false>, idle ? 1 : c->warp_grid, c->warp_wpc * 32, (size_t)c->warp_smem, c->P,
                c->wlay, (const int64_t *)c->d_offsets, c->ncells, l1c, l1, vx, vy, vz, c->d_mstate, c->d_stats,
                c->d_defer2_count, c->d_defer2_list, Q);
       if (auto s = check_launch(c, "cell_step_warp", TRMCR_K_CELL_WARP)) return s;
@@ -667,8 +667,10 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
     if (!want || c->warp_smem > smem_max - 2048) {
       c->wlay.n_cap = 0;     // disabled: the CTA kernel takes every general cell
     } else {
-      const void *fns[] = {(const void *)cell_step_warp<float>, (const void *)cell_step_warp<double>,
-                           (const void *)shock_collide_warp<float>, (const void *)shock_collide_warp<double>};
+      const void *fns[] = {(const void *)cell_step_warp<float, false>, (const void *)cell_step_warp<double, false>,
+                           (const void *)shock_collide_warp<float, false>, (const void *)shock_collide_warp<double, false>,
+                           (const void *)cell_step_warp<float, true>, (const void *)cell_step_warp<double, true>,
+                           (const void *)shock_collide_warp<float, true>, (const void *)shock_collide_warp<double, true>};
       for (const void *f : fns)
         if (allow_max_dyn_smem(f, smem_max) != cudaSuccess) {
           fail(c, TRMCR_ECUDA, "cudaFuncSetAttribute(warp) failed");
@@ -677,16 +679,18 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
       int occ = 1, nsm = 148;
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->dev);
       if (c->dtype == TRMCR_F64)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, shock_collide_warp<double>, c->warp_wpc * 32, c->warp_smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, shock_collide_warp<double, true>, c->warp_wpc * 32, c->warp_smem);
       else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, shock_collide_warp<float>, c->warp_wpc * 32, c->warp_smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, shock_collide_warp<float, true>, c->warp_wpc * 32, c->warp_smem);
       c->warp_grid = std::max(1, std::min((c->ncells + c->warp_wpc - 1) / c->warp_wpc, nsm * std::max(occ, 1)));
       // shock: lock-step kernel (TRMCR_SHOCK_LOCKSTEP=0 disables)
       const char *le = getenv("TRMCR_SHOCK_LOCKSTEP");
       const size_t lsm = slab * kLockWarps;
       if (c->geometry == TRMCR_SHOCK_1D && !v_smem && !(le && atoi(le) == 0) && lsm <= (size_t)smem_max - 1024) {
-        const void *lf = c->dtype == TRMCR_F64 ? (const void *)shock_collide_lock<double>
-                                               : (const void *)shock_collide_lock<float>;
+        const bool wbk = c->P.wb != 0;
+        const void *lf = c->dtype == TRMCR_F64
+                             ? (wbk ? (const void *)shock_collide_lock<double, true> : (const void *)shock_collide_lock<double, false>)
+                             : (wbk ? (const void *)shock_collide_lock<float, true> : (const void *)shock_collide_lock<float, false>);
         int occ_l = 0;
         if (allow_max_dyn_smem(lf, smem_max) == cudaSuccess &&
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_l, lf, kLockWarps * 32, lsm) == cudaSuccess &&
