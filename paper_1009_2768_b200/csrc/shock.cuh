@@ -248,8 +248,9 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
   const int64_t n = off_old[S.C];
   const int64_t tile0 = (int64_t)blockIdx.x * kTile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ Real s_xend[2];
   int d[NG][P4];
-  int disp = 0, emi = 0, dropped = 0, dmin = INT32_MAX, smax = -1;
+  int dropped = 0, dmin = INT32_MAX, dmax = -1, lemi = 0, remi = 0;
   // every load of the tile first (x is rewritten below: the compiler may not
   // move later loads above those stores), then the arithmetic
   Real xa[NG][P4], va[NG][P4];
@@ -269,6 +270,14 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
       }
     }
   }
+  // source cells of the tile's first and last particles (the array is sorted
+  // by cell: every source cell of the tile lies between them), read before
+  // any position of the tile is rewritten
+  if (threadIdx.x == 0 && tile0 < n) {
+    s_xend[0] = x[tile0];
+    s_xend[1] = x[min(n, tile0 + (int64_t)kTile) - 1];
+  }
+  __syncthreads();
 #pragma unroll
   for (int g = 0; g < NG; ++g) {
     const int64_t i0 = tile0 + ((int64_t)g * kTransportThreads + threadIdx.x) * P4;
@@ -279,8 +288,6 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
     for (int k = 0; k < P4; ++k) {
       d[g][k] = -1;
       if (i0 + k >= n) continue;
-      const int src = cell_of(S, (double)xs[k]) - S.cbase;
-      smax = max(smax, src);
       const Real xn = add_rn<Real>(xs[k], mul_rn<Real>(vs[k], (Real)S.dt));
       xs[k] = xn;
       const double xd = (double)xn;
@@ -289,10 +296,12 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
       if (!keep) {
         ++dropped;
       } else if (dl >= 0 && dl < S.C) {
-        disp = max(disp, abs(dl - src));
         dmin = min(dmin, dl);
+        dmax = max(dmax, dl);
+      } else if (dl < 0) {
+        lemi = 1;
       } else {
-        emi = max(emi, dl < 0 ? src + 1 : S.C - src);
+        remi = 1;
       }
       if (!vec) { x[i0 + k] = xn; dest[i0 + k] = dl; }
       d[g][k] = dl;
@@ -308,21 +317,28 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
 #pragma unroll
     for (int k = 0; k < P4; ++k) if (d[g][k] < 0 || d[g][k] >= S.C) d[g][k] = -1;   // counted below: local only
   }
-  // CTA reductions: window base, max displacement, emigrant width, dropped
+  // CTA reductions: destination window, emigrant sides, dropped.  With the
+  // tile's source cells in [s0, s1], W[0] = max(dmax - s0, s1 - dmin) bounds
+  // every local displacement and W[1] = s1 + 1 (left) / C - s0 (right) every
+  // emigrant's source distance from the edge (bounds: wider scans, same result)
   dmin = __reduce_min_sync(0xffffffffu, dmin);
-  const int wd = __reduce_max_sync(0xffffffffu, disp), we = __reduce_max_sync(0xffffffffu, emi);
+  const int wdx = __reduce_max_sync(0xffffffffu, dmax);
+  const int wl = __reduce_or_sync(0xffffffffu, lemi), wr = __reduce_or_sync(0xffffffffu, remi);
   const int wdr = __reduce_add_sync(0xffffffffu, dropped);
-  const int wsm = __reduce_max_sync(0xffffffffu, smax);
   if (threadIdx.x < kHist) s_hist[threadIdx.x] = 0;
-  if (lane == 0) { s_red[0][warp] = dmin; s_red[1][warp] = wd; s_red[2][warp] = we; s_red[3][warp] = wsm; }
+  if (lane == 0) { s_red[0][warp] = dmin; s_red[1][warp] = wdx; s_red[2][warp] = wl; s_red[3][warp] = wr; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int m = INT32_MAX, md = 0, me = 0, ms = -1;
+    int m = INT32_MAX, mx = -1, l = 0, r = 0;
     for (int w = 0; w < kTransportThreads / 32; ++w) {
-      m = min(m, s_red[0][w]); md = max(md, s_red[1][w]); me = max(me, s_red[2][w]); ms = max(ms, s_red[3][w]);
+      m = min(m, s_red[0][w]); mx = max(mx, s_red[1][w]); l |= s_red[2][w]; r |= s_red[3][w];
     }
     s_dmin = m;
-    if (tile_meta) tile_meta[blockIdx.x] = make_int2(m, ms);
+    const int s0 = tile0 < n ? cell_of(S, (double)s_xend[0]) - S.cbase : 0;
+    const int s1 = tile0 < n ? cell_of(S, (double)s_xend[1]) - S.cbase : -1;
+    if (tile_meta) tile_meta[blockIdx.x] = make_int2(m, s1);
+    const int md = mx >= 0 ? max(mx - s0, s1 - m) : 0;
+    const int me = max(l ? s1 + 1 : 0, r ? S.C - s0 : 0);
     if (md > 0 && md > *((volatile int *)W)) atomicMax(W, md);
     if (me > 0 && me > *((volatile int *)(W + 1))) atomicMax(W + 1, me);
   }
