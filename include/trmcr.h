@@ -200,8 +200,9 @@ trmcr_status trmcr_step_host(trmcr_ctx *ctx, const void *vx, const void *vy, con
  * ECAPACITY at the next sync if more than `capacity` particles emigrate or a
  * particle crosses a whole slab. */
 int64_t trmcr_exchange_bytes(int32_t dtype, int64_t capacity);
-/* Sort diagnostics of the last shock step (syncs): out[0] = max cell
- * displacement W of a local particle, out[1] = emigrant scan width, out[2] = 1
+/* Sort diagnostics of the last shock step (syncs): out[0] = W, a bound of the
+ * cell displacement of every local particle (per transport tile: its
+ * destinations against its source-cell range), out[1] = emigrant scan width, out[2] = 1
  * when the scatter sort could not be used and the collision
  * kernels gathered instead (a tile's destinations spanned more than 64 cells
  * or an edge particle landed more than 4096 cells from its edge), out[3] = 1

@@ -7,7 +7,7 @@
 //                             IR(rho_B Lg / w) particles of M(rho_B,u_B,T_B) [R26];
 //                             transported; survivors counted per destination cell
 //   transport_kernel          x <- x + v_x dt (splitting); destination
-//                             cell; per-cell counts; max displacement W
+//                             cell; per-cell counts; displacement bound W
 //   scan_offsets              exclusive scan -> new offsets (capacity check)
 //   edge_place                ghosts + immigrants (few) placed at their stable
 //                             positions at the ends of their cells
@@ -230,7 +230,7 @@ __global__ void ghost_gen(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, c
 // a small window: counts are accumulated in a shared-memory histogram over
 // [dmin, dmin + kHist) and flushed with one global atomic per touched cell
 // (a destination outside the window falls back to a global atomic).
-// W[0] = max local displacement, W[1] = emigrant scan width, acct[2] = dropped.
+// W[0] = bound of the local displacements, W[1] = emigrant scan width, acct[2] = dropped.
 constexpr int kTransportThreads = 256, kTransportPer = 4, kTransportGroups = 4, kHist = 256;
 // particles per transport tile: thread t of the CTA owns the 4-particle groups
 // t, t + 256, t + 512, t + 768 of the tile (16-byte coalesced I/O)
