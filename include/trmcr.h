@@ -204,7 +204,7 @@ int64_t trmcr_exchange_bytes(int32_t dtype, int64_t capacity);
  * cell displacement of every local particle (per transport tile: its
  * destinations against its source-cell range), out[1] = emigrant scan width, out[2] = 1
  * when the scatter sort could not be used and the collision
- * kernels gathered instead (a tile's destinations spanned more than 64 cells
+ * kernels gathered instead (a tile's destinations spanned more than 256 cells
  * or an edge particle landed more than 4096 cells from its edge), out[3] = 1
  * when the scatter sort is enabled for this context.  EINVAL for a
  * homogeneous context. */
