@@ -13,12 +13,12 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-fil
     python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/ev/ncu_launch.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:thermal_warp_kernel -s 2 -c 1 \
     -o gpurun_out/ev/c3_thermal python tools/prof_run.py c3 4 > gpurun_out/ev/ncu_c3.log 2>&1
-for k in shock_collide_warp scatter_sorted transport_kernel; do
+for k in shock_collide_lock scatter_sorted transport_kernel; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
       -o gpurun_out/ev/c5_$k python tools/prof_run.py c5 4 > gpurun_out/ev/ncu_c5_$k.log 2>&1
 done
-ncu --set full --clock-control none --import-source on -k regex:shock_collide_warp -s 2 -c 1 \
-    -o gpurun_out/ev/c4_shock_collide_warp python tools/prof_run.py c4 4 > gpurun_out/ev/ncu_c4.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:shock_collide_lock -s 2 -c 1 \
+    -o gpurun_out/ev/c4_shock_collide_lock python tools/prof_run.py c4 4 > gpurun_out/ev/ncu_c4.log 2>&1
 ls -la gpurun_out/ev
 # summaries on the box (the copy-back limit is 64 MiB)
 for r in gpurun_out/ev/*.ncu-rep; do
@@ -27,5 +27,5 @@ for r in gpurun_out/ev/*.ncu-rep; do
   ncu -i $r --page source --csv --print-source cuda,sass > $b.src.csv 2>/dev/null && python tools/ncu_hot.py $b.src.csv 40 > $b.hot.txt; rm -f $b.src.csv
   ncu -i $r --page raw --csv > $b.raw.csv 2>/dev/null
 done
-rm -f gpurun_out/ev/c5_scatter_sorted.ncu-rep gpurun_out/ev/c5_transport_kernel.ncu-rep gpurun_out/ev/c4_shock_collide_warp.ncu-rep
+rm -f gpurun_out/ev/c5_scatter_sorted.ncu-rep gpurun_out/ev/c5_transport_kernel.ncu-rep gpurun_out/ev/c4_shock_collide_lock.ncu-rep
 du -sh gpurun_out/ev; ls -la gpurun_out/ev
