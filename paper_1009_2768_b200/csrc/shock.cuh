@@ -887,9 +887,6 @@ shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
 // stall on instruction fetch: 5.3 cycles per issue, 0.2 in lock step).  Small
 // groups bound the barrier idle of unequal cells.  Sorted cells only (no
 // gather); results identical to the free-running kernel.
-#ifndef TRMCR_LOCK_MODE
-#define TRMCR_LOCK_MODE 2      // 0: barrier per RAD attempt (C5 1.61 ms); 2: retries free-running (1.53 ms)
-#endif
 constexpr int kLockWarps = 4;   // measured: 16 -> 2.02 ms, 8 -> 1.80, 4 -> 1.66 (C5), free-running 1.75
 template <typename Real, bool WB>
 __global__ void __launch_bounds__(kLockWarps * 32, 16 / kLockWarps)
@@ -935,33 +932,19 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
       }
     }
     const bool work = run;
-#if TRMCR_LOCK_MODE == 0
-    while (__syncthreads_or(run)) {
-      if (run) {
-        rc = wphase_attempt<Real, WB>(P, B, sh, usplit, P.cell_base + (uint32_t)c, Q.log, Q.log_count, Q.log_cap);
-        run = rc == kOk && !sh.done;
-      }
-    }
-#else
+    // the begin phase ends in lock step; the attempts (attempt 0 and any RAD
+    // retries) run free - a barrier per attempt measured slower (C5 1.61 vs
+    // 1.53 ms: retries are a minority of the cells)
     __syncthreads();
-    // attempt 0 in lock step, RAD retries (a minority of the cells) free-running
-    for (int att = 0; run; ++att) {
+    while (run) {
       rc = wphase_attempt<Real, WB>(P, B, sh, usplit, P.cell_base + (uint32_t)c, Q.log, Q.log_count, Q.log_cap);
       run = rc == kOk && !sh.done;
-#if TRMCR_LOCK_MODE == 1
-      if (att == 0) { __syncwarp(); }
-#endif
     }
-#endif
     if (work && rc == kOk)
       wphase_end<Real, WB>(P, B, sh, B.vx, B.vy, B.vz, P.cell_base + (uint32_t)c, m_state + c,
                        stats + (size_t)c * TRMCR_NSTATS);
     if (c < S.C && rc != kOk && lane == 0) defer_list[atomicAdd(defer_count, 1)] = c;
-#if TRMCR_LOCK_MODE != 3
-    __syncthreads();
-#else
-    __syncwarp();
-#endif
+    __syncthreads();                          // round in lock step (dropping it measured slower)
   }
 }
 
