@@ -310,6 +310,10 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
   for (int d = 1; d <= top; ++d) {
     const int Cd = B.C[d], Sd = B.S[d];
     if (Cd == 0) continue;
+    const int nw = blockDim.x >> 5;
+    // large levels: ranks by all warps (chunk histograms in the level's own,
+    // not yet written, cslot range: nw * d ints <= 2 Cd)
+    const bool par = Cd >= 2048 && nw * d <= 2 * Cd;
     if (warp == 0) {
       // fold level pd's demands into base[] and clear its histogram (cnt)
       // (two passes through cons[], idle during execution: every read of the
@@ -320,6 +324,47 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
         for (int p = lane; p < pd; p += 32) { B.base[p] = B.cons[p]; B.cnt[p] = 0; }
         __syncwarp();
       }
+    }
+    if (par) {
+      // same ranks as the serial loop below: warp w owns collisions
+      // [w chunk, (w + 1) chunk); H[w][a] = its count of type a, then the
+      // exclusive prefix over warps, then the in-order walk
+      int32_t *H = reinterpret_cast<int32_t *>(B.cslot + 2 * (size_t)Sd);
+      const int chunk = (Cd + nw - 1) / nw;
+      for (int q = tid; q < nw * d; q += blockDim.x) H[q] = 0;
+      __syncthreads();
+      const int j_lo = warp * chunk, j_hi = min(Cd, j_lo + chunk);
+      for (int j0 = j_lo; j0 < j_hi; j0 += 32) {
+        const int j = j0 + lane;
+        const bool valid = j < j_hi;
+        const uint32_t a = valid ? B.ctype[Sd + j] : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xffffffffu, a);
+        if (valid && (__ffs(peers) - 1) == lane) H[warp * d + (int)a] += __popc(peers);
+        __syncwarp();
+      }
+      __syncthreads();
+      for (int t = tid; t < d; t += blockDim.x) {
+        int run = 0;
+        for (int w = 0; w < nw; ++w) { const int v = H[w * d + t]; H[w * d + t] = run; run += v; }
+        B.cnt[t] = run;                       // the level's type histogram
+      }
+      __syncthreads();
+      for (int j0 = j_lo; j0 < j_hi; j0 += 32) {
+        const int j = j0 + lane;
+        const bool valid = j < j_hi;
+        const uint32_t a = valid ? B.ctype[Sd + j] : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xffffffffu, a);
+        const unsigned lt = (1u << lane) - 1u;
+        int c0 = 0;
+        if (valid) c0 = H[warp * d + (int)a];
+        __syncwarp();
+        if (valid) {
+          B.crank[Sd + j] = (uint32_t)(c0 + __popc(peers & lt));
+          if ((peers & lt) == 0u) H[warp * d + (int)a] = c0 + __popc(peers);
+        }
+        __syncwarp();
+      }
+    } else if (warp == 0) {
       // in-level stable ranks per type (32 collisions per round); cnt ends as
       // this level's type histogram
       for (int j0 = 0; j0 < Cd; j0 += 32) {

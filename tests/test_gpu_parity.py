@@ -125,6 +125,18 @@ def test_homogeneous_fp64_trmc_wb(orc, api, monkeypatch, wb, warp_path):
     _parity(orc, api, v[:3], v[3], 3, model=1, m_fixed=10, wb=wb, wb_max=2, eps=2.0, dt=0.3, seed=17)
 
 
+def test_giant_cell_parallel_ranks_fp64(orc, api):
+    """One 60,000-particle cell (global-memory CTA path) whose low levels hold
+    thousands of collisions: in-level ranks computed by all warps (chunk
+    histograms) must equal the serial definition - every record and velocity
+    as the oracle's."""
+    v = synth.anisotropic_gaussian(60_000, seed=18)
+    v = tuple(np.asarray(a, dtype=np.float64) for a in v)
+    sim, o = _parity(orc, api, v, np.array([0, 60_000]), 2, log_cap=200_000, model=1, m_fixed=24, eps=1.0,
+                     dt=0.1, seed=19)
+    assert o.stats["proposals"][0] > 8000
+
+
 def test_homogeneous_fp64_hs_m4_indicator(orc, api):
     v = synth.ragged_cells(30, 500, seed=9)
     _parity(orc, api, v[:3], v[3], 4, model=1, adaptive=1, m_init=4, m_cap=32, indicator=1, eps=0.2,
