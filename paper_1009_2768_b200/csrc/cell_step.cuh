@@ -15,6 +15,7 @@
 #pragma once
 #include "device_common.cuh"
 #include "../../include/trmcr.h"
+#include <cooperative_groups.h>
 
 namespace trmcr {
 
@@ -220,9 +221,60 @@ __device__ __forceinline__ void gauss3(const RngKey &K, uint32_t slot, Real &g0,
 // and one of f_{d-1-a}.  Quotas only on [lo, hi].  Guard: if the
 // leaves cons_0 exceed `budget`, drop the top quota level and re-plan.
 // ---------------------------------------------------------------------------
-template <typename Real>
-__device__ void plan_counts(const RngKey &K, CellBuf<Real> &B, CellShared &sh) {
-  const int tid = threadIdx.x;
+// ---- execution teams of the CTA-level step code: one CTA (BlockTeam), or
+// the whole grid of a cooperative launch (GridTeam: one giant cell on every
+// SM).  tid/size/sync/reductions are the team's; reductions are two-level
+// and in a fixed order (deterministic). ----
+constexpr int kGridSlots = 8;
+struct GridTeam {
+  double *part;              // [kGridSlots][gridDim.x][8] per-block partial sums (rotating)
+  int32_t *hbuf;             // rank scratch [hcap]
+  int64_t hcap;
+  int slot;
+  __device__ __forceinline__ int tid() const { return blockIdx.x * blockDim.x + threadIdx.x; }
+  __device__ __forceinline__ int size() const { return gridDim.x * blockDim.x; }
+  // cooperative-groups grid barrier: release/acquire at gpu scope, so plain
+  // loads after it see every write made before it
+  __device__ __forceinline__ void sync() const { cooperative_groups::this_grid().sync(); }
+  template <int NV> __device__ void sum(double (&v)[NV], double *red) {
+    static_assert(NV <= 8, "at most 8 sums");
+    block_sum<NV>(v, red);
+    double *pp = part + (size_t)slot * gridDim.x * 8;
+    if (threadIdx.x == 0)
+      for (int k = 0; k < NV; ++k) pp[blockIdx.x * 8 + k] = v[k];
+    sync();
+    for (int k = 0; k < NV; ++k) {
+      double t = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) t += pp[b * 8 + k];   // block order: deterministic
+      v[k] = t;
+    }
+    slot = (slot + 1) % kGridSlots;
+  }
+  __device__ double max(double x, double *red) {
+    x = block_max(x, red);
+    double *pp = part + (size_t)slot * gridDim.x * 8;
+    if (threadIdx.x == 0) pp[blockIdx.x * 8] = x;
+    sync();
+    double t = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) t = fmax(t, pp[b * 8]);
+    slot = (slot + 1) % kGridSlots;
+    return t;
+  }
+};
+
+struct BlockTeam {
+  int32_t *hbuf = nullptr;   // no separate rank scratch (the level's slot range is used)
+  int64_t hcap = 0;
+  __device__ __forceinline__ int tid() const { return threadIdx.x; }
+  __device__ __forceinline__ int size() const { return blockDim.x; }
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+  template <int NV> __device__ __forceinline__ void sum(double (&v)[NV], double *red) { block_sum<NV>(v, red); }
+  __device__ __forceinline__ double max(double x, double *red) { return block_max(x, red); }
+};
+
+template <typename Real, class Team>
+__device__ void plan_counts(Team &T, const RngKey &K, CellBuf<Real> &B, CellShared &sh) {
+  const int tid = T.tid();
   if (tid == 0) {
     int top = sh.hi;
     while (top >= sh.lo && B.Q[top] == 0) top--;
@@ -230,34 +282,34 @@ __device__ void plan_counts(const RngKey &K, CellBuf<Real> &B, CellShared &sh) {
     sh.planned = 0;
     sh.done = 0;
   }
-  __syncthreads();
+  T.sync();
   for (;;) {
     if (sh.top < sh.lo || sh.top < 1) {    // nothing to plan
       if (tid == 0) { sh.top = 0; sh.L = 0; }
-      __syncthreads();
+      T.sync();
       return;
     }
     if (sh.top > B.L_cap) {
       if (tid == 0) sh.flag = kOverflow;
-      __syncthreads();
+      T.sync();
       return;
     }
     const int top = sh.top;
-    for (int d = tid; d <= top; d += blockDim.x) B.cons[d] = 0;
-    __syncthreads();
+    for (int d = tid; d <= top; d += T.size()) B.cons[d] = 0;
+    T.sync();
     int Sacc = 0;
     for (int d = top; d >= 1; --d) {
       const int Qd = (d >= sh.lo) ? B.Q[d] : 0;
       const int Cd = (Qd + B.cons[d] + 1) >> 1;   // all threads read the same value
       if ((int64_t)Sacc + Cd > B.K_cap) {
-        __syncthreads();
+        T.sync();
         if (tid == 0) sh.flag = kOverflow;
-        __syncthreads();
+        T.sync();
         return;
       }
-      __syncthreads();                            // every thread has read cons[d]
+      T.sync();                            // every thread has read cons[d]
       if (tid == 0) { B.C[d] = Cd; B.S[d] = Sacc; }
-      for (int j = tid; j < Cd; j += blockDim.x) {
+      for (int j = tid; j < Cd; j += T.size()) {
         const uint32_t w = K(kType, sh.r, d, j).x;
         const uint32_t a = __umulhi(w, (uint32_t)d);  // floor(w d / 2^32)
         B.ctype[Sacc + j] = a;
@@ -265,7 +317,7 @@ __device__ void plan_counts(const RngKey &K, CellBuf<Real> &B, CellShared &sh) {
         atomicAdd(&B.cons[d - 1 - a], 1);
       }
       Sacc += Cd;
-      __syncthreads();
+      T.sync();
     }
     if (tid == 0) {
       if (B.cons[0] <= sh.budget) {
@@ -277,7 +329,7 @@ __device__ void plan_counts(const RngKey &K, CellBuf<Real> &B, CellShared &sh) {
         sh.top = t;
       }
     }
-    __syncthreads();
+    T.sync();
     if (sh.done) return;
   }
 }
@@ -287,22 +339,22 @@ __device__ void plan_counts(const RngKey &K, CellBuf<Real> &B, CellShared &sh) {
 // demands (type d-1-p).  Pool p's t-th demand takes output pi_p(t) of level
 // p (pi_0 = leaf order of the cell).  Output side s of a collision keeps the
 // slot of its input side s; collisions of one level touch disjoint slots.
-template <typename Real>
-__device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real> &B, CellShared &sh,
+template <typename Real, class Team>
+__device__ void plan_execute(Team &T, const StepParams &P, const RngKey &K, CellBuf<Real> &B, CellShared &sh,
                              const Perm &pi0, Real sigma, trmcr_coll_rec *log,
                              unsigned long long *log_count, int64_t log_cap) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = T.tid(), lane = tid & 31, warp = tid >> 5;
   const int top = sh.top;
   if (top < 1) return;
-  for (int d = tid; d <= top; d += blockDim.x) {
+  for (int d = tid; d <= top; d += T.size()) {
     B.base[d] = 0;
     B.cnt[d] = 0;
     if (d >= 1) B.rk[d] = K(kPerm, sh.r, d, 0);
   }
   const int ktot = B.S[1] + B.C[1];                // collisions of the plan (levels top..1 stored from 0)
-  if (P.wb) for (int o = tid; o < 2 * ktot; o += blockDim.x) B.wused[o] = 0;
+  if (P.wb) for (int o = tid; o < 2 * ktot; o += T.size()) B.wused[o] = 0;
   if (tid == 0) sh.ktot = ktot;
-  __syncthreads();
+  T.sync();
   unsigned acc = 0, viol = 0;
   const int r = sh.r;
   const int leaf_off = sh.leaf_off;
@@ -310,10 +362,11 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
   for (int d = 1; d <= top; ++d) {
     const int Cd = B.C[d], Sd = B.S[d];
     if (Cd == 0) continue;
-    const int nw = blockDim.x >> 5;
+    const int nw = T.size() >> 5;
     // large levels: ranks by all warps (chunk histograms in the level's own,
-    // not yet written, cslot range: nw * d ints <= 2 Cd)
-    const bool par = Cd >= 2048 && nw * d <= 2 * Cd;
+    // not yet written, cslot range: nw * d ints <= 2 Cd; a grid team has its
+    // own scratch)
+    const bool par = Cd >= 2048 && (T.hbuf ? (int64_t)nw * d <= T.hcap : nw * d <= 2 * Cd);
     if (warp == 0) {
       // fold level pd's demands into base[] and clear its histogram (cnt)
       // (two passes through cons[], idle during execution: every read of the
@@ -329,10 +382,10 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
       // same ranks as the serial loop below: warp w owns collisions
       // [w chunk, (w + 1) chunk); H[w][a] = its count of type a, then the
       // exclusive prefix over warps, then the in-order walk
-      int32_t *H = reinterpret_cast<int32_t *>(B.cslot + 2 * (size_t)Sd);
+      int32_t *H = T.hbuf ? T.hbuf : reinterpret_cast<int32_t *>(B.cslot + 2 * (size_t)Sd);
       const int chunk = (Cd + nw - 1) / nw;
-      for (int q = tid; q < nw * d; q += blockDim.x) H[q] = 0;
-      __syncthreads();
+      for (int q = tid; q < nw * d; q += T.size()) H[q] = 0;
+      T.sync();
       const int j_lo = warp * chunk, j_hi = min(Cd, j_lo + chunk);
       for (int j0 = j_lo; j0 < j_hi; j0 += 32) {
         const int j = j0 + lane;
@@ -342,13 +395,13 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
         if (valid && (__ffs(peers) - 1) == lane) H[warp * d + (int)a] += __popc(peers);
         __syncwarp();
       }
-      __syncthreads();
-      for (int t = tid; t < d; t += blockDim.x) {
+      T.sync();
+      for (int t = tid; t < d; t += T.size()) {
         int run = 0;
         for (int w = 0; w < nw; ++w) { const int v = H[w * d + t]; H[w * d + t] = run; run += v; }
         B.cnt[t] = run;                       // the level's type histogram
       }
-      __syncthreads();
+      T.sync();
       for (int j0 = j_lo; j0 < j_hi; j0 += 32) {
         const int j = j0 + lane;
         const bool valid = j < j_hi;
@@ -384,8 +437,8 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
       }
     }
     pd = d;
-    __syncthreads();
-    for (int j = tid; j < Cd; j += blockDim.x) {
+    T.sync();
+    for (int j = tid; j < Cd; j += T.size()) {
       const uint32_t a = B.ctype[Sd + j], b = (uint32_t)d - 1u - a;
       const uint32_t rank = B.crank[Sd + j];
       const uint32_t t[2] = {(uint32_t)B.base[a] + rank, (uint32_t)(B.base[b] + B.cnt[b]) + rank};
@@ -428,11 +481,11 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
       }
     }
     if (tid == 0) sh.prop += (unsigned long long)Cd;
-    __syncthreads();
+    T.sync();
   }
   atomicAdd(&sh.acc, (unsigned long long)acc);
   atomicAdd(&sh.viol, (unsigned long long)viol);
-  __syncthreads();
+  T.sync();
 }
 
 // RAD indicator estimate with Theta taken analytically:
@@ -440,12 +493,12 @@ __device__ void plan_execute(const StepParams &P, const RngKey &K, CellBuf<Real>
 // term)] / n.  Theta's particles are still their pre-step values, so the
 // non-Theta sum is (sum over all slots) - (sum over Theta's slots): one pass
 // over the cell plus one over Theta's slots, no membership table.
-template <typename Real>
-__device__ void rad_estimate(const StepParams &P, CellBuf<Real> &B, CellShared &sh, const Perm &pi0) {
-  const int tid = threadIdx.x, n = sh.n, nT = sh.nT;
+template <typename Real, class Team>
+__device__ void rad_estimate(Team &T, const StepParams &P, CellBuf<Real> &B, CellShared &sh, const Perm &pi0) {
+  const int tid = T.tid(), n = sh.n, nT = sh.nT;
   const bool pxx = P.indicator == TRMCR_IND_PXX;
   double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // all-slot indicator sum; Theta: indicator, momentum, |v|^2
-  for (int i = tid; i < n; i += blockDim.x) {
+  for (int i = tid; i < n; i += T.size()) {
     const double x = B.vx[i], y = B.vy[i], z = B.vz[i];
     if (pxx) {
       const double dx = x - sh.ux;
@@ -455,7 +508,7 @@ __device__ void rad_estimate(const StepParams &P, CellBuf<Real> &B, CellShared &
       v[0] += v2 * v2;
     }
   }
-  for (int q = tid; q < nT; q += blockDim.x) {
+  for (int q = tid; q < nT; q += T.size()) {
     const uint32_t s = pi0((uint32_t)(sh.Ltot + q));
     if (s >= (uint32_t)n) { atomicOr(P.err, kErrInternal); continue; }
     const double x = B.vx[s], y = B.vy[s], z = B.vz[s];
@@ -469,7 +522,7 @@ __device__ void rad_estimate(const StepParams &P, CellBuf<Real> &B, CellShared &
     v[2] += x; v[3] += y; v[4] += z;
     v[5] += x * x + y * y + z * z;
   }
-  block_sum<6>(reinterpret_cast<double(&)[6]>(v), B.red);
+  T.template sum<6>(reinterpret_cast<double(&)[6]>(v), B.red);
   if (tid == 0) {
     double s = v[0] - v[1];
     if (nT > 0) {
@@ -486,16 +539,16 @@ __device__ void rad_estimate(const StepParams &P, CellBuf<Real> &B, CellShared &
     if (sh.S0 != 0.0) sh.E1 = fabs(sh.S_est - sh.S0) / fabs(sh.S0);
     else sh.E1 = (sh.S_est == 0.0) ? 0.0 : INFINITY;
   }
-  __syncthreads();
+  T.sync();
 }
 
 // Conservative Maxwellian (A8) over Theta = pi0 positions [Ltot, Ltot+nT)
 // plus, under TRMC-WB, the final outputs whose tree is longer than wb_max
 // (index q < nT: pi0(Ltot + q); q >= nT: output q - nT of the plan).
-template <typename Real>
-__device__ void maxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> &B, CellShared &sh,
+template <typename Real, class Team>
+__device__ void maxwellian(Team &T, const StepParams &P, const RngKey &K, CellBuf<Real> &B, CellShared &sh,
                            const Perm &pi0, double ec_all) {
-  const int tid = threadIdx.x, nT = sh.nT;
+  const int tid = T.tid(), nT = sh.nT;
   const int nq = nT + (P.wb ? 2 * sh.ktot : 0);
   auto member = [&](int q, uint32_t &s) -> bool {
     if (q < nT) { s = pi0((uint32_t)(sh.Ltot + q)); return true; }
@@ -507,32 +560,32 @@ __device__ void maxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> &
   int nwb = 0;
   if (P.wb) {
     double c1[1] = {0.0};
-    for (int o = tid; o < 2 * sh.ktot; o += blockDim.x)
+    for (int o = tid; o < 2 * sh.ktot; o += T.size())
       c1[0] += (!B.wused[o] && B.wlen[o >> 1] > (double)P.wb_max) ? 1.0 : 0.0;
-    block_sum<1>(c1, B.red);
+    T.template sum<1>(c1, B.red);
     nwb = (int)c1[0];
   }
   if (tid == 0) sh.nwb = nwb;
   const int nTT = nT + nwb;
-  if (nTT < 2) { __syncthreads(); return; }
+  if (nTT < 2) { T.sync(); return; }
   const bool full = (nT == sh.n);          // Theta = every slot: skip the permutation
   double ux, uy, uz, ec;
   if (full) {
     ux = sh.ux; uy = sh.uy; uz = sh.uz; ec = ec_all;
   } else {
     double v[3] = {0, 0, 0};
-    for (int q = tid; q < nq; q += blockDim.x) {
+    for (int q = tid; q < nq; q += T.size()) {
       uint32_t s;
       if (!member(q, s)) continue;
       if (s >= (uint32_t)sh.n) { atomicOr(P.err, kErrInternal); continue; }
       v[0] += (double)B.vx[s]; v[1] += (double)B.vy[s]; v[2] += (double)B.vz[s];
     }
-    block_sum<3>(v, B.red);
+    T.template sum<3>(v, B.red);
     ux = v[0] / nTT; uy = v[1] / nTT; uz = v[2] / nTT;
     ec = 0;
   }
   double g[5] = {0, 0, 0, 0, 0};   // sum g (3), sum |g|^2, centred energy of Theta
-  for (int q = tid; q < nq; q += blockDim.x) {
+  for (int q = tid; q < nq; q += T.size()) {
     uint32_t s = (uint32_t)q;
     if (!full && !member(q, s)) continue;
     if (s >= (uint32_t)sh.n) { atomicOr(P.err, kErrInternal); continue; }
@@ -546,14 +599,14 @@ __device__ void maxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> &
     g[0] += g0; g[1] += g1; g[2] += g2;
     g[3] += (double)g0 * g0 + (double)g1 * g1 + (double)g2 * g2;
   }
-  block_sum<5>(g, B.red);
+  T.template sum<5>(g, B.red);
   if (!full) ec = g[4];
   const double gx = g[0] / nTT, gy = g[1] / nTT, gz = g[2] / nTT;
   const double D = g[3] - nTT * (gx * gx + gy * gy + gz * gz);
   const double sc = (D > 0.0 && ec > 0.0) ? sqrt(ec / D) : 0.0;
   const Real rsc = (Real)sc, rgx = (Real)gx, rgy = (Real)gy, rgz = (Real)gz;
   const Real rux = (Real)ux, ruy = (Real)uy, ruz = (Real)uz;
-  for (int q = tid; q < nq; q += blockDim.x) {
+  for (int q = tid; q < nq; q += T.size()) {
     uint32_t s = (uint32_t)q;
     if (!full && !member(q, s)) continue;
     if (s >= (uint32_t)sh.n) continue;
@@ -561,19 +614,19 @@ __device__ void maxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> &
     B.vy[s] = ruy + rsc * (B.vy[s] - rgy);
     B.vz[s] = ruz + rsc * (B.vz[s] - rgz);
   }
-  __syncthreads();
+  T.sync();
 }
 
 // Full per-cell step.  in_* = the cell's particles (global), out_* = where the
 // result goes (may alias in_*).  kLoad: copy in_* into B's arrays first;
 // otherwise B.v* already hold the cell (staged in shared memory by a gather,
 // or aliasing global memory).  kStore: write B.v* to out_* at the end.
-template <typename Real, bool kLoad, bool kStore>
-__device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &sh, const Real *in_x,
+template <typename Real, bool kLoad, bool kStore, class Team>
+__device__ int process_cell(Team &T, const StepParams &P, CellBuf<Real> &B, CellShared &sh, const Real *in_x,
                             const Real *in_y, const Real *in_z, Real *out_x, Real *out_y, Real *out_z,
                             int n, uint32_t gcell, int32_t *m_state, double *stats_row,
                             trmcr_coll_rec *log, unsigned long long *log_count, int64_t log_cap) {
-  const int tid = threadIdx.x;
+  const int tid = T.tid();
   if (n > B.n_cap) return kOverflow;
   PHASE_MARK(t_ph);
   const RngKey K{P.k0, P.k1, gcell, P.step};
@@ -588,18 +641,18 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
   }
   // ---- A3: moments ----
   double s3[3] = {0, 0, 0};
-  for (int i = tid; i < n; i += blockDim.x) {
+  for (int i = tid; i < n; i += T.size()) {
     Real x, y, z;
     if (kLoad) load3(in_x, in_y, in_z, i, x, y, z);
     else { x = B.vx[i]; y = B.vy[i]; z = B.vz[i]; }
     if (kLoad) { B.vx[i] = x; B.vy[i] = y; B.vz[i] = z; }
     s3[0] += x; s3[1] += y; s3[2] += z;
   }
-  block_sum<3>(s3, B.red);
+  T.template sum<3>(s3, B.red);
   const double ux = s3[0] / n, uy = s3[1] / n, uz = s3[2] / n;
   double c3[3] = {0, 0, 0};  // Pxx sum, M4 sum, centred energy
   double dv2 = 0.0;
-  for (int i = tid; i < n; i += blockDim.x) {
+  for (int i = tid; i < n; i += T.size()) {
     const double x = B.vx[i], y = B.vy[i], z = B.vz[i];
     const double dx = x - ux, dy = y - uy, dz = z - uz;
     const double r2 = dx * dx + dy * dy + dz * dz;
@@ -609,12 +662,12 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
     c3[1] += v2 * v2;
     c3[2] += r2;
   }
-  for (int d = tid; d < kSplitPre; d += blockDim.x) {   // split uniforms, in parallel
+  for (int d = tid; d < kSplitPre; d += T.size()) {   // split uniforms, in parallel
     const uint4 w = K(kSplit, 0, (uint32_t)d, 0);
     sh.usplit[d] = u53(w.x, w.y);
   }
-  block_sum<3>(c3, B.red);
-  dv2 = block_max(dv2, B.red);
+  T.template sum<3>(c3, B.red);
+  dv2 = T.max(dv2, B.red);
   if (tid == 0) {
     sh.n = n; sh.ux = ux; sh.uy = uy; sh.uz = uz;
     sh.sums[0] = s3[0]; sh.sums[1] = s3[1]; sh.sums[2] = s3[2];
@@ -645,17 +698,17 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
     sh.r = 0; sh.lo = 1; sh.hi = sh.d < B.L_cap ? sh.d : B.L_cap;
     sh.budget = n; sh.leaf_off = 0; sh.ktot = 0; sh.nwb = 0;
   }
-  __syncthreads();
+  T.sync();
   PHASE_ADD(0, t_ph);   // moments + split
   if (sh.flag != kOk) return sh.flag;
   Perm pi0;
   pi0.init(K(kPerm, 0, 0, 0), (uint32_t)n);
   const Real sigma = (Real)sh.sigma;
   // ---- A5/A6: attempt 0 ----
-  plan_counts<Real>(K, B, sh);
+  plan_counts<Real>(T, K, B, sh);
   PHASE_ADD(1, t_ph);   // plan counts
   if (sh.flag != kOk) return sh.flag;
-  plan_execute<Real>(P, K, B, sh, pi0, sigma, log, log_count, log_cap);
+  plan_execute<Real>(T, P, K, B, sh, pi0, sigma, log, log_count, log_cap);
   PHASE_ADD(2, t_ph);   // plan execute
   if (tid == 0) {
     sh.Ltot = sh.L;
@@ -664,11 +717,11 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
     sh.m_next = sh.m_cur;
     sh.S_est = sh.S0; sh.E1 = 0.0;
   }
-  __syncthreads();
+  T.sync();
   // ---- A7: TRMC-RAD ----
   if (P.adaptive) {
     for (;;) {
-      rad_estimate<Real>(P, B, sh, pi0);
+      rad_estimate<Real>(T, P, B, sh, pi0);
       PHASE_ADD(3, t_ph);   // RAD estimate
       if (tid == 0) {
         sh.done = 1;
@@ -684,38 +737,38 @@ __device__ int process_cell(const StepParams &P, CellBuf<Real> &B, CellShared &s
           sh.done = 0;
         }
       }
-      __syncthreads();
+      T.sync();
       if (sh.flag != kOk) return sh.flag;
       if (sh.done) break;
-      plan_counts<Real>(K, B, sh);
+      plan_counts<Real>(T, K, B, sh);
       if (sh.flag != kOk) return sh.flag;
-      plan_execute<Real>(P, K, B, sh, pi0, sigma, log, log_count, log_cap);
+      plan_execute<Real>(T, P, K, B, sh, pi0, sigma, log, log_count, log_cap);
       PHASE_ADD(4, t_ph);   // RAD retries
       if (tid == 0) { sh.Ltot += sh.L; sh.nT -= sh.L; }
-      __syncthreads();
+      T.sync();
       if (P.debug_stop > 0 && sh.r >= P.debug_stop) {
         if (kStore)
-          for (int i = tid; i < n; i += blockDim.x) { out_x[i] = B.vx[i]; out_y[i] = B.vy[i]; out_z[i] = B.vz[i]; }
+          for (int i = tid; i < n; i += T.size()) { out_x[i] = B.vx[i]; out_y[i] = B.vy[i]; out_z[i] = B.vz[i]; }
         return kOk;
       }
     }
     if (tid == 0) {
       sh.m_next = (sh.E1 < P.delta1) ? (sh.m_cur / 2 > 1 ? sh.m_cur / 2 : 1) : sh.m_cur;
     }
-    __syncthreads();
+    T.sync();
   }
   if (P.debug_stop < 0) {   // debug: stop before the Maxwellian
     if (kStore)
-      for (int i = tid; i < n; i += blockDim.x) { out_x[i] = B.vx[i]; out_y[i] = B.vy[i]; out_z[i] = B.vz[i]; }
+      for (int i = tid; i < n; i += T.size()) { out_x[i] = B.vx[i]; out_y[i] = B.vy[i]; out_z[i] = B.vz[i]; }
     return kOk;
   }
   // ---- A8: Maxwellian of Theta ----
   PHASE_ADD(5, t_ph);
-  maxwellian<Real>(P, K, B, sh, pi0, c3[2]);
+  maxwellian<Real>(T, P, K, B, sh, pi0, c3[2]);
   PHASE_ADD(6, t_ph);   // Maxwellian
   // ---- write back + stats ----
   if (kStore) {
-    for (int i = tid; i < n; i += blockDim.x) {
+    for (int i = tid; i < n; i += T.size()) {
       out_x[i] = B.vx[i]; out_y[i] = B.vy[i]; out_z[i] = B.vz[i];
     }
   }

@@ -185,6 +185,11 @@ struct trmcr_ctx {
   int lock_grid = 0, lock_smem = 0;   // shock lock-step collision kernel (0: free-running warps)   // L2 prefetch of each warp's next cell (TRMCR_THERMAL_PREFETCH=0 disables)
   int fast_ok = 1, fast_pending = 0, fast_grid = 0, smem_grid = 0, last_defer = -1, last_ovf = -1;
   unsigned char *d_scratch = nullptr;
+  int giant_min = 0, giant_grid = 0;       // cells with n >= giant_min: cell_step_giant (0: off)
+  trmcr::CellShared *d_gsh = nullptr;
+  double *d_gpart = nullptr;
+  int32_t *d_ghbuf = nullptr;
+  int64_t ghcap = 0;
   trmcr::GmemScratch gs{};
   int G = 1;
   int gmem_threads = trmcr::kGmemThreads;

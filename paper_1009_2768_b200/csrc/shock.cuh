@@ -953,6 +953,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS)
 shock_collide_smem(StepParams P, SmemLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats,
                    const int *list_count, const int *list, QueueArgs Q) {
+  BlockTeam team;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CellShared sh;
   __shared__ int wcnt[32];
@@ -969,7 +970,7 @@ shock_collide_smem(StepParams P, SmemLayout Lay, ShockDev S, GatherSrc G, const 
     gather_cell<Real>(S, G, c, B.vx, B.vy, B.vz, ox + base, wcnt);
     __syncthreads();
     PHASE_ADD(8, t_g);   // gather
-    rc = process_cell<Real, false, true>(P, B, sh, nullptr, nullptr, nullptr, ovx + base, ovy + base,
+    rc = process_cell<Real, false, true>(team, P, B, sh, nullptr, nullptr, nullptr, ovx + base, ovy + base,
                                          ovz + base, n, P.cell_base + (uint32_t)c, m_state + c,
                                          stats + (size_t)c * TRMCR_NSTATS, Q.log, Q.log_count, Q.log_cap);
   }
@@ -985,6 +986,7 @@ template <typename Real>
 __global__ void __launch_bounds__(kGmemThreads)
 shock_collide_gmem(StepParams P, GmemScratch GS, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, QueueArgs Q) {
+  BlockTeam team;
   __shared__ CellShared sh;
   __shared__ double red[32 * 8];
   __shared__ int wcnt[32];
@@ -998,7 +1000,7 @@ shock_collide_gmem(StepParams P, GmemScratch GS, ShockDev S, GatherSrc G, const 
     B.vx = ovx + base; B.vy = ovy + base; B.vz = ovz + base;
     gather_cell<Real>(S, G, c, B.vx, B.vy, B.vz, ox + base, wcnt);
     __syncthreads();
-    const int rc = process_cell<Real, false, false>(P, B, sh, nullptr, nullptr, nullptr, B.vx, B.vy, B.vz, n,
+    const int rc = process_cell<Real, false, false>(team, P, B, sh, nullptr, nullptr, nullptr, B.vx, B.vy, B.vz, n,
                                                     P.cell_base + (uint32_t)c, m_state + c,
                                                     stats + (size_t)c * TRMCR_NSTATS, Q.log, Q.log_count,
                                                     Q.log_cap);

@@ -34,6 +34,7 @@ cell_step_smem(StepParams P, SmemLayout Lay, const int64_t *__restrict__ offsets
                const int *list_count, const int *list, Real *vx, Real *vy, Real *vz, int32_t *m_state,
                double *stats, QueueArgs Q, GmemScratch GS, int inline_gmem) {
   step_kernel_prologue(Q.zero_next);
+  BlockTeam team;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CellShared sh;
   CellBuf<Real> B;
@@ -43,7 +44,7 @@ cell_step_smem(StepParams P, SmemLayout Lay, const int64_t *__restrict__ offsets
     const int c = list ? list[k] : k;
     const int64_t off = offsets[c];
     const int n = (int)(offsets[c + 1] - off);
-    const int rc = process_cell<Real, true, true>(P, B, sh, vx + off, vy + off, vz + off, vx + off,
+    const int rc = process_cell<Real, true, true>(team, P, B, sh, vx + off, vy + off, vz + off, vx + off,
                                                   vy + off, vz + off, n, P.cell_base + (uint32_t)c,
                                                   m_state + c, stats + (size_t)c * TRMCR_NSTATS, Q.log,
                                                   Q.log_count, Q.log_cap);
@@ -54,7 +55,7 @@ cell_step_smem(StepParams P, SmemLayout Lay, const int64_t *__restrict__ offsets
       CellBuf<Real> BG;
       bind_gmem(BG, GS, B.red);
       BG.vx = vx + off; BG.vy = vy + off; BG.vz = vz + off;
-      const int rg = process_cell<Real, false, false>(P, BG, sh, vx + off, vy + off, vz + off, vx + off,
+      const int rg = process_cell<Real, false, false>(team, P, BG, sh, vx + off, vy + off, vz + off, vx + off,
                                                       vy + off, vz + off, n, P.cell_base + (uint32_t)c,
                                                       m_state + c, stats + (size_t)c * TRMCR_NSTATS, Q.log,
                                                       Q.log_count, Q.log_cap);
@@ -71,8 +72,9 @@ cell_step_smem(StepParams P, SmemLayout Lay, const int64_t *__restrict__ offsets
 template <typename Real>
 __global__ void __launch_bounds__(kGmemThreads)
 cell_step_gmem(StepParams P, GmemScratch G, const int64_t *__restrict__ offsets, Real *vx, Real *vy,
-               Real *vz, int32_t *m_state, double *stats, QueueArgs Q) {
+               Real *vz, int32_t *m_state, double *stats, QueueArgs Q, int giant_min) {
   step_kernel_prologue(Q.zero_next);
+  BlockTeam team;
   __shared__ CellShared sh;
   __shared__ double red[32 * 8];
   const int count = *Q.ovf_count;
@@ -82,8 +84,9 @@ cell_step_gmem(StepParams P, GmemScratch G, const int64_t *__restrict__ offsets,
     const int c = Q.ovf_list[k];
     const int64_t off = offsets[c];
     const int n = (int)(offsets[c + 1] - off);
+    if (giant_min > 0 && n >= giant_min) continue;   // cell_step_giant (whole grid) takes it
     B.vx = vx + off; B.vy = vy + off; B.vz = vz + off;
-    const int rc = process_cell<Real, false, false>(P, B, sh, vx + off, vy + off, vz + off, vx + off,
+    const int rc = process_cell<Real, false, false>(team, P, B, sh, vx + off, vy + off, vz + off, vx + off,
                                              vy + off, vz + off, n, P.cell_base + (uint32_t)c,
                                              m_state + c, stats + (size_t)c * TRMCR_NSTATS, Q.log,
                                              Q.log_count, Q.log_cap);
@@ -91,6 +94,38 @@ cell_step_gmem(StepParams P, GmemScratch G, const int64_t *__restrict__ offsets,
     __syncthreads();
   }
   step_kernel_epilogue();
+}
+
+
+// Giant cells (n >= giant_min, e.g. config 2's single 10^6-particle cell):
+// one cell at a time on the whole grid of a cooperative launch - the CTA step
+// code with a GridTeam (grid barriers, two-level deterministic reductions,
+// the cell's plan in global scratch slab 0, its shared scalars in global memory).
+constexpr int kGiantThreads = 256;
+template <typename Real>
+__global__ void __launch_bounds__(kGiantThreads)
+cell_step_giant(StepParams P, GmemScratch G, CellShared *gsh, double *part, int32_t *hbuf, int64_t hcap,
+                const int64_t *__restrict__ offsets, Real *vx, Real *vy, Real *vz, int32_t *m_state,
+                double *stats, QueueArgs Q, int giant_min) {
+  GridTeam team{part, hbuf, hcap, 0};
+  __shared__ double red[32 * 8];
+  CellBuf<Real> B;
+  G.stride = 0;                                   // every block binds the same plan slab
+  bind_gmem(B, G, red);
+  const int count = *Q.ovf_count;
+  for (int k = 0; k < count; ++k) {
+    const int c = Q.ovf_list[k];
+    const int64_t off = offsets[c];
+    const int n = (int)(offsets[c + 1] - off);
+    if (n < giant_min) continue;
+    B.vx = vx + off; B.vy = vy + off; B.vz = vz + off;
+    const int rc = process_cell<Real, false, false>(team, P, B, *gsh, vx + off, vy + off, vz + off, vx + off,
+                                                    vy + off, vz + off, n, P.cell_base + (uint32_t)c,
+                                                    m_state + c, stats + (size_t)c * TRMCR_NSTATS, Q.log,
+                                                    Q.log_count, Q.log_cap);
+    if (rc != kOk && team.tid() == 0) atomicOr(Q.err, 1);
+    team.sync();
+  }
 }
 
 // General cells, one warp each (cell_warp.cuh), over the thermal kernel's
@@ -276,7 +311,7 @@ trmcr_status launch_collide(trmcr_ctx *c) {
                c->thermal_prefetch, nxt);
       if (auto s = check_launch(c, "thermal_warp_kernel", TRMCR_K_THERMAL)) return s;
     }
-    const bool idle = fast && c->fast_ok && c->last_defer == 0 && c->last_ovf == 0;
+    const bool idle = fast && c->fast_ok && c->last_defer == 0 && c->last_ovf == 0 && c->giant_min == 0;
     // idle (nothing deferred lately): skip the warp kernel, the CTA kernel
     // (one CTA) drains whatever this step defers
     const bool use_warp = c->wlay.n_cap > 0 && !idle;
@@ -300,8 +335,24 @@ trmcr_status launch_collide(trmcr_ctx *c) {
     if (!idle) {   // idle: the single CTA above handled overflowing cells itself
       prof_begin(c, TRMCR_K_CELL_GMEM);
       launch_k(c, cell_step_gmem<Real>, c->G, c->gmem_threads, 0, c->P, c->gs, (const int64_t *)c->d_offsets, vx,
-               vy, vz, c->d_mstate, c->d_stats, Q);
+               vy, vz, c->d_mstate, c->d_stats, Q, c->giant_min);
       if (auto s = check_launch(c, "cell_step_gmem", TRMCR_K_CELL_GMEM)) return s;
+      if (c->giant_min > 0) {
+        StepParams Pg = c->P;
+        GmemScratch gs = c->gs;
+        CellShared *gsh = c->d_gsh;
+        double *gpart = c->d_gpart;
+        int32_t *ghb = c->d_ghbuf;
+        int64_t ghc = c->ghcap;
+        const int64_t *offs = c->d_offsets;
+        int32_t *ms = c->d_mstate;
+        double *st = c->d_stats;
+        int gmin = c->giant_min;
+        void *args[] = {&Pg, &gs, &gsh, &gpart, &ghb, &ghc, &offs, &vx, &vy, &vz, &ms, &st, &Q, &gmin};
+        CUDA_TRY(c, cudaLaunchCooperativeKernel((const void *)cell_step_giant<Real>, dim3(c->giant_grid),
+                                                dim3(kGiantThreads), args, 0, c->stream));
+        if (auto s = check_launch(c, "cell_step_giant", TRMCR_K_CELL_GMEM)) return s;
+      }
     }
     if (!c->fast_pending && (c->step % 8 == 0 || !c->fast_ok)) {
       CUDA_TRY(c, cudaMemcpyAsync(c->h_defer, c->d_defer_count, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -719,6 +770,29 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
   c->G = G;
   if (dalloc(c, &c->d_scratch, stride * G)) return bail(TRMCR_ENOMEM);
   c->gs = GmemScratch{c->d_scratch, stride, n_cap_g, (int)K_cap_g, L_cap_g, c->P.wb != 0 ? 1 : 0};
+
+  // ---- giant cells: the whole grid per cell (cooperative launch) ----
+  {
+    const char *ge = getenv("TRMCR_GIANT");
+    const int gmin = ge ? atoi(ge) : 32768;       // 0 disables
+    int coop = 0, nsm = 148, occ_g = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->dev);
+    if (gmin > 0 && c->geometry == TRMCR_HOMOGENEOUS && max_cell >= gmin && coop) {
+      const void *gf = c->dtype == TRMCR_F64 ? (const void *)cell_step_giant<double> : (const void *)cell_step_giant<float>;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_g, gf, kGiantThreads, 0) == cudaSuccess && occ_g > 0) {
+        c->giant_grid = nsm;                      // one block per SM: short cross-block prefixes
+        c->ghcap = (int64_t)c->giant_grid * (kGiantThreads / 32) * 64;
+        if (dalloc(c, &c->d_gsh, sizeof(CellShared)) ||
+            dalloc(c, &c->d_gpart, sizeof(double) * kGridSlots * 8 * (size_t)c->giant_grid) ||
+            dalloc(c, &c->d_ghbuf, sizeof(int32_t) * (size_t)c->ghcap))
+          return bail(TRMCR_ENOMEM);
+        c->giant_min = gmin;
+      } else {
+        cudaGetLastError();
+      }
+    }
+  }
 
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
     fail(c, TRMCR_ECUDA, "init synchronisation failed");
