@@ -781,7 +781,10 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
     if (gmin > 0 && c->geometry == TRMCR_HOMOGENEOUS && max_cell >= gmin && coop) {
       const void *gf = c->dtype == TRMCR_F64 ? (const void *)cell_step_giant<double> : (const void *)cell_step_giant<float>;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_g, gf, kGiantThreads, 0) == cudaSuccess && occ_g > 0) {
-        c->giant_grid = nsm;                      // one block per SM: short cross-block prefixes
+        // 32 blocks: the step is bound by its grid barriers, whose cost grows
+        // with the block count (C2: 148 blocks 2.19 ms, 64 1.42, 32 1.17, 16 1.20)
+        c->giant_grid = std::min(32, nsm * occ_g);
+        if (const char *gg = getenv("TRMCR_GIANT_GRID")) c->giant_grid = std::max(1, std::min(nsm * occ_g, atoi(gg)));
         c->ghcap = (int64_t)c->giant_grid * (kGiantThreads / 32) * 64;
         if (dalloc(c, &c->d_gsh, sizeof(CellShared)) ||
             dalloc(c, &c->d_gpart, sizeof(double) * kGridSlots * 8 * (size_t)c->giant_grid) ||
