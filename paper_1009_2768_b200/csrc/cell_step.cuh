@@ -313,8 +313,12 @@ __device__ void plan_counts(Team &T, const RngKey &K, CellBuf<Real> &B, CellShar
         const uint32_t w = K(kType, sh.r, d, j).x;
         const uint32_t a = __umulhi(w, (uint32_t)d);  // floor(w d / 2^32)
         B.ctype[Sacc + j] = a;
-        atomicAdd(&B.cons[a], 1);
-        atomicAdd(&B.cons[d - 1 - a], 1);
+        // warp-aggregated demand counts (one atomic per distinct pool per warp)
+        const unsigned act = __activemask();
+        const unsigned pa = __match_any_sync(act, a), pb = __match_any_sync(act, (uint32_t)d - 1u - a);
+        const int lane_ = threadIdx.x & 31;
+        if ((__ffs(pa) - 1) == lane_) atomicAdd(&B.cons[a], __popc(pa));
+        if ((__ffs(pb) - 1) == lane_) atomicAdd(&B.cons[d - 1 - a], __popc(pb));
       }
       Sacc += Cd;
       T.sync();
