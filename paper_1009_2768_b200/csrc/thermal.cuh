@@ -19,7 +19,7 @@ namespace trmcr {
 template <typename Real> struct ThermalCap;
 template <> struct ThermalCap<float> { static constexpr int value = 1024; };
 template <> struct ThermalCap<double> { static constexpr int value = 512; };
-constexpr int kThermalWarps = 8;
+constexpr int kThermalWarps = 1;   // one warp per CTA, 16 CTAs per SM: measured 97.2 us vs 101.1 (8 warps x 2 CTAs) on C3
 
 // 16-byte vector of Real (4 floats or 2 doubles) for coalesced, batched I/O.
 template <typename Real> struct Vec;
@@ -479,7 +479,7 @@ __device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, const KeyS
 }
 
 template <typename Real>
-__global__ void __launch_bounds__(kThermalWarps * 32, 2)
+__global__ void __launch_bounds__(kThermalWarps * 32, 16)
 thermal_warp_kernel(StepParams P, KeySched ks, const int64_t *__restrict__ offsets, int ncells, Real *vx,
                     Real *vy, Real *vz, int32_t *m_state, double *stats, int *defer_count, int *defer_list,
                     int prefetch, int *zero_next) {
