@@ -41,17 +41,17 @@ UNIT = "particle-updates/s"
 def workload(name: str, rank: int = 0, world: int = 1, eps_override=None):
     """Synthetic inputs shaped like BASELINE.json configs."""
     if name == "c3":
+        # independent cells: weak scaling (tier rule 5) - every rank owns a full
+        # 16,384-cell ensemble with its own global cell ids (own RNG streams)
         ncells, ppc = 16_384, 1024
-        lo, hi = rank * ncells // world, (rank + 1) * ncells // world
         vx, vy, vz, off = synth.bimodal_cells(ncells, ppc, seed=1)
-        sl = slice(lo * ppc, hi * ppc)
-        return dict(kind="hom", vx=vx[sl], vy=vy[sl], vz=vz[sl], offsets=off[lo:hi + 1] - off[lo],
-                    cell_base=lo, dtype=np.float32,
+        return dict(kind="hom", vx=vx, vy=vy, vz=vz, offsets=off, cell_base=rank * ncells, dtype=np.float32,
                     kw=dict(model=1, m_fixed=64, eps=eps_override or 0.01, dt=0.1, seed=1),
-                    cfg=dict(workload="configs[2] batched homogeneous hard spheres", cells=ncells,
-                             ppc=ppc, particles=ncells * ppc, eps=eps_override or 0.01, dt=0.1,
-                             truncation="TRMC-R m=64", sharding="cells", global_moments="allreduce/step"),
-                    global_cells=ncells)
+                    cfg=dict(workload="configs[2] batched homogeneous hard spheres", cells_per_gpu=ncells,
+                             ppc=ppc, particles_per_gpu=ncells * ppc, cells=ncells * world,
+                             eps=eps_override or 0.01, dt=0.1, truncation="TRMC-R m=64",
+                             sharding="cells (weak: 16,384 cells per GPU)", global_moments="allreduce/step"),
+                    global_cells=ncells * world, scaling="weak")
     if name in ("c4", "c5"):
         if name == "c4":
             setup = synth.shock_setup(mach=3.0, ncells=2000, n_total=1_000_000, x_min=-20, x_max=20)
@@ -83,16 +83,17 @@ def workload(name: str, rank: int = 0, world: int = 1, eps_override=None):
         vx, vy, vz = synth.anisotropic_gaussian(n, seed=1)
         eps = eps_override or 1.0
         return dict(kind="hom", vx=vx.astype(np.float32), vy=vy.astype(np.float32),
-                    vz=vz.astype(np.float32), offsets=np.array([0, n]), cell_base=0, dtype=np.float32,
+                    vz=vz.astype(np.float32), offsets=np.array([0, n]), cell_base=rank, dtype=np.float32,
                     kw=dict(model=1, adaptive=True, m_init=2, m_cap=4096, eps=eps, dt=0.05, seed=1),
                     cfg=dict(workload="configs[1] homogeneous hard spheres, one cell", cells=1,
-                             particles=n, eps=eps, dt=0.05, truncation="TRMC-RAD"), global_cells=1)
+                             particles=n, eps=eps, dt=0.05, truncation="TRMC-RAD"), global_cells=world,
+                    scaling="weak")
     if name == "c1":
         vx, vy, vz = synth.two_maxwellians(10_000, seed=1)
-        return dict(kind="hom", vx=vx, vy=vy, vz=vz, offsets=np.array([0, 10_000]), cell_base=0,
+        return dict(kind="hom", vx=vx, vy=vy, vz=vz, offsets=np.array([0, 10_000]), cell_base=rank,
                     dtype=np.float64, kw=dict(model=0, m_fixed=64, eps=1.0, dt=0.1, seed=1),
                     cfg=dict(workload="configs[0] Maxwell molecules, one cell", cells=1, particles=10_000,
-                             eps=1.0, dt=0.1, truncation="TRMC-R m=64"), global_cells=1)
+                             eps=1.0, dt=0.1, truncation="TRMC-R m=64"), global_cells=world, scaling="weak")
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -395,7 +396,7 @@ def run_trmcr(args, rank, world, local_rank):
                l2="inputs larger than L2 (no flush)" if n_local * 3 * rs > 126e6 else "inputs L2-resident")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None,
+            "scaling": W.get("scaling", "strong"), "vs_baseline": None,
             "dtype": "f32" if td == torch.float32 else "f64", "data": "synthetic", "config": cfg,
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks, "e2e": e2e,
             "gpu_launches": int(launches), "impl": "trmcr"}
