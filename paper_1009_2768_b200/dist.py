@@ -85,7 +85,9 @@ class ShockSlab:
     [first, first + ncells) plus its exchange buffers."""
 
     def __init__(self, api, setup: dict, first: int, ncells: int, vx, vy, vz, *, x, device,
-                 exchange_capacity: int = 1 << 16, **kw):
+                 exchange_capacity: int = 1 << 13, **kw):
+        # capacity: particles crossing one slab edge in one step (a few hundred at
+        # CFL 0.5 on C5; the whole buffer travels, so it is kept small: 8192 x 20 B)
         import torch
         self.first, self.ncells = first, ncells
         C = setup["ncells"]
