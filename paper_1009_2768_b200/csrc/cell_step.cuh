@@ -307,7 +307,8 @@ __device__ void plan_counts(Team &T, const RngKey &K, CellBuf<Real> &B, CellShar
         T.sync();
         return;
       }
-      T.sync();                            // every thread has read cons[d]
+      // (no barrier here: level d's draws only add to cons[a < d], never to the
+      // cons[d] every thread has just read; the end-of-level barrier orders levels)
       if (tid == 0) { B.C[d] = Cd; B.S[d] = Sacc; }
       for (int j = tid; j < Cd; j += T.size()) {
         const uint32_t w = K(kType, sh.r, d, j).x;
