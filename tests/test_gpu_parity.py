@@ -137,6 +137,17 @@ def test_giant_cell_parallel_ranks_fp64(orc, api):
     assert o.stats["proposals"][0] > 8000
 
 
+def test_giant_cell_vhs_wb_fp64(orc, api):
+    """A 40,000-particle cell on the grid-cooperative kernel with VHS molecules
+    (alpha = 0.6) and TRMC-WB (1 + mean, m_max = 2): every decision and
+    velocity as the oracle's."""
+    v = synth.anisotropic_gaussian(40_000, seed=20)
+    v = tuple(np.asarray(a, dtype=np.float64) for a in v)
+    _, o = _parity(orc, api, v, np.array([0, 40_000]), 2, log_cap=200_000, model=2, alpha=0.6, m_fixed=12,
+                   wb=2, wb_max=2, eps=1.0, dt=0.1, seed=21)
+    assert o.stats["maxw"][0] > 0 and o.stats["proposals"][0] > 4000
+
+
 def test_homogeneous_fp64_hs_m4_indicator(orc, api):
     v = synth.ragged_cells(30, 500, seed=9)
     _parity(orc, api, v[:3], v[3], 4, model=1, adaptive=1, m_init=4, m_cap=32, indicator=1, eps=0.2,
