@@ -140,6 +140,7 @@ struct ShockState {
   int2 *d_tile_meta = nullptr;              // [ntiles] (first histogram cell dmin, last source cell)
   int32_t *d_lcnt = nullptr;                // [kEdgeBins] left-edge (ghost + immigrant) particles per cell
   int ntiles = 0;
+  int tile_ng = 4;                          // transport / sort tile = 1024 * tile_ng particles (1 or 4)
   int scatter = 1;                          // sort by scatter (TRMCR_SHOCK_SCATTER=0: gather in the collide kernel)
   unsigned long long *d_acct = nullptr;     // [4] injected L, injected R, dropped, generated
 };

@@ -234,19 +234,20 @@ __global__ void ghost_gen(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, c
 constexpr int kTransportThreads = 256, kTransportPer = 4, kTransportGroups = 4, kHist = 256;
 // particles per transport tile: thread t of the CTA owns the 4-particle groups
 // t, t + 256, t + 512, t + 768 of the tile (16-byte coalesced I/O)
-constexpr int kTile = kTransportThreads * kTransportPer * kTransportGroups;
+constexpr int kTile = kTransportThreads * kTransportPer * kTransportGroups;   // large problems
+__host__ __device__ constexpr int tile_of(int ng) { return kTransportThreads * kTransportPer * ng; }
 constexpr int kEdgeBins = 4096;   // cells from a domain / slab edge that ghosts and immigrants may reach
 
-template <typename Real>
+template <typename Real, int NG>
 __global__ void __launch_bounds__(kTransportThreads)
 transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const Real *__restrict__ vx,
                  int32_t *dest, int32_t *counts, int *W, unsigned long long *acct, int32_t *tileH, int2 *tile_meta) {
-  constexpr int P4 = kTransportPer, NG = kTransportGroups;
+  constexpr int P4 = kTransportPer, TILE = tile_of(NG);
   __shared__ int s_hist[kHist];
   __shared__ int s_red[4][kTransportThreads / 32];
   __shared__ int s_dmin;
   const int64_t n = off_old[S.C];
-  const int64_t tile0 = (int64_t)blockIdx.x * kTile;
+  const int64_t tile0 = (int64_t)blockIdx.x * TILE;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ Real s_xend[2];
   int d[NG][P4];
@@ -275,7 +276,7 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
   // any position of the tile is rewritten
   if (threadIdx.x == 0 && tile0 < n) {
     s_xend[0] = x[tile0];
-    s_xend[1] = x[min(n, tile0 + (int64_t)kTile) - 1];
+    s_xend[1] = x[min(n, tile0 + (int64_t)TILE) - 1];
   }
   __syncthreads();
 #pragma unroll
@@ -463,18 +464,26 @@ __global__ void immigrant_count(ShockDev S, const void *recv_l, const void *recv
 // their cells, pos = off_new[d] + running count; lcnt[d] = how many (read by
 // scatter_sorted).  side 1: right immigrants, then right reservoir ghosts: the
 // last particles of their cells, pos = off_new[d + 1] - total[d] + running.
-// One warp per side (these segments hold a few hundred particles).
+// One CTA per side: each round covers kEdgeThreads consecutive particles of a
+// segment; the payload and off_new loads of all warps are in flight at once
+// and only the running-count update is ordered (warp by warp, a short chain in
+// shared memory), so the ranks are the index-order ones.
+constexpr int kEdgeThreads = 512;
 template <typename Real>
-__global__ void __launch_bounds__(32)
+__global__ void __launch_bounds__(kEdgeThreads)
 edge_place(ShockDev S, const int64_t *__restrict__ off_new, const int *ng, const void *recv_l, const void *recv_r,
            int xcap, const Real *gx0, const Real *gvx0, const Real *gvy0, const Real *gvz0, const int32_t *gd0,
            const Real *gx1, const Real *gvx1, const Real *gvy1, const Real *gvz1, const int32_t *gd1,
            int32_t *lcnt, Real *ox, Real *ovx, Real *ovy, Real *ovz, int *W) {
+  constexpr int NW = kEdgeThreads / 32;
   __shared__ int run[kEdgeBins];
   __shared__ int tot[kEdgeBins];
-  const int side = blockIdx.x, lane = threadIdx.x;
-  for (int b = lane; b < kEdgeBins; b += 32) { run[b] = 0; tot[b] = 0; }
-  __syncwarp();
+  __shared__ int turn;
+  volatile int *vrun = run, *vturn = &turn;
+  const int side = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int b = tid; b < kEdgeBins; b += kEdgeThreads) { run[b] = 0; tot[b] = 0; }
+  if (tid == 0) turn = 0;
+  __syncthreads();
   // segment order for this side: side 0: ghosts(0), immigrants(0); side 1: immigrants(1), ghosts(1)
   for (int pass = side == 0 ? 1 : 0; pass < 2; ++pass) {    // side 1: pass 0 counts, pass 1 places
     for (int seg = 0; seg < 2; ++seg) {
@@ -495,8 +504,8 @@ edge_place(ShockDev S, const int64_t *__restrict__ off_new, const int *ng, const
         px = X.x; pvx = X.vx; pvy = X.vy; pvz = X.vz; pd = X.dest;
         shift = S.cbase;                      // immigrants carry global destinations
       }
-      for (int k0 = 0; k0 < cnt; k0 += 32) {
-        const int k = k0 + lane;
+      for (int k0 = 0; k0 < cnt; k0 += kEdgeThreads) {
+        const int k = k0 + tid;
         int d = -1;
         if (k < cnt) {
           const int dd = pd[k];
@@ -506,29 +515,48 @@ edge_place(ShockDev S, const int64_t *__restrict__ off_new, const int *ng, const
         if (bin >= kEdgeBins) W[2] = 1;     // out of reach of the edge bins: gather this step
         const bool ok = bin >= 0 && bin < kEdgeBins;
         const unsigned peers = __match_any_sync(0xffffffffu, ok ? bin : -1 - lane);
-        const int leader = __ffs(peers) - 1;
+        const bool leader = __ffs(peers) - 1 == lane;
         if (side == 1 && pass == 0) {
-          if (ok && leader == lane) tot[bin] += __popc(peers);
+          if (ok && leader) atomicAdd(&tot[bin], __popc(peers));
         } else {
-          int rank = 0;
-          if (ok) rank = run[bin] + __popc(peers & ((1u << lane) - 1u));
-          __syncwarp();
-          if (ok && leader == lane) run[bin] += __popc(peers);
+          Real a = Real(0), bx = Real(0), by = Real(0), bz = Real(0);
+          int64_t base = 0;
           if (ok) {
-            const int64_t pos = side == 0 ? off_new[d] + rank : off_new[d + 1] - tot[bin] + rank;
-            ox[pos] = px[k]; ovx[pos] = pvx[k]; ovy[pos] = pvy[k]; ovz[pos] = pvz[k];
+            a = px[k]; bx = pvx[k]; by = pvy[k]; bz = pvz[k];
+            base = side == 0 ? off_new[d] : off_new[d + 1] - tot[bin];
           }
+          // this warp's turn: every earlier warp of the round has counted
+          if (__any_sync(0xffffffffu, ok)) {
+            if (lane == 0)
+              while (*vturn != warp) {}
+            __syncwarp();
+            int rank = 0;
+            if (ok) rank = vrun[bin] + __popc(peers & ((1u << lane) - 1u));
+            __syncwarp();
+            if (ok && leader) vrun[bin] = rank + __popc(peers);
+            __threadfence_block();
+            __syncwarp();
+            if (ok) {
+              const int64_t pos = base + rank;
+              ox[pos] = a; ovx[pos] = bx; ovy[pos] = by; ovz[pos] = bz;
+            }
+          } else if (lane == 0) {
+            while (*vturn != warp) {}
+          }
+          if (lane == 0) *vturn = warp + 1;
         }
-        __syncwarp();
+        __syncthreads();
+        if (tid == 0) turn = 0;
+        __syncthreads();
       }
     }
   }
   if (side == 0)
-    for (int b = lane; b < kEdgeBins; b += 32) lcnt[b] = run[b];
+    for (int b = tid; b < kEdgeBins; b += kEdgeThreads) lcnt[b] = run[b];
 }
 
 // ---- A2 by scatter: interior particles ----
-// Tile t = transport tile t (kTile consecutive particles of the cell-sorted
+// Tile t = transport tile t (tile_of(NG) consecutive particles of the cell-sorted
 // source array).  A particle's stable position in its destination cell d is
 // off_new[d] + lcnt[d] + (particles of earlier tiles with destination d) +
 // (its rank among the tile's particles with destination d, in index order).
@@ -537,7 +565,7 @@ edge_place(ShockDev S, const int64_t *__restrict__ off_new, const int *ng, const
 // any earlier one, can reach it); transport_kernel stored each tile's
 // destination histogram over [dmin, dmin + kHist).
 constexpr int kScatterThreads = 512;
-template <typename Real>
+template <typename Real, int NG>
 __global__ void __launch_bounds__(kScatterThreads)
 scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *__restrict__ off_new,
                const Real *__restrict__ x, const Real *__restrict__ vx, const Real *__restrict__ vy,
@@ -545,7 +573,9 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
                const int2 *__restrict__ tile_meta, const int32_t *__restrict__ lcnt, const int *W,
                Real *__restrict__ ox, Real *__restrict__ ovx, Real *__restrict__ ovy, Real *__restrict__ ovz) {
   constexpr int NW = kScatterThreads / 32, PARTS = kScatterThreads / kHist;
-  constexpr int CHUNK = kTile / NW, ROUNDS = CHUNK / 32;   // each warp: CHUNK consecutive particles
+  constexpr int TILE = tile_of(NG);
+  constexpr int CHUNK = TILE / NW, ROUNDS = CHUNK / 32;   // each warp: CHUNK consecutive particles
+  static_assert(ROUNDS >= 1, "tile smaller than the CTA");
   __shared__ int s_part[PARTS][kHist];
   __shared__ int s_wc[NW][kHist];                          // per-warp counts, then running positions
   __shared__ int64_t s_off[kHist];                         // off_new of the tile's destination cells
@@ -554,7 +584,7 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
   const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (W[2]) return;                                   // gather fallback this step
   const int64_t n = off_old[S.C];
-  const int64_t i_begin = (int64_t)t * kTile;
+  const int64_t i_begin = (int64_t)t * TILE;
   if (i_begin >= n) return;
   const int dmin = tile_meta[t].x;
   if (dmin == INT32_MAX) return;                     // no local destination in this tile
@@ -630,7 +660,7 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
     __syncwarp();
   }
   // ---- data movement: independent 4-round batches of loads, then the stores ----
-  constexpr int BATCH = 4;
+  constexpr int BATCH = ROUNDS < 4 ? ROUNDS : 4;
 #pragma unroll
   for (int r0 = 0; r0 < ROUNDS; r0 += BATCH) {
     Real a[BATCH], bx[BATCH], by[BATCH], bz[BATCH];
@@ -1056,7 +1086,11 @@ inline trmcr_status shock_init(trmcr_ctx *c, const trmcr_cells *cc, int *max_cel
       if (dalloc(c, &s.gv[k][j], c->rs * s.cap_g)) return TRMCR_ENOMEM;
   }
   if (const char *se = getenv("TRMCR_SHOCK_SCATTER")) s.scatter = atoi(se) != 0;
-  s.ntiles = (int)((c->cap + kTile - 1) / kTile);
+  // transport / sort tiles: 4096 particles for large problems, 1024 below 8 M
+  // particles (more CTAs in flight: C4 has 1 M)
+  s.tile_ng = c->cap >= (int64_t)8 << 20 ? kTransportGroups : 1;
+  if (const char *te = getenv("TRMCR_TILE_NG")) s.tile_ng = atoi(te) == 1 ? 1 : kTransportGroups;
+  s.ntiles = (int)((c->cap + tile_of(s.tile_ng) - 1) / tile_of(s.tile_ng));
   if (s.scatter && (dalloc(c, &s.d_tileH, sizeof(int32_t) * kHist * (size_t)std::max(s.ntiles, 1)) ||
                     dalloc(c, &s.d_tile_meta, sizeof(int2) * (size_t)std::max(s.ntiles, 1)) ||
                     dalloc(c, &s.d_lcnt, sizeof(int32_t) * kEdgeBins)))
@@ -1112,11 +1146,12 @@ trmcr_status shock_begin(trmcr_ctx *c) {
     if (auto e = check_launch(c, "ghost_gen", TRMCR_K_GHOST_GEN)) return e;
   }
   {
-    const int per_block = kTile;
+    const int per_block = tile_of(s.tile_ng);
     const unsigned blocks = (unsigned)((c->cap + per_block - 1) / per_block);
     prof_begin(c, TRMCR_K_TRANSPORT);
     const bool sc = s.scatter && c->wlay.n_cap > 0 && !c->wlay.v_smem;
-    transport_kernel<Real><<<blocks, kTransportThreads, 0, c->stream>>>(
+    auto *tk = s.tile_ng == 1 ? transport_kernel<Real, 1> : transport_kernel<Real, kTransportGroups>;
+    tk<<<blocks, kTransportThreads, 0, c->stream>>>(
         d, s.d_off[cur], (Real *)c->x[cur], (const Real *)c->v[cur][0], s.d_dest, s.d_counts, s.d_W, s.d_acct,
         sc ? s.d_tileH : nullptr, sc ? s.d_tile_meta : nullptr);
     if (auto e = check_launch(c, "transport_kernel", TRMCR_K_TRANSPORT)) return e;
@@ -1168,13 +1203,14 @@ trmcr_status shock_finish(trmcr_ctx *c) {
   G.scatter = s.scatter && use_warp && !c->wlay.v_smem;
   if (G.scatter) {
     prof_begin(c, TRMCR_K_SCATTER);
-    edge_place<Real><<<2, 32, 0, c->stream>>>(
+    edge_place<Real><<<2, kEdgeThreads, 0, c->stream>>>(
         d, s.d_off[nxt], s.d_ng, G.recv[0], G.recv[1], s.xcap, (const Real *)s.gx[0], (const Real *)s.gv[0][0],
         (const Real *)s.gv[0][1], (const Real *)s.gv[0][2], s.d_gdest[0], (const Real *)s.gx[1],
         (const Real *)s.gv[1][0], (const Real *)s.gv[1][1], (const Real *)s.gv[1][2], s.d_gdest[1], s.d_lcnt, ox,
         ovx, ovy, ovz, s.d_W);
     if (auto e = check_launch(c, "edge_place")) return e;
-    scatter_sorted<Real><<<std::max(s.ntiles, 1), kScatterThreads, 0, c->stream>>>(
+    auto *sk = s.tile_ng == 1 ? scatter_sorted<Real, 1> : scatter_sorted<Real, kTransportGroups>;
+    sk<<<std::max(s.ntiles, 1), kScatterThreads, 0, c->stream>>>(
         d, s.d_off[cur], s.d_off[nxt], (const Real *)c->x[cur], (const Real *)c->v[cur][0],
         (const Real *)c->v[cur][1], (const Real *)c->v[cur][2], s.d_dest, s.d_tileH, s.d_tile_meta, s.d_lcnt,
         s.d_W, ox, ovx, ovy, ovz);

@@ -232,8 +232,8 @@ def test_fp32_conservation(api):
 
 
 # ---------------------------------------------------------------- shock
-def _shock_pair(orc, api, mach, ncells, ntot, steps, eps, dtype, seed=1, x_min=-4.0, x_max=4.0):
-    setup = synth.shock_setup(mach=mach, ncells=ncells, n_total=ntot, x_min=x_min, x_max=x_max)
+def _shock_pair(orc, api, mach, ncells, ntot, steps, eps, dtype, seed=1, x_min=-4.0, x_max=4.0, cfl=0.5):
+    setup = synth.shock_setup(mach=mach, ncells=ncells, n_total=ntot, x_min=x_min, x_max=x_max, cfl=cfl)
     x, vx, vy, vz = synth.shock_particles(setup, seed=seed)
     inv = setup["ncells"] / (setup["x_max"] - setup["x_min"])
     cell = np.clip(np.floor((x - setup["x_min"]) * inv), 0, ncells - 1)
@@ -265,6 +265,25 @@ def test_shock_fp64_parity(orc, api, monkeypatch, scatter):
         _cmp_v(g, o.vx[:n], o.vy[:n], o.vz[:n], o.offsets)
         _cmp_stats(sim.stats(), o.stats)
     assert o.counts[0] > 0     # reservoir particles entered
+
+
+def test_shock_fp64_parity_dense_edges(orc, api):
+    """20000 particles per cell, CFL 4: each step's entering reservoir
+    particles span several edge_place rounds (512 per round, ranks chained
+    warp by warp) and scatter_sorted looks back over many tiles."""
+    setup, sim, o = _shock_pair(orc, api, 3.0, 40, 800_000, 0, 0.2, np.float64, cfl=4.0)
+    for s in range(6):
+        sim.step(1)
+        o.step(1)
+        assert not sim.sort_info()["gathered"]
+        g = sim.particles()
+        np.testing.assert_array_equal(g["offsets"], o.offsets)
+        n = o.n
+        np.testing.assert_allclose(g["x"], o.x[:n], rtol=0, atol=1e-12)
+        _cmp_v(g, o.vx[:n], o.vy[:n], o.vz[:n], o.offsets)
+        _cmp_stats(sim.stats(), o.stats)
+    print("entered per step (L, R):", o.counts[0] / 6, o.counts[1] / 6)
+    assert o.counts[0] / 6 > 2 * 512     # left-edge segment: more than two rounds per step
 
 
 def test_shock_fp32_mass_accounting_and_sort(api):
