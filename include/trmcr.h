@@ -112,6 +112,12 @@ typedef struct {
                                 requires adaptive = 0                                  */
   int32_t wb_max;            /* TRMC-WB m_max: final samples with longer trees are
                                 resampled from the local Maxwellian                   */
+  int32_t sigma_update;      /* majorant variant (remark after Alg 4.4):
+                                0 = Sigma' frozen for the step (default); 1 = raised
+                                to sigma_ij after every proposal, in the canonical
+                                order (level ascending, index ascending, RAD attempts
+                                in order).  tau (and mu) still come from the pre-step
+                                Sigma'; the stats row reports the pre-step Sigma'.     */
 } trmcr_kernel;
 
 /* Per-cell statistics row (doubles), trmcr_stats(): */

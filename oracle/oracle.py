@@ -43,7 +43,7 @@ class Params(C.Structure):
         ("m_init", C.c_int32), ("m_cap", C.c_int32), ("indicator", C.c_int32),
         ("delta1", C.c_double), ("delta2", C.c_double), ("eps", C.c_double), ("dt", C.c_double),
         ("seed", C.c_uint64), ("literal", C.c_int32), ("pad", C.c_int32), ("alpha", C.c_double),
-        ("wb", C.c_int32), ("wb_max", C.c_int32),
+        ("wb", C.c_int32), ("wb_max", C.c_int32), ("sigma_update", C.c_int32),
     ]
 
 
@@ -203,11 +203,12 @@ class Config:
     alpha: float = 1.0          # VHS exponent (model = VHS)
     wb: int = 0                 # TRMC-WB length: 0 off, 1 min (def:2), 2 mean (def:3), 3 level (def:1)
     wb_max: int = 0             # TRMC-WB threshold m_max
+    sigma_update: int = 0       # 1: majorant raised after each collision
 
     def c(self) -> Params:
         return Params(self.model, self.adaptive, self.m_fixed, self.m_init, self.m_cap,
                       self.indicator, self.delta1, self.delta2, self.eps, self.dt, self.seed,
-                      self.literal, 0, self.alpha, self.wb, self.wb_max)
+                      self.literal, 0, self.alpha, self.wb, self.wb_max, self.sigma_update)
 
 
 class HomogeneousState:

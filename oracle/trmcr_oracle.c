@@ -282,18 +282,20 @@ typedef struct {
  * xi Sigma < sigma_ij with sigma_ij = K|q|^alpha and Sigma = K (2 dv)^alpha
  * (K cancels [R7]); Sigma here is Sigma' = (2 dv)^alpha.  HS (alpha = 1)
  * compares |q| itself; Maxwell (alpha = 0) always accepts.  A violation is
- * a pair above the bound (|q|^alpha > Sigma'). */
-static int vhs_accept(const orc_params *P, double sigma, double q, double xa, double *viol) {
-  if (P->model == ORC_HARD_SPHERE) {
-    if (q > sigma) *viol += 1;
-    return xa * sigma < q;
-  }
-  if (P->model == ORC_VHS) {
-    const double qa = pow(q, P->alpha);
-    if (qa > sigma) *viol += 1;
-    return xa * sigma < qa;
-  }
-  return 1;
+ * a pair above the bound (|q|^alpha > Sigma').
+ * Majorant variant (remark after Alg 4.4: "update the upper
+ * bound itself, after each collision"): with sigma_update the bound becomes
+ * max(Sigma, sigma_ij) after every proposal, in the canonical order (level
+ * ascending, collision index ascending; RAD attempts in order) [R33]. */
+static int vhs_accept(const orc_params *P, double *sigma, double q, double xa, double *viol) {
+  double s;
+  if (P->model == ORC_HARD_SPHERE) s = q;
+  else if (P->model == ORC_VHS) s = pow(q, P->alpha);
+  else return 1;
+  if (s > *sigma) *viol += 1;
+  const int acc = xa * *sigma < s;
+  if (P->sigma_update && s > *sigma) *sigma = s;
+  return acc;
 }
 
 static void tree_collision(cellctx *X, int r, int d, int64_t j, int64_t si, int64_t sk) {
@@ -308,7 +310,7 @@ static void tree_collision(cellctx *X, int r, int d, int64_t j, int64_t si, int6
   if (X->P->model != ORC_MAXWELL) {
     double qx = vi[0] - vk[0], qy = vi[1] - vk[1], qz = vi[2] - vk[2];
     double q = sqrt(qx * qx + qy * qy + qz * qz);
-    acc = vhs_accept(X->P, X->sigma, q, xa, &X->st->violations);
+    acc = vhs_accept(X->P, &X->sigma, q, xa, &X->st->violations);
   }
   if (acc) {
     orc_collide_pair(vi, vk, xi1, xi2);
@@ -519,7 +521,7 @@ static void lit_sample(literal_t *T, int lev, int64_t *oi, int64_t *oj) {
   if (X->P->model != ORC_MAXWELL) {
     double qx = vi[0] - vj[0], qy = vi[1] - vj[1], qz = vi[2] - vj[2];
     double q = sqrt(qx * qx + qy * qy + qz * qz);
-    acc = vhs_accept(X->P, X->sigma, q, xa, &X->st->violations);
+    acc = vhs_accept(X->P, &X->sigma, q, xa, &X->st->violations);
   }
   if (acc) {
     orc_collide_pair(vi, vj, xi1, xi2);

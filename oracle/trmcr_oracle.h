@@ -39,6 +39,8 @@ typedef struct {
                        /* 1 + min, 2 eq.(def:3) 1 + mean, 3 eq.(def:1) = level  */
   int32_t wb_max;      /* m_max of Alg 4.6: final samples with L > wb_max are   */
                        /* resampled from the local Maxwellian                   */
+  int32_t sigma_update;/* 1: majorant raised to sigma_ij after each proposal    */
+                       /* (remark after Alg 4.4); 0: frozen per step */
 } orc_params;
 
 /* Length of one collision tree given as the path list of Alg 4.5:

@@ -59,7 +59,7 @@ class _Kernel(C.Structure):
     _fields_ = [("model", C.c_int32), ("adaptive", C.c_int32), ("m_fixed", C.c_int32),
                 ("m_init", C.c_int32), ("m_cap", C.c_int32), ("indicator", C.c_int32),
                 ("delta1", C.c_double), ("delta2", C.c_double), ("seed", C.c_uint64), ("alpha", C.c_double),
-                ("wb", C.c_int32), ("wb_max", C.c_int32)]
+                ("wb", C.c_int32), ("wb_max", C.c_int32), ("sigma_update", C.c_int32)]
 
 
 _lib = None
@@ -141,7 +141,7 @@ class Simulation:
                  x=None, model: int = HARD_SPHERE, adaptive: bool = False, m_fixed: int = 64,
                  m_init: int = 2, m_cap: int = 4096, delta1: float = 0.005, delta2: float = 0.01,
                  indicator: int = IND_PXX, seed: int = 1, cell_base: int = 0, capacity: int = 0,
-                 stream=None, alpha: float = 1.0, wb: int = 0, wb_max: int = 0):
+                 stream=None, alpha: float = 1.0, wb: int = 0, wb_max: int = 0, sigma_update: bool = False):
         L = lib()
         self._keep = [vx, vy, vz, x]
         pvx, host, dt_code = _ptr(vx)
@@ -170,7 +170,7 @@ class Simulation:
                            self.neighbors)
             self.geometry = SHOCK_1D
         kern = _Kernel(model, int(bool(adaptive)), m_fixed, m_init, m_cap, indicator, delta1, delta2,
-                       seed & 0xFFFFFFFFFFFFFFFF, float(alpha), int(wb), int(wb_max))
+                       seed & 0xFFFFFFFFFFFFFFFF, float(alpha), int(wb), int(wb_max), int(bool(sigma_update)))
         if stream is None:
             try:
                 import torch

@@ -41,6 +41,7 @@ struct StepParams {
   int model, adaptive, m_fixed, m_cap, indicator, log_on;
   double alpha;            // VHS exponent
   int wb, wb_max;          // TRMC-WB definition (0 off) and threshold
+  int sigma_update;        // majorant raised after each proposal [R33]
   double delta1, delta2, dt, eps;
   uint32_t k0, k1, step, cell_base;
   int shock;               // rho_c = n w / dx when 1, else 1
@@ -78,6 +79,7 @@ constexpr int kSplitPre = 72;
 // Scalars shared by the CTA.
 struct CellShared {
   double ux, uy, uz, S0, sigma, p, mu, S_est, E1;
+  double sig_run;             // running majorant (sigma_update) [R33]
   double sums[8];
   int n, m, m_cur, m_next, d, top, lo, hi, r, planned, flag, done;
   int64_t rem;
@@ -150,6 +152,25 @@ __device__ __forceinline__ void load3(const Real *a, const Real *b, const Real *
   x = a[i]; y = b[i]; z = c[i];
 }
 
+// (qx^2 + qy^2) + qz^2 and |q|, every product and sum rounded (no FMA
+// contraction: the oracle's order, and the same value wherever it is taken;
+// for a two-particle cell |q| and Sigma' = 2 max|v - u| tie mathematically)
+__device__ __forceinline__ double sq3(double qx, double qy, double qz) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(qx, qx), __dmul_rn(qy, qy)), __dmul_rn(qz, qz));
+}
+__device__ __forceinline__ double qnorm(double qx, double qy, double qz) { return sqrt(sq3(qx, qy, qz)); }
+__device__ __forceinline__ float qnorm(float qx, float qy, float qz) {
+  return sqrtf(__fadd_rn(__fadd_rn(__fmul_rn(qx, qx), __fmul_rn(qy, qy)), __fmul_rn(qz, qz)));
+}
+
+// sigma_ij / K of the pair in slots (si, sk): |q| (HS) or |q|^alpha (VHS).
+// Used by the majorant variant [R33] to find a level's largest proposal.
+template <typename Real>
+__device__ __forceinline__ Real pair_sigma(const StepParams &P, const CellBuf<Real> &B, uint32_t si, uint32_t sk) {
+  const Real q = qnorm(B.vx[si] - B.vx[sk], B.vy[si] - B.vy[sk], B.vz[si] - B.vz[sk]);
+  return P.model == TRMCR_VHS ? RealOps<Real>::pow_(q, (Real)P.alpha) : q;
+}
+
 // One (dummy) collision of a tree node (A6).  Returns accepted.
 template <typename Real>
 __device__ __forceinline__ int tree_collision(const StepParams &P, const RngKey &K, CellBuf<Real> &B,
@@ -167,8 +188,7 @@ __device__ __forceinline__ int tree_collision(const StepParams &P, const RngKey 
   }
   const Real ax = B.vx[si], ay = B.vy[si], az = B.vz[si];
   const Real bx = B.vx[sk], by = B.vy[sk], bz = B.vz[sk];
-  const Real qx = ax - bx, qy = ay - by, qz = az - bz;
-  const Real q = O::sqrt_(qx * qx + qy * qy + qz * qz);
+  const Real q = qnorm(ax - bx, ay - by, az - bz);
   int acc = 1;
   if (P.model == TRMCR_HARD_SPHERE) {       // accept iff xi Sigma' < |q|  [R7]
     viol += (q > sigma) ? 1u : 0u;
@@ -339,6 +359,20 @@ __device__ void plan_counts(Team &T, const RngKey &K, CellBuf<Real> &B, CellShar
   }
 }
 
+// Decision-log record of one collision (parity mode).
+__device__ __forceinline__ void log_collision(const StepParams &P, const RngKey &K, trmcr_coll_rec *log,
+                                              unsigned long long *log_count, int64_t log_cap, int r, int d,
+                                              int j, int ok, uint32_t s0, uint32_t s1) {
+  if (!P.log_on) return;
+  const unsigned long long at = atomicAdd(log_count, 1ull);
+  if ((int64_t)at < log_cap) {
+    trmcr_coll_rec rec;
+    rec.cell = (int32_t)K.cell; rec.attempt = r; rec.level = d; rec.accepted = ok;
+    rec.j = j; rec.slot_i = s0; rec.slot_k = s1;
+    log[at] = rec;
+  }
+}
+
 // Bottom-up slot resolution + execution (A5, A6): level d's demand on pool p
 // has rank base_p + (in-level rank); side-0 demands (type p) precede side-1
 // demands (type d-1-p).  Pool p's t-th demand takes output pi_p(t) of level
@@ -473,15 +507,42 @@ __device__ void plan_execute(Team &T, const StepParams &P, const RngKey &K, Cell
       B.cslot[2 * (Sd + j)] = slot[0];
       B.cslot[2 * (Sd + j) + 1] = slot[1];
       if (P.wb) B.wlen[Sd + j] = wb_combine(P.wb, d, ln[0], ln[1]);
-      const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, slot[0], slot[1], viol);
-      acc += ok;
-      if (P.log_on) {
-        const unsigned long long at = atomicAdd(log_count, 1ull);
-        if ((int64_t)at < log_cap) {
-          trmcr_coll_rec rec;
-          rec.cell = (int32_t)K.cell; rec.attempt = r; rec.level = d; rec.accepted = ok;
-          rec.j = j; rec.slot_i = slot[0]; rec.slot_k = slot[1];
-          log[at] = rec;
+      if (!P.sigma_update) {
+        const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, slot[0], slot[1], viol);
+        acc += ok;
+        log_collision(P, K, log, log_count, log_cap, r, d, j, ok, slot[0], slot[1]);
+      }
+    }
+    if (P.sigma_update) {
+      // majorant raised after each proposal [R33]: the level's collisions are
+      // independent, so if none of them exceeds the running bound they all
+      // run in parallel with it; otherwise one thread runs the level in
+      // canonical order, raising the bound as it goes (rare: violations)
+      T.sync();
+      double mx = 0.0;
+      for (int j = tid; j < Cd; j += T.size())
+        mx = fmax(mx, (double)pair_sigma<Real>(P, B, B.cslot[2 * (Sd + j)], B.cslot[2 * (Sd + j) + 1]));
+      mx = T.max(mx, B.red);
+      if (mx > (double)sigma) {
+        if (tid == 0) {
+          for (int j = 0; j < Cd; ++j) {
+            const uint32_t s0 = B.cslot[2 * (Sd + j)], s1 = B.cslot[2 * (Sd + j) + 1];
+            const Real sj = pair_sigma<Real>(P, B, s0, s1);
+            const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, s0, s1, viol);
+            acc += ok;
+            log_collision(P, K, log, log_count, log_cap, r, d, j, ok, s0, s1);
+            if (sj > sigma) sigma = sj;
+          }
+          sh.sig_run = (double)sigma;
+        }
+        T.sync();
+        sigma = (Real)sh.sig_run;
+      } else {
+        for (int j = tid; j < Cd; j += T.size()) {
+          const uint32_t s0 = B.cslot[2 * (Sd + j)], s1 = B.cslot[2 * (Sd + j) + 1];
+          const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, s0, s1, viol);
+          acc += ok;
+          log_collision(P, K, log, log_count, log_cap, r, d, j, ok, s0, s1);
         }
       }
     }
@@ -660,7 +721,7 @@ __device__ int process_cell(Team &T, const StepParams &P, CellBuf<Real> &B, Cell
   for (int i = tid; i < n; i += T.size()) {
     const double x = B.vx[i], y = B.vy[i], z = B.vz[i];
     const double dx = x - ux, dy = y - uy, dz = z - uz;
-    const double r2 = dx * dx + dy * dy + dz * dz;
+    const double r2 = sq3(dx, dy, dz);         // the oracle's rounding (Sigma' ties |q|)
     dv2 = fmax(dv2, r2);
     c3[0] += dx * dx;
     const double v2 = x * x + y * y + z * z;
@@ -689,6 +750,7 @@ __device__ int process_cell(Team &T, const StepParams &P, CellBuf<Real> &B, Cell
       sh.sigma = 0.0;
       sh.mu = rho_c;
     }
+    sh.sig_run = sh.sigma;
     const double x = sh.mu * P.dt / P.eps;
     sh.p = exp(-x);
     sh.m = m0; sh.m_cur = m0; sh.flag = kOk;
@@ -708,12 +770,11 @@ __device__ int process_cell(Team &T, const StepParams &P, CellBuf<Real> &B, Cell
   if (sh.flag != kOk) return sh.flag;
   Perm pi0;
   pi0.init(K(kPerm, 0, 0, 0), (uint32_t)n);
-  const Real sigma = (Real)sh.sigma;
   // ---- A5/A6: attempt 0 ----
   plan_counts<Real>(T, K, B, sh);
   PHASE_ADD(1, t_ph);   // plan counts
   if (sh.flag != kOk) return sh.flag;
-  plan_execute<Real>(T, P, K, B, sh, pi0, sigma, log, log_count, log_cap);
+  plan_execute<Real>(T, P, K, B, sh, pi0, (Real)sh.sig_run, log, log_count, log_cap);
   PHASE_ADD(2, t_ph);   // plan execute
   if (tid == 0) {
     sh.Ltot = sh.L;
@@ -747,7 +808,7 @@ __device__ int process_cell(Team &T, const StepParams &P, CellBuf<Real> &B, Cell
       if (sh.done) break;
       plan_counts<Real>(T, K, B, sh);
       if (sh.flag != kOk) return sh.flag;
-      plan_execute<Real>(T, P, K, B, sh, pi0, sigma, log, log_count, log_cap);
+      plan_execute<Real>(T, P, K, B, sh, pi0, (Real)sh.sig_run, log, log_count, log_cap);
       PHASE_ADD(4, t_ph);   // RAD retries
       if (tid == 0) { sh.Ltot += sh.L; sh.nT -= sh.L; }
       T.sync();

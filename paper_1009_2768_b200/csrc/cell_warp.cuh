@@ -19,6 +19,7 @@ constexpr int kWarpCellWarps = 4;
 // Per-warp scalars (in the warp's slab, lane 0 writes, __syncwarp publishes).
 struct WarpShared {
   double ux, uy, uz, S0, sigma, p, mu, S_est, E1, c2;
+  double sig_run;             // running majorant (sigma_update) [R33]
   uint4 pk;                // key of pi0
   double sums[4];
   int n, m_cur, m_next, d, top, lo, hi, r, flag, done;
@@ -230,21 +231,42 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
       }
       B.cslot16[2 * (Sd + j)] = (uint16_t)slot[0];
       B.cslot16[2 * (Sd + j) + 1] = (uint16_t)slot[1];
-      const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, slot[0], slot[1], viol);
-      acc += ok;
-      if (P.log_on) {
-        const unsigned long long at = atomicAdd(log_count, 1ull);
-        if ((int64_t)at < log_cap) {
-          trmcr_coll_rec rec;
-          rec.cell = (int32_t)K.cell; rec.attempt = r; rec.level = d; rec.accepted = ok;
-          rec.j = j; rec.slot_i = slot[0]; rec.slot_k = slot[1];
-          log[at] = rec;
+      if (!(WB && P.sigma_update)) {
+        const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, slot[0], slot[1], viol);
+        acc += ok;
+        log_collision(P, K, log, log_count, log_cap, r, d, j, ok, slot[0], slot[1]);
+      }
+    }
+    if (WB && P.sigma_update) {              // majorant raised after each proposal [R33]
+      __syncwarp();
+      double mx = 0.0;
+      for (int j = lane; j < Cd; j += 32)
+        mx = fmax(mx, (double)pair_sigma<Real>(P, B, B.cslot16[2 * (Sd + j)], B.cslot16[2 * (Sd + j) + 1]));
+      mx = warp_max(mx);
+      if (mx > (double)sigma) {              // a violation in this level: canonical order, one lane
+        if (lane == 0)
+          for (int j = 0; j < Cd; ++j) {
+            const uint32_t s0 = B.cslot16[2 * (Sd + j)], s1 = B.cslot16[2 * (Sd + j) + 1];
+            const Real sj = pair_sigma<Real>(P, B, s0, s1);
+            const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, s0, s1, viol);
+            acc += ok;
+            log_collision(P, K, log, log_count, log_cap, r, d, j, ok, s0, s1);
+            if (sj > sigma) sigma = sj;
+          }
+        sigma = __shfl_sync(0xffffffffu, sigma, 0);
+      } else {
+        for (int j = lane; j < Cd; j += 32) {
+          const uint32_t s0 = B.cslot16[2 * (Sd + j)], s1 = B.cslot16[2 * (Sd + j) + 1];
+          const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, s0, s1, viol);
+          acc += ok;
+          log_collision(P, K, log, log_count, log_cap, r, d, j, ok, s0, s1);
         }
       }
     }
     prop += (unsigned long long)Cd;
     __syncwarp();
   }
+  if (WB && P.sigma_update && lane == 0) sh.sig_run = (double)sigma;
   acc = __reduce_add_sync(0xffffffffu, acc);
   viol = __reduce_add_sync(0xffffffffu, viol);
   if (lane == 0) { sh.prop += prop; sh.acc += acc; sh.viol += viol; }
@@ -415,7 +437,7 @@ __device__ int wphase_begin(const StepParams &P, CellBuf<Real> &B, WarpShared &s
     for (int i = lane; i < n; i += 32) {
       const double x = B.vx[i], y = B.vy[i], z = B.vz[i];
       const double dx = x - ux, dy = y - uy, dz = z - uz;
-      const double r2 = dx * dx + dy * dy + dz * dz;
+      const double r2 = sq3(dx, dy, dz);       // the oracle's rounding (Sigma' ties |q|)
       dv2 = fmax(dv2, r2);
       c0 += dx * dx;
       const double v2 = x * x + y * y + z * z;
@@ -438,6 +460,7 @@ __device__ int wphase_begin(const StepParams &P, CellBuf<Real> &B, WarpShared &s
     if (P.model == TRMCR_HARD_SPHERE) { sh.sigma = 2.0 * sqrt(dv2); sh.mu = rho_c * sh.sigma; }
     else if (P.model == TRMCR_VHS) { sh.sigma = vhs_majorant(dv2, P.alpha); sh.mu = rho_c * sh.sigma; }
     else { sh.sigma = 0.0; sh.mu = rho_c; }
+    sh.sig_run = sh.sigma;
     sh.p = exp(-(sh.mu * P.dt / P.eps));
     sh.m_cur = m0; sh.flag = kOk;
     sh.prop = 0; sh.acc = 0; sh.viol = 0;
@@ -467,7 +490,7 @@ __device__ int wphase_attempt(const StepParams &P, CellBuf<Real> &B, WarpShared 
   const int attempt = sh.r;
   wplan_counts<Real>(K, B, sh);
   if (sh.flag != kOk) return sh.flag;
-  wplan_execute<Real, WB>(P, K, B, sh, pi0, (Real)sh.sigma, log, log_count, log_cap);
+  wplan_execute<Real, WB>(P, K, B, sh, pi0, (Real)sh.sig_run, log, log_count, log_cap);
   if (lane == 0) {
     if (attempt == 0) {
       sh.Ltot = sh.L;

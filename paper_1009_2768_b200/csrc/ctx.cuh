@@ -257,6 +257,11 @@ inline void prof_event(trmcr_ctx *c) {
   }
   cudaEventRecord(c->ev_pool[c->ev_used++], c->stream);
 }
+// The warp / lock-step kernels come in two instantiations: the plain one and
+// the extended one (TRMC-WB and/or the majorant-update variant), so that the
+// default path carries none of their code.
+inline bool ext_variant(const trmcr_ctx *c) { return c->P.wb != 0 || c->P.sigma_update != 0; }
+
 inline void prof_begin(trmcr_ctx *c, int kid) {
   if (!c->prof || !((c->prof_mask >> kid) & 1u)) return;
   c->ev_kid.push_back(kid);

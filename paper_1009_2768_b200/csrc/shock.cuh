@@ -1219,7 +1219,7 @@ trmcr_status shock_finish(trmcr_ctx *c) {
   if (use_warp) {
     CUDA_TRY(c, cudaMemsetAsync(c->d_defer_count, 0, sizeof(int), c->stream));
     prof_begin(c, TRMCR_K_SHOCK_WARP);
-    const bool wb = c->P.wb != 0;
+    const bool wb = ext_variant(c);
     if (G.scatter && c->lock_grid > 0)
       (wb ? shock_collide_lock<Real, true> : shock_collide_lock<Real, false>)
           <<<c->lock_grid, kLockWarps * 32, c->lock_smem, c->stream>>>(

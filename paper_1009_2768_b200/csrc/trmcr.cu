@@ -318,7 +318,7 @@ trmcr_status launch_collide(trmcr_ctx *c) {
     const int *l1c = fast ? c->d_defer_count : nullptr, *l1 = fast ? c->d_defer_list : nullptr;
     if (use_warp) {
       prof_begin(c, TRMCR_K_CELL_WARP);
-      launch_k(c, c->P.wb ? cell_step_warp<Real, true> : cell_step_warp<Real, false>, idle ? 1 : c->warp_grid, c->warp_wpc * 32, (size_t)c->warp_smem, c->P,
+      launch_k(c, ext_variant(c) ? cell_step_warp<Real, true> : cell_step_warp<Real, false>, idle ? 1 : c->warp_grid, c->warp_wpc * 32, (size_t)c->warp_smem, c->P,
                c->wlay, (const int64_t *)c->d_offsets, c->ncells, l1c, l1, vx, vy, vz, c->d_mstate, c->d_stats,
                c->d_defer2_count, c->d_defer2_list, Q);
       if (auto s = check_launch(c, "cell_step_warp", TRMCR_K_CELL_WARP)) return s;
@@ -551,7 +551,7 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
   StepParams &P = c->P;
   P.model = kk->model; P.alpha = kk->model == TRMCR_VHS ? kk->alpha : (kk->model == TRMCR_HARD_SPHERE ? 1.0 : 0.0);
   P.adaptive = kk->adaptive;
-  P.wb = kk->wb; P.wb_max = kk->wb_max; P.m_fixed = kk->m_fixed; P.m_cap = kk->m_cap;
+  P.wb = kk->wb; P.wb_max = kk->wb_max; P.sigma_update = kk->sigma_update != 0 && kk->model != TRMCR_MAXWELL; P.m_fixed = kk->m_fixed; P.m_cap = kk->m_cap;
   P.indicator = kk->indicator; P.log_on = 0;
   P.delta1 = kk->delta1; P.delta2 = kk->delta2; P.dt = dt; P.eps = eps;
   P.k0 = (uint32_t)kk->seed; P.k1 = (uint32_t)(kk->seed >> 32);
@@ -738,7 +738,7 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
       const char *le = getenv("TRMCR_SHOCK_LOCKSTEP");
       const size_t lsm = slab * kLockWarps;
       if (c->geometry == TRMCR_SHOCK_1D && !v_smem && !(le && atoi(le) == 0) && lsm <= (size_t)smem_max - 1024) {
-        const bool wbk = c->P.wb != 0;
+        const bool wbk = ext_variant(c);
         const void *lf = c->dtype == TRMCR_F64
                              ? (wbk ? (const void *)shock_collide_lock<double, true> : (const void *)shock_collide_lock<double, false>)
                              : (wbk ? (const void *)shock_collide_lock<float, true> : (const void *)shock_collide_lock<float, false>);

@@ -87,6 +87,21 @@ def ragged_cells(ncells: int, max_ppc: int, seed: int = 1, dtype=np.float64, emp
     return v[0].astype(dtype), v[1].astype(dtype), v[2].astype(dtype), offsets
 
 
+def cold_beams(ncells: int, ppc: int, seed: int = 1, speed: float = 2.0, spread: float = 0.05,
+               dtype=np.float64):
+    """Counter-streaming cold beams (a two-Maxwellian mix far from equilibrium,
+    T_beam = spread^2): per cell, even particles at +speed, odd at -speed along
+    x.  Collisions between beam and scattered particles push relative speeds
+    above the pre-step bound 2 max|v - u|, so majorant violations
+    actually occur.  Offsets: ncells equal cells of ppc particles."""
+    g = _rng(seed, 8)
+    n = ncells * ppc
+    v = g.standard_normal((3, n)) * spread
+    v[0] += np.where(np.arange(n) % 2 == 0, speed, -speed)
+    offsets = np.arange(ncells + 1, dtype=np.int64) * ppc
+    return v[0].astype(dtype), v[1].astype(dtype), v[2].astype(dtype), offsets
+
+
 def rankine_hugoniot(mach: float, gamma: float = 5.0 / 3.0, rho_L: float = 1.0, T_L: float = 1.0):
     """Upstream/downstream states of a normal shock, p = rho T.
 

@@ -125,6 +125,27 @@ def test_homogeneous_fp64_trmc_wb(orc, api, monkeypatch, wb, warp_path):
     _parity(orc, api, v[:3], v[3], 3, model=1, m_fixed=10, wb=wb, wb_max=2, eps=2.0, dt=0.3, seed=17)
 
 
+@pytest.mark.parametrize("model,alpha,warp_path", [(1, 1.0, "1"), (2, 0.5, "1"), (1, 1.0, "0")])
+def test_majorant_update_fp64(orc, api, monkeypatch, model, alpha, warp_path):
+    """Majorant raised after each collision [R33] on counter-streaming
+    cold beams (violations happen): levels with a violation run in canonical
+    order on one lane / thread, the others in parallel; RAD attempts carry the
+    raised bound.  Every decision, counter and velocity as the oracle's."""
+    monkeypatch.setenv("TRMCR_WARP_PATH", warp_path)
+    v = synth.cold_beams(24, 400, seed=4)
+    sim, o = _parity(orc, api, v[:3], v[3], 1, model=model, alpha=alpha, adaptive=1, m_init=4, m_cap=64,
+                     eps=0.15, dt=0.1, seed=5, sigma_update=1)
+    assert o.stats["violations"].sum() > 10 and o.stats["attempts"].max() > 1
+
+
+def test_majorant_update_giant_cell_fp64(orc, api):
+    """The same variant on the grid-cooperative kernel (one 40,000-particle cell)."""
+    v = synth.cold_beams(1, 40_000, seed=22)
+    _, o = _parity(orc, api, v[:3], v[3], 1, log_cap=400_000, model=1, m_fixed=24, eps=0.3, dt=0.1, seed=23,
+                   sigma_update=1)
+    assert o.stats["violations"][0] > 0
+
+
 def test_giant_cell_parallel_ranks_fp64(orc, api):
     """One 60,000-particle cell (global-memory CTA path) whose low levels hold
     thousands of collisions: in-level ranks computed by all warps (chunk

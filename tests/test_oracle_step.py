@@ -331,3 +331,73 @@ def test_trmc_wb_limits_nesting_conservation(orc):
         maxw[wb] = st.stats["maxw"]
     assert np.all(maxw[1] <= maxw[2]) and np.all(maxw[2] <= maxw[3])
     assert maxw[3].sum() > maxw[1].sum() > ref.stats["maxw"].sum()
+
+
+def _canon(log):
+    order = np.lexsort((log["j"], log["level"], log["attempt"], log["cell"]))
+    return log[order]
+
+
+@pytest.mark.parametrize("model,alpha", [(1, 1.0), (2, 0.5)])
+def test_majorant_update_variant(orc, model, alpha):
+    """Majorant raised after each collision (remark after Alg 4.4) [R33].
+    Both runs draw the same keyed uniforms, so up to a cell's first differing
+    decision the two trajectories are identical; the running bound only grows
+    (Sigma_run >= Sigma'), hence that first difference must be a pair the frozen
+    bound accepts and the raised bound rejects.  A cell with no violation under
+    the frozen bound never raises it: bit-identical.  Maxwell molecules have no
+    bound: unaffected.  Counter-streaming cold beams make violations happen."""
+    vx, vy, vz, off = synth.cold_beams(24, 400, seed=4)
+    kw = dict(model=model, alpha=alpha, adaptive=1, m_init=4, m_cap=64, eps=0.15, dt=0.1, seed=5)
+    fr = orc.HomogeneousState(orc.Config(**kw), vx, vy, vz, off, log_cap=400_000)
+    up = orc.HomogeneousState(orc.Config(sigma_update=1, **kw), vx, vy, vz, off, log_cap=400_000)
+    fr.step(1)
+    up.step(1)
+    lf, lu = _canon(fr.collisions()), _canon(up.collisions())
+    assert fr.log_n <= 400_000 and up.log_n <= 400_000
+    np.testing.assert_array_equal(fr.stats["proposals"], up.stats["proposals"])   # plans do not depend on Sigma
+    np.testing.assert_array_equal(fr.stats["sigma"], up.stats["sigma"])           # reported: the pre-step bound
+    raised = 0
+    for c in range(len(off) - 1):
+        a, b = lf[lf["cell"] == c], lu[lu["cell"] == c]
+        vf, vu = fr.stats["violations"][c], up.stats["violations"][c]
+        assert (vf > 0) == (vu > 0)            # the first violation happens in both runs
+        sl = slice(off[c], off[c + 1])
+        if vf == 0:
+            assert np.array_equal(a, b)
+            for k in ("vx", "vy", "vz"):
+                np.testing.assert_array_equal(getattr(fr, k)[sl], getattr(up, k)[sl])
+            continue
+        # identical plans (same attempt/level/j) as long as the decisions agree
+        m = min(len(a), len(b))
+        diff = np.nonzero((a["accepted"][:m] != b["accepted"][:m]) | (a["slot_i"][:m] != b["slot_i"][:m]))[0]
+        if len(diff):
+            k = diff[0]
+            assert a["slot_i"][k] == b["slot_i"][k] and a["slot_k"][k] == b["slot_k"][k]
+            assert a["accepted"][k] == 1 and b["accepted"][k] == 0
+            raised += 1
+    assert raised >= 3
+    assert up.stats["accepted"].sum() < fr.stats["accepted"].sum()
+    # conservation is unaffected (collisions stay elastic, Maxwellian exact)
+    for st in (up,):
+        for c in range(len(off) - 1):
+            sl = slice(off[c], off[c + 1])
+            V0 = np.stack([vx[sl], vy[sl], vz[sl]], 1)
+            V1 = np.stack([st.vx[sl], st.vy[sl], st.vz[sl]], 1)
+            np.testing.assert_allclose(V1.sum(0), V0.sum(0), atol=1e-10 * np.abs(V0).sum())
+            assert abs((V1 ** 2).sum() - (V0 ** 2).sum()) <= 1e-10 * (V0 ** 2).sum()
+
+
+def test_majorant_update_maxwell_and_no_violation_identity(orc):
+    """Maxwell molecules (no acceptance test) and cells without any violation
+    (thermal data: every pair below 2 max|v - u|) are unchanged by the variant."""
+    vx, vy, vz, off = synth.ragged_cells(16, 300, seed=6)
+    for model in (0, 1):
+        kw = dict(model=model, m_fixed=8, eps=0.5, dt=0.2, seed=7)
+        a = orc.HomogeneousState(orc.Config(**kw), vx, vy, vz, off)
+        b = orc.HomogeneousState(orc.Config(sigma_update=1, **kw), vx, vy, vz, off)
+        a.step(2)
+        b.step(2)
+        assert a.stats["violations"].sum() == 0
+        for k in ("vx", "vy", "vz"):
+            np.testing.assert_array_equal(getattr(a, k), getattr(b, k))
