@@ -118,6 +118,13 @@ typedef struct {
                                 order (level ascending, index ascending, RAD attempts
                                 in order).  tau (and mu) still come from the pre-step
                                 Sigma'; the stats row reports the pre-step Sigma'.     */
+  int32_t literal;           /* 1: the paper's own layout instead of the level-synchronous
+                                plan: Alg 4.3/4.4 literally (recursive builds, stored
+                                siblings, one sequential keyed stream per cell), one
+                                thread per cell (for measuring the
+                                LS reformulation).  Homogeneous cells, fixed m <= 128,
+                                no RAD / TRMC-WB; TRMCR_ECAPACITY if a cell's trees
+                                need more f_0 particles than it holds.                */
 } trmcr_kernel;
 
 /* Per-cell statistics row (doubles), trmcr_stats(): */
@@ -234,7 +241,7 @@ int64_t trmcr_launch_count(const trmcr_ctx *ctx);
 enum {
   TRMCR_K_CELL_SMEM = 0, TRMCR_K_CELL_GMEM, TRMCR_K_MOMENTS, TRMCR_K_GHOST_COUNT, TRMCR_K_GHOST_GEN,
   TRMCR_K_TRANSPORT, TRMCR_K_SCAN, TRMCR_K_SHOCK_SMEM, TRMCR_K_SHOCK_GMEM, TRMCR_K_THERMAL,
-  TRMCR_K_CELL_WARP, TRMCR_K_SHOCK_WARP, TRMCR_K_SCATTER, TRMCR_NKERNELS
+  TRMCR_K_CELL_WARP, TRMCR_K_SHOCK_WARP, TRMCR_K_SCATTER, TRMCR_K_LITERAL, TRMCR_NKERNELS
 };
 trmcr_status trmcr_set_profiling(trmcr_ctx *ctx, int32_t on);
 /* Same, restricted to the kernel ids whose bit is set in `mask` (fewer events

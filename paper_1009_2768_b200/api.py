@@ -29,7 +29,8 @@ GLOBAL_FIELDS = ["n", "px", "py", "pz", "energy", "nPxx", "proposals", "accepted
 MOMENT_FIELDS = ["n", "rho", "ux", "uy", "uz", "T", "E", "p", "Pxx", "M4", "M4c", "m_max"]
 KERNELS = ["cell_step_smem", "cell_step_gmem", "moments_kernel", "ghost_count", "ghost_gen",
            "transport_kernel", "scan_offsets", "shock_collide_smem", "shock_collide_gmem",
-           "thermal_warp_kernel", "cell_step_warp", "shock_collide_warp", "scatter_sorted"]
+           "thermal_warp_kernel", "cell_step_warp", "shock_collide_warp", "scatter_sorted",
+           "literal_step_kernel"]
 STATS_DTYPE = np.dtype([(f, "<f8") for f in STAT_FIELDS])
 COLL_DTYPE = np.dtype([("cell", "<i4"), ("attempt", "<i4"), ("level", "<i4"), ("accepted", "<i4"),
                        ("j", "<i8"), ("slot_i", "<i8"), ("slot_k", "<i8")])
@@ -59,7 +60,8 @@ class _Kernel(C.Structure):
     _fields_ = [("model", C.c_int32), ("adaptive", C.c_int32), ("m_fixed", C.c_int32),
                 ("m_init", C.c_int32), ("m_cap", C.c_int32), ("indicator", C.c_int32),
                 ("delta1", C.c_double), ("delta2", C.c_double), ("seed", C.c_uint64), ("alpha", C.c_double),
-                ("wb", C.c_int32), ("wb_max", C.c_int32), ("sigma_update", C.c_int32)]
+                ("wb", C.c_int32), ("wb_max", C.c_int32), ("sigma_update", C.c_int32),
+                ("literal", C.c_int32)]
 
 
 _lib = None
@@ -141,7 +143,8 @@ class Simulation:
                  x=None, model: int = HARD_SPHERE, adaptive: bool = False, m_fixed: int = 64,
                  m_init: int = 2, m_cap: int = 4096, delta1: float = 0.005, delta2: float = 0.01,
                  indicator: int = IND_PXX, seed: int = 1, cell_base: int = 0, capacity: int = 0,
-                 stream=None, alpha: float = 1.0, wb: int = 0, wb_max: int = 0, sigma_update: bool = False):
+                 stream=None, alpha: float = 1.0, wb: int = 0, wb_max: int = 0, sigma_update: bool = False,
+                 literal: bool = False):
         L = lib()
         self._keep = [vx, vy, vz, x]
         pvx, host, dt_code = _ptr(vx)
@@ -170,7 +173,8 @@ class Simulation:
                            self.neighbors)
             self.geometry = SHOCK_1D
         kern = _Kernel(model, int(bool(adaptive)), m_fixed, m_init, m_cap, indicator, delta1, delta2,
-                       seed & 0xFFFFFFFFFFFFFFFF, float(alpha), int(wb), int(wb_max), int(bool(sigma_update)))
+                       seed & 0xFFFFFFFFFFFFFFFF, float(alpha), int(wb), int(wb_max), int(bool(sigma_update)),
+                       int(bool(literal)))
         if stream is None:
             try:
                 import torch

@@ -171,23 +171,16 @@ __device__ __forceinline__ Real pair_sigma(const StepParams &P, const CellBuf<Re
   return P.model == TRMCR_VHS ? RealOps<Real>::pow_(q, (Real)P.alpha) : q;
 }
 
-// One (dummy) collision of a tree node (A6).  Returns accepted.
+// A6 on the pair in slots (si, sk) of (vx, vy, vz) with the collision's
+// uniforms: acceptance against the bound (dummy collision when rejected),
+// then v' = G +- (|q|/2) sigma.  Returns accepted.
 template <typename Real>
-__device__ __forceinline__ int tree_collision(const StepParams &P, const RngKey &K, CellBuf<Real> &B,
-                                              Real sigma, int r, int d, uint32_t j, uint32_t si,
-                                              uint32_t sk, unsigned &viol) {
+__device__ __forceinline__ int pair_collide(const StepParams &P, Real *vx, Real *vy, Real *vz, Real sigma,
+                                            Real xa, Real xi1, Real xi2, uint32_t si, uint32_t sk,
+                                            unsigned &viol) {
   using O = RealOps<Real>;
-  Real xa, xi1, xi2;
-  if constexpr (sizeof(Real) == 8) {
-    const uint4 w = K(kColl, r, d, j);
-    const uint4 w2 = K(kColl2, r, d, j);
-    xa = u53(w.x, w.y); xi1 = u53(w.z, w.w); xi2 = u53(w2.x, w2.y);
-  } else {
-    const uint4 w = K(kColl, r, d, j);
-    xa = u24(w.x); xi1 = u24(w.y); xi2 = u24(w.z);
-  }
-  const Real ax = B.vx[si], ay = B.vy[si], az = B.vz[si];
-  const Real bx = B.vx[sk], by = B.vy[sk], bz = B.vz[sk];
+  const Real ax = vx[si], ay = vy[si], az = vz[si];
+  const Real bx = vx[sk], by = vy[sk], bz = vz[sk];
   const Real q = qnorm(ax - bx, ay - by, az - bz);
   int acc = 1;
   if (P.model == TRMCR_HARD_SPHERE) {       // accept iff xi Sigma' < |q|  [R7]
@@ -206,10 +199,28 @@ __device__ __forceinline__ int tree_collision(const StepParams &P, const RngKey 
     const Real h = Real(0.5) * q;
     const Real hx = h * (s * cp), hy = h * (s * sp), hz = h * c;
     const Real gx = Real(0.5) * (ax + bx), gy = Real(0.5) * (ay + by), gz = Real(0.5) * (az + bz);
-    B.vx[si] = gx + hx; B.vy[si] = gy + hy; B.vz[si] = gz + hz;
-    B.vx[sk] = gx - hx; B.vy[sk] = gy - hy; B.vz[sk] = gz - hz;
+    vx[si] = gx + hx; vy[si] = gy + hy; vz[si] = gz + hz;
+    vx[sk] = gx - hx; vy[sk] = gy - hy; vz[sk] = gz - hz;
   }
   return acc;
+}
+
+// One (dummy) collision of a tree node (A6) with its keyed draws
+// (COLL, attempt, level, j).  Returns accepted.
+template <typename Real>
+__device__ __forceinline__ int tree_collision(const StepParams &P, const RngKey &K, CellBuf<Real> &B,
+                                              Real sigma, int r, int d, uint32_t j, uint32_t si,
+                                              uint32_t sk, unsigned &viol) {
+  Real xa, xi1, xi2;
+  if constexpr (sizeof(Real) == 8) {
+    const uint4 w = K(kColl, r, d, j);
+    const uint4 w2 = K(kColl2, r, d, j);
+    xa = u53(w.x, w.y); xi1 = u53(w.z, w.w); xi2 = u53(w2.x, w2.y);
+  } else {
+    const uint4 w = K(kColl, r, d, j);
+    xa = u24(w.x); xi1 = u24(w.y); xi2 = u24(w.z);
+  }
+  return pair_collide<Real>(P, B.vx, B.vy, B.vz, sigma, xa, xi1, xi2, si, sk, viol);
 }
 
 // Draw three standard normals for Theta slot `slot` (Box-Muller).

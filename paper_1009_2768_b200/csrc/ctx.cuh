@@ -186,6 +186,9 @@ struct trmcr_ctx {
   int lock_grid = 0, lock_smem = 0;   // shock lock-step collision kernel (0: free-running warps)   // L2 prefetch of each warp's next cell (TRMCR_THERMAL_PREFETCH=0 disables)
   int fast_ok = 1, fast_pending = 0, fast_grid = 0, smem_grid = 0, last_defer = -1, last_ovf = -1;
   unsigned char *d_scratch = nullptr;
+  int literal = 0;                         // Alg 4.3/4.4 literally, one thread per cell (literal.cuh)
+  uint8_t *d_lit_flag = nullptr;           // [cap] Theta membership (literal mode)
+  double *d_lit_g = nullptr;               // [3 cap] Gaussian draws of Theta (literal mode)
   int giant_min = 0, giant_grid = 0;       // cells with n >= giant_min: cell_step_giant (0: off)
   trmcr::CellShared *d_gsh = nullptr;
   double *d_gpart = nullptr;
@@ -284,6 +287,7 @@ inline trmcr_status sync_check(trmcr_ctx *c) {
   if (err & 2) return fail(c, TRMCR_ECAPACITY, "particle capacity exceeded (shock inflow)");
   if (err & 16) return fail(c, TRMCR_ECUDA, "internal fault: tree index out of range");
   if (err & 32) return fail(c, TRMCR_ECAPACITY, "a particle crossed more than one slab in a step");
+  if (err & 64) return fail(c, TRMCR_ECAPACITY, "literal mode: the trees needed more f_0 particles than the cell holds");
   return TRMCR_OK;
 }
 

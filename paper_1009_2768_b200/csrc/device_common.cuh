@@ -10,7 +10,7 @@ namespace trmcr {
 // Purposes of the Philox counter word 1.
 enum : uint32_t {
   kSplit = 1, kType = 2, kPerm = 3, kColl = 4, kColl2 = 5,
-  kMaxw = 6, kMaxw2 = 7, kResv = 8, kResv2 = 9
+  kMaxw = 6, kMaxw2 = 7, kResv = 8, kResv2 = 9, kLiteral = 10
 };
 
 // Philox4x32-10: 10 rounds of the (0xD2511F53, 0xCD9E8D57) multiply-xor

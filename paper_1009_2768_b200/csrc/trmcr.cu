@@ -21,6 +21,7 @@
 #include "ctx.cuh"
 #include "shock.cuh"
 #include "thermal.cuh"
+#include "literal.cuh"
 
 using namespace trmcr;
 
@@ -283,6 +284,13 @@ trmcr_status launch_collide(trmcr_ctx *c) {
   c->d_defer_count = cnt; c->d_ovf_count = cnt + 1; c->d_defer2_count = cnt + 2;
   QueueArgs Q{c->d_ovf_count, c->d_ovf_list, c->d_err, c->d_log, c->d_log_count, c->log_cap, nxt};
   c->P.step = c->step;
+  if (c->literal) {   // the paper's layout: Alg 4.3/4.4 literally, one thread per cell
+    if (c->ncells == 0) return TRMCR_OK;
+    prof_begin(c, TRMCR_K_LITERAL);
+    literal_step_kernel<Real><<<(c->ncells + kLitThreads - 1) / kLitThreads, kLitThreads, 0, c->stream>>>(
+        c->P, c->d_offsets, c->ncells, vx, vy, vz, c->d_stats, c->d_lit_flag, c->d_lit_g);
+    return check_launch(c, "literal_step_kernel", TRMCR_K_LITERAL);
+  }
   if (c->ncells > 0) {
     // Counts of the last observed step (pinned async copy, read when ready):
     // the thermal fast path runs while it handles most cells (re-tried every
@@ -354,7 +362,9 @@ trmcr_status launch_collide(trmcr_ctx *c) {
         if (auto s = check_launch(c, "cell_step_giant", TRMCR_K_CELL_GMEM)) return s;
       }
     }
-    if (!c->fast_pending && (c->step % 8 == 0 || !c->fast_ok)) {
+    // sample the counts only of a step that ran the thermal kernel (otherwise
+    // nothing was deferred to count, and a zero would read as "all thermal")
+    if (!c->fast_pending && fast && (c->step % 8 == 0 || !c->fast_ok)) {
       CUDA_TRY(c, cudaMemcpyAsync(c->h_defer, c->d_defer_count, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
       CUDA_TRY(c, cudaEventRecord(c->ev_defer, c->stream));
       c->fast_pending = 1;
@@ -495,6 +505,9 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
   if (kk->wb < 0 || kk->wb > 3 || (kk->wb && (kk->adaptive || kk->wb_max < 0)))
     return fail(nullptr, TRMCR_EINVAL, "TRMC-WB: wb in 0..3, wb_max >= 0, not with adaptive (RAD)");
   if (kk->indicator != TRMCR_IND_PXX && kk->indicator != TRMCR_IND_M4) return fail(nullptr, TRMCR_EINVAL, "bad indicator");
+  if (kk->literal && (kk->adaptive || kk->wb || cc->geometry != TRMCR_HOMOGENEOUS || kk->m_fixed < 1 ||
+                      kk->m_fixed > kLitMaxLevel))
+    return fail(nullptr, TRMCR_EINVAL, "literal mode: homogeneous cells, fixed 1 <= m <= 128, no RAD, no TRMC-WB");
   if (kk->adaptive) {
     if (kk->m_init < 1 || kk->m_cap < kk->m_init || kk->m_cap > 16384)
       return fail(nullptr, TRMCR_EINVAL, "need 1 <= m_init <= m_cap <= 16384");
@@ -581,6 +594,9 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
       dalloc(c, &c->d_defer2_list, sizeof(int) * std::max(c->ncells, 1)) || dalloc(c, &c->d_gm_partial, sizeof(double) * 10 * kGmBlocks) ||
       dalloc(c, &c->d_gm_done, sizeof(unsigned)) || dalloc(c, &c->d_defer_list, sizeof(int) * std::max(c->ncells, 1)))
     return bail(TRMCR_ENOMEM);
+  c->literal = kk->literal != 0;
+  if (c->literal && (dalloc(c, &c->d_lit_flag, (size_t)c->cap) || dalloc(c, &c->d_lit_g, sizeof(double) * 3 * (size_t)c->cap)))
+    return bail(TRMCR_ENOMEM);
   c->d_defer_count = c->d_cnt; c->d_ovf_count = c->d_cnt + 1; c->d_defer2_count = c->d_cnt + 2;
   if (const char *pe = getenv("TRMCR_PDL")) c->use_pdl = atoi(pe) != 0;
   if (cudaMallocHost(&c->h_defer, 2 * sizeof(int)) != cudaSuccess ||
@@ -645,7 +661,7 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
   const char *kcap_env = getenv("TRMCR_SMEM_KCAP");
   for (;;) {
     const int K_cap = kcap_env ? atoi(kcap_env)
-                               : (c->geometry == TRMCR_SHOCK_1D ? std::max(256, n_cap / 4) : std::max(256, n_cap / 2));
+                               : (c->geometry == TRMCR_SHOCK_1D ? std::max(256, n_cap / 4) : std::max(256, n_cap));
     c->lay.build(n_cap, K_cap, L_cap, c->rs, c->P.wb != 0);
     if ((int)c->lay.total <= budget || n_cap <= 32) break;
     n_cap = std::max(32, n_cap / 2 / 32 * 32);
@@ -703,7 +719,10 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
     const bool want = !(wenv && atoi(wenv) == 0);
     int wn = c->geometry == TRMCR_SHOCK_1D ? std::max(64, (2 * max_cell + 31) / 32 * 32)
                                            : std::max(32, (max_cell + 31) / 32 * 32);
-    const int wK = c->geometry == TRMCR_SHOCK_1D ? std::max(256, std::min(512, wn / 4)) : std::max(256, wn / 2);
+    // tree capacity: collisions per cell ~ n x / 2 untruncated, and deep trees
+    // (x > 1 at fixed m) reach ~0.75 n: homogeneous slabs hold n collisions
+    // (a shock cell's slab is sized for twice its particles, its trees are shallow)
+    const int wK = c->geometry == TRMCR_SHOCK_1D ? std::max(256, std::min(512, wn / 4)) : std::max(256, wn);
     // shock: velocities are gathered into the output buffer and processed in
     // place (a deferred cell is re-gathered); homogeneous: staged in the slab
     // (in place would corrupt the input of a deferred cell)
@@ -756,16 +775,16 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
   }
 
   // ---- global-memory plan scratch for large / overflowing cells ----
-  int big = 0;   // cells that will not fit the smem path at all
-  if (c->geometry == TRMCR_HOMOGENEOUS)
-    for (int i = 0; i < c->ncells; ++i) big += (c->h_offsets[i + 1] - c->h_offsets[i]) > c->lay.n_cap;
   const int n_cap_g = c->geometry == TRMCR_HOMOGENEOUS
                           ? std::max(max_cell, 32)
                           : (int)std::min<int64_t>(c->cap, std::max(16 * max_cell, 65536));
   const int L_cap_g = std::max(kk->adaptive ? kk->m_cap : kk->m_fixed, 64) + 1;
   const int64_t K_cap_g = std::min<int64_t>(4LL * n_cap_g + 65536, 0x3FFFFFFFLL);
   const size_t stride = gmem_stride(n_cap_g, K_cap_g, L_cap_g, c->P.wb != 0);
-  int G = std::max(1, std::min(c->ncells, big > 0 ? 148 : (c->geometry == TRMCR_SHOCK_1D ? 16 : 8)));
+  // CTAs of the global-memory kernel: one per SM (2 per SM when the scratch is
+  // small) - many cells can overflow the shared-memory plans at once (deep
+  // trees); bounded by 4 GB of scratch
+  int G = std::max(1, std::min(c->ncells, (double)stride * 296 <= 1e9 ? 296 : 148));
   while (G > 1 && (double)G * stride > 4e9) G /= 2;
   c->G = G;
   if (dalloc(c, &c->d_scratch, stride * G)) return bail(TRMCR_ENOMEM);

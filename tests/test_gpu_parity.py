@@ -81,7 +81,6 @@ def _parity(orc, api, v, offsets, steps, log_cap=400_000, **kw):
     ocfg = orc.Config(**{k: kw[k] for k in kw if k in orc.Config.__dataclass_fields__})
     o = orc.HomogeneousState(ocfg, v[0], v[1], v[2], offsets, log_cap=log_cap)
     gkw = dict(kw)
-    gkw.pop("literal", None)
     sim = api.Simulation(_dev(v[0]), _dev(v[1]), _dev(v[2]), offsets=offsets, **gkw)
     sim.set_log(log_cap)
     for s in range(steps):
@@ -144,6 +143,24 @@ def test_majorant_update_giant_cell_fp64(orc, api):
     _, o = _parity(orc, api, v[:3], v[3], 1, log_cap=400_000, model=1, m_fixed=24, eps=0.3, dt=0.1, seed=23,
                    sigma_update=1)
     assert o.stats["violations"][0] > 0
+
+
+@pytest.mark.parametrize("model,kw", [(1, dict(eps=0.5, dt=0.1)), (0, dict(eps=1.0, dt=0.2)),
+                                      (2, dict(alpha=0.6, eps=0.5, dt=0.1))])
+def test_literal_layout_fp64(orc, api, model, kw):
+    """The paper's own layout (Alg 4.3/4.4 literally: recursive builds, stored
+    siblings, one sequential keyed stream per cell; one GPU thread per cell)
+    against the oracle's literal mode: every counter and velocity."""
+    # the literal algorithm has no finite-N guard: Maxwell cells stay large
+    v = synth.ragged_cells(40, 400, seed=24) if model else synth.uniform_cells(32, 300, seed=24)
+    _parity(orc, api, v[:3], v[3], 3, model=model, m_fixed=12, seed=25, literal=1, **kw)
+
+
+def test_literal_layout_majorant_update_fp64(orc, api):
+    v = synth.cold_beams(12, 300, seed=26)
+    _, o = _parity(orc, api, v[:3], v[3], 1, model=1, m_fixed=32, eps=0.15, dt=0.1, seed=27, literal=1,
+                   sigma_update=1)
+    assert o.stats["violations"].sum() > 0
 
 
 def test_giant_cell_parallel_ranks_fp64(orc, api):

@@ -1,0 +1,65 @@
+"""Which kernels run: the scheduling decisions of trmcr_step on a B200.
+
+Results do not depend on these decisions (parity tests cover every path);
+these tests guard the launch choices that set the speed."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _sim(api, v, **kw):
+    T = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(device="cuda", dtype=torch.float32)
+    return api.Simulation(T(v[0]), T(v[1]), T(v[2]), offsets=v[3], **kw)
+
+
+def test_collisional_cells_run_the_warp_kernel():
+    """Cells outside the fluid regime must go to the warp-per-cell kernel every
+    step (a step that skipped the thermal kernel once read its deferral count
+    as zero and sent every cell to a single CTA)."""
+    from paper_1009_2768_b200 import api
+    sim = _sim(api, synth.uniform_cells(2000, 500, seed=1, dtype=np.float32), model=api.HARD_SPHERE,
+               m_fixed=16, eps=1.0, dt=0.1, seed=1)
+    sim.step(4)
+    sim.set_profiling(True)
+    sim.step(12)
+    kt = sim.kernel_times()
+    sim.set_profiling(False)
+    assert kt.get("cell_step_warp", (0, 0))[1] == 12, kt
+    assert kt["cell_step_smem"][0] / 12 < 0.05, kt          # ms per step: nothing left for the CTA kernel
+
+
+def test_deep_trees_stay_parallel():
+    """Deep trees (x ~ 2.7 at m = 16: ~0.75 n collisions per cell) fit the warp
+    slabs; the global-memory kernel is not the bottleneck."""
+    from paper_1009_2768_b200 import api
+    sim = _sim(api, synth.uniform_cells(4096, 1024, seed=2, dtype=np.float32), model=api.HARD_SPHERE,
+               m_fixed=16, eps=0.3, dt=0.1, seed=2)
+    sim.step(3)
+    sim.set_profiling(True)
+    sim.step(5)
+    kt = sim.kernel_times()
+    sim.set_profiling(False)
+    assert kt["cell_step_warp"][1] == 5, kt
+    assert kt.get("cell_step_gmem", (0.0, 1))[0] / 5 < 0.1, kt
+
+
+def test_fluid_cells_run_the_thermal_kernel_only():
+    from paper_1009_2768_b200 import api
+    sim = _sim(api, synth.uniform_cells(2048, 1024, seed=3, dtype=np.float32), model=api.HARD_SPHERE,
+               m_fixed=64, eps=0.01, dt=0.1, seed=3)
+    sim.step(20)
+    sim.set_profiling(True)
+    sim.step(8)
+    kt = sim.kernel_times()
+    sim.set_profiling(False)
+    assert kt["thermal_warp_kernel"][1] == 8 and "cell_step_warp" not in kt, kt
