@@ -784,7 +784,8 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
   // CTAs of the global-memory kernel: one per SM (2 per SM when the scratch is
   // small) - many cells can overflow the shared-memory plans at once (deep
   // trees); bounded by 4 GB of scratch
-  int G = std::max(1, std::min(c->ncells, (double)stride * 296 <= 1e9 ? 296 : 148));
+  int G = c->geometry == TRMCR_SHOCK_1D ? 16 : ((double)stride * 296 <= 1e9 ? 296 : 148);   // shock: rare
+  G = std::max(1, std::min(c->ncells, G));
   while (G > 1 && (double)G * stride > 4e9) G /= 2;
   c->G = G;
   if (dalloc(c, &c->d_scratch, stride * G)) return bail(TRMCR_ENOMEM);
