@@ -25,7 +25,6 @@ for r in gpurun_out/ev/*.ncu-rep; do
   b=${r%.ncu-rep}
   python tools/ncu_summary.py $r > $b.summary.json 2>/dev/null
   ncu -i $r --page source --csv --print-source cuda,sass > $b.src.csv 2>/dev/null && python tools/ncu_hot.py $b.src.csv 40 > $b.hot.txt; rm -f $b.src.csv
-  ncu -i $r --page raw --csv > $b.raw.csv 2>/dev/null
 done
-rm -f gpurun_out/ev/c5_scatter_sorted.ncu-rep gpurun_out/ev/c5_transport_kernel.ncu-rep gpurun_out/ev/c4_shock_collide_lock.ncu-rep
+rm -f gpurun_out/ev/*.ncu-rep   # the copy-back limit is 64 MiB: summaries only
 du -sh gpurun_out/ev; ls -la gpurun_out/ev
