@@ -292,9 +292,12 @@ static int vhs_accept(const orc_params *P, double *sigma, double q, double xa, d
   if (P->model == ORC_HARD_SPHERE) s = q;
   else if (P->model == ORC_VHS) s = pow(q, P->alpha);
   else return 1;
-  if (s > *sigma) *viol += 1;
+  /* a violation exceeds the bound by more than its rounding [R35]: in a
+   * two-particle cell |q| = 2 max|v - u| exactly */
+  const int over = s > *sigma * (1.0 + 0x1p-40);
+  if (over) *viol += 1;
   const int acc = xa * *sigma < s;
-  if (P->sigma_update && s > *sigma) *sigma = s;
+  if (P->sigma_update && over) *sigma = s;
   return acc;
 }
 

@@ -68,7 +68,7 @@ typedef struct {
   double thermalised;  /* |Theta|                                                */
   double proposals;    /* collisions (tree nodes), dummy included                */
   double accepted;     /* accepted collisions                                   */
-  double violations;   /* pairs with |q| > Sigma'                                */
+  double violations;   /* pairs with |q|^a > Sigma' (1 + 2^-40) [R35]           */
   double maxw;         /* Maxwellian samples drawn                               */
 } orc_cell_stats;
 

@@ -163,6 +163,13 @@ __device__ __forceinline__ float qnorm(float qx, float qy, float qz) {
   return sqrtf(__fadd_rn(__fadd_rn(__fmul_rn(qx, qx), __fmul_rn(qy, qy)), __fmul_rn(qz, qz)));
 }
 
+// A violation is a pair above the bound by more than the bound's own rounding
+// [R35]: in a two-particle cell |q| = 2 max|v - u| exactly, and a strict
+// comparison would count rounding noise.  Sigma' (1 + 2^-40) in fp64,
+// Sigma' (1 + 2^-20) in fp32 (the oracle: the fp64 one).
+__device__ __forceinline__ double viol_bound(double s) { return s * (1.0 + 0x1p-40); }
+__device__ __forceinline__ float viol_bound(float s) { return s * (1.0f + 0x1p-20f); }
+
 // sigma_ij / K of the pair in slots (si, sk): |q| (HS) or |q|^alpha (VHS).
 // Used by the majorant variant [R33] to find a level's largest proposal.
 template <typename Real>
@@ -184,11 +191,11 @@ __device__ __forceinline__ int pair_collide(const StepParams &P, Real *vx, Real 
   const Real q = qnorm(ax - bx, ay - by, az - bz);
   int acc = 1;
   if (P.model == TRMCR_HARD_SPHERE) {       // accept iff xi Sigma' < |q|  [R7]
-    viol += (q > sigma) ? 1u : 0u;
+    viol += (q > viol_bound(sigma)) ? 1u : 0u;
     acc = (xa * sigma < q);
   } else if (P.model == TRMCR_VHS) {        // accept iff xi Sigma' < |q|^alpha (sec. VHS)
     const Real qa = O::pow_(q, (Real)P.alpha);
-    viol += (qa > sigma) ? 1u : 0u;
+    viol += (qa > viol_bound(sigma)) ? 1u : 0u;
     acc = (xa * sigma < qa);
   }
   if (acc) {
@@ -534,7 +541,7 @@ __device__ void plan_execute(Team &T, const StepParams &P, const RngKey &K, Cell
       for (int j = tid; j < Cd; j += T.size())
         mx = fmax(mx, (double)pair_sigma<Real>(P, B, B.cslot[2 * (Sd + j)], B.cslot[2 * (Sd + j) + 1]));
       mx = T.max(mx, B.red);
-      if (mx > (double)sigma) {
+      if (mx > (double)viol_bound(sigma)) {
         if (tid == 0) {
           for (int j = 0; j < Cd; ++j) {
             const uint32_t s0 = B.cslot[2 * (Sd + j)], s1 = B.cslot[2 * (Sd + j) + 1];
@@ -542,7 +549,7 @@ __device__ void plan_execute(Team &T, const StepParams &P, const RngKey &K, Cell
             const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, s0, s1, viol);
             acc += ok;
             log_collision(P, K, log, log_count, log_cap, r, d, j, ok, s0, s1);
-            if (sj > sigma) sigma = sj;
+            if (sj > viol_bound(sigma)) sigma = sj;
           }
           sh.sig_run = (double)sigma;
         }

@@ -243,7 +243,7 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
       for (int j = lane; j < Cd; j += 32)
         mx = fmax(mx, (double)pair_sigma<Real>(P, B, B.cslot16[2 * (Sd + j)], B.cslot16[2 * (Sd + j) + 1]));
       mx = warp_max(mx);
-      if (mx > (double)sigma) {              // a violation in this level: canonical order, one lane
+      if (mx > (double)viol_bound(sigma)) {  // a violation in this level: canonical order, one lane
         if (lane == 0)
           for (int j = 0; j < Cd; ++j) {
             const uint32_t s0 = B.cslot16[2 * (Sd + j)], s1 = B.cslot16[2 * (Sd + j) + 1];
@@ -251,7 +251,7 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
             const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, s0, s1, viol);
             acc += ok;
             log_collision(P, K, log, log_count, log_cap, r, d, j, ok, s0, s1);
-            if (sj > sigma) sigma = sj;
+            if (sj > viol_bound(sigma)) sigma = sj;
           }
         sigma = __shfl_sync(0xffffffffu, sigma, 0);
       } else {

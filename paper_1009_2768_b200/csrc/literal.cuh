@@ -181,7 +181,7 @@ literal_step_kernel(StepParams P, const int64_t *__restrict__ offsets, int ncell
           }
           acc += pair_collide<Real>(P, vx, vy, vz, sig, (Real)xa, (Real)xi1, (Real)xi2, (uint32_t)F.i,
                                     (uint32_t)F.j, viol);
-          if (P.sigma_update && sj > sig) sig = sj;
+          if (P.sigma_update && sj > viol_bound(sig)) sig = sj;
           ra = F.i; rb = F.j;
           --sp;
         }
