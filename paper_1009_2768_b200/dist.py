@@ -2,7 +2,9 @@
 
 * Homogeneous ensembles shard by contiguous global cell ranges; the RNG is
   keyed by global cell id so per-cell results do not depend on the number of
-  GPUs.  The only collective is the all-reduce of the global sums.
+  GPUs.  The only collective is the all-reduce of the global sums (per step,
+  asynchronous); `global_sums_exact` gives sums that are bitwise the same for
+  any number of GPUs (report steps).
 * The 1D shock is split into slabs of contiguous cells balanced by particle
   count; each step every slab sends the particles that moved into a
   neighbouring slab to rank +- 1 (fixed-capacity buffers with a count header,
@@ -21,6 +23,37 @@ import numpy as np
 def shard_range(n: int, rank: int, world: int) -> Tuple[int, int]:
     """Contiguous near-equal partition of [0, n)."""
     return rank * n // world, (rank + 1) * n // world
+
+
+GLOBAL_FIELDS = ["n", "px", "py", "pz", "energy", "nPxx", "proposals", "accepted", "maxw", "cost"]
+
+
+def global_rows(stats: np.ndarray) -> np.ndarray:
+    """Per-cell rows of GLOBAL_FIELDS from a statistics table (Simulation.stats()):
+    the quantities trmcr_global_moments sums (cost = proposals + maxw / 2)."""
+    return np.stack([stats["n"], stats["px"], stats["py"], stats["pz"], stats["energy"],
+                     stats["n"] * stats["S0"], stats["proposals"], stats["accepted"], stats["maxw"],
+                     stats["proposals"] + 0.5 * stats["maxw"]], axis=1) if len(stats) else np.zeros((0, 10))
+
+
+def global_sums_exact(rows: np.ndarray, first_cell: int, group=None) -> np.ndarray:
+    """Global sums that do not depend on the partition: every rank
+    contributes its per-cell rows (host float64 [local cells x k], global cells
+    first_cell...) to an all-gather, and every rank adds all rows with
+    math.fsum - the correctly rounded sum, independent of order, so the result is
+    bitwise identical for any number of GPUs.  Report steps only: the per-step
+    path uses the asynchronous all-reduce of trmcr_global_moments."""
+    import math
+    import torch.distributed as dist
+    rows = np.ascontiguousarray(rows, dtype=np.float64)
+    if dist.is_available() and dist.is_initialized():
+        parts = [None] * dist.get_world_size(group)
+        dist.all_gather_object(parts, (int(first_cell), rows), group=group)
+    else:
+        parts = [(int(first_cell), rows)]
+    parts.sort(key=lambda p: p[0])
+    allr = np.concatenate([p[1] for p in parts], axis=0) if parts else np.zeros((0, rows.shape[1]))
+    return np.array([math.fsum(allr[:, k]) for k in range(allr.shape[1])])
 
 
 def shard_homogeneous(offsets: np.ndarray, rank: int, world: int):

@@ -111,3 +111,24 @@ def test_slab_cuts_balance_particles():
         load = [counts[a:a + n].sum() for a, n in cuts]
         assert max(load) / (counts.sum() / world) < 1.05     # equal-cell slabs would be ~1.56 at P = 2
         assert all(n >= 4 for _, n in cuts)
+
+
+def _exact_sums_case(rank, world, out_dir):
+    rng = np.random.default_rng(7)
+    rows = rng.standard_normal((101, 10)) * 10.0 ** rng.integers(-8, 9, (101, 1))
+    lo, hi = D.shard_range(101, rank, world)
+    tot = D.global_sums_exact(rows[lo:hi], lo)
+    np.save(os.path.join(out_dir, f"sums_{world}_{rank}.npy"), tot)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_global_sums_exact_are_partition_independent(world, tmp_path):
+    """All-gather + correctly rounded sums: every rank of every world size gets
+    the same bits, equal to math.fsum over all rows."""
+    import math
+    _run(_exact_sums_case, world, str(tmp_path))
+    rng = np.random.default_rng(7)
+    rows = rng.standard_normal((101, 10)) * 10.0 ** rng.integers(-8, 9, (101, 1))
+    ref = np.array([math.fsum(rows[:, k]) for k in range(10)])
+    for r in range(world):
+        np.testing.assert_array_equal(np.load(tmp_path / f"sums_{world}_{r}.npy"), ref)

@@ -69,6 +69,10 @@ def test_config3_full_fp32_bench_configuration():
     gm = gm.cpu().numpy()
     assert gm[0] == 16_384 * 1024 and gm[api.GLOBAL_FIELDS.index("maxw")] == 16_384 * 1024
     np.testing.assert_allclose(gm[1], st["px"].sum(), rtol=1e-9, atol=1e-6)
+    # the device's deterministic two-level sums against the correctly rounded ones
+    from paper_1009_2768_b200 import dist as D
+    ex = D.global_sums_exact(D.global_rows(st), 0)
+    np.testing.assert_allclose(gm, ex, rtol=1e-12, atol=1e-9)
 
 
 def test_config2_full_single_cell_rad():
