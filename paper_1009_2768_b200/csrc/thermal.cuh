@@ -478,8 +478,11 @@ __device__ __forceinline__ bool thermal_cell_f32(const StepParams &P, const KeyS
   return thermal_f32_compute(P, ks, vx, vy, vz, off, n, c, wx, wy, wz, m_state, stats);
 }
 
+#ifndef TRMCR_THERMAL_MINB
+#define TRMCR_THERMAL_MINB 16   // one-warp CTAs per SM (12 KB of staging each); 17 measured slower (C3 97.9 -> 105.6 us: 96-register cap)
+#endif
 template <typename Real>
-__global__ void __launch_bounds__(kThermalWarps * 32, 16)
+__global__ void __launch_bounds__(kThermalWarps * 32, TRMCR_THERMAL_MINB)
 thermal_warp_kernel(StepParams P, KeySched ks, const int64_t *__restrict__ offsets, int ncells, Real *vx,
                     Real *vy, Real *vz, int32_t *m_state, double *stats, int *defer_count, int *defer_list,
                     int prefetch, int *zero_next) {
