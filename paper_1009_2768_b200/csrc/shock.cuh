@@ -917,7 +917,10 @@ shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
 // stall on instruction fetch: 5.3 cycles per issue, 0.2 in lock step).  Small
 // groups bound the barrier idle of unequal cells.  Sorted cells only (no
 // gather); results identical to the free-running kernel.
-constexpr int kLockWarps = 4;   // measured: 16 -> 2.02 ms, 8 -> 1.80, 4 -> 1.66 (C5), free-running 1.75
+#ifndef TRMCR_LOCK_WARPS
+#define TRMCR_LOCK_WARPS 4
+#endif
+constexpr int kLockWarps = TRMCR_LOCK_WARPS;   // measured: 16 -> 2.02 ms, 8 -> 1.80, 4 -> 1.66, 2 -> +0.09 ms (C5), free-running 1.75
 template <typename Real, bool WB>
 __global__ void __launch_bounds__(kLockWarps * 32, 16 / kLockWarps)
 shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
