@@ -84,6 +84,7 @@ struct CellShared {
   int n, m, m_cur, m_next, d, top, lo, hi, r, planned, flag, done;
   int64_t rem;
   int32_t L, Ltot, U, nT, budget, leaf_off, attempts, ktot, nwb;
+  int32_t solo_from, cnt_d, cnt_S;   // grid team: levels small enough for block 0 alone
   unsigned long long prop, acc, viol;
   double usplit[kSplitPre];   // split uniforms of levels < kSplitPre, drawn in parallel
 };
@@ -264,19 +265,29 @@ __device__ __forceinline__ void gauss3(const RngKey &K, uint32_t slot, Real &g0,
 // SM).  tid/size/sync/reductions are the team's; reductions are two-level
 // and in a fixed order (deterministic). ----
 constexpr int kGridSlots = 8;
+// Levels with fewer collisions than this run on block 0 alone ("solo": CTA
+// barriers instead of grid barriers; the rest of the grid waits at the next
+// grid barrier) - a grid barrier costs more than such a level's work.
+constexpr int kSoloMax = 2048;
 struct GridTeam {
+  static constexpr bool kGrid = true;
   double *part;              // [kGridSlots][gridDim.x][8] per-block partial sums (rotating)
   int32_t *hbuf;             // rank scratch [hcap]
   int64_t hcap;
   int slot;
-  __device__ __forceinline__ int tid() const { return blockIdx.x * blockDim.x + threadIdx.x; }
-  __device__ __forceinline__ int size() const { return gridDim.x * blockDim.x; }
+  bool solo = false;         // block 0 alone (tid/size/sync/reductions of the CTA)
+  __device__ __forceinline__ int tid() const { return solo ? (int)threadIdx.x : blockIdx.x * blockDim.x + threadIdx.x; }
+  __device__ __forceinline__ int size() const { return solo ? (int)blockDim.x : gridDim.x * blockDim.x; }
   // cooperative-groups grid barrier: release/acquire at gpu scope, so plain
   // loads after it see every write made before it
-  __device__ __forceinline__ void sync() const { cooperative_groups::this_grid().sync(); }
+  __device__ __forceinline__ void sync() const {
+    if (solo) __syncthreads();
+    else cooperative_groups::this_grid().sync();
+  }
   template <int NV> __device__ void sum(double (&v)[NV], double *red) {
     static_assert(NV <= 8, "at most 8 sums");
     block_sum<NV>(v, red);
+    if (solo) return;
     double *pp = part + (size_t)slot * gridDim.x * 8;
     if (threadIdx.x == 0)
       for (int k = 0; k < NV; ++k) pp[blockIdx.x * 8 + k] = v[k];
@@ -290,6 +301,7 @@ struct GridTeam {
   }
   __device__ double max(double x, double *red) {
     x = block_max(x, red);
+    if (solo) return x;
     double *pp = part + (size_t)slot * gridDim.x * 8;
     if (threadIdx.x == 0) pp[blockIdx.x * 8] = x;
     sync();
@@ -301,6 +313,8 @@ struct GridTeam {
 };
 
 struct BlockTeam {
+  static constexpr bool kGrid = false;
+  bool solo = false;
   int32_t *hbuf = nullptr;   // no separate rank scratch (the level's slot range is used)
   int64_t hcap = 0;
   __device__ __forceinline__ int tid() const { return threadIdx.x; }
@@ -336,7 +350,43 @@ __device__ void plan_counts(Team &T, const RngKey &K, CellBuf<Real> &B, CellShar
     for (int d = tid; d <= top; d += T.size()) B.cons[d] = 0;
     T.sync();
     int Sacc = 0;
-    for (int d = top; d >= 1; --d) {
+    int d = top;
+    if constexpr (Team::kGrid) {
+      // the small top levels on block 0 alone, up to the first large one
+      if (blockIdx.x == 0) {
+        T.solo = true;
+        const int t0 = T.tid();
+        for (; d >= 1; --d) {
+          const int Qd = (d >= sh.lo) ? B.Q[d] : 0;
+          const int Cd = (Qd + B.cons[d] + 1) >> 1;
+          if (Cd >= kSoloMax) break;
+          if ((int64_t)Sacc + Cd > B.K_cap) { d = -1; break; }
+          if (t0 == 0) { B.C[d] = Cd; B.S[d] = Sacc; }
+          for (int j = t0; j < Cd; j += T.size()) {
+            const uint32_t w = K(kType, sh.r, d, j).x;
+            const uint32_t a = __umulhi(w, (uint32_t)d);
+            B.ctype[Sacc + j] = a;
+            const unsigned act = __activemask();
+            const unsigned pa = __match_any_sync(act, a), pb = __match_any_sync(act, (uint32_t)d - 1u - a);
+            const int lane_ = threadIdx.x & 31;
+            if ((__ffs(pa) - 1) == lane_) atomicAdd(&B.cons[a], __popc(pa));
+            if ((__ffs(pb) - 1) == lane_) atomicAdd(&B.cons[d - 1 - a], __popc(pb));
+          }
+          Sacc += Cd;
+          T.sync();
+        }
+        T.solo = false;
+        if (t0 == 0) {
+          sh.cnt_d = d; sh.cnt_S = Sacc;
+          if (d < 0) sh.flag = kOverflow;
+        }
+      }
+      T.sync();
+      d = sh.cnt_d;
+      Sacc = sh.cnt_S;
+      if (d < 0) return;
+    }
+    for (; d >= 1; --d) {
       const int Qd = (d >= sh.lo) ? B.Q[d] : 0;
       const int Cd = (Qd + B.cons[d] + 1) >> 1;   // all threads read the same value
       if ((int64_t)Sacc + Cd > B.K_cap) {
@@ -410,13 +460,25 @@ __device__ void plan_execute(Team &T, const StepParams &P, const RngKey &K, Cell
   }
   const int ktot = B.S[1] + B.C[1];                // collisions of the plan (levels top..1 stored from 0)
   if (P.wb) for (int o = tid; o < 2 * ktot; o += T.size()) B.wused[o] = 0;
-  if (tid == 0) sh.ktot = ktot;
+  if (tid == 0) {
+    sh.ktot = ktot;
+    int sf = top + 1;                               // levels >= sf are all small
+    while (sf > 1 && B.C[sf - 1] < kSoloMax) --sf;
+    sh.solo_from = sf;
+  }
   T.sync();
+  const int solo_from = sh.solo_from;
   unsigned acc = 0, viol = 0;
   const int r = sh.r;
   const int leaf_off = sh.leaf_off;
   int pd = 0;            // last level with collisions: its histogram is still in cnt[]
   for (int d = 1; d <= top; ++d) {
+    if constexpr (Team::kGrid) {
+      if (!T.solo && d >= solo_from) {     // the remaining levels are small: block 0 alone
+        if (blockIdx.x != 0) break;
+        T.solo = true;
+      }
+    }
     const int Cd = B.C[d], Sd = B.S[d];
     if (Cd == 0) continue;
     const int nw = T.size() >> 5;
@@ -567,6 +629,7 @@ __device__ void plan_execute(Team &T, const StepParams &P, const RngKey &K, Cell
     if (tid == 0) sh.prop += (unsigned long long)Cd;
     T.sync();
   }
+  T.solo = false;        // every block meets at the grid barrier below
   atomicAdd(&sh.acc, (unsigned long long)acc);
   atomicAdd(&sh.viol, (unsigned long long)viol);
   T.sync();
