@@ -27,7 +27,7 @@ STAT_FIELDS = ["n", "p", "mu", "sigma", "S0", "S_est", "E1", "m_used", "m_next",
                "violations", "maxw", "px", "py", "pz", "energy"]
 GLOBAL_FIELDS = ["n", "px", "py", "pz", "energy", "nPxx", "proposals", "accepted", "maxw", "cost"]
 MOMENT_FIELDS = ["n", "rho", "ux", "uy", "uz", "T", "E", "p", "Pxx", "M4", "M4c", "m_max"]
-KERNELS = ["cell_step_smem", "cell_step_gmem", "moments_kernel", "ghost_count", "ghost_gen",
+KERNELS = ["cell_step_smem", "cell_step_gmem", "moments_kernel", "shock_prologue", "ghost_gen",
            "transport_kernel", "scan_offsets", "shock_collide_smem", "shock_collide_gmem",
            "thermal_warp_kernel", "cell_step_warp", "shock_collide_warp", "scatter_sorted",
            "literal_step_kernel"]

@@ -2,7 +2,7 @@
 // stable counting sort by cell (A2), fused with the per-cell collision step.
 //
 // Step (all on the context stream, no host round trip):
-//   ghost_count / ghost_gen   ghost slabs [x_min-Lg, x_min) and [x_max, x_max+Lg),
+//   shock_prologue / ghost_gen   ghost slabs [x_min-Lg, x_min) and [x_max, x_max+Lg),
 //                             Lg = (|u_B| + 6 sqrt(T_B)) dt, refilled with
 //                             IR(rho_B Lg / w) particles of M(rho_B,u_B,T_B) [R26];
 //                             transported; survivors counted per destination cell
@@ -168,7 +168,17 @@ __global__ void __launch_bounds__(1024) scan_offsets(const int32_t *__restrict__
 }
 
 // ---- A1: reservoir ghost counts IR(rho_B Lg / w) ----
-__global__ void ghost_count(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, int *ng, int *err) {
+// First kernel of a shock step: zeroes the step's destination counts, window
+// bounds, accounting and overflow counter (one launch instead of four memsets)
+// and draws the number of reservoir ghosts per side.
+__global__ void __launch_bounds__(256) shock_prologue(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, int *ng,
+                                                      int *err, int32_t *counts, int *W, unsigned long long *acct,
+                                                      int *ovf_count) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < S.C; i += gridDim.x * blockDim.x) counts[i] = 0;
+  if (blockIdx.x != 0) return;
+  if (threadIdx.x < 3) W[threadIdx.x] = 0;
+  if (threadIdx.x < 4) acct[threadIdx.x] = 0ull;
+  if (threadIdx.x == 4) *ovf_count = 0;
   const int side = threadIdx.x;
   if (side > 1) return;
   if (side == 0 ? S.has_left : S.has_right) { ng[side] = 0; return; }   // a neighbour, not a reservoir
@@ -1132,13 +1142,10 @@ trmcr_status shock_begin(trmcr_ctx *c) {
   ShockState &s = c->shock;
   const ShockDev d = shock_dev(c);
   const int cur = c->cur;
-  CUDA_TRY(c, cudaMemsetAsync(c->d_ovf_count, 0, sizeof(int), c->stream));
-  CUDA_TRY(c, cudaMemsetAsync(s.d_counts, 0, sizeof(int32_t) * s.C, c->stream));
-  CUDA_TRY(c, cudaMemsetAsync(s.d_W, 0, 3 * sizeof(int), c->stream));
-  CUDA_TRY(c, cudaMemsetAsync(s.d_acct, 0, sizeof(unsigned long long) * 4, c->stream));
   prof_begin(c, TRMCR_K_GHOST_COUNT);
-  ghost_count<<<1, 32, 0, c->stream>>>(d, c->P.k0, c->P.k1, c->step, s.d_ng, c->d_err);
-  if (auto e = check_launch(c, "ghost_count", TRMCR_K_GHOST_COUNT)) return e;
+  shock_prologue<<<std::max(1, std::min(32, (s.C + 4095) / 4096)), 256, 0, c->stream>>>(
+      d, c->P.k0, c->P.k1, c->step, s.d_ng, c->d_err, s.d_counts, s.d_W, s.d_acct, c->d_ovf_count);
+  if (auto e = check_launch(c, "shock_prologue", TRMCR_K_GHOST_COUNT)) return e;
   {
     dim3 grid((unsigned)((s.cap_g + 255) / 256), 2);
     prof_begin(c, TRMCR_K_GHOST_GEN);
