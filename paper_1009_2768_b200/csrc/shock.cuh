@@ -173,12 +173,13 @@ __global__ void __launch_bounds__(1024) scan_offsets(const int32_t *__restrict__
 // and draws the number of reservoir ghosts per side.
 __global__ void __launch_bounds__(256) shock_prologue(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, int *ng,
                                                       int *err, int32_t *counts, int *W, unsigned long long *acct,
-                                                      int *ovf_count) {
+                                                      int *ovf_count, int *defer_count) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < S.C; i += gridDim.x * blockDim.x) counts[i] = 0;
   if (blockIdx.x != 0) return;
   if (threadIdx.x < 3) W[threadIdx.x] = 0;
   if (threadIdx.x < 4) acct[threadIdx.x] = 0ull;
   if (threadIdx.x == 4) *ovf_count = 0;
+  if (threadIdx.x == 5) *defer_count = 0;
   const int side = threadIdx.x;
   if (side > 1) return;
   if (side == 0 ? S.has_left : S.has_right) { ng[side] = 0; return; }   // a neighbour, not a reservoir
@@ -1144,7 +1145,8 @@ trmcr_status shock_begin(trmcr_ctx *c) {
   const int cur = c->cur;
   prof_begin(c, TRMCR_K_GHOST_COUNT);
   shock_prologue<<<std::max(1, std::min(32, (s.C + 4095) / 4096)), 256, 0, c->stream>>>(
-      d, c->P.k0, c->P.k1, c->step, s.d_ng, c->d_err, s.d_counts, s.d_W, s.d_acct, c->d_ovf_count);
+      d, c->P.k0, c->P.k1, c->step, s.d_ng, c->d_err, s.d_counts, s.d_W, s.d_acct, c->d_ovf_count,
+      c->d_defer_count);
   if (auto e = check_launch(c, "shock_prologue", TRMCR_K_GHOST_COUNT)) return e;
   {
     dim3 grid((unsigned)((s.cap_g + 255) / 256), 2);
@@ -1227,7 +1229,6 @@ trmcr_status shock_finish(trmcr_ctx *c) {
     if (auto e = check_launch(c, "scatter_sorted", TRMCR_K_SCATTER)) return e;
   }
   if (use_warp) {
-    CUDA_TRY(c, cudaMemsetAsync(c->d_defer_count, 0, sizeof(int), c->stream));
     prof_begin(c, TRMCR_K_SHOCK_WARP);
     const bool wb = ext_variant(c);
     if (G.scatter && c->lock_grid > 0)
