@@ -141,6 +141,8 @@ struct ShockState {
   int32_t *d_lcnt = nullptr;                // [kEdgeBins] left-edge (ghost + immigrant) particles per cell
   int ntiles = 0;
   int tile_ng = 4;                          // transport / sort tile = 1024 * tile_ng particles (1 or 4)
+  unsigned long long *d_scan_status = nullptr;   // [ceil(C / 4096)] look-back status words of scan_offsets_lb
+  uint32_t scan_epoch = 0;                  // per-call stamp of those words (30 bits used)
   int scatter = 1;                          // sort by scatter (TRMCR_SHOCK_SCATTER=0: gather in the collide kernel)
   unsigned long long *d_acct = nullptr;     // [4] injected L, injected R, dropped, generated
 };

@@ -167,6 +167,115 @@ __global__ void __launch_bounds__(1024) scan_offsets(const int32_t *__restrict__
   }
 }
 
+// Multi-CTA exclusive scan with decoupled look-back: CTA b scans its 4096
+// counts, publishes its aggregate, then adds the predecessors' aggregates
+// (or the first inclusive prefix it meets) and publishes its own inclusive
+// prefix.  Status words: epoch (bits 34+) | flag (bits 32-33: 1 aggregate,
+// 2 inclusive prefix) | value (bits 0-31; totals stay below 2^31) - stamped
+// with a per-call epoch, so nothing needs zeroing between calls.  Every CTA
+// is resident at once (a few dozen at most), so the spin-waits progress.
+constexpr int kScanThreads = 256, kScanItems = 16, kScanTile = kScanThreads * kScanItems;
+// 30-bit stamps, never 0 (the status words start zeroed)
+inline uint32_t next_scan_epoch(ShockState &s) {
+  s.scan_epoch = (s.scan_epoch + 1u) & 0x3FFFFFFFu;
+  if (s.scan_epoch == 0u) s.scan_epoch = 1u;
+  return s.scan_epoch;
+}
+__global__ void __launch_bounds__(kScanThreads) scan_offsets_lb(const int32_t *__restrict__ counts, int C,
+                                                                int64_t *off, int64_t cap, int *err,
+                                                                unsigned long long *status, uint32_t epoch) {
+  __shared__ int64_t wsum[kScanThreads / 32];
+  __shared__ int64_t s_excl;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, b = blockIdx.x;
+  const int i0 = b * kScanTile + tid * kScanItems;
+  const bool vec = ((reinterpret_cast<uintptr_t>(counts) | reinterpret_cast<uintptr_t>(off)) & 15) == 0 &&
+                   i0 + kScanItems <= C;
+  int v[kScanItems];
+  if (vec) {
+#pragma unroll
+    for (int q = 0; q < kScanItems / 4; ++q) {
+      const int4 w = *reinterpret_cast<const int4 *>(counts + i0 + 4 * q);
+      v[4 * q] = w.x; v[4 * q + 1] = w.y; v[4 * q + 2] = w.z; v[4 * q + 3] = w.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) v[k] = i0 + k < C ? counts[i0 + k] : 0;
+  }
+  int64_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) sum += v[k];
+  int64_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = lane < kScanThreads / 32 ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += t;
+    }
+    if (lane < kScanThreads / 32) wsum[lane] = w;
+    const int64_t agg = __shfl_sync(0xffffffffu, w, kScanThreads / 32 - 1);
+    const unsigned long long tag = (unsigned long long)epoch << 34;
+    int64_t excl = 0;
+    if (b == 0) {
+      if (lane == 0) atomicExch(&status[0], tag | (2ull << 32) | (unsigned long long)agg);
+    } else {
+      if (lane == 0) atomicExch(&status[b], tag | (1ull << 32) | (unsigned long long)agg);
+      // look back over the predecessors, 32 at a time
+      for (int j0 = b - 1;; j0 -= 32) {
+        const int j = j0 - lane;
+        unsigned long long st = 0;
+        if (j >= 0) {
+          do {
+            st = atomicAdd(&status[j], 0ull);
+          } while ((st >> 34) != (unsigned long long)epoch || ((st >> 32) & 3ull) == 0ull);
+        }
+        const bool pre = j >= 0 && ((st >> 32) & 3ull) == 2ull;
+        const unsigned pm = __ballot_sync(0xffffffffu, pre);
+        const int stop = pm ? __ffs(pm) - 1 : 32;     // first inclusive prefix (nearest predecessor)
+        int64_t add = (j >= 0 && lane <= stop) ? (int64_t)(st & 0xFFFFFFFFull) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+        excl += add;
+        if (pm || j0 - 31 <= 0) break;
+      }
+      if (lane == 0)
+        atomicExch(&status[b], tag | (2ull << 32) | (unsigned long long)(excl + agg));
+    }
+    if (lane == 0) {
+      s_excl = excl;
+      if (b == (int)gridDim.x - 1) {
+        off[C] = excl + agg;
+        if (excl + agg > cap) atomicOr(err, 2);
+      }
+    }
+  }
+  __syncthreads();
+  int64_t run = s_excl + (warp > 0 ? wsum[warp - 1] : 0) + incl - sum;
+  if (vec) {
+#pragma unroll
+    for (int q = 0; q < kScanItems / 2; ++q) {
+      const int64_t a = run;
+      run += v[2 * q];
+      const int64_t c2 = run;
+      run += v[2 * q + 1];
+      *reinterpret_cast<longlong2 *>(off + i0 + 2 * q) = make_longlong2(a, c2);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      if (i0 + k < C) off[i0 + k] = run;
+      run += v[k];
+    }
+  }
+}
+
 // ---- A1: reservoir ghost counts IR(rho_B Lg / w) ----
 // First kernel of a shock step: zeroes the step's destination counts, window
 // bounds, accounting and overflow counter (one launch instead of four memsets)
@@ -1109,6 +1218,10 @@ inline trmcr_status shock_init(trmcr_ctx *c, const trmcr_cells *cc, int *max_cel
                     dalloc(c, &s.d_tile_meta, sizeof(int2) * (size_t)std::max(s.ntiles, 1)) ||
                     dalloc(c, &s.d_lcnt, sizeof(int32_t) * kEdgeBins)))
     return TRMCR_ENOMEM;
+  const int scan_blocks = std::max(1, (s.C + kScanTile - 1) / kScanTile);
+  if (dalloc(c, &s.d_scan_status, sizeof(unsigned long long) * scan_blocks)) return TRMCR_ENOMEM;
+  CUDA_TRY(c, cudaMemsetAsync(s.d_scan_status, 0, sizeof(unsigned long long) * scan_blocks, c->stream));
+  s.scan_epoch = 0;
   CUDA_TRY(c, cudaMemsetAsync(s.d_counts, 0, sizeof(int32_t) * s.C, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(s.d_acct, 0, sizeof(unsigned long long) * 4, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(s.d_ng, 0, sizeof(int) * 2, c->stream));
@@ -1194,7 +1307,8 @@ trmcr_status shock_finish(trmcr_ctx *c) {
     if (auto e = check_launch(c, "immigrant_count")) return e;
   }
   prof_begin(c, TRMCR_K_SCAN);
-  scan_offsets<<<1, 1024, 0, c->stream>>>(s.d_counts, s.C, s.d_off[nxt], c->cap, c->d_err);
+  scan_offsets_lb<<<std::max(1, (s.C + kScanTile - 1) / kScanTile), kScanThreads, 0, c->stream>>>(
+      s.d_counts, s.C, s.d_off[nxt], c->cap, c->d_err, s.d_scan_status, next_scan_epoch(s));
   if (auto e = check_launch(c, "scan_offsets", TRMCR_K_SCAN)) return e;
 
   GatherSrc G;

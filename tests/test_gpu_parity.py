@@ -305,6 +305,23 @@ def test_shock_fp64_parity(orc, api, monkeypatch, scatter):
     assert o.counts[0] > 0     # reservoir particles entered
 
 
+def test_shock_fp64_parity_many_cells(orc, api):
+    """10,000 cells: the offsets scan spans three CTAs (decoupled look-back over
+    4096-cell tiles) and the sort many tiles; every position, offset and
+    velocity as the oracle's."""
+    setup, sim, o = _shock_pair(orc, api, 3.0, 10_000, 200_000, 0, 0.5, np.float64, x_min=-20.0, x_max=20.0)
+    for s in range(3):
+        sim.step(1)
+        o.step(1)
+        assert not sim.sort_info()["gathered"]
+        g = sim.particles()
+        np.testing.assert_array_equal(g["offsets"], o.offsets)
+        n = o.n
+        np.testing.assert_allclose(g["x"], o.x[:n], rtol=0, atol=1e-12)
+        _cmp_v(g, o.vx[:n], o.vy[:n], o.vz[:n], o.offsets)
+        _cmp_stats(sim.stats(), o.stats)
+
+
 def test_shock_fp64_parity_dense_edges(orc, api):
     """20000 particles per cell, CFL 4: each step's entering reservoir
     particles span several edge_place rounds (512 per round, ranks chained
