@@ -597,78 +597,77 @@ edge_place(ShockDev S, const int64_t *__restrict__ off_new, const int *ng, const
            int32_t *lcnt, Real *ox, Real *ovx, Real *ovy, Real *ovz, int *W) {
   constexpr int NW = kEdgeThreads / 32;
   __shared__ int run[kEdgeBins];
-  __shared__ int tot[kEdgeBins];
   __shared__ int turn;
   volatile int *vrun = run, *vturn = &turn;
   const int side = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int b = tid; b < kEdgeBins; b += kEdgeThreads) { run[b] = 0; tot[b] = 0; }
+  for (int b = tid; b < kEdgeBins; b += kEdgeThreads) run[b] = 0;
   if (tid == 0) turn = 0;
   __syncthreads();
-  // segment order for this side: side 0: ghosts(0), immigrants(0); side 1: immigrants(1), ghosts(1)
-  for (int pass = side == 0 ? 1 : 0; pass < 2; ++pass) {    // side 1: pass 0 counts, pass 1 places
-    for (int seg = 0; seg < 2; ++seg) {
-      const bool ghosts = (side == 0) == (seg == 0);
-      int cnt = 0, shift = 0;
-      const Real *px, *pvx, *pvy, *pvz;
-      const int32_t *pd;
-      if (ghosts) {
-        if (side == 0 ? S.has_left : S.has_right) continue;
-        cnt = ng[side];
-        px = side ? gx1 : gx0; pvx = side ? gvx1 : gvx0; pvy = side ? gvy1 : gvy0; pvz = side ? gvz1 : gvz0;
-        pd = side ? gd1 : gd0;
-      } else {
-        const void *rb = side == 0 ? recv_l : recv_r;
-        if (rb == nullptr) continue;
-        const XBuf<Real> X = XBuf<Real>::bind(const_cast<void *>(rb), xcap);
-        cnt = min(*X.count, xcap);
-        px = X.x; pvx = X.vx; pvy = X.vy; pvz = X.vz; pd = X.dest;
-        shift = S.cbase;                      // immigrants carry global destinations
+  // side 0 fills cells from their start, in index order: ghosts(0), then
+  // immigrants(0).  Side 1 fills them from their end, backwards: the canonical
+  // order there is immigrants(1), ghosts(1), so ghosts(1) come first, each
+  // segment in reverse index order (no count pass needed).
+  const bool back = side == 1;
+  const int my_turn = back ? NW - 1 - warp : warp;                    // order of the warps in a round
+  const unsigned rank_mask = back ? ~((2u << lane) - 1u) : ((1u << lane) - 1u);   // peers placed before
+  for (int seg = 0; seg < 2; ++seg) {
+    const bool ghosts = seg == 0;
+    int cnt = 0, shift = 0;
+    const Real *px, *pvx, *pvy, *pvz;
+    const int32_t *pd;
+    if (ghosts) {
+      if (side == 0 ? S.has_left : S.has_right) continue;
+      cnt = ng[side];
+      px = side ? gx1 : gx0; pvx = side ? gvx1 : gvx0; pvy = side ? gvy1 : gvy0; pvz = side ? gvz1 : gvz0;
+      pd = side ? gd1 : gd0;
+    } else {
+      const void *rb = side == 0 ? recv_l : recv_r;
+      if (rb == nullptr) continue;
+      const XBuf<Real> X = XBuf<Real>::bind(const_cast<void *>(rb), xcap);
+      cnt = min(*X.count, xcap);
+      px = X.x; pvx = X.vx; pvy = X.vy; pvz = X.vz; pd = X.dest;
+      shift = S.cbase;                      // immigrants carry global destinations
+    }
+    for (int r0 = 0; r0 < cnt; r0 += kEdgeThreads) {
+      const int k = back ? cnt - r0 - kEdgeThreads + tid : r0 + tid;
+      int d = -1;
+      if (k >= 0 && k < cnt) {
+        const int dd = pd[k];
+        if (dd != kDropped && dd - shift >= 0 && dd - shift < S.C) d = dd - shift;
       }
-      for (int k0 = 0; k0 < cnt; k0 += kEdgeThreads) {
-        const int k = k0 + tid;
-        int d = -1;
-        if (k < cnt) {
-          const int dd = pd[k];
-          if (dd != kDropped && dd - shift >= 0 && dd - shift < S.C) d = dd - shift;
-        }
-        const int bin = d < 0 ? -1 : (side == 0 ? d : S.C - 1 - d);
-        if (bin >= kEdgeBins) W[2] = 1;     // out of reach of the edge bins: gather this step
-        const bool ok = bin >= 0 && bin < kEdgeBins;
-        const unsigned peers = __match_any_sync(0xffffffffu, ok ? bin : -1 - lane);
-        const bool leader = __ffs(peers) - 1 == lane;
-        if (side == 1 && pass == 0) {
-          if (ok && leader) atomicAdd(&tot[bin], __popc(peers));
-        } else {
-          Real a = Real(0), bx = Real(0), by = Real(0), bz = Real(0);
-          int64_t base = 0;
-          if (ok) {
-            a = px[k]; bx = pvx[k]; by = pvy[k]; bz = pvz[k];
-            base = side == 0 ? off_new[d] : off_new[d + 1] - tot[bin];
-          }
-          // this warp's turn: every earlier warp of the round has counted
-          if (__any_sync(0xffffffffu, ok)) {
-            if (lane == 0)
-              while (*vturn != warp) {}
-            __syncwarp();
-            int rank = 0;
-            if (ok) rank = vrun[bin] + __popc(peers & ((1u << lane) - 1u));
-            __syncwarp();
-            if (ok && leader) vrun[bin] = rank + __popc(peers);
-            __threadfence_block();
-            __syncwarp();
-            if (ok) {
-              const int64_t pos = base + rank;
-              ox[pos] = a; ovx[pos] = bx; ovy[pos] = by; ovz[pos] = bz;
-            }
-          } else if (lane == 0) {
-            while (*vturn != warp) {}
-          }
-          if (lane == 0) *vturn = warp + 1;
-        }
-        __syncthreads();
-        if (tid == 0) turn = 0;
-        __syncthreads();
+      const int bin = d < 0 ? -1 : (side == 0 ? d : S.C - 1 - d);
+      if (bin >= kEdgeBins) W[2] = 1;     // out of reach of the edge bins: gather this step
+      const bool ok = bin >= 0 && bin < kEdgeBins;
+      const unsigned peers = __match_any_sync(0xffffffffu, ok ? bin : -1 - lane);
+      const bool leader = __ffs(peers) - 1 == lane;
+      Real a = Real(0), bx = Real(0), by = Real(0), bz = Real(0);
+      int64_t base = 0;
+      if (ok) {
+        a = px[k]; bx = pvx[k]; by = pvy[k]; bz = pvz[k];
+        base = back ? off_new[d + 1] - 1 : off_new[d];
       }
+      // this warp's turn: every warp placed before it in this round has counted
+      if (__any_sync(0xffffffffu, ok)) {
+        if (lane == 0)
+          while (*vturn != my_turn) {}
+        __syncwarp();
+        int r = 0, rank = 0;
+        if (ok) { r = vrun[bin]; rank = r + __popc(peers & rank_mask); }
+        __syncwarp();
+        if (ok && leader) vrun[bin] = r + __popc(peers);
+        __threadfence_block();
+        __syncwarp();
+        if (ok) {
+          const int64_t pos = back ? base - rank : base + rank;
+          ox[pos] = a; ovx[pos] = bx; ovy[pos] = by; ovz[pos] = bz;
+        }
+      } else if (lane == 0) {
+        while (*vturn != my_turn) {}
+      }
+      if (lane == 0) *vturn = my_turn + 1;
+      __syncthreads();
+      if (tid == 0) turn = 0;
+      __syncthreads();
     }
   }
   if (side == 0)
