@@ -262,6 +262,23 @@ inline void prof_event(trmcr_ctx *c) {
   }
   cudaEventRecord(c->ev_pool[c->ev_used++], c->stream);
 }
+// Kernel launch, with the programmatic-stream-serialization attribute when
+// PDL is on (the kernel must begin with step_kernel_prologue / pdl_wait).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(const trmcr_ctx *c, void (*k)(KArgs...), dim3 grid, int block, size_t smem, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = c->use_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 // The warp / lock-step kernels come in two instantiations: the plain one and
 // the extended one (TRMC-WB and/or the majorant-update variant), so that the
 // default path carries none of their code.

@@ -184,6 +184,7 @@ inline uint32_t next_scan_epoch(ShockState &s) {
 __global__ void __launch_bounds__(kScanThreads) scan_offsets_lb(const int32_t *__restrict__ counts, int C,
                                                                 int64_t *off, int64_t cap, int *err,
                                                                 unsigned long long *status, uint32_t epoch) {
+  pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   __shared__ int64_t wsum[kScanThreads / 32];
   __shared__ int64_t s_excl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, b = blockIdx.x;
@@ -274,6 +275,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_offsets_lb(const int32_t *_
       run += v[k];
     }
   }
+  pdl_trigger();
 }
 
 // ---- A1: reservoir ghost counts IR(rho_B Lg / w) ----
@@ -283,6 +285,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_offsets_lb(const int32_t *_
 __global__ void __launch_bounds__(256) shock_prologue(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, int *ng,
                                                       int *err, int32_t *counts, int *W, unsigned long long *acct,
                                                       int *ovf_count, int *defer_count) {
+  pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < S.C; i += gridDim.x * blockDim.x) counts[i] = 0;
   if (blockIdx.x != 0) return;
   if (threadIdx.x < 3) W[threadIdx.x] = 0;
@@ -299,6 +302,7 @@ __global__ void __launch_bounds__(256) shock_prologue(ShockDev S, uint32_t k0, u
   int64_t N = (int64_t)fl + ((u53(w.x, w.y) < y - fl) ? 1 : 0);
   if (N > S.cap_g) { atomicOr(err, 2); N = S.cap_g; }
   ng[side] = (int)N;
+  pdl_trigger();
 }
 
 // ---- A1: ghost particles, transported; survivors counted ----
@@ -306,6 +310,7 @@ template <typename Real>
 __global__ void ghost_gen(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, const int *ng, Real *gx0,
                           Real *gx1, Real *gvx0, Real *gvy0, Real *gvz0, Real *gvx1, Real *gvy1, Real *gvz1,
                           int32_t *gd0, int32_t *gd1, int32_t *counts, int *W, unsigned long long *acct) {
+  pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   const int side = blockIdx.y;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= ng[side]) return;
@@ -341,6 +346,7 @@ __global__ void ghost_gen(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, c
       atomicMax(W + 1, S.C + 1);   // emigrating ghost: pack kernel scans the ghosts
     }
   }
+  pdl_trigger();
 }
 
 // ---- A1: free transport of the interior particles ----
@@ -362,6 +368,7 @@ template <typename Real, int NG>
 __global__ void __launch_bounds__(kTransportThreads)
 transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const Real *__restrict__ vx,
                  int32_t *dest, int32_t *counts, int *W, unsigned long long *acct, int32_t *tileH, int2 *tile_meta) {
+  pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   constexpr int P4 = kTransportPer, TILE = tile_of(NG);
   __shared__ int s_hist[kHist];
   __shared__ int s_red[4][kTransportThreads / 32];
@@ -481,6 +488,7 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
     if (h > 0) atomicAdd(&counts[base + threadIdx.x], h);
     if (tileH) tileH[(size_t)blockIdx.x * kHist + threadIdx.x] = h;
   }
+  pdl_trigger();
 }
 
 // ---- slab exchange: pack emigrants (stable, canonical order) ----
@@ -494,6 +502,7 @@ pack_emigrants(ShockDev S, const int64_t *__restrict__ off_old, const int *ng, c
                const Real *gvx0, const Real *gvy0, const Real *gvz0, const int32_t *gd0, const Real *gx1,
                const Real *gvx1, const Real *gvy1, const Real *gvz1, const int32_t *gd1, void *send_l,
                void *send_r, int cap, int *err) {
+  pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   constexpr int R = 8;
   __shared__ int wcnt[32];
   const int side = blockIdx.x;
@@ -559,6 +568,7 @@ pack_emigrants(ShockDev S, const int64_t *__restrict__ off_old, const int *ng, c
     if (running > cap) { atomicOr(err, 2); running = cap; }
     *B.count = running;
   }
+  pdl_trigger();
 }
 
 // ---- slab exchange: immigrants (received) join the local counts ----
@@ -567,6 +577,7 @@ pack_emigrants(ShockDev S, const int64_t *__restrict__ off_old, const int *ng, c
 template <typename Real>
 __global__ void immigrant_count(ShockDev S, const void *recv_l, const void *recv_r, int cap, int32_t *counts,
                                 int *W, int *err) {
+  pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   const int side = blockIdx.y;
   if (side == 0 ? !S.has_left : !S.has_right) return;
   const XBuf<Real> B = XBuf<Real>::bind(const_cast<void *>(side == 0 ? recv_l : recv_r), cap);
@@ -577,6 +588,7 @@ __global__ void immigrant_count(ShockDev S, const void *recv_l, const void *recv
   if (d < 0 || d >= S.C) { atomicOr(err, 32); return; }   // would need more than one hop
   atomicAdd(&counts[d], 1);
   atomicMax(W, side == 0 ? d + 1 : S.C - d);
+  pdl_trigger();
 }
 
 // ---- A2 by scatter: ghosts and immigrants (canonical order) ----
@@ -595,6 +607,7 @@ edge_place(ShockDev S, const int64_t *__restrict__ off_new, const int *ng, const
            int xcap, const Real *gx0, const Real *gvx0, const Real *gvy0, const Real *gvz0, const int32_t *gd0,
            const Real *gx1, const Real *gvx1, const Real *gvy1, const Real *gvz1, const int32_t *gd1,
            int32_t *lcnt, Real *ox, Real *ovx, Real *ovy, Real *ovz, int *W) {
+  pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   constexpr int NW = kEdgeThreads / 32;
   __shared__ int run[kEdgeBins];
   __shared__ int turn;
@@ -672,6 +685,7 @@ edge_place(ShockDev S, const int64_t *__restrict__ off_new, const int *ng, const
   }
   if (side == 0)
     for (int b = tid; b < kEdgeBins; b += kEdgeThreads) lcnt[b] = run[b];
+  pdl_trigger();
 }
 
 // ---- A2 by scatter: interior particles ----
@@ -691,6 +705,7 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
                const Real *__restrict__ vz, const int32_t *__restrict__ dest, const int32_t *__restrict__ tileH,
                const int2 *__restrict__ tile_meta, const int32_t *__restrict__ lcnt, const int *W,
                Real *__restrict__ ox, Real *__restrict__ ovx, Real *__restrict__ ovy, Real *__restrict__ ovz) {
+  pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   constexpr int NW = kScatterThreads / 32, PARTS = kScatterThreads / kHist;
   constexpr int TILE = tile_of(NG);
   constexpr int CHUNK = TILE / NW, ROUNDS = CHUNK / 32;   // each warp: CHUNK consecutive particles
@@ -797,6 +812,7 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
       }
     }
   }
+  pdl_trigger();
 }
 
 struct GatherSrc {
@@ -987,6 +1003,7 @@ __global__ void __launch_bounds__(kWarpCellWarps * 32, TRMCR_WARP_MINB)
 shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, int *defer_count,
                    int *defer_list, QueueArgs Q) {
+  pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char *slab = smem + (size_t)warp * Lay.per_warp;
@@ -1026,6 +1043,7 @@ shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
     if (rc != kOk && lane == 0) defer_list[atomicAdd(defer_count, 1)] = c;
     __syncwarp();
   }
+  pdl_trigger();
 }
 
 // Lock-step variant of shock_collide_warp: CTAs of kLockWarps warps take
@@ -1045,6 +1063,7 @@ __global__ void __launch_bounds__(kLockWarps * 32, 16 / kLockWarps)
 shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, int *defer_count,
                    int *defer_list, QueueArgs Q) {
+  pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char *slab = smem + (size_t)warp * Lay.per_warp;
@@ -1098,6 +1117,7 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
     if (c < S.C && rc != kOk && lane == 0) defer_list[atomicAdd(defer_count, 1)] = c;
     __syncthreads();                          // round in lock step (dropping it measured slower)
   }
+  pdl_trigger();
 }
 
 template <typename Real, int THREADS>
@@ -1105,6 +1125,7 @@ __global__ void __launch_bounds__(THREADS, 768 / THREADS)
 shock_collide_smem(StepParams P, SmemLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats,
                    const int *list_count, const int *list, QueueArgs Q) {
+  pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   BlockTeam team;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CellShared sh;
@@ -1132,12 +1153,14 @@ shock_collide_smem(StepParams P, SmemLayout Lay, ShockDev S, GatherSrc G, const 
   }
   __syncthreads();
   }
+  pdl_trigger();
 }
 
 template <typename Real>
 __global__ void __launch_bounds__(kGmemThreads)
 shock_collide_gmem(StepParams P, GmemScratch GS, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, QueueArgs Q) {
+  pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   BlockTeam team;
   __shared__ CellShared sh;
   __shared__ double red[32 * 8];
@@ -1159,6 +1182,7 @@ shock_collide_gmem(StepParams P, GmemScratch GS, ShockDev S, GatherSrc G, const 
     if (rc != kOk && threadIdx.x == 0) atomicOr(Q.err, 1);
     __syncthreads();
   }
+  pdl_trigger();
 }
 
 inline ShockDev shock_dev(const trmcr_ctx *c) {
@@ -1256,15 +1280,14 @@ trmcr_status shock_begin(trmcr_ctx *c) {
   const ShockDev d = shock_dev(c);
   const int cur = c->cur;
   prof_begin(c, TRMCR_K_GHOST_COUNT);
-  shock_prologue<<<std::max(1, std::min(32, (s.C + 4095) / 4096)), 256, 0, c->stream>>>(
-      d, c->P.k0, c->P.k1, c->step, s.d_ng, c->d_err, s.d_counts, s.d_W, s.d_acct, c->d_ovf_count,
+
+  launch_k(c, shock_prologue, std::max(1, std::min(32, (s.C + 4095) / 4096)), 256, (size_t)(0), d, c->P.k0, c->P.k1, c->step, s.d_ng, c->d_err, s.d_counts, s.d_W, s.d_acct, c->d_ovf_count,
       c->d_defer_count);
   if (auto e = check_launch(c, "shock_prologue", TRMCR_K_GHOST_COUNT)) return e;
   {
     dim3 grid((unsigned)((s.cap_g + 255) / 256), 2);
     prof_begin(c, TRMCR_K_GHOST_GEN);
-    ghost_gen<Real><<<grid, 256, 0, c->stream>>>(
-        d, c->P.k0, c->P.k1, c->step, s.d_ng, (Real *)s.gx[0], (Real *)s.gx[1], (Real *)s.gv[0][0],
+    launch_k(c, ghost_gen<Real>, grid, 256, (size_t)(0), d, c->P.k0, c->P.k1, c->step, s.d_ng, (Real *)s.gx[0], (Real *)s.gx[1], (Real *)s.gv[0][0],
         (Real *)s.gv[0][1], (Real *)s.gv[0][2], (Real *)s.gv[1][0], (Real *)s.gv[1][1], (Real *)s.gv[1][2],
         s.d_gdest[0], s.d_gdest[1], s.d_counts, s.d_W, s.d_acct);
     if (auto e = check_launch(c, "ghost_gen", TRMCR_K_GHOST_GEN)) return e;
@@ -1275,15 +1298,13 @@ trmcr_status shock_begin(trmcr_ctx *c) {
     prof_begin(c, TRMCR_K_TRANSPORT);
     const bool sc = s.scatter && c->wlay.n_cap > 0 && !c->wlay.v_smem;
     auto *tk = s.tile_ng == 1 ? transport_kernel<Real, 1> : transport_kernel<Real, kTransportGroups>;
-    tk<<<blocks, kTransportThreads, 0, c->stream>>>(
-        d, s.d_off[cur], (Real *)c->x[cur], (const Real *)c->v[cur][0], s.d_dest, s.d_counts, s.d_W, s.d_acct,
+    launch_k(c, tk, blocks, kTransportThreads, (size_t)(0), d, s.d_off[cur], (Real *)c->x[cur], (const Real *)c->v[cur][0], s.d_dest, s.d_counts, s.d_W, s.d_acct,
         sc ? s.d_tileH : nullptr, sc ? s.d_tile_meta : nullptr);
     if (auto e = check_launch(c, "transport_kernel", TRMCR_K_TRANSPORT)) return e;
   }
   if (s.has_left || s.has_right) {
     if (!s.xsend[0] && !s.xsend[1]) return fail(c, TRMCR_EINVAL, "slab exchange buffers not set (trmcr_shock_set_exchange)");
-    pack_emigrants<Real><<<2, 1024, 0, c->stream>>>(
-        d, s.d_off[cur], s.d_ng, s.d_W, (const Real *)c->x[cur], (const Real *)c->v[cur][0],
+    launch_k(c, pack_emigrants<Real>, 2, 1024, (size_t)(0), d, s.d_off[cur], s.d_ng, s.d_W, (const Real *)c->x[cur], (const Real *)c->v[cur][0],
         (const Real *)c->v[cur][1], (const Real *)c->v[cur][2], s.d_dest, (const Real *)s.gx[0],
         (const Real *)s.gv[0][0], (const Real *)s.gv[0][1], (const Real *)s.gv[0][2], s.d_gdest[0],
         (const Real *)s.gx[1], (const Real *)s.gv[1][0], (const Real *)s.gv[1][1], (const Real *)s.gv[1][2],
@@ -1302,12 +1323,11 @@ trmcr_status shock_finish(trmcr_ctx *c) {
   const int cur = c->cur, nxt = cur ^ 1;
   if (s.has_left || s.has_right) {
     dim3 grid((unsigned)((s.xcap + 255) / 256), 2);
-    immigrant_count<Real><<<grid, 256, 0, c->stream>>>(d, s.xrecv[0], s.xrecv[1], s.xcap, s.d_counts, s.d_W, c->d_err);
+    launch_k(c, immigrant_count<Real>, grid, 256, (size_t)(0), d, s.xrecv[0], s.xrecv[1], s.xcap, s.d_counts, s.d_W, c->d_err);
     if (auto e = check_launch(c, "immigrant_count")) return e;
   }
   prof_begin(c, TRMCR_K_SCAN);
-  scan_offsets_lb<<<std::max(1, (s.C + kScanTile - 1) / kScanTile), kScanThreads, 0, c->stream>>>(
-      s.d_counts, s.C, s.d_off[nxt], c->cap, c->d_err, s.d_scan_status, next_scan_epoch(s));
+  launch_k(c, scan_offsets_lb, std::max(1, (s.C + kScanTile - 1) / kScanTile), kScanThreads, (size_t)(0), s.d_counts, s.C, s.d_off[nxt], c->cap, c->d_err, s.d_scan_status, next_scan_epoch(s));
   if (auto e = check_launch(c, "scan_offsets", TRMCR_K_SCAN)) return e;
 
   GatherSrc G;
@@ -1328,15 +1348,13 @@ trmcr_status shock_finish(trmcr_ctx *c) {
   G.scatter = s.scatter && use_warp && !c->wlay.v_smem;
   if (G.scatter) {
     prof_begin(c, TRMCR_K_SCATTER);
-    edge_place<Real><<<2, kEdgeThreads, 0, c->stream>>>(
-        d, s.d_off[nxt], s.d_ng, G.recv[0], G.recv[1], s.xcap, (const Real *)s.gx[0], (const Real *)s.gv[0][0],
+    launch_k(c, edge_place<Real>, 2, kEdgeThreads, (size_t)(0), d, s.d_off[nxt], s.d_ng, G.recv[0], G.recv[1], s.xcap, (const Real *)s.gx[0], (const Real *)s.gv[0][0],
         (const Real *)s.gv[0][1], (const Real *)s.gv[0][2], s.d_gdest[0], (const Real *)s.gx[1],
         (const Real *)s.gv[1][0], (const Real *)s.gv[1][1], (const Real *)s.gv[1][2], s.d_gdest[1], s.d_lcnt, ox,
         ovx, ovy, ovz, s.d_W);
     if (auto e = check_launch(c, "edge_place")) return e;
     auto *sk = s.tile_ng == 1 ? scatter_sorted<Real, 1> : scatter_sorted<Real, kTransportGroups>;
-    sk<<<std::max(s.ntiles, 1), kScatterThreads, 0, c->stream>>>(
-        d, s.d_off[cur], s.d_off[nxt], (const Real *)c->x[cur], (const Real *)c->v[cur][0],
+    launch_k(c, sk, std::max(s.ntiles, 1), kScatterThreads, (size_t)(0), d, s.d_off[cur], s.d_off[nxt], (const Real *)c->x[cur], (const Real *)c->v[cur][0],
         (const Real *)c->v[cur][1], (const Real *)c->v[cur][2], s.d_dest, s.d_tileH, s.d_tile_meta, s.d_lcnt,
         s.d_W, ox, ovx, ovy, ovz);
     if (auto e = check_launch(c, "scatter_sorted", TRMCR_K_SCATTER)) return e;
@@ -1345,26 +1363,21 @@ trmcr_status shock_finish(trmcr_ctx *c) {
     prof_begin(c, TRMCR_K_SHOCK_WARP);
     const bool wb = ext_variant(c);
     if (G.scatter && c->lock_grid > 0)
-      (wb ? shock_collide_lock<Real, true> : shock_collide_lock<Real, false>)
-          <<<c->lock_grid, kLockWarps * 32, c->lock_smem, c->stream>>>(
-              c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
+      launch_k(c, (wb ? shock_collide_lock<Real, true> : shock_collide_lock<Real, false>), c->lock_grid, kLockWarps * 32, (size_t)(c->lock_smem), c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
               c->d_defer_list, Q);
     else
-      (wb ? shock_collide_warp<Real, true> : shock_collide_warp<Real, false>)
-          <<<c->warp_grid, c->warp_wpc * 32, c->warp_smem, c->stream>>>(
-              c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
+      launch_k(c, (wb ? shock_collide_warp<Real, true> : shock_collide_warp<Real, false>), c->warp_grid, c->warp_wpc * 32, (size_t)(c->warp_smem), c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
               c->d_defer_list, Q);
     if (auto e = check_launch(c, "shock_collide_warp", TRMCR_K_SHOCK_WARP)) return e;
   }
   prof_begin(c, TRMCR_K_SHOCK_SMEM);
   auto kern = c->smem_threads == 64 ? shock_collide_smem<Real, 64>
               : (c->smem_threads == 128 ? shock_collide_smem<Real, 128> : shock_collide_smem<Real, 256>);
-  kern<<<use_warp ? c->smem_grid : s.C, c->smem_threads, c->lay.total, c->stream>>>(
-      c->P, c->lay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats,
+  launch_k(c, kern, use_warp ? c->smem_grid : s.C, c->smem_threads, (size_t)(c->lay.total), c->P, c->lay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats,
       use_warp ? c->d_defer_count : nullptr, use_warp ? c->d_defer_list : nullptr, Q);
   if (auto e = check_launch(c, "shock_collide_smem", TRMCR_K_SHOCK_SMEM)) return e;
   prof_begin(c, TRMCR_K_SHOCK_GMEM);
-  shock_collide_gmem<Real><<<c->G, c->gmem_threads, 0, c->stream>>>(c->P, c->gs, d, G, s.d_off[nxt], ox, ovx, ovy,
+  launch_k(c, shock_collide_gmem<Real>, c->G, c->gmem_threads, (size_t)(0), c->P, c->gs, d, G, s.d_off[nxt], ox, ovx, ovy,
                                                                  ovz, c->d_mstate, c->d_stats, Q);
   if (auto e = check_launch(c, "shock_collide_gmem", TRMCR_K_SHOCK_GMEM)) return e;
   c->cur = nxt;

@@ -258,22 +258,6 @@ __global__ void fill_i32(int32_t *a, int n, int32_t v) {
 
 namespace {
 
-// Kernel launch, with the programmatic-stream-serialization attribute when
-// PDL is on (the kernel must begin with step_kernel_prologue / pdl_wait).
-template <typename... KArgs, typename... Args>
-cudaError_t launch_k(const trmcr_ctx *c, void (*k)(KArgs...), int grid, int block, size_t smem, Args &&...args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3((unsigned)block);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = c->stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = c->use_pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
-}
 
 template <typename Real>
 trmcr_status launch_collide(trmcr_ctx *c) {
