@@ -697,7 +697,10 @@ edge_place(ShockDev S, const int64_t *__restrict__ off_new, const int *ng, const
 // than W cells before the tile's first destination (none of its particles, nor
 // any earlier one, can reach it); transport_kernel stored each tile's
 // destination histogram over [dmin, dmin + kHist).
-constexpr int kScatterThreads = 512;
+#ifndef TRMCR_SCATTER_THREADS
+#define TRMCR_SCATTER_THREADS 512   // measured on C5: 256 -> 0.62 ms, 1024 -> 0.69, 512 -> 0.50
+#endif
+constexpr int kScatterThreads = TRMCR_SCATTER_THREADS;
 template <typename Real, int NG>
 __global__ void __launch_bounds__(kScatterThreads)
 scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *__restrict__ off_new,
