@@ -466,6 +466,10 @@ __device__ void plan_execute(Team &T, const StepParams &P, const RngKey &K, Cell
     while (sf > 1 && B.C[sf - 1] < kSoloMax) --sf;
     sh.solo_from = sf;
   }
+  if (T.hbuf) {            // grid team: the large levels' rank scratch starts zeroed
+    const int64_t hz = min((int64_t)(T.size() >> 5) * top, T.hcap);
+    for (int64_t q = tid; q < hz; q += T.size()) T.hbuf[q] = 0;
+  }
   T.sync();
   const int solo_from = sh.solo_from;
   unsigned acc = 0, viol = 0;
@@ -503,8 +507,10 @@ __device__ void plan_execute(Team &T, const StepParams &P, const RngKey &K, Cell
       // exclusive prefix over warps, then the in-order walk
       int32_t *H = T.hbuf ? T.hbuf : reinterpret_cast<int32_t *>(B.cslot + 2 * (size_t)Sd);
       const int chunk = (Cd + nw - 1) / nw;
-      for (int q = tid; q < nw * d; q += T.size()) H[q] = 0;
-      T.sync();
+      if (!T.hbuf) {          // a grid team's scratch is kept zeroed between levels
+        for (int q = tid; q < nw * d; q += T.size()) H[q] = 0;
+        T.sync();
+      }
       const int j_lo = warp * chunk, j_hi = min(Cd, j_lo + chunk);
       for (int j0 = j_lo; j0 < j_hi; j0 += 32) {
         const int j = j0 + lane;
@@ -627,6 +633,8 @@ __device__ void plan_execute(Team &T, const StepParams &P, const RngKey &K, Cell
       }
     }
     if (tid == 0) sh.prop += (unsigned long long)Cd;
+    if (par && T.hbuf)     // re-zero the rank scratch for the next large level (no barrier of its own)
+      for (int q = tid; q < nw * d; q += T.size()) T.hbuf[q] = 0;
     T.sync();
   }
   T.solo = false;        // every block meets at the grid barrier below
