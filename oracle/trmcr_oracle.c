@@ -26,10 +26,17 @@
  *                       invariants, isotropy E[sigma]=0, E[sigma sigma^T]=I/3.
  *   orc_maxwellian      pinned: exact prescribed moments, Gaussian law (KS).
  *   orc_step_cells      pinned: Maxwell-molecule closed forms (Pxx, M4 decay),
- *                       truncated-map R_m(tau) at small m, conservation,
+ *                       truncated-map R_m(tau) for m = 1..16 (pins the
+ *                       plan's type law and matching independence), McKean
+ *                       tree-shape law prod 1/k_v (chi^2 on levels 3-5),
+ *                       C_d = ceil((N_d + cons_d)/2), conservation,
  *                       tau->0 identity, tau->1 Maxwellian (AP),
- *                       equilibrium invariance, literal Alg 4.3/4.4 vs LS
- *                       statistical equivalence, Sigma >= pairwise max.
+ *                       equilibrium invariance, literal Alg 4.3/4.4 = LS at
+ *                       m <= 2 and != eq. WST at m >= 4 (DESIGN R2),
+ *                       Sigma >= pairwise max.
+ *     rad_estimate      pinned: E1 against the N -> inf closed forms (Pxx:
+ *                       (1 - R_m) A_xx/(T + A_xx); M4: y_k recursion) and
+ *                       S_est = E[post-step indicator] on drifting cells.
  *   orc_shock_step      pinned: reservoir inflow vs one-sided flux closed
  *                       form, stable sort vs brute force, RH plateaus;
  *                       interior shock profile: PARITY UNPINNED (no closed

@@ -38,10 +38,20 @@ def _dev(a, dtype=torch.float64):
 
 
 def _dedupe(log):
+    """Canonical order of a GPU log.  A cell handed from one kernel to a larger one
+    (overflow) is re-run from its unmodified input, so the records its first kernel
+    wrote before handing it over reappear; such duplicates must be IDENTICAL (same
+    keyed draws on the same data) - any difference fails here instead of being
+    dropped silently."""
     if len(log) == 0:
         return log
     keys = np.stack([log["cell"], log["attempt"], log["level"], log["j"]], 1)
-    _, idx = np.unique(keys, axis=0, return_index=True)
+    _, idx, inv = np.unique(keys, axis=0, return_index=True, return_inverse=True)
+    inv = inv.reshape(-1)
+    for f in ("slot_i", "slot_k", "accepted"):
+        first = log[f][idx][inv]
+        bad = np.nonzero(log[f] != first)[0]
+        assert len(bad) == 0, ("duplicate GPU records differ", f, log[bad[:4]])
     out = log[np.sort(idx)]
     order = np.lexsort((out["j"], out["level"], out["attempt"], out["cell"]))
     return out[order]

@@ -68,4 +68,4 @@ def test_random_configs(orc, seed, warp_path, monkeypatch):
         g = sim.particles()
         for a, b in ((g["vx"], o.vx), (g["vy"], o.vy), (g["vz"], o.vz)):
             scale = 1.0 + np.abs(b)
-            assert np.all(np.abs(a - b) <= 1e-12 * scale * 10), (it, kw)
+            assert np.all(np.abs(a - b) <= 1e-12 * scale), (it, kw, (np.abs(a - b) / scale).max())

@@ -100,25 +100,161 @@ def test_maxwell_closed_form_relaxation(orc):
     assert abs(dM.mean()) < 0.1 * 3.0
 
 
-@pytest.mark.parametrize("m,R", [(1, 0.625), (2, 0.671875)])
-def test_truncated_map_R_m(orc, m, R):
-    """One step at tau = 1/2 with truncation m: A <- R_m(tau) A (eq. WST with
-    r_k = C(2k,k)/4^k); m = 1, 2 are the paper's first/second-order TRMC."""
-    n = 100_000
-    ratios = []
-    for seed in range(1, 9):
+def _R(m, tau):
+    """R_m(tau) = (1 - tau) sum_{k<=m} tau^k r_k, r_k = C(2k,k)/4^k."""
+    s, r = 0.0, 1.0
+    for k in range(m + 1):
+        s += tau ** k * r
+        r *= (2 * k + 1) / (2 * k + 2)
+    return (1 - tau) * s
+
+
+def _stress_ratios(orc, m, literal, seeds=64, n=100_000):
+    """A_xx after / before one Maxwell step at tau = 1/2 (x = ln 2) with truncation m."""
+    out = []
+    for seed in range(1, seeds + 1):
         v = synth.anisotropic_gaussian(n, seed=seed)
         T, A, _ = _centred(*v)
-        st = _hom(orc, orc.Config(model=0, m_fixed=m, eps=1.0, dt=math.log(2.0), seed=seed),
-                  v, [0, n])
+        st = _hom(orc, orc.Config(model=0, m_fixed=m, eps=1.0, dt=math.log(2.0), seed=seed,
+                                  literal=literal), v, [0, n])
         st.step(1)
         T1, A1, _ = _centred(st.vx, st.vy, st.vz)
-        ratios.append(A1[0, 0] / A[0, 0])
-    r = np.array(ratios)
-    assert abs(r.mean() - R) < 4 * r.std() / math.sqrt(len(r)) + 2e-3
-    # resolves neighbouring orders
-    other = 0.671875 if m == 1 else 0.625
-    assert abs(r.mean() - other) > 10 * r.std() / math.sqrt(len(r))
+        out.append(A1[0, 0] / A[0, 0])
+    r = np.array(out)
+    return r.mean(), r.std() / math.sqrt(len(r))
+
+
+def test_truncated_map_values():
+    """The closed form itself: R_1, R_2, R_4 at tau = 1/2 and the
+    untruncated limit R_inf = sqrt(1 - tau) = e^{-x/2} (eq. WS)."""
+    assert _R(1, 0.5) == 0.625 and _R(2, 0.5) == 0.671875
+    assert _R(4, 0.5) == pytest.approx(0.69995, abs=1e-5)
+    assert _R(200, 0.5) == pytest.approx(math.sqrt(0.5), rel=1e-12)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 8, 16])
+def test_truncated_map_R_m(orc, m):
+    """One step at tau = 1/2 with truncation m: A <- R_m(tau) A (eq. WST, P:277-285,
+    with the stress of f_k equal to r_k A, r_k = C(2k,k)/4^k, from eq. CF P:256-261:
+    A(f_k) = (1/(2k)) sum_{a<k} A(f_a) for independent f_a, f_{k-1-a} inputs).
+    m = 1, 2 are the paper's first/second-order TRMC; from m = 3 on the
+    level-d collisions of type a = (d-1)/2 take two samples of the same f_a, so the
+    law of the plan's types (uniform a) and the independence of the
+    pools' matchings are pinned here: a biased type draw or a matching that
+    re-pairs the outputs of one collision moves the ratio off R_m (the literal
+    recursion does exactly that, test_literal_recursion_deviates_from_wild_sum)."""
+    mean, se = _stress_ratios(orc, m, literal=0)
+    assert abs(mean - _R(m, 0.5)) < 4 * se + 2e-4, (mean, _R(m, 0.5), se)
+    if m <= 4:   # resolves neighbouring orders
+        for other in (m - 1, m + 1):
+            if other >= 1:
+                assert abs(mean - _R(other, 0.5)) > 10 * se
+
+
+@pytest.mark.parametrize("m", [1, 2])
+def test_literal_recursion_matches_wild_sum_at_low_order(orc, m):
+    """The literal Alg 4.3/4.4 (stored siblings c_k in {0, 1}) realises eq. WST at
+    m <= 2: no level below 3 has a type whose two inputs come from the same f_k."""
+    mean, se = _stress_ratios(orc, m, literal=1)
+    assert abs(mean - _R(m, 0.5)) < 4 * se + 2e-4, (mean, _R(m, 0.5), se)
+
+
+@pytest.mark.parametrize("m", [4, 8, 16])
+def test_literal_recursion_deviates_from_wild_sum(orc, m):
+    """At m >= 3 the literal recursion is NOT eq. WST: a symmetric split
+    (k = n-k-1) whose store is empty builds one f_k sample fresh,
+    stores its sibling, and takes that sibling for the second input, so the two
+    outputs of one collision meet again - a correlated pair, not two independent
+    f_k samples as eq. CF requires.  The stress then relaxes less than
+    R_m predicts (measured +6..9 SE at 32 seeds; > 5 SE asserted at 64).  The
+    level-synchronous plan [R2] is the faithful realisation (test above)."""
+    mean, se = _stress_ratios(orc, m, literal=1)
+    assert mean - _R(m, 0.5) > 5 * se, (mean, _R(m, 0.5), se)
+
+
+def _wild_y(m, y0, a2):
+    """y_k of f_k, k <= m: y_0 = y, y_k = (2/(3k)) sum_{a<k} y_a - |A|^2/(3k)
+    (y = M4c - 15 T^2, from one Maxwell collision of independent
+    f_a, f_b samples: y' = (y_a + y_b - tr(A_a A_b))/3 and sum_a r_a r_{k-1-a} = 1)."""
+    y = [y0]
+    for k in range(1, m + 1):
+        y.append(2.0 / (3 * k) * sum(y) - a2 / (3 * k))
+    return y
+
+
+@pytest.mark.parametrize("indicator", [0, 1])
+def test_rad_indicator_closed_form(orc, indicator):
+    """TRMC-RAD's estimate E1 (the Maxwellian part analytic)
+    against its N -> infinity closed form for Maxwell molecules at tau = 1/2 and
+    m = 1, 2, 4, 8 (one attempt: delta2 out of reach):
+      S = Pxx:  E1 = (1 - R_m) A_xx / (T + A_xx)
+      S = M4:   E1 = |sum_{k<=m} (1-tau) tau^k y_k - y| / M4
+    (the Theta part contributes tau^{m+1} T and tau^{m+1} 15 T^2: no stress, y = 0)."""
+    n, tau = 100_000, 0.5
+    for m in (1, 2, 4, 8):
+        got, pred = [], []
+        for seed in range(1, 33):
+            v = synth.anisotropic_gaussian(n, seed=seed)
+            T, A, M4c = _centred(*v)
+            cfg = orc.Config(model=0, adaptive=1, m_init=m, m_cap=4096, indicator=indicator,
+                             delta1=1e-12, delta2=1e12, eps=1.0, dt=math.log(2.0), seed=seed)
+            st = _hom(orc, cfg, v, [0, n])
+            st.step(1)
+            s = st.stats[0]
+            assert s["attempts"] == 1 and s["m_used"] == m
+            w = [(1 - tau) * tau ** k for k in range(m + 1)]
+            if indicator == 0:
+                e = (1 - _R(m, tau)) * A[0, 0] / (T + A[0, 0])
+            else:
+                y0 = M4c - 15 * T * T
+                y = _wild_y(m, y0, (A * A).sum())
+                e = abs(sum(a * b for a, b in zip(w, y)) - y0) / M4c
+            got.append(s["E1"])
+            pred.append(e)
+        d = np.array(got) - np.array(pred)
+        se = d.std() / math.sqrt(len(d))
+        assert abs(d.mean()) < 4 * se + 1e-4, (m, d.mean(), se)
+        assert se < 0.02 * np.mean(pred)               # the pin resolves a 10 % error
+
+
+def _drifting_cells(ncells, ppc, drift, seed):
+    vx, vy, vz, off = synth.uniform_cells(ncells, ppc, seed=seed)
+    u = np.random.default_rng(seed).uniform(-drift, drift, size=(3, ncells))
+    return (vx + np.repeat(u[0], ppc), vy + np.repeat(u[1], ppc), vz + np.repeat(u[2], ppc), off)
+
+
+@pytest.mark.parametrize("indicator", [0, 1])
+def test_rad_estimate_is_expected_post_step_indicator(orc, indicator):
+    """The analytic part of S_est is the conditional expectation of what
+    the conservative Maxwellian (A8) will produce: given the non-Theta
+    particles, E[S^{n+1}] = S_est.  For Theta (k particles, mean u_T, temperature
+    T_T) shift-and-rescale gives sum (v_x - u_x)^2 = k (T_T + (u_Tx - u_x)^2) in
+    expectation (the direction is uniform) and sum |v|^4 = k (|u_T|^4 + 10 |u_T|^2
+    T_T) + sum |w|^4 -> k (|u_T|^4 + 10 |u_T|^2 T_T + 15 T_T^2).  Small drifting
+    cells make the shift term (u_Tx - u_x)^2 matter (~ 0.05 per cell here: dropping
+    it fails by > 30 SE); strong drifts make the 10 |u|^2 T term matter (writing 6
+    fails by > 100 SE).  tau = 0.9, m = 1: Theta is ~ 80 % of each cell."""
+    if indicator == 0:
+        ncells, ppc, drift = 40_000, 12, 1.0
+    else:
+        ncells, ppc, drift = 64, 4000, 2.0
+    for seed in (3, 4):
+        vx, vy, vz, off = _drifting_cells(ncells, ppc, drift, seed)
+        cfg = orc.Config(model=0, adaptive=1, m_init=1, m_cap=4096, indicator=indicator,
+                         delta1=1e-12, delta2=1e12, eps=1.0, dt=math.log(10.0), seed=seed)
+        st = orc.HomogeneousState(cfg, vx, vy, vz, off)
+        st.step(1)
+        V = np.stack([st.vx, st.vy, st.vz]).reshape(3, ncells, ppc)
+        if indicator == 0:
+            post = ((V[0] - V[0].mean(1, keepdims=True)) ** 2).mean(1)
+        else:
+            post = ((V * V).sum(0) ** 2).mean(1)
+        est = st.stats["S_est"]
+        assert st.stats["thermalised"].mean() > 0.7 * ppc
+        d = (post - est) / (1.0 if indicator == 0 else est)
+        se = d.std() / math.sqrt(len(d))
+        assert abs(d.mean()) < 4 * se, (d.mean(), se)
+        assert se < (0.01 if indicator == 0 else 0.003)
 
 
 @pytest.mark.parametrize("model", [0, 1])
@@ -139,27 +275,32 @@ def test_equilibrium_invariance(orc, model):
 
 
 @pytest.mark.parametrize("model", [0, 1])
-def test_literal_algorithm_equivalence(orc, model):
-    """LS realisation [R2] vs the literal recursive Alg 4.3/4.4: same law of the
-    post-step moments and of the collision count (64 seeds each)."""
+def test_literal_algorithm_equivalence_low_order(orc, model):
+    """LS realisation [R2] vs the literal recursive Alg 4.3/4.4 at m = 2 (where the
+    two have the same law, see test_literal_recursion_matches_wild_sum_at_low_order):
+    same law of the post-step moments and of the collision count (64 seeds each).
+    At m >= 3 the laws differ (test_literal_recursion_deviates_from_wild_sum); the
+    collision COUNT still agrees there (it does not depend on which samples meet),
+    checked at m = 8."""
     n, steps = 2000, 3
-    out = {0: [], 1: []}
-    for lit in (0, 1):
-        for seed in range(1, 65):
-            v = synth.two_maxwellians(n, seed=seed)
-            cfg = orc.Config(model=model, m_fixed=8, eps=1.0, dt=0.25 if model == 0 else 0.05,
-                             seed=seed, literal=lit)
-            st = _hom(orc, cfg, v, [0, n])
-            props = 0.0
-            for _ in range(steps):
-                st.step(1)
-                props += st.stats["proposals"][0]
-            m = st.moments()[0]
-            out[lit].append([m[8], m[10], props])
-    a, b = np.array(out[0]), np.array(out[1])
-    for k in range(3):
-        se = math.sqrt(a[:, k].var() / len(a) + b[:, k].var() / len(b))
-        assert abs(a[:, k].mean() - b[:, k].mean()) < 4.5 * se + 1e-9, (k, a[:, k].mean(), b[:, k].mean(), se)
+    for m, cols in ((2, (0, 1, 2)), (8, (2,))):
+        out = {0: [], 1: []}
+        for lit in (0, 1):
+            for seed in range(1, 65):
+                v = synth.two_maxwellians(n, seed=seed)
+                cfg = orc.Config(model=model, m_fixed=m, eps=1.0, dt=0.25 if model == 0 else 0.05,
+                                 seed=seed, literal=lit)
+                st = _hom(orc, cfg, v, [0, n])
+                props = 0.0
+                for _ in range(steps):
+                    st.step(1)
+                    props += st.stats["proposals"][0]
+                mo = st.moments()[0]
+                out[lit].append([mo[8], mo[10], props])
+        a, b = np.array(out[0]), np.array(out[1])
+        for k in cols:
+            se = math.sqrt(a[:, k].var() / len(a) + b[:, k].var() / len(b))
+            assert abs(a[:, k].mean() - b[:, k].mean()) < 4.5 * se + 1e-9, (m, k, a[:, k].mean(), b[:, k].mean(), se)
 
 
 def test_hs_majorant_bounds_pairwise_max(orc):
@@ -209,12 +350,24 @@ def test_plan_structure(orc):
         assert len(np.unique(s)) == len(s)
         assert np.array_equal(np.sort(L["j"]), np.arange(len(L)))
     last = {}
+    top = int(log["level"].max())
+    cons = np.zeros(top + 1, dtype=np.int64)           # demands on pool a (samples of f_a)
     for r in log:                                       # log order = execution order
-        for s in (r["slot_i"], r["slot_k"]):
-            assert last.get(s, 0) < r["level"]
+        a = [last.get(s, 0) for s in (r["slot_i"], r["slot_k"])]
+        # a level-d collision takes one sample of f_a and one of f_{d-1-a} (eq. CF)
+        assert a[0] + a[1] == r["level"] - 1
+        for s, lev in zip((r["slot_i"], r["slot_k"]), a):
+            assert lev < r["level"]
+            cons[lev] += 1
             last[s] = r["level"]
     # leaves are exactly the slots touched by collisions
-    assert len(last) == st.stats["leaves"][0]
+    assert len(last) == st.stats["leaves"][0] == cons[0]
+    # top-down counts: C_d = ceil((N_d + cons_d)/2) with N_d the Alg 4.2 split (P:487-505 [R14])
+    N, rem, depth = orc.split(st.stats["p"][0], n, 12, seed=7, gcell=0, step=0)
+    assert depth == st.stats["depth"][0] and depth >= 4
+    for d in range(1, top + 1):
+        C = int((log["level"] == d).sum())
+        assert C == (N[d] + cons[d] + 1) // 2, (d, C, N[d], cons[d])
 
 
 def test_rad_keep_and_extend_prefix(orc):
@@ -401,3 +554,67 @@ def test_majorant_update_maxwell_and_no_violation_identity(orc):
         assert a.stats["violations"].sum() == 0
         for k in ("vx", "vy", "vz"):
             np.testing.assert_array_equal(getattr(a, k), getattr(b, k))
+
+
+def _plane_trees(k):
+    """All ordered binary trees with k internal nodes (None = an f_0 leaf)."""
+    if k == 0:
+        return [None]
+    return [(l, r) for a in range(k) for l in _plane_trees(a) for r in _plane_trees(k - 1 - a)]
+
+
+def _size(t):
+    return 0 if t is None else 1 + _size(t[0]) + _size(t[1])
+
+
+def _wild_prob(t):
+    """Probability of McKean tree t among f_k samples: prod over internal nodes v of
+    1/k_v, k_v = internal nodes of v's subtree - the uniform split of eq. CF
+    (f_{k+1} = 1/(k+1) sum_h P(f_h, f_{k-h}); "uniformly")."""
+    if t is None:
+        return 1.0
+    return _wild_prob(t[0]) * _wild_prob(t[1]) / _size(t)
+
+
+def test_wild_tree_shape_law_enumeration():
+    """SURVEY App A.1: the shape law sums to 1 for every k <= 7 (Catalan(k) shapes);
+    k = 2: two shapes at 1/2; k = 3: {1/6, 1/6, 1/3, 1/6, 1/6}."""
+    catalan = [1, 1, 2, 5, 14, 42, 132, 429]
+    for k in range(8):
+        ts = _plane_trees(k)
+        assert len(ts) == catalan[k]
+        assert sum(_wild_prob(t) for t in ts) == pytest.approx(1.0, abs=1e-14)
+    assert sorted(_wild_prob(t) for t in _plane_trees(2)) == [0.5, 0.5]
+    assert sorted(_wild_prob(t) for t in _plane_trees(3)) == pytest.approx([1 / 6] * 4 + [1 / 3])
+
+
+def test_plan_tree_shapes_follow_wild_law(orc):
+    """The oracle's plan realises the Wild tree law: the McKean tree of every
+    level-d collision (rebuilt from the decision log: the shapes of the two input
+    samples, in order) is distributed as prod 1/k_v over the Catalan(d) ordered
+    shapes, d = 3, 4, 5 (chi^2).  Catches a non-uniform type draw and a matching
+    that pairs correlated samples (e.g. the two outputs of one collision at a
+    symmetric split: the (f_2, f_2) diagonal at d = 5)."""
+    from scipy import stats
+    n = 200_000
+    v = synth.anisotropic_gaussian(n, seed=11)
+    st = _hom(orc, orc.Config(model=0, m_fixed=6, eps=1.0, dt=1.2, seed=11), v, [0, n],
+              log_cap=2_000_000)
+    st.step(1)
+    log = st.collisions()
+    assert st.log_n == len(log)
+    shape = {}
+    counts = {3: {}, 4: {}, 5: {}}
+    for r in log:
+        t = (shape.get(r["slot_i"]), shape.get(r["slot_k"]))
+        shape[r["slot_i"]] = shape[r["slot_k"]] = t
+        d = int(r["level"])
+        assert _size(t) == d
+        if d in counts:
+            counts[d][t] = counts[d].get(t, 0) + 1
+    for d, c in counts.items():
+        ts = _plane_trees(d)
+        obs = np.array([c.get(t, 0) for t in ts], dtype=float)
+        assert obs.sum() == sum(c.values()) and obs.sum() > 40 * len(ts)
+        exp = np.array([_wild_prob(t) for t in ts]) * obs.sum()
+        assert stats.chisquare(obs, exp).pvalue > 1e-4, (d, obs, exp)
