@@ -1,16 +1,22 @@
 #!/usr/bin/env python
 """TRMC-R benchmark (driver contract).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c5|c4|c2|c1]
-                    [--impl trmcr|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5|c3|c4|c2|c1]
+                    [--secondary c3|none] [--impl trmcr|reference]
 
 Prints ONE JSON line (rank 0).  Metric: particle-updates/s of the TRMC-R
-step (BASELINE.json).  Default workload: configs[2], the batched ensemble of
-16,384 independent hard-sphere cells x 1,024 particles (16.8 M particles,
-fp32, eps = 0.01, dt = 0.1) sharded across GPUs by cell with an NCCL
-all-reduce of the global moments every step (DESIGN.md §7 explains the
-choice).  Inputs (201 MB) are larger than L2 (126 MB): no flush needed.
+step (BASELINE.json).  Default workload: configs[4], the large Mach-5 1D
+shock (65,536 cells, 65.5 M fp32 particles, eps = 0.01, RAD): the north
+star's "large shock workload" - a full step is reservoirs + transport (A1),
+the counting sort by cell (A2) and the collision step (A3-A8); its 1.05 GB of
+state exceeds L2 (126 MB), so no flush is needed.  Slab-partitioned across
+GPUs (strong scaling) with a neighbour exchange.  The same line carries
+configs[2] (16,384 independent hard-sphere cells x 1,024, eps = 0.01) as the
+"secondary" record (sharded by cell, strong scaling, NCCL all-reduce of the
+global moments every step).
 
+--gpus N > 1 without torchrun: the script re-launches itself under
+torch.distributed.run (one process per GPU, 127.0.0.1 rendezvous).
 --impl reference times the CPU oracle (oracle/, single-threaded, fp64) on a
 bounded sample of the same workload (the tier's reference arm).
 """
@@ -40,18 +46,31 @@ UNIT = "particle-updates/s"
 # ----------------------------------------------------------------------------- workloads
 def workload(name: str, rank: int = 0, world: int = 1, eps_override=None):
     """Synthetic inputs shaped like BASELINE.json configs."""
-    if name == "c3":
-        # independent cells: weak scaling (tier rule 5) - every rank owns a full
-        # 16,384-cell ensemble with its own global cell ids (own RNG streams)
+    if name in ("c3", "c3weak"):
+        # configs[2]: ONE 16,384-cell ensemble sharded across the GPUs by contiguous
+        # global cell ranges (strong scaling; RNG keyed by global cell id, so a
+        # cell's result does not depend on the GPU count).  c3weak: every GPU owns
+        # a full ensemble of its own (weak scaling, secondary).
         ncells, ppc = 16_384, 1024
         vx, vy, vz, off = synth.bimodal_cells(ncells, ppc, seed=1)
-        return dict(kind="hom", vx=vx, vy=vy, vz=vz, offsets=off, cell_base=rank * ncells, dtype=np.float32,
+        weak = name == "c3weak"
+        if weak:
+            lo, cells_here, base = 0, ncells, rank * ncells
+        else:
+            from paper_1009_2768_b200 import dist as D
+            off, base, sl = D.shard_homogeneous(off, rank, world)
+            vx, vy, vz = vx[sl], vy[sl], vz[sl]
+            cells_here = len(off) - 1
+        return dict(kind="hom", vx=vx, vy=vy, vz=vz, offsets=off, cell_base=base, dtype=np.float32,
                     kw=dict(model=1, m_fixed=64, eps=eps_override or 0.01, dt=0.1, seed=1),
-                    cfg=dict(workload="configs[2] batched homogeneous hard spheres", cells_per_gpu=ncells,
-                             ppc=ppc, particles_per_gpu=ncells * ppc, cells=ncells * world,
+                    cfg=dict(workload="configs[2] batched homogeneous hard spheres", cells_per_gpu=cells_here,
+                             ppc=ppc, cells=ncells * (world if weak else 1),
+                             particles=ncells * ppc * (world if weak else 1),
                              eps=eps_override or 0.01, dt=0.1, truncation="TRMC-R m=64",
-                             sharding="cells (weak: 16,384 cells per GPU)", global_moments="allreduce/step"),
-                    global_cells=ncells * world, scaling="weak")
+                             sharding=("cells (weak: 16,384 cells per GPU)" if weak else
+                                       "one 16,384-cell ensemble sharded by cell (strong)"),
+                             global_moments="allreduce/step"),
+                    global_cells=ncells * (world if weak else 1), scaling="weak" if weak else "strong")
     if name in ("c4", "c5"):
         if name == "c4":
             setup = synth.shock_setup(mach=3.0, ncells=2000, n_total=1_000_000, x_min=-20, x_max=20)
@@ -237,23 +256,25 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
-def run_trmcr(args, rank, world, local_rank):
+def measure(args, wl_name, rank, world, local_rank, cpu_seconds):
+    """Time K steps of workload wl_name on this rank's GPU; the JSON record (rank 0)."""
     import torch
     import torch.distributed as dist
     from paper_1009_2768_b200 import api
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    W = workload(args.workload, rank, world, args.eps)
+    W = workload(wl_name, rank, world, args.eps if wl_name == args.workload else None)
     td = torch.float32 if W["dtype"] == np.float32 else torch.float64
     T = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(device=dev, dtype=td)
     stream = torch.cuda.current_stream(dev)
+    from paper_1009_2768_b200 import dist as D
     if W["kind"] == "hom":
         sim = api.Simulation(T(W["vx"]), T(W["vy"]), T(W["vz"]), offsets=W["offsets"],
                              cell_base=W["cell_base"], stream=stream.cuda_stream, **W["kw"])
         n_local = int(W["offsets"][-1])
+        slab = None
     else:
-        from paper_1009_2768_b200 import dist as D
         slab = D.ShockSlab(api, W["setup"], W["first"], W["local_cells"], T(W["vx"]), T(W["vy"]), T(W["vz"]),
                            x=T(W["x"]), device=dev, stream=stream.cuda_stream, **W["kw"])
         sim = slab.sim
@@ -264,7 +285,7 @@ def run_trmcr(args, rank, world, local_rank):
     gms = [torch.zeros(len(api.GLOBAL_FIELDS), dtype=torch.float64, device=dev) for _ in range(2)]
     pending = [None, None]
     counter = [0]
-    xchg = lambda s: D.exchange_p2p(s.send_l, s.send_r, s.recv_l, s.recv_r, rank, world)
+    xchg = lambda s_: D.exchange_p2p(s_.send_l, s_.send_r, s_.recv_l, s_.recv_r, rank, world)
 
     def one_step():
         if W["kind"] == "hom":
@@ -338,9 +359,7 @@ def run_trmcr(args, rank, world, local_rank):
     dom, (dom_ms, dom_n) = max(ktimes.items(), key=lambda kv: kv[1][0])
     rs = 4 if td == torch.float32 else 8
     if dom in ("cell_step_smem", "cell_step_gmem", "thermal_warp_kernel", "cell_step_warp"):
-        bytes_per = 2 * 3 * rs            # read v, write the changed v (f_chg = 1 here)
-        if W["kind"] == "hom" and W["kw"]["eps"] > 0.05:
-            bytes_per = 2 * 3 * rs        # upper bound; changed fraction < 1 (dense write-back)
+        bytes_per = 2 * 3 * rs            # read v, write v (f_chg = 1: fluid regime)
     elif dom in ("shock_collide_smem", "shock_collide_gmem", "shock_collide_warp"):
         # SURVEY 8(d) D3, collision step: read every v, write the changed ones:
         # 3 rs (1 + f_chg), f_chg = 1 - untouched / n of this run's last step
@@ -354,45 +373,79 @@ def run_trmcr(args, rank, world, local_rank):
     else:
         bytes_per = 3 * rs
     peak, peak_kind = measured_peaks()
-    achieved = bytes_per * 0.5 * (n_before + n_after) / (dom_ms / dom_n * 1e-3) / 1e9
-    traffic = ncu_traffic(args.workload)
+    n_mean = 0.5 * (n_before + n_after)
+    achieved = bytes_per * n_mean / (dom_ms / dom_n * 1e-3) / 1e9
+    traffic = ncu_traffic(wl_name)
+    # the whole step against its fused minimum: homogeneous
+    # read + write v (6 rs), shock read + write (x, v) (8 rs) per particle
+    step_bytes = (6 if W["kind"] == "hom" else 8) * rs
+    step_gbs = step_bytes * n_mean * args.steps / (ms_local * 1e-3) / 1e9
     roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
             "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
             "traffic": traffic, "algorithmic_bytes_per_particle": round(bytes_per, 3),
             "kernel_share_of_step": round(dom_ms / ms_local, 4),
+            "step": {"algorithmic_bytes_per_particle": step_bytes, "achieved": round(step_gbs, 1),
+                     "frac": round(step_gbs / peak, 4)},
             "kernel_ms_probe": kernel_ms_probe}
 
-    # ---- e2e: host buffers through the public API (homogeneous: step_host) ----
-    e2e = None
+    # ---- e2e: host buffers through the public API, every step ----
+    ke = max(3, min(args.steps, 20))
+    out = np.zeros((sim.ncells, len(api.MOMENT_FIELDS)))
     if W["kind"] == "hom":
         hv = [torch.as_tensor(np.ascontiguousarray(W[k])).to(td).pin_memory().numpy() for k in ("vx", "vy", "vz")]
-        out = np.zeros((sim.ncells, len(api.MOMENT_FIELDS)))
-        ke = max(3, min(args.steps, 20))
-        sim.step_host(*hv, out=out)
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(ke):
+
+        def e2e_step():
             sim.step_host(*hv, out=out)
-        t_e2e = time.perf_counter() - t0
-        tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        h2d = 3 * rs * n_local
+        path = "Simulation.step_host (trmcr_step_host): pinned host velocities in, per-cell moments out"
+    else:
+        hv = [torch.as_tensor(np.ascontiguousarray(W[k])).to(td).pin_memory().numpy()
+              for k in ("x", "vx", "vy", "vz")]
+        h2d = 4 * rs * len(hv[0])
+        if slab.neighbors == 0:
+            def e2e_step():
+                sim.step_host_particles(*hv, out=out)
+            path = ("Simulation.step_host_particles (trmcr_step_host_particles): pinned host (x, v) in, "
+                    "rebinned on the device, one step, per-cell moments out")
+        else:
+            def e2e_step():
+                sim.set_particles(hv[1], hv[2], hv[3], x=hv[0])
+                slab.step(xchg)
+                out[:] = sim.moments()
+            path = ("Simulation.set_particles + ShockSlab.step + Simulation.moments: pinned host (x, v) of the "
+                    "slab in, one step with the neighbour exchange, per-cell moments out")
+    e2e_step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(ke):
+        e2e_step()
+    t_e2e = time.perf_counter() - t0
+    tt = torch.tensor([t_e2e, float(h2d), float(out.nbytes)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
+    e2e_updates = updates / args.steps        # particles per step, all ranks (state at the timed steps)
+    if W["kind"] == "shock":
+        tn = torch.tensor([float(sum(len(a) for a in hv[:1]))], dtype=torch.float64, device=dev)
         if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e = {"value": n_local * world * ke / float(tt.item()), "unit": UNIT,
-               "h2d_bytes_per_step": int(3 * rs * n_local * world),
-               "d2h_bytes_per_step": int(out.nbytes * world), "steps": ke,
-               "path": "Simulation.step_host (trmcr_step_host): pinned host velocities in, per-cell moments out"}
+            dist.all_reduce(tn)
+        e2e_updates = float(tn.item())
+    e2e = {"value": e2e_updates * ke / float(tt[0].item()), "unit": UNIT,
+           "h2d_bytes_per_step": int(tt[1].item()), "d2h_bytes_per_step": int(tt[2].item()), "steps": ke,
+           "path": path}
 
     if rank != 0:
-        return
+        sim.close()
+        return None
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        rate, info = oracle_rate(W, seconds=args.cpu_seconds)
+    if world == 1 and cpu_seconds > 0:
+        rate, info = oracle_rate(W, seconds=cpu_seconds)
         cpu = {"value": rate, "unit": UNIT, "cores": info["cores"], "kind": "oracle",
                "sample": info["sample"]}
     clocks = clk.summary()
     cfg = dict(W["cfg"])
-    cfg.update(parallelism=f"{'cells' if W['kind'] == 'hom' else 'single'}x{world}",
+    cfg.update(parallelism=f"{'cells' if W['kind'] == 'hom' else 'slabs'}x{world}",
                l2="inputs larger than L2 (no flush)" if n_local * 3 * rs > 126e6 else "inputs L2-resident")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -400,21 +453,51 @@ def run_trmcr(args, rank, world, local_rank):
             "dtype": "f32" if td == torch.float32 else "f64", "data": "synthetic", "config": cfg,
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks, "e2e": e2e,
             "gpu_launches": int(launches), "impl": "trmcr"}
-    print(json.dumps(line), flush=True)
     sim.close()
+    return line
+
+
+def run_trmcr(args, rank, world, local_rank):
+    line = measure(args, args.workload, rank, world, local_rank,
+                   0.0 if args.no_cpu_baseline else args.cpu_seconds)
+    sec = None
+    if args.secondary != "none" and args.secondary != args.workload:
+        import torch
+        torch.cuda.empty_cache()
+        sec = measure(args, args.secondary, rank, world, local_rank, 0.0)
+    if rank == 0:
+        if sec is not None:
+            sec.pop("cpu_baseline", None)
+            sec.pop("impl", None)
+            line["secondary"] = sec
+        print(json.dumps(line), flush=True)
+
+
+def self_launch(args):
+    """--gpus N > 1 outside torchrun: one process per GPU under torch.distributed.run."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c3weak", "c4", "c5"])
+    ap.add_argument("--secondary", default="c3", choices=["none", "c1", "c2", "c3", "c3weak", "c4", "c5"])
     ap.add_argument("--eps", type=float, default=None)
     ap.add_argument("--impl", default="trmcr", choices=["trmcr", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

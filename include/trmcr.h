@@ -198,6 +198,24 @@ trmcr_status trmcr_set_velocities(trmcr_ctx *ctx, const void *vx, const void *vy
 trmcr_status trmcr_step_host(trmcr_ctx *ctx, const void *vx, const void *vy, const void *vz,
                              double *host_moments);
 
+/* Replace the whole particle state (any geometry) from host (host = 1) or
+ * device memory: n particles, SoA in the context dtype.  HOMOGENEOUS: x must be
+ * NULL and n equal to the context's count (same cell layout; = set_velocities).
+ * SHOCK_1D: positions inside this slab and sorted by cell (validated); the
+ * cell offsets are rebuilt (count + scan on the device).  Synchronises.
+ * Errors: EINVAL (bad arrays, particle outside the slab or not sorted: the
+ * context then holds no particles until the next successful call, but stays
+ * usable), ECAPACITY (n > capacity). */
+trmcr_status trmcr_set_particles(trmcr_ctx *ctx, const void *x, const void *vx, const void *vy, const void *vz,
+                                 int64_t n, int32_t host);
+
+/* Host-buffer step for any geometry (the e2e path of the shock):
+ * trmcr_set_particles(host) + one step + per-cell moments to host_moments
+ * [n_cells * TRMCR_NMOMENTS].  A slab with neighbours returns EINVAL (it steps
+ * with trmcr_shock_begin / exchange / trmcr_shock_finish).  Syncs. */
+trmcr_status trmcr_step_host_particles(trmcr_ctx *ctx, const void *x, const void *vx, const void *vy,
+                                       const void *vz, int64_t n, double *host_moments);
+
 /* ---- 1D shock slab decomposition (multi-GPU) ----
  * Exchange buffer of `capacity` particles, trmcr_exchange_bytes() bytes, layout
  * [int32 count | pad to 16 B][capacity x][vx][vy][vz][capacity int32 global dest],

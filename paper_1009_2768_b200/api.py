@@ -84,6 +84,8 @@ def lib():
         L.trmcr_copy_particles.argtypes = [vp, vp, vp, vp, vp, vp, C.c_int32]
         L.trmcr_set_velocities.argtypes = [vp, vp, vp, vp, C.c_int32]
         L.trmcr_step_host.argtypes = [vp, vp, vp, vp, P(C.c_double)]
+        L.trmcr_set_particles.argtypes = [vp, vp, vp, vp, vp, C.c_int64, C.c_int32]
+        L.trmcr_step_host_particles.argtypes = [vp, vp, vp, vp, vp, C.c_int64, P(C.c_double)]
         L.trmcr_set_log.argtypes = [vp, C.c_int64]
         L.trmcr_get_log.argtypes = [vp, vp, P(C.c_int64)]
         L.trmcr_shock_sort_info.argtypes = [C.c_void_p, C.c_void_p]
@@ -112,7 +114,7 @@ def lib():
         L.trmcr_destroy.argtypes = [vp]
         for f in ("trmcr_init", "trmcr_step", "trmcr_moments", "trmcr_stats", "trmcr_num_particles",
                   "trmcr_copy_particles", "trmcr_set_velocities", "trmcr_step_host", "trmcr_set_log",
-                  "trmcr_get_log"):
+                  "trmcr_get_log", "trmcr_set_particles", "trmcr_step_host_particles"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -131,6 +133,32 @@ def _ptr(a):
     return a.ctypes.data, 1, {np.dtype(np.float32): F32, np.dtype(np.float64): F64}.get(a.dtype)
 
 
+def _arrays(arrays, dtype_code=None, n=None, host=None):
+    """Pointers of same-kind arrays: one dtype (= dtype_code if given), all host or
+    all device, one length (= n if given).  Raises instead of letting the library
+    read past a short array or misread its bytes."""
+    ptrs, kinds, codes, lens = [], set(), set(), set()
+    for a in arrays:
+        p, h, code = _ptr(a)
+        ptrs.append(p)
+        kinds.add(h)
+        codes.add(code)
+        lens.add(int(a.shape[0]))
+    if len(codes) != 1 or None in codes:
+        raise TypeError("particle arrays must share one dtype (float32 or float64)")
+    if dtype_code is not None and codes != {dtype_code}:
+        raise TypeError("particle arrays must have the context's dtype")
+    if len(kinds) != 1:
+        raise TypeError("particle arrays must be all host or all device memory")
+    if host is not None and kinds != {host}:
+        raise TypeError("host arrays required" if host else "device arrays required")
+    if len(lens) != 1:
+        raise ValueError("particle arrays must have one length")
+    if n is not None and lens != {n}:
+        raise ValueError(f"particle arrays must have length {n}")
+    return ptrs, kinds.pop(), codes.pop(), lens.pop()
+
+
 class Simulation:
     """A TRMC-R simulation on the current CUDA device (one context per device/stream).
 
@@ -147,15 +175,10 @@ class Simulation:
                  literal: bool = False):
         L = lib()
         self._keep = [vx, vy, vz, x]
-        pvx, host, dt_code = _ptr(vx)
-        pvy, _, _ = _ptr(vy)
-        pvz, _, _ = _ptr(vz)
-        if dt_code is None:
-            raise TypeError("velocities must be float32 or float64")
+        (pvx, pvy, pvz, *rest), host, dt_code, n = _arrays([vx, vy, vz] + ([x] if x is not None else []))
         self.dtype = dt_code
         self.host_init = host
-        n = int(vx.shape[0])
-        px = _ptr(x)[0] if x is not None else None
+        px = rest[0] if x is not None else None
         part = _Particles(dt_code, host, n, int(capacity), pvx, pvy, pvz, px)
         if shock is None:
             off = np.ascontiguousarray(offsets, dtype=np.int64)
@@ -238,16 +261,40 @@ class Simulation:
             out["x"] = x[:n]
         return out
 
-    def set_velocities(self, vx, vy, vz):
-        p, host, _ = _ptr(vx)
-        self._check(lib().trmcr_set_velocities(self._h, p, _ptr(vy)[0], _ptr(vz)[0], host))
-
-    def step_host(self, vx, vy, vz, out: Optional[np.ndarray] = None) -> np.ndarray:
-        """e2e path: host velocities in, one step, host per-cell moments out."""
+    def _moments_out(self, out):
         if out is None:
             out = np.zeros((self.ncells, len(MOMENT_FIELDS)))
-        self._check(lib().trmcr_step_host(self._h, _ptr(vx)[0], _ptr(vy)[0], _ptr(vz)[0],
-                                          out.ctypes.data_as(C.POINTER(C.c_double))))
+        if out.dtype != np.float64 or out.size < self.ncells * len(MOMENT_FIELDS) or not out.flags.c_contiguous:
+            raise ValueError("out must be a contiguous float64 array of ncells x 12")
+        return out
+
+    def set_velocities(self, vx, vy, vz):
+        (p, q, r), host, _, _ = _arrays([vx, vy, vz], self.dtype, self.num_particles())
+        self._check(lib().trmcr_set_velocities(self._h, p, q, r, host))
+
+    def step_host(self, vx, vy, vz, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """e2e path (homogeneous): host velocities in, one step, host per-cell moments out."""
+        out = self._moments_out(out)
+        (p, q, r), _, _, _ = _arrays([vx, vy, vz], self.dtype, self.num_particles(), host=1)
+        self._check(lib().trmcr_step_host(self._h, p, q, r, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def set_particles(self, vx, vy, vz, x=None):
+        """Replace the particle state (shock: positions sorted by cell; rebinned on the device)."""
+        arrs = [x, vx, vy, vz] if x is not None else [vx, vy, vz]
+        ptrs, host, _, n = _arrays(arrs, self.dtype)
+        px, (p, q, r) = (ptrs[0], ptrs[1:]) if x is not None else (None, ptrs)
+        self._check(lib().trmcr_set_particles(self._h, px, p, q, r, n, host))
+
+    def step_host_particles(self, x, vx, vy, vz, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """e2e path (any geometry): host particles in (shock: x sorted by cell), one step,
+        host per-cell moments out (trmcr_step_host_particles)."""
+        out = self._moments_out(out)
+        arrs = [x, vx, vy, vz] if x is not None else [vx, vy, vz]
+        ptrs, _, _, n = _arrays(arrs, self.dtype, host=1)
+        px, (p, q, r) = (ptrs[0], ptrs[1:]) if x is not None else (None, ptrs)
+        self._check(lib().trmcr_step_host_particles(self._h, px, p, q, r, n,
+                                                    out.ctypes.data_as(C.POINTER(C.c_double))))
         return out
 
     def set_log(self, capacity: int):

@@ -143,6 +143,7 @@ struct ShockState {
   int tile_ng = 4;                          // transport / sort tile = 1024 * tile_ng particles (1 or 4)
   unsigned long long *d_scan_status = nullptr;   // [ceil(C / 4096)] look-back status words of scan_offsets_lb
   uint32_t scan_epoch = 0;                  // per-call stamp of those words (30 bits used)
+  int scan_lb = 1;                          // multi-CTA look-back scan (else the one-CTA scan)
   int scatter = 1;                          // sort by scatter (TRMCR_SHOCK_SCATTER=0: gather in the collide kernel)
   unsigned long long *d_acct = nullptr;     // [4] injected L, injected R, dropped, generated
 };
@@ -298,10 +299,13 @@ inline trmcr_status check_launch(trmcr_ctx *c, const char *what, int kid = -1) {
   return TRMCR_OK;
 }
 
+// Device-side errors corrupt or drop part of the state: they are sticky (the
+// context returns TRMCR_ESTATE afterwards).
 inline trmcr_status sync_check(trmcr_ctx *c) {
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   int err = 0;
   CUDA_TRY(c, cudaMemcpy(&err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err & ~12) c->sticky = 1;
   if (err & 1) return fail(c, TRMCR_ECAPACITY, "a cell's collision tree exceeded the global-memory plan capacity");
   if (err & 2) return fail(c, TRMCR_ECAPACITY, "particle capacity exceeded (shock inflow)");
   if (err & 16) return fail(c, TRMCR_ECUDA, "internal fault: tree index out of range");

@@ -36,6 +36,7 @@ struct ShockDev {
   double x_min, x_max, inv_dx, dt;
   double rho[2], u[2], T[2], Lg[2], y[2];
   int cap_g;
+  int64_t cap;                 // particle capacity of the buffers: no store at or beyond it
 };
 
 constexpr int kDropped = INT32_MIN;   // destination of a particle that left the domain
@@ -98,6 +99,7 @@ __global__ void shock_bin_init(ShockDev S, const Real *__restrict__ x, int64_t n
 // (16-byte I/O) on full rounds, scalar on the ragged last one.
 __global__ void __launch_bounds__(1024) scan_offsets(const int32_t *__restrict__ counts, int C, int64_t *off,
                                                      int64_t cap, int *err) {
+  pdl_wait();   // no-op without programmatic dependent launch
   __shared__ int64_t wsum[32];
   __shared__ int64_t carry;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -165,6 +167,7 @@ __global__ void __launch_bounds__(1024) scan_offsets(const int32_t *__restrict__
     off[C] = carry;
     if (carry > cap) atomicOr(err, 2);
   }
+  pdl_trigger();
 }
 
 // Multi-CTA exclusive scan with decoupled look-back: CTA b scans its 4096
@@ -672,7 +675,7 @@ edge_place(ShockDev S, const int64_t *__restrict__ off_new, const int *ng, const
         __syncwarp();
         if (ok) {
           const int64_t pos = back ? base - rank : base + rank;
-          ox[pos] = a; ovx[pos] = bx; ovy[pos] = by; ovz[pos] = bz;
+          if (pos >= 0 && pos < S.cap) { ox[pos] = a; ovx[pos] = bx; ovy[pos] = by; ovz[pos] = bz; }
         }
       } else if (lane == 0) {
         while (*vturn != my_turn) {}
@@ -720,6 +723,7 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
   __shared__ int s_nb, s_more;
   const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (W[2]) return;                                   // gather fallback this step
+  if (off_new[S.C] > S.cap) return;                   // capacity exceeded (err set by the scan): no stores
   const int64_t n = off_old[S.C];
   const int64_t i_begin = (int64_t)t * TILE;
   if (i_begin >= n) return;
@@ -811,7 +815,7 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
       const int bin = bins[r0 + q];
       if (bin >= 0) {
         const int64_t pos = s_off[bin] + rk[r0 + q];
-        ox[pos] = a[q]; ovx[pos] = bx[q]; ovy[pos] = by[q]; ovz[pos] = bz[q];
+        if (pos < S.cap) { ox[pos] = a[q]; ovx[pos] = bx[q]; ovy[pos] = by[q]; ovz[pos] = bz[q]; }
       }
     }
   }
@@ -1007,6 +1011,7 @@ shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, int *defer_count,
                    int *defer_list, QueueArgs Q) {
   pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
+  if (off_new[S.C] > S.cap) { pdl_trigger(); return; }   // capacity exceeded (err set by the scan): no stores
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char *slab = smem + (size_t)warp * Lay.per_warp;
@@ -1067,6 +1072,7 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, int *defer_count,
                    int *defer_list, QueueArgs Q) {
   pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
+  if (off_new[S.C] > S.cap) { pdl_trigger(); return; }   // capacity exceeded (err set by the scan): no stores
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char *slab = smem + (size_t)warp * Lay.per_warp;
@@ -1129,6 +1135,7 @@ shock_collide_smem(StepParams P, SmemLayout Lay, ShockDev S, GatherSrc G, const 
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats,
                    const int *list_count, const int *list, QueueArgs Q) {
   pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
+  if (off_new[S.C] > S.cap) { pdl_trigger(); return; }   // capacity exceeded (err set by the scan): no stores
   BlockTeam team;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CellShared sh;
@@ -1164,6 +1171,7 @@ __global__ void __launch_bounds__(kGmemThreads)
 shock_collide_gmem(StepParams P, GmemScratch GS, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, QueueArgs Q) {
   pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
+  if (off_new[S.C] > S.cap) { pdl_trigger(); return; }   // capacity exceeded (err set by the scan): no stores
   BlockTeam team;
   __shared__ CellShared sh;
   __shared__ double red[32 * 8];
@@ -1198,8 +1206,11 @@ inline ShockDev shock_dev(const trmcr_ctx *c) {
     d.y[k] = s.rho[k] * s.Lg[k] / s.weight;
   }
   d.cap_g = s.cap_g;
+  d.cap = c->cap;
   return d;
 }
+
+inline trmcr_status shock_rebin(trmcr_ctx *c, int *max_cell);
 
 // Allocate shock state, validate + count the initial particles (inside this
 // slab, sorted by cell), build offsets.  Synchronises (init only).
@@ -1245,34 +1256,60 @@ inline trmcr_status shock_init(trmcr_ctx *c, const trmcr_cells *cc, int *max_cel
                     dalloc(c, &s.d_lcnt, sizeof(int32_t) * kEdgeBins)))
     return TRMCR_ENOMEM;
   const int scan_blocks = std::max(1, (s.C + kScanTile - 1) / kScanTile);
+  {   // decoupled look-back needs every scan CTA resident at once (spin-waits on predecessors)
+    int nsm = 148, occ = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_offsets_lb, kScanThreads, 0) != cudaSuccess) {
+      cudaGetLastError();
+      occ = 0;
+    }
+    s.scan_lb = scan_blocks <= nsm * occ / 2;
+  }
   if (dalloc(c, &s.d_scan_status, sizeof(unsigned long long) * scan_blocks)) return TRMCR_ENOMEM;
   CUDA_TRY(c, cudaMemsetAsync(s.d_scan_status, 0, sizeof(unsigned long long) * scan_blocks, c->stream));
   s.scan_epoch = 0;
-  CUDA_TRY(c, cudaMemsetAsync(s.d_counts, 0, sizeof(int32_t) * s.C, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(s.d_acct, 0, sizeof(unsigned long long) * 4, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(s.d_ng, 0, sizeof(int) * 2, c->stream));
+  c->cur = 0;
+  return shock_rebin(c, max_cell);
+}
+
+// Bin the c->n particles of buffer c->cur (positions inside this slab, sorted by
+// cell: validated) into d_off[cur]; *max_cell = the largest cell.  Used by init
+// and by trmcr_set_particles.  Synchronises.  EINVAL (not sticky) on bad input.
+inline trmcr_status shock_rebin(trmcr_ctx *c, int *max_cell) {
+  ShockState &s = c->shock;
+  const int cur = c->cur;
+  CUDA_TRY(c, cudaMemsetAsync(s.d_counts, 0, sizeof(int32_t) * s.C, c->stream));
   const ShockDev d = shock_dev(c);
   if (c->n > 0) {
     const unsigned blocks = (unsigned)((c->n + 255) / 256);
     if (c->dtype == TRMCR_F64)
-      shock_bin_init<double><<<blocks, 256, 0, c->stream>>>(d, (const double *)c->x[0], c->n, s.d_counts, c->d_err);
+      shock_bin_init<double><<<blocks, 256, 0, c->stream>>>(d, (const double *)c->x[cur], c->n, s.d_counts, c->d_err);
     else
-      shock_bin_init<float><<<blocks, 256, 0, c->stream>>>(d, (const float *)c->x[0], c->n, s.d_counts, c->d_err);
+      shock_bin_init<float><<<blocks, 256, 0, c->stream>>>(d, (const float *)c->x[cur], c->n, s.d_counts, c->d_err);
     if (auto e = check_launch(c, "shock_bin_init")) return e;
   }
-  scan_offsets<<<1, 1024, 0, c->stream>>>(s.d_counts, s.C, s.d_off[0], c->cap, c->d_err);
+  scan_offsets<<<1, 1024, 0, c->stream>>>(s.d_counts, s.C, s.d_off[cur], c->cap, c->d_err);
   if (auto e = check_launch(c, "scan_offsets")) return e;
   std::vector<int32_t> counts(s.C);
   CUDA_TRY(c, cudaMemcpyAsync(counts.data(), s.d_counts, sizeof(int32_t) * s.C, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   int err = 0;
   CUDA_TRY(c, cudaMemcpy(&err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost));
-  if (err & 4) return fail(c, TRMCR_EINVAL, "particle outside this slab of the shock domain");
-  if (err & 8) return fail(c, TRMCR_EINVAL, "shock particles must be sorted by cell (stable order)");
-  *max_cell = 0;
-  for (int32_t v : counts) *max_cell = std::max(*max_cell, (int)v);
-  c->cur = 0;
-  c->d_offsets = s.d_off[0];
+  c->d_offsets = s.d_off[cur];
+  if (err & 12) {                          // input errors: cleared, the call fails, the context stays usable
+    const int rest = err & ~12;
+    CUDA_TRY(c, cudaMemcpy(c->d_err, &rest, sizeof(int), cudaMemcpyHostToDevice));
+    c->n = 0;                                // no valid state until the next successful set
+    CUDA_TRY(c, cudaMemsetAsync(s.d_off[cur], 0, sizeof(int64_t) * (s.C + 1), c->stream));
+    if (err & 4) return fail(c, TRMCR_EINVAL, "particle outside this slab of the shock domain");
+    return fail(c, TRMCR_EINVAL, "shock particles must be sorted by cell (stable order)");
+  }
+  if (max_cell) {
+    *max_cell = 0;
+    for (int32_t v : counts) *max_cell = std::max(*max_cell, (int)v);
+  }
   return TRMCR_OK;
 }
 
@@ -1330,7 +1367,10 @@ trmcr_status shock_finish(trmcr_ctx *c) {
     if (auto e = check_launch(c, "immigrant_count")) return e;
   }
   prof_begin(c, TRMCR_K_SCAN);
-  launch_k(c, scan_offsets_lb, std::max(1, (s.C + kScanTile - 1) / kScanTile), kScanThreads, (size_t)(0), s.d_counts, s.C, s.d_off[nxt], c->cap, c->d_err, s.d_scan_status, next_scan_epoch(s));
+  if (s.scan_lb)
+    launch_k(c, scan_offsets_lb, std::max(1, (s.C + kScanTile - 1) / kScanTile), kScanThreads, (size_t)(0), s.d_counts, s.C, s.d_off[nxt], c->cap, c->d_err, s.d_scan_status, next_scan_epoch(s));
+  else   // more scan tiles than can be resident at once: the look-back could wait on an unscheduled CTA
+    launch_k(c, scan_offsets, 1, 1024, (size_t)(0), (const int32_t *)s.d_counts, s.C, s.d_off[nxt], c->cap, c->d_err);
   if (auto e = check_launch(c, "scan_offsets", TRMCR_K_SCAN)) return e;
 
   GatherSrc G;

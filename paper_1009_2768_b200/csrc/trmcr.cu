@@ -928,6 +928,36 @@ trmcr_status trmcr_set_velocities(trmcr_ctx *c, const void *vx, const void *vy, 
   return TRMCR_OK;
 }
 
+trmcr_status trmcr_set_particles(trmcr_ctx *c, const void *x, const void *vx, const void *vy, const void *vz,
+                                 int64_t n, int32_t host) {
+  if (!c) return fail(nullptr, TRMCR_EINVAL, "null ctx");
+  if (c->sticky) return TRMCR_ESTATE;
+  if (n < 0 || (n > 0 && (!vx || !vy || !vz))) return fail(c, TRMCR_EINVAL, "bad particle arrays");
+  if (c->geometry == TRMCR_HOMOGENEOUS) {
+    if (x) return fail(c, TRMCR_EINVAL, "homogeneous geometry takes no positions");
+    if (n != c->n) return fail(c, TRMCR_EINVAL, "homogeneous geometry: n must equal the context's particle count");
+    return n > 0 ? trmcr_set_velocities(c, vx, vy, vz, host) : TRMCR_OK;
+  }
+  if (n > 0 && !x) return fail(c, TRMCR_EINVAL, "shock geometry needs positions");
+  if (n > c->cap) return fail(c, TRMCR_ECAPACITY, "more particles than the context capacity");
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));   // the previous step may still read the buffers
+  const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  const void *src[4] = {x, vx, vy, vz};
+  void *dst[4] = {c->x[c->cur], c->v[c->cur][0], c->v[c->cur][1], c->v[c->cur][2]};
+  for (int k = 0; k < 4; ++k)
+    if (n > 0) CUDA_TRY(c, cudaMemcpyAsync(dst[k], src[k], (size_t)n * c->rs, kind, c->stream));
+  c->n = n;
+  return shock_rebin(c, nullptr);
+}
+
+trmcr_status trmcr_step_host_particles(trmcr_ctx *c, const void *x, const void *vx, const void *vy,
+                                       const void *vz, int64_t n, double *host_moments) {
+  if (!c || !host_moments) return fail(c, TRMCR_EINVAL, "null argument");
+  if (trmcr_status s = trmcr_set_particles(c, x, vx, vy, vz, n, 1)) return s;
+  if (trmcr_status s = do_step(c)) return s;
+  return trmcr_moments(c, host_moments);
+}
+
 trmcr_status trmcr_step_host(trmcr_ctx *c, const void *vx, const void *vy, const void *vz, double *host_moments) {
   if (!c || !host_moments) return fail(c, TRMCR_EINVAL, "null argument");
   if (c->geometry != TRMCR_HOMOGENEOUS) return fail(c, TRMCR_EINVAL, "trmcr_step_host: homogeneous geometry only");
@@ -940,6 +970,16 @@ trmcr_status trmcr_set_log(trmcr_ctx *c, int64_t capacity) {
   if (!c || capacity < 0) return fail(c, TRMCR_EINVAL, "bad argument");
   if (c->sticky) return TRMCR_ESTATE;
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (c->d_log && capacity > 0 && capacity <= c->log_cap) {   // reuse the buffer
+    c->log_cap = capacity;
+    c->P.log_on = 1;
+    CUDA_TRY(c, cudaMemset(c->d_log_count, 0, sizeof(unsigned long long)));
+    return TRMCR_OK;
+  }
+  if (c->d_log) {                                              // release the old buffer
+    c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void *)c->d_log), c->allocs.end());
+    cudaFree(c->d_log);
+  }
   c->d_log = nullptr;
   c->log_cap = 0;
   c->P.log_on = 0;

@@ -398,3 +398,38 @@ def test_shock_fp32_statistical_parity(orc, api):
         O.append(np.mean(ao, 0))
     z = _zstats(G, O).ravel()
     assert np.mean(z <= 3) >= 0.99 and z.max() <= 5, (np.mean(z <= 3), z.max())
+
+
+def test_shock_step_host_particles_parity(orc, api):
+    """The shock e2e call (trmcr_step_host_particles): host (x, v) in, rebinned on the
+    device, one step, per-cell moments out - equals the oracle's step of the same
+    state (step counter 0, then 1 on a fresh upload of the same state); a bad
+    upload (unsorted) is EINVAL and leaves the context usable."""
+    setup, sim, o = _shock_pair(orc, api, 3.0, 40, 8000, 0, 0.2, np.float64)
+    x, vx, vy, vz = (np.ascontiguousarray(a[:o.n]) for a in (o.x, o.vx, o.vy, o.vz))
+    mstate = None
+    for s in range(2):
+        out = sim.step_host_particles(x, vx, vy, vz)
+        ref = orc.ShockState(o.cfg, setup, x, vx, vy, vz)
+        ref.step_count = s
+        if mstate is not None:           # RAD's m_max per cell carries over (context state)
+            ref.m_state[:] = mstate
+        ref.step(1)
+        mstate = ref.m_state.copy()
+        mo = ref.moments()
+        np.testing.assert_array_equal(out[:, 0], mo[:, 0])
+        np.testing.assert_allclose(out[:, 1:11], mo[:, 1:11], rtol=1e-11, atol=1e-11)
+        g = sim.particles()
+        np.testing.assert_array_equal(g["offsets"], ref.offsets)
+        _cmp_v(g, ref.vx[:ref.n], ref.vy[:ref.n], ref.vz[:ref.n], ref.offsets)
+        _cmp_stats(sim.stats(), ref.stats)
+    bad = x[::-1].copy()
+    with pytest.raises(api.TrmcrError) as e:
+        sim.step_host_particles(bad, vx, vy, vz)
+    assert e.value.status == api.EINVAL
+    sim.set_particles(vx, vy, vz, x=x)
+    assert sim.num_particles() == len(x)
+    with pytest.raises(TypeError):
+        sim.set_particles(vx.astype(np.float32), vy, vz, x=x)
+    with pytest.raises(ValueError):
+        sim.set_particles(vx[:-1], vy, vz, x=x)
