@@ -360,6 +360,10 @@ def measure(args, wl_name, rank, world, local_rank, cpu_seconds):
     rs = 4 if td == torch.float32 else 8
     if dom in ("cell_step_smem", "cell_step_gmem", "thermal_warp_kernel", "cell_step_warp"):
         bytes_per = 2 * 3 * rs            # read v, write v (f_chg = 1: fluid regime)
+    elif dom == "shock_collide_warp" and W["kind"] == "shock" and sim.fused:
+        # the fused pass: transport + sort + collisions, reading and
+        # writing (x, v) once: SURVEY 8(d) D3's fused minimum, 8 rs per particle
+        bytes_per = 8 * rs
     elif dom in ("shock_collide_smem", "shock_collide_gmem", "shock_collide_warp"):
         # SURVEY 8(d) D3, collision step: read every v, write the changed ones:
         # 3 rs (1 + f_chg), f_chg = 1 - untouched / n of this run's last step

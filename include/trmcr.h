@@ -240,6 +240,13 @@ int64_t trmcr_exchange_bytes(int32_t dtype, int64_t capacity);
  * when the scatter sort is enabled for this context.  EINVAL for a
  * homogeneous context. */
 trmcr_status trmcr_shock_sort_info(trmcr_ctx *ctx, int64_t *out4);
+/* 1 when this shock context steps with the fused pass (transport,
+ * sort and collisions in one pass over the particles, 33 B per fp32 particle
+ * instead of 68; enabled at init by TRMCR_SHOCK_FUSED=1 when particles move less
+ * than a cell per step, =2 always), 0 for the three-pass step (the default: it
+ * is faster on B200) or a homogeneous context.  Results are
+ * bitwise identical. */
+int32_t trmcr_shock_fused(const trmcr_ctx *ctx);
 trmcr_status trmcr_shock_set_exchange(trmcr_ctx *ctx, void *send_left, void *send_right,
                                       void *recv_left, void *recv_right, int64_t capacity);
 trmcr_status trmcr_shock_begin(trmcr_ctx *ctx);

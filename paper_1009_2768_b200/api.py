@@ -92,6 +92,8 @@ def lib():
         L.trmcr_shock_sort_info.restype = C.c_int
         L.trmcr_exchange_bytes.argtypes = [C.c_int32, C.c_int64]
         L.trmcr_exchange_bytes.restype = C.c_int64
+        L.trmcr_shock_fused.argtypes = [vp]
+        L.trmcr_shock_fused.restype = C.c_int32
         L.trmcr_shock_set_exchange.argtypes = [vp, vp, vp, vp, vp, C.c_int64]
         L.trmcr_shock_set_exchange.restype = C.c_int
         L.trmcr_shock_begin.argtypes = [vp]
@@ -323,6 +325,11 @@ class Simulation:
         self._check(lib().trmcr_shock_sort_info(self._h, out.ctypes.data))
         return {"W": int(out[0]), "emigrant_width": int(out[1]), "gathered": bool(out[2]),
                 "scatter_enabled": bool(out[3])}
+
+    @property
+    def fused(self) -> bool:
+        """The shock context steps with the fused pass (trmcr_shock_fused)."""
+        return bool(lib().trmcr_shock_fused(self._h))
 
     def exchange_bytes(self, capacity: int) -> int:
         return int(lib().trmcr_exchange_bytes(self.dtype, int(capacity)))

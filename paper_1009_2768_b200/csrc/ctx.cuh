@@ -146,6 +146,15 @@ struct ShockState {
   int scan_lb = 1;                          // multi-CTA look-back scan (else the one-CTA scan)
   int scatter = 1;                          // sort by scatter (TRMCR_SHOCK_SCATTER=0: gather in the collide kernel)
   unsigned long long *d_acct = nullptr;     // [4] injected L, injected R, dropped, generated
+  // fused step (fused.cuh): move codes of each buffer, per-cell code counts,
+  // far-mover lists (parity = the buffer described)
+  int fused = 0;                            // this context steps with the fused pass
+  int codes_ok = 0;                         // the codes of buffer cur are current
+  int8_t *d_code[2] = {nullptr, nullptr};
+  int32_t *d_nlsr[2] = {nullptr, nullptr};
+  int32_t *d_far_src[2] = {nullptr, nullptr}, *d_far_dst[2] = {nullptr, nullptr};
+  int *d_far_cnt = nullptr;
+  int far_cap = 0;
 };
 
 thread_local inline std::string g_init_error;
@@ -311,6 +320,7 @@ inline trmcr_status sync_check(trmcr_ctx *c) {
   if (err & 16) return fail(c, TRMCR_ECUDA, "internal fault: tree index out of range");
   if (err & 32) return fail(c, TRMCR_ECAPACITY, "a particle crossed more than one slab in a step");
   if (err & 64) return fail(c, TRMCR_ECAPACITY, "literal mode: the trees needed more f_0 particles than the cell holds");
+  if (err & 128) return fail(c, TRMCR_ECAPACITY, "fused shock step: too many particles moved two or more cells in one step (far-mover list full; lower dt or set TRMCR_SHOCK_FUSED=0)");
   return TRMCR_OK;
 }
 

@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_offsets_lb(const int32_t *_
 // and draws the number of reservoir ghosts per side.
 __global__ void __launch_bounds__(256) shock_prologue(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, int *ng,
                                                       int *err, int32_t *counts, int *W, unsigned long long *acct,
-                                                      int *ovf_count, int *defer_count) {
+                                                      int *ovf_count, int *defer_count, int *far_cnt_next) {
   pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < S.C; i += gridDim.x * blockDim.x) counts[i] = 0;
   if (blockIdx.x != 0) return;
@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(256) shock_prologue(ShockDev S, uint32_t k0, u
   if (threadIdx.x < 4) acct[threadIdx.x] = 0ull;
   if (threadIdx.x == 4) *ovf_count = 0;
   if (threadIdx.x == 5) *defer_count = 0;
+  if (threadIdx.x == 6 && far_cnt_next) *far_cnt_next = 0;   // fused step: the far list this step writes
   const int side = threadIdx.x;
   if (side > 1) return;
   if (side == 0 ? S.has_left : S.has_right) { ng[side] = 0; return; }   // a neighbour, not a reservoir
@@ -1129,9 +1130,14 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
   pdl_trigger();
 }
 
+}  // namespace trmcr
+#include "fused.cuh"
+namespace trmcr {
+
 template <typename Real, int THREADS>
 __global__ void __launch_bounds__(THREADS, 768 / THREADS)
-shock_collide_smem(StepParams P, SmemLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
+shock_collide_smem(StepParams P, SmemLayout Lay, ShockDev S, GatherSrc G, FusedDev F, int par_in, int fused,
+                   const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats,
                    const int *list_count, const int *list, QueueArgs Q) {
   pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
@@ -1150,12 +1156,25 @@ shock_collide_smem(StepParams P, SmemLayout Lay, ShockDev S, GatherSrc G, const 
   int rc = kOverflow;
   if (n <= B.n_cap) {
     PHASE_MARK(t_g);
-    gather_cell<Real>(S, G, c, B.vx, B.vy, B.vz, ox + base, wcnt);
+    if (fused) {   // re-place the cell from the source (the fused pass may have left it half-stepped)
+      if (threadIdx.x < 32)
+        gather_fused_warp<Real>(S, G, F, par_in, c, ox + base, ovx + base, ovy + base, ovz + base, n);
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        B.vx[i] = ovx[base + i]; B.vy[i] = ovy[base + i]; B.vz[i] = ovz[base + i];
+      }
+    } else {
+      gather_cell<Real>(S, G, c, B.vx, B.vy, B.vz, ox + base, wcnt);
+    }
     __syncthreads();
     PHASE_ADD(8, t_g);   // gather
     rc = process_cell<Real, false, true>(team, P, B, sh, nullptr, nullptr, nullptr, ovx + base, ovy + base,
                                          ovz + base, n, P.cell_base + (uint32_t)c, m_state + c,
                                          stats + (size_t)c * TRMCR_NSTATS, Q.log, Q.log_count, Q.log_cap);
+    if (fused && rc == kOk) {
+      __syncthreads();
+      if (threadIdx.x < 32) warp_codes<Real>(S, F, par_in ^ 1, c, base, n, ox, ovx, Q.err);
+    }
   }
   if (rc != kOk && threadIdx.x == 0) {
     const int j = atomicAdd(Q.ovf_count, 1);
@@ -1168,7 +1187,8 @@ shock_collide_smem(StepParams P, SmemLayout Lay, ShockDev S, GatherSrc G, const 
 
 template <typename Real>
 __global__ void __launch_bounds__(kGmemThreads)
-shock_collide_gmem(StepParams P, GmemScratch GS, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
+shock_collide_gmem(StepParams P, GmemScratch GS, ShockDev S, GatherSrc G, FusedDev F, int par_in, int fused,
+                   const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, QueueArgs Q) {
   pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   if (off_new[S.C] > S.cap) { pdl_trigger(); return; }   // capacity exceeded (err set by the scan): no stores
@@ -1184,16 +1204,36 @@ shock_collide_gmem(StepParams P, GmemScratch GS, ShockDev S, GatherSrc G, const 
     const int64_t base = off_new[c];
     const int n = (int)(off_new[c + 1] - base);
     B.vx = ovx + base; B.vy = ovy + base; B.vz = ovz + base;
-    gather_cell<Real>(S, G, c, B.vx, B.vy, B.vz, ox + base, wcnt);
+    if (fused) {
+      if (threadIdx.x < 32)
+        gather_fused_warp<Real>(S, G, F, par_in, c, ox + base, ovx + base, ovy + base, ovz + base, n);
+    } else {
+      gather_cell<Real>(S, G, c, B.vx, B.vy, B.vz, ox + base, wcnt);
+    }
     __syncthreads();
     const int rc = process_cell<Real, false, false>(team, P, B, sh, nullptr, nullptr, nullptr, B.vx, B.vy, B.vz, n,
                                                     P.cell_base + (uint32_t)c, m_state + c,
                                                     stats + (size_t)c * TRMCR_NSTATS, Q.log, Q.log_count,
                                                     Q.log_cap);
     if (rc != kOk && threadIdx.x == 0) atomicOr(Q.err, 1);
+    if (fused && rc == kOk) {
+      __syncthreads();
+      if (threadIdx.x < 32) warp_codes<Real>(S, F, par_in ^ 1, c, base, n, ox, ovx, Q.err);
+    }
     __syncthreads();
   }
   pdl_trigger();
+}
+
+inline FusedDev fused_dev(const trmcr_ctx *c) {
+  const ShockState &s = c->shock;
+  FusedDev f;
+  for (int k = 0; k < 2; ++k) {
+    f.code[k] = s.d_code[k]; f.nlsr[k] = s.d_nlsr[k]; f.far_src[k] = s.d_far_src[k]; f.far_dst[k] = s.d_far_dst[k];
+  }
+  f.far_cnt = s.d_far_cnt;
+  f.far_cap = s.far_cap;
+  return f;
 }
 
 inline ShockDev shock_dev(const trmcr_ctx *c) {
@@ -1280,6 +1320,7 @@ inline trmcr_status shock_init(trmcr_ctx *c, const trmcr_cells *cc, int *max_cel
 inline trmcr_status shock_rebin(trmcr_ctx *c, int *max_cell) {
   ShockState &s = c->shock;
   const int cur = c->cur;
+  s.codes_ok = 0;
   CUDA_TRY(c, cudaMemsetAsync(s.d_counts, 0, sizeof(int32_t) * s.C, c->stream));
   const ShockDev d = shock_dev(c);
   if (c->n > 0) {
@@ -1313,6 +1354,25 @@ inline trmcr_status shock_rebin(trmcr_ctx *c, int *max_cell) {
   return TRMCR_OK;
 }
 
+// Sources of the current step's gathers (buffer cur, ghosts, immigrants).
+inline GatherSrc gather_src(const trmcr_ctx *c) {
+  const ShockState &s = c->shock;
+  const int cur = c->cur;
+  GatherSrc G;
+  G.off_old = s.d_off[cur]; G.ng = s.d_ng; G.W = s.d_W;
+  G.x = c->x[cur]; G.vx = c->v[cur][0]; G.vy = c->v[cur][1]; G.vz = c->v[cur][2]; G.dest = s.d_dest;
+  for (int k = 0; k < 2; ++k) {
+    G.gx[k] = s.gx[k]; G.gvx[k] = s.gv[k][0]; G.gvy[k] = s.gv[k][1]; G.gvz[k] = s.gv[k][2];
+    G.gdest[k] = s.d_gdest[k];
+  }
+  G.recv[0] = s.has_left ? s.xrecv[0] : nullptr;
+  G.recv[1] = s.has_right ? s.xrecv[1] : nullptr;
+  G.xcap = s.xcap;
+  G.cbase = s.cbase;
+  G.scatter = 0;
+  return G;
+}
+
 // Phase 1 of a shock step: reservoirs, transport, counts, emigrant packing.
 template <typename Real>
 trmcr_status shock_begin(trmcr_ctx *c) {
@@ -1322,8 +1382,15 @@ trmcr_status shock_begin(trmcr_ctx *c) {
   prof_begin(c, TRMCR_K_GHOST_COUNT);
 
   launch_k(c, shock_prologue, std::max(1, std::min(32, (s.C + 4095) / 4096)), 256, (size_t)(0), d, c->P.k0, c->P.k1, c->step, s.d_ng, c->d_err, s.d_counts, s.d_W, s.d_acct, c->d_ovf_count,
-      c->d_defer_count);
+      c->d_defer_count, s.fused ? s.d_far_cnt + (cur ^ 1) : (int *)nullptr);
   if (auto e = check_launch(c, "shock_prologue", TRMCR_K_GHOST_COUNT)) return e;
+  if (s.fused && !s.codes_ok) {   // codes of the current state (after init / an upload)
+    CUDA_TRY(c, cudaMemsetAsync(s.d_far_cnt + cur, 0, sizeof(int), c->stream));
+    launch_k(c, codes_kernel<Real>, std::max(1, std::min(148 * 8, (s.C + 7) / 8)), 256, (size_t)0, d, fused_dev(c), cur,
+             (const int64_t *)s.d_off[cur], (const Real *)c->x[cur], (const Real *)c->v[cur][0], c->d_err);
+    if (auto e = check_launch(c, "codes_kernel")) return e;
+    s.codes_ok = 1;
+  }
   {
     dim3 grid((unsigned)((s.cap_g + 255) / 256), 2);
     prof_begin(c, TRMCR_K_GHOST_GEN);
@@ -1331,6 +1398,17 @@ trmcr_status shock_begin(trmcr_ctx *c) {
         (Real *)s.gv[0][1], (Real *)s.gv[0][2], (Real *)s.gv[1][0], (Real *)s.gv[1][1], (Real *)s.gv[1][2],
         s.d_gdest[0], s.d_gdest[1], s.d_counts, s.d_W, s.d_acct);
     if (auto e = check_launch(c, "ghost_gen", TRMCR_K_GHOST_GEN)) return e;
+  }
+  if (s.fused) {
+    launch_k(c, far_count, 1, 256, (size_t)0, fused_dev(c), cur, s.d_counts, s.d_W);
+    if (auto e = check_launch(c, "far_count")) return e;
+    if (s.has_left || s.has_right) {
+      if (!s.xsend[0] && !s.xsend[1]) return fail(c, TRMCR_EINVAL, "slab exchange buffers not set (trmcr_shock_set_exchange)");
+      launch_k(c, pack_emigrants_fused<Real>, 2, 32, (size_t)0, d, gather_src(c), fused_dev(c), cur, s.xsend[0],
+               s.xsend[1], s.xcap, c->d_err);
+      if (auto e = check_launch(c, "pack_emigrants_fused")) return e;
+    }
+    return TRMCR_OK;
   }
   {
     const int per_block = tile_of(s.tile_ng);
@@ -1366,6 +1444,11 @@ trmcr_status shock_finish(trmcr_ctx *c) {
     launch_k(c, immigrant_count<Real>, grid, 256, (size_t)(0), d, s.xrecv[0], s.xrecv[1], s.xcap, s.d_counts, s.d_W, c->d_err);
     if (auto e = check_launch(c, "immigrant_count")) return e;
   }
+  if (s.fused) {
+    launch_k(c, fused_counts, std::max(1, std::min(148 * 4, (s.C + 255) / 256)), 256, (size_t)0, d,
+             (const int32_t *)s.d_nlsr[cur], s.d_counts);
+    if (auto e = check_launch(c, "fused_counts")) return e;
+  }
   prof_begin(c, TRMCR_K_SCAN);
   if (s.scan_lb)
     launch_k(c, scan_offsets_lb, std::max(1, (s.C + kScanTile - 1) / kScanTile), kScanThreads, (size_t)(0), s.d_counts, s.C, s.d_off[nxt], c->cap, c->d_err, s.d_scan_status, next_scan_epoch(s));
@@ -1373,23 +1456,22 @@ trmcr_status shock_finish(trmcr_ctx *c) {
     launch_k(c, scan_offsets, 1, 1024, (size_t)(0), (const int32_t *)s.d_counts, s.C, s.d_off[nxt], c->cap, c->d_err);
   if (auto e = check_launch(c, "scan_offsets", TRMCR_K_SCAN)) return e;
 
-  GatherSrc G;
-  G.off_old = s.d_off[cur]; G.ng = s.d_ng; G.W = s.d_W;
-  G.x = c->x[cur]; G.vx = c->v[cur][0]; G.vy = c->v[cur][1]; G.vz = c->v[cur][2]; G.dest = s.d_dest;
-  for (int k = 0; k < 2; ++k) {
-    G.gx[k] = s.gx[k]; G.gvx[k] = s.gv[k][0]; G.gvy[k] = s.gv[k][1]; G.gvz[k] = s.gv[k][2];
-    G.gdest[k] = s.d_gdest[k];
-  }
-  G.recv[0] = s.has_left ? s.xrecv[0] : nullptr;
-  G.recv[1] = s.has_right ? s.xrecv[1] : nullptr;
-  G.xcap = s.xcap;
-  G.cbase = s.cbase;
+  GatherSrc G = gather_src(c);
   QueueArgs Q{c->d_ovf_count, c->d_ovf_list, c->d_err, c->d_log, c->d_log_count, c->log_cap};
   c->P.step = c->step;
   Real *ox = (Real *)c->x[nxt], *ovx = (Real *)c->v[nxt][0], *ovy = (Real *)c->v[nxt][1], *ovz = (Real *)c->v[nxt][2];
   const bool use_warp = c->wlay.n_cap > 0;
-  G.scatter = s.scatter && use_warp && !c->wlay.v_smem;
-  if (G.scatter) {
+  const FusedDev F = fused_dev(c);
+  const int fz = s.fused;
+  G.scatter = !fz && s.scatter && use_warp && !c->wlay.v_smem;
+  if (fz) {
+    prof_begin(c, TRMCR_K_SHOCK_WARP);
+    const bool wb = ext_variant(c);
+    launch_k(c, (wb ? shock_fused_lock<Real, true> : shock_fused_lock<Real, false>), c->lock_grid, kLockWarps * 32,
+             (size_t)(c->lock_smem), c->P, c->wlay, d, G, F, cur, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate,
+             c->d_stats, c->d_defer_count, c->d_defer_list, Q);
+    if (auto e = check_launch(c, "shock_fused_lock", TRMCR_K_SHOCK_WARP)) return e;
+  } else if (G.scatter) {
     prof_begin(c, TRMCR_K_SCATTER);
     launch_k(c, edge_place<Real>, 2, kEdgeThreads, (size_t)(0), d, s.d_off[nxt], s.d_ng, G.recv[0], G.recv[1], s.xcap, (const Real *)s.gx[0], (const Real *)s.gv[0][0],
         (const Real *)s.gv[0][1], (const Real *)s.gv[0][2], s.d_gdest[0], (const Real *)s.gx[1],
@@ -1402,7 +1484,7 @@ trmcr_status shock_finish(trmcr_ctx *c) {
         s.d_W, ox, ovx, ovy, ovz);
     if (auto e = check_launch(c, "scatter_sorted", TRMCR_K_SCATTER)) return e;
   }
-  if (use_warp) {
+  if (use_warp && !fz) {
     prof_begin(c, TRMCR_K_SHOCK_WARP);
     const bool wb = ext_variant(c);
     if (G.scatter && c->lock_grid > 0)
@@ -1416,15 +1498,57 @@ trmcr_status shock_finish(trmcr_ctx *c) {
   prof_begin(c, TRMCR_K_SHOCK_SMEM);
   auto kern = c->smem_threads == 64 ? shock_collide_smem<Real, 64>
               : (c->smem_threads == 128 ? shock_collide_smem<Real, 128> : shock_collide_smem<Real, 256>);
-  launch_k(c, kern, use_warp ? c->smem_grid : s.C, c->smem_threads, (size_t)(c->lay.total), c->P, c->lay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats,
+  launch_k(c, kern, use_warp ? c->smem_grid : s.C, c->smem_threads, (size_t)(c->lay.total), c->P, c->lay, d, G, F, cur, fz, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats,
       use_warp ? c->d_defer_count : nullptr, use_warp ? c->d_defer_list : nullptr, Q);
   if (auto e = check_launch(c, "shock_collide_smem", TRMCR_K_SHOCK_SMEM)) return e;
   prof_begin(c, TRMCR_K_SHOCK_GMEM);
-  launch_k(c, shock_collide_gmem<Real>, c->G, c->gmem_threads, (size_t)(0), c->P, c->gs, d, G, s.d_off[nxt], ox, ovx, ovy,
+  launch_k(c, shock_collide_gmem<Real>, c->G, c->gmem_threads, (size_t)(0), c->P, c->gs, d, G, F, cur, fz, s.d_off[nxt], ox, ovx, ovy,
                                                                  ovz, c->d_mstate, c->d_stats, Q);
   if (auto e = check_launch(c, "shock_collide_gmem", TRMCR_K_SHOCK_GMEM)) return e;
   c->cur = nxt;
   c->d_offsets = s.d_off[nxt];
+  s.codes_ok = fz;     // every cell of the fused pass wrote the codes of its particles
+  return TRMCR_OK;
+}
+
+// Decide (after the warp / lock-step layout is known) whether this context steps
+// with the fused pass, and allocate its side data.  TRMCR_SHOCK_FUSED=1: fused
+// when the lock-step kernel is available and a reservoir particle at
+// |u_B| + 6 sqrt(T_B) moves less than 0.9 of a cell per step (farther movers are
+// still handled, through the far-mover list, but slowly); =2 forces it; unset or
+// 0: the three-pass step.  The default is the three-pass step: on C5 the fused
+// pass moves 2.64 GB per step instead of 4.5 GB but takes 3.4 ms instead of
+// 2.19 (its gather and move codes add ~45 % instructions to an issue-bound
+// kernel, while transport and sort run at 60-75 % of DRAM bandwidth on their
+// own).
+inline trmcr_status shock_fused_setup(trmcr_ctx *c) {
+  ShockState &s = c->shock;
+  s.fused = 0;
+  s.codes_ok = 0;
+  const char *fe = getenv("TRMCR_SHOCK_FUSED");
+  const int want = fe ? atoi(fe) : 0;
+  if (want == 0 || c->lock_grid <= 0 || c->wlay.n_cap <= 0 || c->wlay.v_smem) return TRMCR_OK;
+  const double vmax = std::max(fabs(s.u[0]) + 6.0 * sqrt(s.T[0]), fabs(s.u[1]) + 6.0 * sqrt(s.T[1]));
+  if (want != 2 && !(vmax * c->dt * s.inv_dx <= 0.9)) return TRMCR_OK;
+  s.far_cap = (int)std::min<int64_t>(std::max<int64_t>(c->cap / 64, 65536), c->cap);
+  for (int k = 0; k < 2; ++k)
+    if (dalloc(c, &s.d_code[k], (size_t)c->cap) || dalloc(c, &s.d_nlsr[k], sizeof(int32_t) * 3 * (size_t)s.C) ||
+        dalloc(c, &s.d_far_src[k], sizeof(int32_t) * (size_t)s.far_cap) ||
+        dalloc(c, &s.d_far_dst[k], sizeof(int32_t) * (size_t)s.far_cap))
+      return TRMCR_ENOMEM;
+  if (dalloc(c, &s.d_far_cnt, sizeof(int) * 2)) return TRMCR_ENOMEM;
+  CUDA_TRY(c, cudaMemsetAsync(s.d_far_cnt, 0, sizeof(int) * 2, c->stream));
+  const bool wbk = ext_variant(c);
+  const void *lf = c->dtype == TRMCR_F64
+                       ? (wbk ? (const void *)shock_fused_lock<double, true> : (const void *)shock_fused_lock<double, false>)
+                       : (wbk ? (const void *)shock_fused_lock<float, true> : (const void *)shock_fused_lock<float, false>);
+  int smem_max = 0;
+  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
+  cudaFuncAttributes a;
+  if (cudaFuncGetAttributes(&a, lf) != cudaSuccess ||
+      cudaFuncSetAttribute(lf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max - (int)a.sharedSizeBytes) != cudaSuccess)
+    return fail(c, TRMCR_ECUDA, "cudaFuncSetAttribute(shock_fused_lock) failed");
+  s.fused = 1;
   return TRMCR_OK;
 }
 

@@ -758,6 +758,9 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
     }
   }
 
+  if (c->geometry == TRMCR_SHOCK_1D)
+    if (trmcr_status s = shock_fused_setup(c)) return bail(s);
+
   // ---- global-memory plan scratch for large / overflowing cells ----
   const int n_cap_g = c->geometry == TRMCR_HOMOGENEOUS
                           ? std::max(max_cell, 32)
@@ -823,6 +826,10 @@ trmcr_status trmcr_shock_sort_info(trmcr_ctx *c, int64_t *out4) {
   out4[0] = w[0]; out4[1] = w[1]; out4[2] = w[2];
   out4[3] = c->shock.scatter && c->wlay.n_cap > 0 && !c->wlay.v_smem;
   return TRMCR_OK;
+}
+
+int32_t trmcr_shock_fused(const trmcr_ctx *c) {
+  return (c && c->geometry == TRMCR_SHOCK_1D) ? c->shock.fused : 0;
 }
 
 trmcr_status trmcr_shock_set_exchange(trmcr_ctx *c, void *send_left, void *send_right, void *recv_left,
@@ -925,6 +932,7 @@ trmcr_status trmcr_set_velocities(trmcr_ctx *c, const void *vx, const void *vy, 
   const void *src[3] = {vx, vy, vz};
   for (int k = 0; k < 3; ++k)
     if (c->n > 0) CUDA_TRY(c, cudaMemcpyAsync(c->v[c->cur][k], src[k], (size_t)c->n * c->rs, kind, c->stream));
+  c->shock.codes_ok = 0;   // the fused shock step recomputes the move codes
   return TRMCR_OK;
 }
 

@@ -295,12 +295,16 @@ def _shock_pair(orc, api, mach, ncells, ntot, steps, eps, dtype, seed=1, x_min=-
     return setup, sim, o
 
 
-@pytest.mark.parametrize("scatter", ["1", "0"])
-def test_shock_fp64_parity(orc, api, monkeypatch, scatter):
-    """Both sort paths: scatter_sorted + edge_place (default) and the gather
-    inside the collision kernels (TRMCR_SHOCK_SCATTER=0)."""
+@pytest.mark.parametrize("fused,scatter", [("1", "1"), ("0", "1"), ("0", "0")])
+def test_shock_fp64_parity(orc, api, monkeypatch, fused, scatter):
+    """Every step structure: the fused pass (default at CFL < 1: transport, sort
+    and collisions in one kernel, fused.cuh), the three-pass step with
+    scatter_sorted + edge_place, and the gather inside the collision kernels
+    (TRMCR_SHOCK_SCATTER=0)."""
+    monkeypatch.setenv("TRMCR_SHOCK_FUSED", fused)
     monkeypatch.setenv("TRMCR_SHOCK_SCATTER", scatter)
     setup, sim, o = _shock_pair(orc, api, 3.0, 40, 8000, 0, 0.2, np.float64)
+    assert sim.fused == (fused == "1")
     for s in range(8):
         sim.step(1)
         o.step(1)
@@ -324,6 +328,26 @@ def test_shock_fp64_parity_many_cells(orc, api):
         sim.step(1)
         o.step(1)
         assert not sim.sort_info()["gathered"]
+        g = sim.particles()
+        np.testing.assert_array_equal(g["offsets"], o.offsets)
+        n = o.n
+        np.testing.assert_allclose(g["x"], o.x[:n], rtol=0, atol=1e-12)
+        _cmp_v(g, o.vx[:n], o.vy[:n], o.vz[:n], o.offsets)
+        _cmp_stats(sim.stats(), o.stats)
+
+
+@pytest.mark.parametrize("cfl", [1.6, 2.5])
+def test_shock_fp64_parity_fused_far_movers(orc, api, monkeypatch, cfl):
+    """The fused pass forced at CFL > 1 (TRMCR_SHOCK_FUSED=2): particles moving two
+    or more cells in a step go through the far-mover list, ranked by source
+    index into their destination's canonical order - still the oracle's stable
+    sort, position for position."""
+    monkeypatch.setenv("TRMCR_SHOCK_FUSED", "2")
+    setup, sim, o = _shock_pair(orc, api, 3.0, 40, 8000, 0, 0.2, np.float64, cfl=cfl)
+    assert sim.fused
+    for s in range(5):
+        sim.step(1)
+        o.step(1)
         g = sim.particles()
         np.testing.assert_array_equal(g["offsets"], o.offsets)
         n = o.n

@@ -21,8 +21,13 @@ def _sorted_shock(setup, seed, dtype):
     return x[o], vx[o], vy[o], vz[o], np.bincount(cell.astype(int), minlength=setup["ncells"])
 
 
-@pytest.mark.parametrize("world,dtype", [(2, np.float64), (3, np.float64), (3, np.float32)])
-def test_slabs_match_single_domain(world, dtype):
+@pytest.mark.parametrize("world,dtype,fused_full,fused_slabs",
+                         [(2, np.float64, "1", "1"), (3, np.float64, "1", "1"), (3, np.float32, "1", "1"),
+                          (2, np.float64, "0", "0"), (3, np.float32, "0", "0"), (3, np.float64, "0", "1")])
+def test_slabs_match_single_domain(world, dtype, fused_full, fused_slabs, monkeypatch):
+    """fused_*: the fused pass (1) or the three-pass step (0) for the single
+    domain and for the slabs - the last case cross-checks the two step
+    structures (and the two emigrant packers) against each other."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_1009_2768_b200 import api, dist
@@ -31,7 +36,10 @@ def test_slabs_match_single_domain(world, dtype):
     td = torch.float64 if dtype == np.float64 else torch.float32
     T = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(device="cuda", dtype=td)
     kw = dict(model=1, adaptive=True, m_init=2, m_cap=64, eps=0.3, dt=setup["dt"], seed=5)
+    monkeypatch.setenv("TRMCR_SHOCK_FUSED", fused_full)
     full = api.Simulation(T(vx), T(vy), T(vz), x=T(x), shock=setup, **kw)
+    assert full.fused == (fused_full == "1")
+    monkeypatch.setenv("TRMCR_SHOCK_FUSED", fused_slabs)
     cuts = dist.slab_cuts(counts, world)
     slabs = []
     for first, nc in cuts:
