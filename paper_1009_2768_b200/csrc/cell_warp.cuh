@@ -153,6 +153,12 @@ __device__ void wplan_counts(const RngKey &K, CellBuf<Real> &B, WarpShared &sh) 
   }
 }
 
+// Bottom-up slot resolution + execution (as plan_execute, cell_step.cuh) in
+// three warp passes: (1) per level, the stable in-level ranks and each side's
+// demand index on its pool (pool 0: the cell's leaf order), (2) ALL keyed
+// permutation evaluations of the attempt in one flat pass over its 2 ktot
+// demands - lanes are not left idle by small levels, two walks interleaved per
+// lane - and (3) per level, pool outputs to slots and the collisions.
 template <typename Real, bool WB>
 __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real> &B, WarpShared &sh,
                               const Perm &pi0, Real sigma, trmcr_coll_rec *log, unsigned long long *log_count,
@@ -172,9 +178,8 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
   if (WB && P.wb) for (int o = lane; o < 2 * ktot; o += 32) B.wused[o] = 0;
   if (lane == 0) sh.ktot = ktot;
   __syncwarp();
-  unsigned acc = 0, viol = 0;
-  unsigned long long prop = 0;
   const int r = sh.r, leaf_off = sh.leaf_off, n = sh.n;
+  // ---- pass 1: demand indices (permutation inputs) into cslot16, level into crank16 ----
   int pd = 0;
   for (int d = 1; d <= top; ++d) {
     const int Cd = B.C[d], Sd = B.S[d];
@@ -204,25 +209,58 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
     for (int j = lane; j < Cd; j += 32) {
       const uint32_t a = B.ctype8[Sd + j], b = (uint32_t)d - 1u - a;
       const uint32_t rank = B.crank16[Sd + j];
-      const uint32_t t[2] = {(uint32_t)B.base[a] + rank, (uint32_t)(B.base[b] + B.cnt[b]) + rank};
+      const uint32_t t0 = (uint32_t)B.base[a] + rank, t1 = (uint32_t)(B.base[b] + B.cnt[b]) + rank;
+      B.cslot16[2 * (Sd + j)] = (uint16_t)(a == 0 ? (uint32_t)leaf_off + t0 : t0);
+      B.cslot16[2 * (Sd + j) + 1] = (uint16_t)(b == 0 ? (uint32_t)leaf_off + t1 : t1);
+      B.crank16[Sd + j] = (uint16_t)d;
+    }
+    __syncwarp();
+  }
+  // ---- pass 2: every permutation of the attempt, lanes over demands ----
+  for (int q0 = 0; q0 < 2 * ktot; q0 += 64) {
+    uint32_t x[2], pool[2];
+    bool on[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = q0 + 32 * h + lane;
+      on[h] = q < 2 * ktot;
+      x[h] = 0xFFFFFFFFu; pool[h] = 0;
+      if (on[h]) {
+        const int k = q >> 1;
+        const uint32_t a = B.ctype8[k], d = B.crank16[k];
+        pool[h] = (q & 1) ? d - 1u - a : a;
+        x[h] = B.cslot16[q];
+      }
+    }
+    uint32_t y[2];
+    perm_eval2(x[0], pool[0] == 0 ? pi0.rk : B.rk[pool[0]], pool[0] == 0 ? pi0.D : B.pdom[pool[0]],
+               x[1], pool[1] == 0 ? pi0.rk : B.rk[pool[1]], pool[1] == 0 ? pi0.D : B.pdom[pool[1]], y[0], y[1]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (on[h]) B.cslot16[q0 + 32 * h + lane] = (uint16_t)(y[h] == 0xFFFFFFFFu ? 0xFFFFu : y[h]);
+  }
+  __syncwarp();
+  // ---- pass 3: slots and collisions, level by level ----
+  unsigned acc = 0, viol = 0;
+  unsigned long long prop = 0;
+  for (int d = 1; d <= top; ++d) {
+    const int Cd = B.C[d], Sd = B.S[d];
+    if (Cd == 0) continue;
+    for (int j = lane; j < Cd; j += 32) {
+      const uint32_t a = B.ctype8[Sd + j], b = (uint32_t)d - 1u - a;
       const uint32_t pool[2] = {a, b};
-      // one code path for both sides (pool 0: pi0 at leaf_off + t; pool p:
-      // pi_p at t, then its output slot), cycle walks interleaved
-      uint32_t y[2];
-      perm_eval2(a == 0 ? (uint32_t)leaf_off + t[0] : t[0], a == 0 ? pi0.rk : B.rk[a], a == 0 ? pi0.D : B.pdom[a],
-                 b == 0 ? (uint32_t)leaf_off + t[1] : t[1], b == 0 ? pi0.rk : B.rk[b], b == 0 ? pi0.D : B.pdom[b],
-                 y[0], y[1]);
-      uint32_t slot[2];
+      uint32_t slot[2], y[2];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        slot[s] = (pool[s] == 0 || y[s] == 0xFFFFFFFFu) ? y[s] : (uint32_t)B.cslot16[2u * (uint32_t)B.S[pool[s]] + y[s]];
+        y[s] = B.cslot16[2 * (Sd + j) + s];
+        slot[s] = (pool[s] == 0 || y[s] == 0xFFFFu) ? y[s] : (uint32_t)B.cslot16[2u * (uint32_t)B.S[pool[s]] + y[s]];
         if (slot[s] >= (uint32_t)n) { atomicOr(P.err, kErrInternal); slot[s] = 0; }
       }
       if (WB && P.wb) {                      // TRMC-WB: lengths, consumed outputs
         double ln[2] = {0.0, 0.0};
 #pragma unroll
         for (int s = 0; s < 2; ++s)
-          if (pool[s] != 0 && y[s] != 0xFFFFFFFFu) {
+          if (pool[s] != 0 && y[s] != 0xFFFFu) {
             const uint32_t o = 2u * (uint32_t)B.S[pool[s]] + y[s];
             B.wused[o] = 1;
             ln[s] = B.wlen[o >> 1];
