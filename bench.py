@@ -269,43 +269,40 @@ def measure(args, wl_name, rank, world, local_rank, cpu_seconds):
     T = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(device=dev, dtype=td)
     stream = torch.cuda.current_stream(dev)
     from paper_1009_2768_b200 import dist as D
+    # the library's own NCCL communicator (all-reduce of the global moments,
+    # slab neighbour exchange); torch.distributed only broadcasts its id
+    comm = D.library_comm(api) if world > 1 else None
+    ckw = dict(nccl_id=comm[0], rank=comm[1], nranks=comm[2]) if comm else {}
     if W["kind"] == "hom":
         sim = api.Simulation(T(W["vx"]), T(W["vy"]), T(W["vz"]), offsets=W["offsets"],
-                             cell_base=W["cell_base"], stream=stream.cuda_stream, **W["kw"])
+                             cell_base=W["cell_base"], stream=stream.cuda_stream, **ckw, **W["kw"])
         n_local = int(W["offsets"][-1])
         slab = None
     else:
         slab = D.ShockSlab(api, W["setup"], W["first"], W["local_cells"], T(W["vx"]), T(W["vy"]), T(W["vz"]),
-                           x=T(W["x"]), device=dev, stream=stream.cuda_stream, **W["kw"])
+                           x=T(W["x"]), device=dev, stream=stream.cuda_stream, comm=comm, **W["kw"])
         sim = slab.sim
         n_local = sim.num_particles()
     # global moments every step (configs[2]: "NCCL allreduce of global moments"):
-    # two buffers, the all-reduce of step k runs on NCCL's stream while step
-    # k + 1 collides; a buffer is reused only after its all-reduce
+    # two buffers; the library all-reduces step k's sums on its communication
+    # stream while step k + 1 collides, and orders a buffer's reuse after its
+    # all-reduce
     gms = [torch.zeros(len(api.GLOBAL_FIELDS), dtype=torch.float64, device=dev) for _ in range(2)]
-    pending = [None, None]
     counter = [0]
-    xchg = lambda s_: D.exchange_p2p(s_.send_l, s_.send_r, s_.recv_l, s_.recv_r, rank, world)
+    xchg = None
 
     def one_step():
         if W["kind"] == "hom":
             sim.step(1)
             k = counter[0] & 1
             counter[0] += 1
-            if pending[k] is not None:
-                pending[k].wait()
-                pending[k] = None
-            sim.global_moments(gms[k])
-            if world > 1:
-                pending[k] = dist.all_reduce(gms[k], async_op=True)
+            sim.global_moments(gms[k], all_ranks=world > 1)
         else:
             slab.step(xchg)
 
     def drain():
-        for k in range(2):
-            if pending[k] is not None:
-                pending[k].wait()
-                pending[k] = None
+        if world > 1 and W["kind"] == "hom":
+            sim.comm_wait()
 
     for _ in range(args.warmup):
         one_step()

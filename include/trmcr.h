@@ -157,26 +157,59 @@ typedef struct {
 /* Create a context on the current CUDA device, bound to `cuda_stream`
  * (a cudaStream_t, NULL = legacy default stream).  eps: Knudsen number
  * (P:127-129), dt: time step, both > 0.  Copies the particles (and builds
- * the cell offsets for the shock).  Errors: EINVAL (bad sizes/arguments, eps or dt
- * <= 0, delta1 >= delta2, offsets not monotone, particle outside the shock
- * domain), ENOMEM, ECUDA. */
+ * the cell offsets for the shock).
+ * Multi-GPU: one context per rank of one simulation.  nccl_id:
+ * the 128-byte NCCL unique id from trmcr_get_nccl_id on one rank, moved to every
+ * rank by the caller (e.g. a torch.distributed broadcast); rank in [0, nranks).
+ * NULL with nranks = 1 for a single GPU.  The context then owns an NCCL
+ * communicator (ncclCommInitRank: collective, every rank must call) and uses it
+ * for the global moments (trmcr_global_moments all_ranks, trmcr_global_sums,
+ * trmcr_moments global) and, for a shock slab with neighbours, for the
+ * neighbour exchange inside trmcr_step (rank r must own the r-th slab).
+ * Errors: EINVAL (bad sizes/arguments, eps or dt <= 0, delta1 >= delta2, offsets
+ * not monotone, particle outside the shock domain, rank/slab mismatch), ENOMEM,
+ * ECUDA, ENCCL. */
 trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *particles,
                         const trmcr_cells *cells, double eps, double dt,
-                        const trmcr_kernel *kernel, void *cuda_stream);
+                        const trmcr_kernel *kernel, void *cuda_stream,
+                        const void *nccl_id, int32_t rank, int32_t nranks);
 
-/* Advance n_steps >= 0 time steps (asynchronous). */
+/* Write a fresh NCCL unique id (128 bytes) to out128 (host memory). ENCCL on failure. */
+trmcr_status trmcr_get_nccl_id(void *out128);
+
+/* Ranks of the context's communicator (1 without one). */
+int32_t trmcr_comm_size(const trmcr_ctx *ctx);
+
+/* Advance n_steps >= 0 time steps (asynchronous).  A shock slab with neighbours
+ * needs the NCCL communicator (else: trmcr_shock_begin / exchange / finish). */
 trmcr_status trmcr_step(trmcr_ctx *ctx, int32_t n_steps);
 
-/* Per-cell moments of the current state, host out[n_cells * TRMCR_NMOMENTS]. Syncs. */
-trmcr_status trmcr_moments(trmcr_ctx *ctx, double *host_out);
+/* Per-cell moments of the current state, host
+ * out[cells * TRMCR_NMOMENTS]: this context's cells (global = 0), or every
+ * rank's cells in global cell order (global = 1; collective over the
+ * communicator; out sized for the whole grid).  Syncs. */
+trmcr_status trmcr_moments(trmcr_ctx *ctx, double *host_out, int32_t global);
 
 /* Per-cell statistics of the last step, host out[n_cells * TRMCR_NSTATS]. Syncs. */
 trmcr_status trmcr_stats(trmcr_ctx *ctx, double *host_out);
 
 /* Global sums (TRMCR_NGLOBAL doubles) of the last step's per-cell statistics,
- * written asynchronously to DEVICE memory `dev_out` (e.g. the buffer of an
- * NCCL all-reduce across ranks).  cost = proposals + maxw/2. */
-trmcr_status trmcr_global_moments(trmcr_ctx *ctx, double *dev_out);
+ * written asynchronously to DEVICE memory `dev_out`; cost = proposals + maxw/2
+ * (P:829-832, 878-879).  all_ranks = 1 with a communicator: the sums are then
+ * all-reduced over the ranks on the context's communication stream, overlapping
+ * the following steps (a later call on the same buffer, or trmcr_comm_wait,
+ * orders the context stream after it).  The all-reduced sums depend on the
+ * rank count in the last bits; trmcr_global_sums is partition independent. */
+trmcr_status trmcr_global_moments(trmcr_ctx *ctx, double *dev_out, int32_t all_ranks);
+
+/* Make the context stream wait for every all-reduce in flight (asynchronous). */
+trmcr_status trmcr_comm_wait(trmcr_ctx *ctx);
+
+/* Partition-independent global sums (TRMCR_NGLOBAL doubles, host out) of the last
+ * step's statistics over every rank: the per-cell rows are all-gathered and each
+ * column is summed exactly rounded (Shewchuk's algorithm), so the result is
+ * bitwise the same for any number of GPUs.  Collective; syncs. */
+trmcr_status trmcr_global_sums(trmcr_ctx *ctx, double *host_out);
 
 /* Current particle count (shock: changes with inflow/outflow). Syncs. */
 trmcr_status trmcr_num_particles(trmcr_ctx *ctx, int64_t *n);

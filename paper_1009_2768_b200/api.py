@@ -76,9 +76,18 @@ def lib():
                               "(no CPU fallback exists)")
         L = C.CDLL(LIB_PATH)
         vp, P = C.c_void_p, C.POINTER
-        L.trmcr_init.argtypes = [P(vp), P(_Particles), P(_Cells), C.c_double, C.c_double, P(_Kernel), vp]
+        L.trmcr_init.argtypes = [P(vp), P(_Particles), P(_Cells), C.c_double, C.c_double, P(_Kernel), vp, vp,
+                                 C.c_int32, C.c_int32]
         L.trmcr_step.argtypes = [vp, C.c_int32]
-        L.trmcr_moments.argtypes = [vp, P(C.c_double)]
+        L.trmcr_moments.argtypes = [vp, P(C.c_double), C.c_int32]
+        L.trmcr_get_nccl_id.argtypes = [vp]
+        L.trmcr_get_nccl_id.restype = C.c_int
+        L.trmcr_comm_size.argtypes = [vp]
+        L.trmcr_comm_size.restype = C.c_int32
+        L.trmcr_comm_wait.argtypes = [vp]
+        L.trmcr_comm_wait.restype = C.c_int
+        L.trmcr_global_sums.argtypes = [vp, P(C.c_double)]
+        L.trmcr_global_sums.restype = C.c_int
         L.trmcr_stats.argtypes = [vp, P(C.c_double)]
         L.trmcr_num_particles.argtypes = [vp, P(C.c_int64)]
         L.trmcr_copy_particles.argtypes = [vp, vp, vp, vp, vp, vp, C.c_int32]
@@ -100,7 +109,7 @@ def lib():
         L.trmcr_shock_begin.restype = C.c_int
         L.trmcr_shock_finish.argtypes = [vp]
         L.trmcr_shock_finish.restype = C.c_int
-        L.trmcr_global_moments.argtypes = [vp, vp]
+        L.trmcr_global_moments.argtypes = [vp, vp, C.c_int32]
         L.trmcr_global_moments.restype = C.c_int
         L.trmcr_set_profiling_mask.argtypes = [vp, C.c_uint32]
         L.trmcr_set_profiling_mask.restype = C.c_int
@@ -174,7 +183,7 @@ class Simulation:
                  m_init: int = 2, m_cap: int = 4096, delta1: float = 0.005, delta2: float = 0.01,
                  indicator: int = IND_PXX, seed: int = 1, cell_base: int = 0, capacity: int = 0,
                  stream=None, alpha: float = 1.0, wb: int = 0, wb_max: int = 0, sigma_update: bool = False,
-                 literal: bool = False):
+                 literal: bool = False, nccl_id: Optional[bytes] = None, rank: int = 0, nranks: int = 1):
         L = lib()
         self._keep = [vx, vy, vz, x]
         (pvx, pvy, pvz, *rest), host, dt_code, n = _arrays([vx, vy, vz] + ([x] if x is not None else []))
@@ -208,8 +217,13 @@ class Simulation:
                 stream = 0
         self.stream = stream
         h = C.c_void_p()
+        idbuf = None
+        if nccl_id is not None:
+            if len(nccl_id) != 128:
+                raise ValueError("nccl_id must be the 128 bytes of get_nccl_id()")
+            idbuf = C.create_string_buffer(bytes(nccl_id), 128)
         st = L.trmcr_init(C.byref(h), C.byref(part), C.byref(cells), float(eps), float(dt),
-                          C.byref(kern), C.c_void_p(stream))
+                          C.byref(kern), C.c_void_p(stream), idbuf, int(rank), int(nranks))
         if st != OK:
             raise TrmcrError(st, L.trmcr_last_error(None).decode())
         self._h = h
@@ -236,10 +250,28 @@ class Simulation:
         self._check(lib().trmcr_step(self._h, int(n)))
         return self
 
-    def moments(self) -> np.ndarray:
-        out = np.zeros((self.ncells, len(MOMENT_FIELDS)))
-        self._check(lib().trmcr_moments(self._h, out.ctypes.data_as(C.POINTER(C.c_double))))
+    def moments(self, global_cells: Optional[int] = None) -> np.ndarray:
+        """Per-cell moments of this context's cells, or (global_cells = the grid's
+        cell count) of every rank's cells in global order (collective)."""
+        rows = self.ncells if global_cells is None else int(global_cells)
+        out = np.zeros((rows, len(MOMENT_FIELDS)))
+        self._check(lib().trmcr_moments(self._h, out.ctypes.data_as(C.POINTER(C.c_double)),
+                                        int(global_cells is not None)))
         return out
+
+    @property
+    def comm_size(self) -> int:
+        return int(lib().trmcr_comm_size(self._h))
+
+    def global_sums(self) -> np.ndarray:
+        """Partition-independent global sums (GLOBAL_FIELDS) over every rank (collective)."""
+        out = np.zeros(len(GLOBAL_FIELDS))
+        self._check(lib().trmcr_global_sums(self._h, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def comm_wait(self):
+        """Order the context stream after every global all-reduce in flight."""
+        self._check(lib().trmcr_comm_wait(self._h))
 
     def stats(self) -> np.ndarray:
         out = np.zeros(self.ncells, dtype=STATS_DTYPE)
@@ -312,11 +344,13 @@ class Simulation:
             raise TrmcrError(ECAPACITY, f"log overflow: {cnt.value} > {cap}")
         return buf[: cnt.value].copy()
 
-    def global_moments(self, dev_out):
-        """Asynchronously write the global sums (GLOBAL_FIELDS) into a device float64 tensor."""
+    def global_moments(self, dev_out, all_ranks: bool = False):
+        """Asynchronously write the global sums (GLOBAL_FIELDS) into a device float64
+        tensor; all_ranks: all-reduced over the communicator (overlapping the next steps)."""
         p, host, _ = _ptr(dev_out)
-        assert not host and dev_out.numel() >= len(GLOBAL_FIELDS)
-        self._check(lib().trmcr_global_moments(self._h, C.c_void_p(p)))
+        if host or dev_out.numel() < len(GLOBAL_FIELDS) or dev_out.dtype.itemsize != 8:
+            raise ValueError("dev_out must be a device float64 tensor of >= 10 entries")
+        self._check(lib().trmcr_global_moments(self._h, C.c_void_p(p), int(bool(all_ranks))))
 
     # ---- slab decomposition of the shock (see include/trmcr.h) ----
     def sort_info(self) -> dict:
@@ -368,6 +402,15 @@ class Simulation:
     @property
     def launch_count(self) -> int:
         return int(lib().trmcr_launch_count(self._h))
+
+
+def get_nccl_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for Simulation(..., nccl_id=, rank=, nranks=)."""
+    buf = C.create_string_buffer(128)
+    st = lib().trmcr_get_nccl_id(buf)
+    if st != OK:
+        raise TrmcrError(st, lib().trmcr_last_error(None).decode())
+    return buf.raw
 
 
 def version() -> str:

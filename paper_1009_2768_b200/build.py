@@ -15,6 +15,18 @@ FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-li
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 
 
+def nccl_dir() -> str:
+    """NCCL 2.28 of the Python environment (the one torch.distributed loads)."""
+    import nvidia.nccl
+    return os.path.dirname(nvidia.nccl.__file__) if getattr(nvidia.nccl, "__file__", None) else list(nvidia.nccl.__path__)[0]
+
+
+def nccl_flags():
+    d = nccl_dir()
+    return ["-I", os.path.join(d, "include"), "-L", os.path.join(d, "lib"), "-l:libnccl.so.2",
+            "-Xlinker", "-rpath=" + os.path.join(d, "lib")]
+
+
 def sources():
     return [SRC] + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "trmcr.h")]
 
@@ -30,7 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp, SRC]
+    cmd = [NVCC, *FLAGS, "-o", tmp, SRC, *nccl_flags()]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)

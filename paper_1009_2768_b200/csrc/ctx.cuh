@@ -155,7 +155,11 @@ struct ShockState {
   int32_t *d_far_src[2] = {nullptr, nullptr}, *d_far_dst[2] = {nullptr, nullptr};
   int *d_far_cnt = nullptr;
   int far_cap = 0;
+  size_t xbytes = 0;                        // bytes of one exchange buffer (library-owned buffers)
+  int own_xbuf = 0;                         // the exchange buffers belong to the context (NCCL path)
 };
+
+constexpr int kCommSlots = 4;               // global-moments buffers with an all-reduce in flight
 
 thread_local inline std::string g_init_error;
 
@@ -224,6 +228,15 @@ struct trmcr_ctx {
   size_t ev_used = 0;
   std::vector<int> ev_kid;
   trmcr::ShockState shock{};
+  // multi-GPU (comm.cuh): NCCL communicator over the ranks of one simulation
+  struct ncclComm *comm = nullptr;
+  int rank = 0, nranks = 1;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_comm_ready = nullptr;
+  cudaEvent_t ev_comm_done[trmcr::kCommSlots] = {nullptr, nullptr, nullptr, nullptr};
+  const void *comm_ptr[trmcr::kCommSlots] = {nullptr, nullptr, nullptr, nullptr};
+  int comm_busy[trmcr::kCommSlots] = {0, 0, 0, 0};
+  int comm_next = 0;
   std::vector<void *> allocs;
   std::string err;
   int sticky = 0;

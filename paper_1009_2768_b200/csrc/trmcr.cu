@@ -20,6 +20,7 @@
 #include "cell_step.cuh"
 #include "ctx.cuh"
 #include "shock.cuh"
+#include "comm.cuh"
 #include "thermal.cuh"
 #include "literal.cuh"
 
@@ -377,12 +378,18 @@ cudaError_t allow_max_dyn_smem(const void *f, int smem_optin) {
 }
 
 trmcr_status do_step(trmcr_ctx *c) {
-  if (c->geometry == TRMCR_SHOCK_1D && (c->shock.has_left || c->shock.has_right))
-    return fail(c, TRMCR_EINVAL, "a slab with neighbours steps with trmcr_shock_begin / exchange / trmcr_shock_finish");
+  const bool slab = c->geometry == TRMCR_SHOCK_1D && (c->shock.has_left || c->shock.has_right);
+  if (slab && !c->comm)
+    return fail(c, TRMCR_EINVAL, "a slab with neighbours steps with trmcr_shock_begin / exchange / trmcr_shock_finish "
+                                 "(or give trmcr_init an NCCL id)");
   if (c->log_cap > 0)
     CUDA_TRY(c, cudaMemsetAsync(c->d_log_count, 0, sizeof(unsigned long long), c->stream));
   trmcr_status s;
-  if (c->geometry == TRMCR_SHOCK_1D)
+  if (slab) {                        // begin, NCCL neighbour exchange on the context stream, finish
+    s = c->dtype == TRMCR_F64 ? shock_begin<double>(c) : shock_begin<float>(c);
+    if (!s) s = comm_shock_exchange(c);
+    if (!s) s = c->dtype == TRMCR_F64 ? shock_finish<double>(c) : shock_finish<float>(c);
+  } else if (c->geometry == TRMCR_SHOCK_1D)
     s = c->dtype == TRMCR_F64 ? shock_step<double>(c) : shock_step<float>(c);
   else
     s = c->dtype == TRMCR_F64 ? launch_collide<double>(c) : launch_collide<float>(c);
@@ -406,13 +413,80 @@ const char *trmcr_last_error(const trmcr_ctx *ctx) {
 
 int64_t trmcr_launch_count(const trmcr_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
-trmcr_status trmcr_global_moments(trmcr_ctx *c, double *dev_out) {
+trmcr_status trmcr_global_moments(trmcr_ctx *c, double *dev_out, int32_t all_ranks) {
   if (!c || !dev_out) return fail(c, TRMCR_EINVAL, "null argument");
   if (c->sticky) return TRMCR_ESTATE;
+  const bool ar = all_ranks && c->comm;
+  int slot = -1;
+  if (ar) {                 // the buffer's previous all-reduce must be done before it is rewritten
+    slot = comm_slot(c, dev_out);
+    if (c->comm_busy[slot]) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_comm_done[slot], 0));
+  }
   const int blocks = std::max(1, std::min(kGmBlocks, c->ncells));
   launch_k(c, global_moments_kernel, blocks, 256, 0, (const double *)c->d_stats, c->ncells, c->d_gm_partial,
            c->d_gm_done, dev_out);
-  return check_launch(c, "global_moments_kernel");
+  if (trmcr_status e = check_launch(c, "global_moments_kernel")) return e;
+  if (ar) {                 // all-reduce on the communication stream, overlapping the next step
+    CUDA_TRY(c, cudaEventRecord(c->ev_comm_ready, c->stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_comm_ready, 0));
+    NCCL_TRY(c, ncclAllReduce(dev_out, dev_out, TRMCR_NGLOBAL, ncclDouble, ncclSum, c->comm, c->comm_stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev_comm_done[slot], c->comm_stream));
+    c->comm_busy[slot] = 1;
+  }
+  return TRMCR_OK;
+}
+
+trmcr_status trmcr_comm_wait(trmcr_ctx *c) {
+  if (!c) return fail(nullptr, TRMCR_EINVAL, "null ctx");
+  if (c->sticky) return TRMCR_ESTATE;
+  for (int k = 0; k < kCommSlots; ++k)
+    if (c->comm_busy[k]) {
+      CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_comm_done[k], 0));
+      c->comm_busy[k] = 0;
+    }
+  return TRMCR_OK;
+}
+
+trmcr_status trmcr_get_nccl_id(void *out128) {
+  if (!out128) return fail(nullptr, TRMCR_EINVAL, "null argument");
+  ncclUniqueId id;
+  const ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, TRMCR_ENCCL, std::string("ncclGetUniqueId failed: ") + ncclGetErrorString(r));
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+  memcpy(out128, &id, sizeof(id));
+  return TRMCR_OK;
+}
+
+int32_t trmcr_comm_size(const trmcr_ctx *c) { return c ? c->nranks : 0; }
+
+trmcr_status trmcr_global_sums(trmcr_ctx *c, double *host_out) {
+  if (!c || !host_out) return fail(c, TRMCR_EINVAL, "null argument");
+  if (c->sticky) return TRMCR_ESTATE;
+  if (trmcr_status s = sync_check(c)) return s;
+  // per-cell rows of the summed quantities (the statistics rows of the last step)
+  std::vector<double> st((size_t)c->ncells * TRMCR_NSTATS), rows((size_t)c->ncells * TRMCR_NGLOBAL);
+  CUDA_TRY(c, cudaMemcpy(st.data(), c->d_stats, sizeof(double) * st.size(), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < c->ncells; ++i) {
+    const double *r = &st[(size_t)i * TRMCR_NSTATS];
+    double *o = &rows[(size_t)i * TRMCR_NGLOBAL];
+    o[TRMCR_GM_N] = r[TRMCR_ST_N]; o[TRMCR_GM_PX] = r[TRMCR_ST_PX]; o[TRMCR_GM_PY] = r[TRMCR_ST_PY];
+    o[TRMCR_GM_PZ] = r[TRMCR_ST_PZ]; o[TRMCR_GM_ENERGY] = r[TRMCR_ST_ENERGY];
+    o[TRMCR_GM_NPXX] = r[TRMCR_ST_N] * r[TRMCR_ST_S0];
+    o[TRMCR_GM_PROPOSALS] = r[TRMCR_ST_PROPOSALS]; o[TRMCR_GM_ACCEPTED] = r[TRMCR_ST_ACCEPTED];
+    o[TRMCR_GM_MAXW] = r[TRMCR_ST_MAXW];
+    o[TRMCR_GM_COST] = r[TRMCR_ST_PROPOSALS] + 0.5 * r[TRMCR_ST_MAXW];
+  }
+  double *d_rows = nullptr;
+  if (dalloc(c, &d_rows, sizeof(double) * std::max<size_t>(rows.size(), 1))) return TRMCR_ENOMEM;
+  CUDA_TRY(c, cudaMemcpy(d_rows, rows.data(), sizeof(double) * rows.size(), cudaMemcpyHostToDevice));
+  std::vector<double> all;
+  int64_t total = 0;
+  trmcr_status s = comm_allgather_rows(c, d_rows, TRMCR_NGLOBAL, all, total);
+  c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void *)d_rows), c->allocs.end());
+  cudaFree(d_rows);
+  if (s) return s;
+  for (int k = 0; k < TRMCR_NGLOBAL; ++k) host_out[k] = exact_sum(all.data() + k, (size_t)total, TRMCR_NGLOBAL);
+  return TRMCR_OK;
 }
 
 // Debug builds only: per-phase CTA cycles of the general kernels (reset on read).
@@ -467,6 +541,8 @@ trmcr_status trmcr_kernel_times(trmcr_ctx *c, double *ms, int64_t *launches) {
 void trmcr_destroy(trmcr_ctx *ctx) {
   if (!ctx) return;
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm_stream) cudaStreamSynchronize(ctx->comm_stream);
+  comm_destroy(ctx);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->ev_defer) cudaEventDestroy(ctx->ev_defer);
   if (ctx->h_defer) cudaFreeHost(ctx->h_defer);
@@ -475,9 +551,11 @@ void trmcr_destroy(trmcr_ctx *ctx) {
 }
 
 trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_cells *cc, double eps,
-                        double dt, const trmcr_kernel *kk, void *cuda_stream) {
+                        double dt, const trmcr_kernel *kk, void *cuda_stream, const void *nccl_id, int32_t rank,
+                        int32_t nranks) {
   if (!out || !pp || !cc || !kk) return fail(nullptr, TRMCR_EINVAL, "null argument");
   *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(nullptr, TRMCR_EINVAL, "need 0 <= rank < nranks");
   if (!(eps > 0) || !(dt > 0)) return fail(nullptr, TRMCR_EINVAL, "eps and dt must be > 0");
   if (pp->dtype != TRMCR_F32 && pp->dtype != TRMCR_F64) return fail(nullptr, TRMCR_EINVAL, "bad dtype");
   if (pp->n < 0 || pp->n > 0x7FFFFFFFLL) return fail(nullptr, TRMCR_EINVAL, "bad particle count");
@@ -808,6 +886,11 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
     fail(c, TRMCR_ECUDA, "init synchronisation failed");
     return bail(TRMCR_ECUDA);
   }
+  if (trmcr_status s = comm_init(c, nccl_id, rank, nranks)) return bail(s);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    fail(c, TRMCR_ECUDA, "init synchronisation failed");
+    return bail(TRMCR_ECUDA);
+  }
   *out = c;
   return TRMCR_OK;
 }
@@ -841,6 +924,8 @@ trmcr_status trmcr_shock_set_exchange(trmcr_ctx *c, void *send_left, void *send_
     return fail(c, TRMCR_EINVAL, "missing exchange buffer for an existing neighbour");
   s.xsend[0] = send_left; s.xsend[1] = send_right; s.xrecv[0] = recv_left; s.xrecv[1] = recv_right;
   s.xcap = (int)capacity;
+  s.xbytes = c->dtype == TRMCR_F64 ? XBuf<double>::bytes(s.xcap) : XBuf<float>::bytes(s.xcap);
+  s.own_xbuf = 0;
   return TRMCR_OK;
 }
 
@@ -871,12 +956,19 @@ trmcr_status trmcr_step(trmcr_ctx *c, int32_t n_steps) {
   return TRMCR_OK;
 }
 
-trmcr_status trmcr_moments(trmcr_ctx *c, double *host_out) {
+trmcr_status trmcr_moments(trmcr_ctx *c, double *host_out, int32_t global) {
   if (!c || !host_out) return fail(c, TRMCR_EINVAL, "null argument");
   if (c->sticky) return TRMCR_ESTATE;
   trmcr_status s = c->dtype == TRMCR_F64 ? launch_moments<double>(c) : launch_moments<float>(c);
   if (s) return s;
   if ((s = sync_check(c))) return s;
+  if (global && c->comm) {   // every rank's rows, in global cell order
+    std::vector<double> all;
+    int64_t total = 0;
+    if ((s = comm_allgather_rows(c, c->d_moments, TRMCR_NMOMENTS, all, total))) return s;
+    memcpy(host_out, all.data(), sizeof(double) * all.size());
+    return TRMCR_OK;
+  }
   CUDA_TRY(c, cudaMemcpy(host_out, c->d_moments, sizeof(double) * TRMCR_NMOMENTS * c->ncells,
                          cudaMemcpyDeviceToHost));
   return TRMCR_OK;
@@ -963,7 +1055,7 @@ trmcr_status trmcr_step_host_particles(trmcr_ctx *c, const void *x, const void *
   if (!c || !host_moments) return fail(c, TRMCR_EINVAL, "null argument");
   if (trmcr_status s = trmcr_set_particles(c, x, vx, vy, vz, n, 1)) return s;
   if (trmcr_status s = do_step(c)) return s;
-  return trmcr_moments(c, host_moments);
+  return trmcr_moments(c, host_moments, 0);
 }
 
 trmcr_status trmcr_step_host(trmcr_ctx *c, const void *vx, const void *vy, const void *vz, double *host_moments) {
@@ -971,7 +1063,7 @@ trmcr_status trmcr_step_host(trmcr_ctx *c, const void *vx, const void *vy, const
   if (c->geometry != TRMCR_HOMOGENEOUS) return fail(c, TRMCR_EINVAL, "trmcr_step_host: homogeneous geometry only");
   if (trmcr_status s = trmcr_set_velocities(c, vx, vy, vz, 1)) return s;
   if (trmcr_status s = do_step(c)) return s;
-  return trmcr_moments(c, host_moments);
+  return trmcr_moments(c, host_moments, 0);
 }
 
 trmcr_status trmcr_set_log(trmcr_ctx *c, int64_t capacity) {

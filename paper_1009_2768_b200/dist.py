@@ -9,9 +9,11 @@
   count; each step every slab sends the particles that moved into a
   neighbouring slab to rank +- 1 (fixed-capacity buffers with a count header,
   one message per direction, no size round trip) between
-  trmcr_shock_begin and trmcr_shock_finish.  The exchange uses
-  torch.distributed point-to-point ops, so the same code runs over NCCL
-  (CUDA tensors, NVLink) and gloo (CPU tensors, tests).
+  trmcr_shock_begin and trmcr_shock_finish.
+* On GPUs the collectives run inside the library on its own NCCL communicator
+  (comm.cuh; `library_comm` only broadcasts the unique id); the
+  torch.distributed exchange below (`exchange_p2p`) is the same protocol for
+  gloo (CPU tensors, tests) and for callers that manage the buffers.
 """
 from __future__ import annotations
 
@@ -86,6 +88,22 @@ def slab_cuts(counts: Sequence[int], world: int, min_cells: int = 4) -> List[Tup
     return [(cuts[r], cuts[r + 1] - cuts[r]) for r in range(world)]
 
 
+def library_comm(api, group=None):
+    """(nccl_id, rank, nranks) for Simulation(...): rank 0 draws the NCCL unique id
+    in the library (trmcr_get_nccl_id) and torch.distributed broadcasts its 128
+    bytes - process-group plumbing only; the collectives themselves run inside
+    the library on its own NCCL communicator."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    buf = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        buf.copy_(torch.frombuffer(bytearray(api.get_nccl_id()), dtype=torch.uint8))
+    dist.broadcast(buf, src=0, group=group)
+    return bytes(buf.cpu().numpy().tobytes()), rank, world
+
+
 def exchange_p2p(send_left, send_right, recv_left, recv_right, rank: int, world: int, group=None):
     """Send send_left to rank-1 (its recv_right) and send_right to rank+1 (its
     recv_left); receive symmetrically.  Buffers are torch tensors (CUDA over
@@ -118,15 +136,25 @@ class ShockSlab:
     [first, first + ncells) plus its exchange buffers."""
 
     def __init__(self, api, setup: dict, first: int, ncells: int, vx, vy, vz, *, x, device,
-                 exchange_capacity: int = 1 << 13, **kw):
+                 exchange_capacity: int = 1 << 13, comm=None, **kw):
         # capacity: particles crossing one slab edge in one step (a few hundred at
         # CFL 0.5 on C5; the whole buffer travels, so it is kept small: 8192 x 20 B)
+        # comm = (nccl_id, rank, nranks) from library_comm(): the library exchanges
+        # with the neighbours itself (NCCL send/recv inside trmcr_step); else the
+        # caller's exchange function moves this object's buffers.
         import torch
         self.first, self.ncells = first, ncells
         C = setup["ncells"]
         neighbors = (1 if first > 0 else 0) | (2 if first + ncells < C else 0)
         sh = dict(setup)
         sh.update(local_cells=ncells, neighbors=neighbors)
+        self.neighbors = neighbors
+        self.library_comm = comm is not None
+        if comm is not None:
+            nid, rank, nranks = comm
+            self.sim = api.Simulation(vx, vy, vz, x=x, shock=sh, cell_base=first, nccl_id=nid, rank=rank,
+                                      nranks=nranks, **kw)
+            return
         self.sim = api.Simulation(vx, vy, vz, x=x, shock=sh, cell_base=first, **kw)
         nb = self.sim.exchange_bytes(exchange_capacity)
         mk = lambda: torch.zeros(nb, dtype=torch.uint8, device=device)
@@ -136,9 +164,10 @@ class ShockSlab:
                               exchange_capacity)
         self.neighbors = neighbors
 
-    def step(self, exchange: Callable[["ShockSlab"], None]):
-        """begin (transport, pack) -> exchange(self) -> finish (gather, collide)."""
-        if self.neighbors == 0:
+    def step(self, exchange: Optional[Callable[["ShockSlab"], None]] = None):
+        """begin (transport, pack) -> exchange(self) -> finish (gather, collide); with
+        the library's communicator one trmcr_step does all three."""
+        if self.neighbors == 0 or self.library_comm:
             self.sim.step(1)
             return
         self.sim.shock_begin()
