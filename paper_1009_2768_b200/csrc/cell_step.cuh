@@ -28,9 +28,15 @@ __device__ unsigned long long g_phase_cycles[16];
     if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[k], (unsigned long long)(clock64() - var)); \
     var = clock64();                                                             \
   } while (0)
+#define WPHASE_ADD(k, var)                                                       \
+  do {                                                                           \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[k], (unsigned long long)(clock64() - var)); \
+    var = clock64();                                                             \
+  } while (0)
 #else
 #define PHASE_MARK(var)
 #define PHASE_ADD(k, var)
+#define WPHASE_ADD(k, var)
 #endif
 
 enum : int { kOk = 0, kOverflow = 1, kCapacity = 2 };
@@ -115,10 +121,11 @@ __device__ __forceinline__ double wb_combine(int def, int d, double a, double b)
 
 // IR at split level d with its keyed uniform; exact 0 when y < 2^-53.
 // Uniforms of levels < kSplitPre were drawn in parallel into `pre`.
-__device__ __forceinline__ int64_t ir_split(const RngKey &K, int d, double y, const double *pre) {
+__device__ __forceinline__ int64_t ir_split(const RngKey &K, int d, double y, const double *pre,
+                                            int npre = kSplitPre) {
   if (y < 0x1p-53) return 0;
   double u;
-  if (d < kSplitPre) {
+  if (d < npre) {
     u = pre[d];
   } else {
     const uint4 w = K(kSplit, 0, (uint32_t)d, 0);
@@ -182,19 +189,34 @@ __device__ __forceinline__ Real pair_sigma(const StepParams &P, const CellBuf<Re
 // A6 on the pair in slots (si, sk) of (vx, vy, vz) with the collision's
 // uniforms: acceptance against the bound (dummy collision when rejected),
 // then v' = G +- (|q|/2) sigma.  Returns accepted.
+// RAD indicator of one velocity (R20): (v_x - u_x)^2 (Pxx) or |v|^4 (M4).
 template <typename Real>
+__device__ __forceinline__ Real ind_value(bool pxx, Real ux, Real x, Real y, Real z) {
+  if (pxx) { const Real dx = x - ux; return dx * dx; }
+  const Real v2 = x * x + y * y + z * z;
+  return v2 * v2;
+}
+
+// dS (nullable): an accepted collision adds the change of the cell's indicator
+// sum, ind(a') + ind(b') - ind(a) - ind(b), so the RAD estimate needs no pass
+// over the whole cell (warp kernels; the sum telescopes over a slot's
+// successive collisions).
+// MOD >= 0: the collision model fixed at compile time (the hard-sphere
+// instantiation of the shock kernel carries no VHS / Maxwell code); -1: P.model.
+template <typename Real, int MOD = -1>
 __device__ __forceinline__ int pair_collide(const StepParams &P, Real *vx, Real *vy, Real *vz, Real sigma,
                                             Real xa, Real xi1, Real xi2, uint32_t si, uint32_t sk,
-                                            unsigned &viol) {
+                                            unsigned &viol, double *dS = nullptr, Real ind_ux = Real(0)) {
   using O = RealOps<Real>;
   const Real ax = vx[si], ay = vy[si], az = vz[si];
   const Real bx = vx[sk], by = vy[sk], bz = vz[sk];
   const Real q = qnorm(ax - bx, ay - by, az - bz);
+  const int model = MOD >= 0 ? MOD : P.model;
   int acc = 1;
-  if (P.model == TRMCR_HARD_SPHERE) {       // accept iff xi Sigma' < |q|  [R7]
+  if (model == TRMCR_HARD_SPHERE) {         // accept iff xi Sigma' < |q|  [R7]
     viol += (q > viol_bound(sigma)) ? 1u : 0u;
     acc = (xa * sigma < q);
-  } else if (P.model == TRMCR_VHS) {        // accept iff xi Sigma' < |q|^alpha (sec. VHS)
+  } else if (model == TRMCR_VHS) {          // accept iff xi Sigma' < |q|^alpha (sec. VHS)
     const Real qa = O::pow_(q, (Real)P.alpha);
     viol += (qa > viol_bound(sigma)) ? 1u : 0u;
     acc = (xa * sigma < qa);
@@ -207,18 +229,26 @@ __device__ __forceinline__ int pair_collide(const StepParams &P, Real *vx, Real 
     const Real h = Real(0.5) * q;
     const Real hx = h * (s * cp), hy = h * (s * sp), hz = h * c;
     const Real gx = Real(0.5) * (ax + bx), gy = Real(0.5) * (ay + by), gz = Real(0.5) * (az + bz);
-    vx[si] = gx + hx; vy[si] = gy + hy; vz[si] = gz + hz;
-    vx[sk] = gx - hx; vy[sk] = gy - hy; vz[sk] = gz - hz;
+    const Real nax = gx + hx, nay = gy + hy, naz = gz + hz, nbx = gx - hx, nby = gy - hy, nbz = gz - hz;
+    vx[si] = nax; vy[si] = nay; vz[si] = naz;
+    vx[sk] = nbx; vy[sk] = nby; vz[sk] = nbz;
+    if (dS) {
+      const bool pxx = P.indicator == TRMCR_IND_PXX;
+      const Real dn = ind_value<Real>(pxx, ind_ux, nax, nay, naz) + ind_value<Real>(pxx, ind_ux, nbx, nby, nbz);
+      const Real dold = ind_value<Real>(pxx, ind_ux, ax, ay, az) + ind_value<Real>(pxx, ind_ux, bx, by, bz);
+      *dS += (double)(dn - dold);
+    }
   }
   return acc;
 }
 
 // One (dummy) collision of a tree node (A6) with its keyed draws
 // (COLL, attempt, level, j).  Returns accepted.
-template <typename Real>
+template <typename Real, int MOD = -1>
 __device__ __forceinline__ int tree_collision(const StepParams &P, const RngKey &K, CellBuf<Real> &B,
                                               Real sigma, int r, int d, uint32_t j, uint32_t si,
-                                              uint32_t sk, unsigned &viol) {
+                                              uint32_t sk, unsigned &viol, double *dS = nullptr,
+                                              Real ind_ux = Real(0)) {
   Real xa, xi1, xi2;
   if constexpr (sizeof(Real) == 8) {
     const uint4 w = K(kColl, r, d, j);
@@ -228,7 +258,7 @@ __device__ __forceinline__ int tree_collision(const StepParams &P, const RngKey 
     const uint4 w = K(kColl, r, d, j);
     xa = u24(w.x); xi1 = u24(w.y); xi2 = u24(w.z);
   }
-  return pair_collide<Real>(P, B.vx, B.vy, B.vz, sigma, xa, xi1, xi2, si, sk, viol);
+  return pair_collide<Real, MOD>(P, B.vx, B.vy, B.vz, sigma, xa, xi1, xi2, si, sk, viol, dS, ind_ux);
 }
 
 // Draw three standard normals for Theta slot `slot` (Box-Muller).

@@ -12,6 +12,7 @@
 namespace trmcr {
 
 constexpr int kWarpCellWarps = 4;
+constexpr int kWarpSplitPre = 32;      // split uniforms drawn up front: one per lane (deeper levels draw theirs)
 #ifndef TRMCR_WARP_MINB
 #define TRMCR_WARP_MINB 4        // CTAs of kWarpCellWarps warps per SM the register budget allows (128 regs)
 #endif
@@ -19,8 +20,10 @@ constexpr int kWarpCellWarps = 4;
 // Per-warp scalars (in the warp's slab, lane 0 writes, __syncwarp publishes).
 struct WarpShared {
   double ux, uy, uz, S0, sigma, p, mu, S_est, E1, c2;
+  double cind, dS;            // pre-step indicator sum (n S0) and its change by the collisions so far
   double sig_run;             // running majorant (sigma_update) [R33]
   uint4 pk;                // key of pi0
+  PermDom D0;              // its domain [0, n)
   double sums[4];
   int n, m_cur, m_next, d, top, lo, hi, r, flag, done;
   int64_t rem;
@@ -42,7 +45,7 @@ struct WarpSlabLayout {
     off_red = o; o += 8 * sizeof(double);
     al(16); off_rk = o; o += (size_t)(L + 1) * sizeof(uint4);
     off_pdom = o; o += (size_t)(L + 1) * sizeof(PermDom);
-    off_u = o; o += (size_t)kSplitPre * sizeof(double);
+    off_u = o; o += (size_t)kWarpSplitPre * sizeof(double);
     al(16); off_v = o; if (v_in_smem) o += 3 * (size_t)n * rs;
     al(16); off_cslot = o; o += (size_t)K * 4;     // 2 K uint16
     off_crank = o; o += (size_t)K * 2;             // K uint16
@@ -90,7 +93,7 @@ __device__ __forceinline__ void wsplit_extend(const RngKey &K, WarpShared &sh, i
       break;
     }
     sh.d++;
-    int64_t q = ir_split(K, sh.d, y, usplit);
+    int64_t q = ir_split(K, sh.d, y, usplit, kWarpSplitPre);
     if (q > sh.rem) q = sh.rem;
     if (sh.d <= L_cap) Q[sh.d] = (int32_t)q;
     else if (q > 0) sh.flag = kOverflow;
@@ -159,7 +162,7 @@ __device__ void wplan_counts(const RngKey &K, CellBuf<Real> &B, WarpShared &sh) 
 // permutation evaluations of the attempt in one flat pass over its 2 ktot
 // demands - lanes are not left idle by small levels, two walks interleaved per
 // lane - and (3) per level, pool outputs to slots and the collisions.
-template <typename Real, bool WB>
+template <typename Real, bool WB, int MOD = -1>
 __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real> &B, WarpShared &sh,
                               const Perm &pi0, Real sigma, trmcr_coll_rec *log, unsigned long long *log_count,
                               int64_t log_cap) {
@@ -216,6 +219,7 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
     }
     __syncwarp();
   }
+  PHASE_MARK(t_p2);
   // ---- pass 2: every permutation of the attempt, lanes over demands ----
   for (int q0 = 0; q0 < 2 * ktot; q0 += 64) {
     uint32_t x[2], pool[2];
@@ -240,9 +244,13 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
       if (on[h]) B.cslot16[q0 + 32 * h + lane] = (uint16_t)(y[h] == 0xFFFFFFFFu ? 0xFFFFu : y[h]);
   }
   __syncwarp();
+  WPHASE_ADD(12, t_p2);   // plan_execute pass 2 (permutations)
   // ---- pass 3: slots and collisions, level by level ----
   unsigned acc = 0, viol = 0;
   unsigned long long prop = 0;
+  double dS = 0.0;                         // this lane's share of the indicator change (RAD)
+  double *dSp = P.adaptive ? &dS : nullptr;
+  const Real iux = (Real)sh.ux;
   for (int d = 1; d <= top; ++d) {
     const int Cd = B.C[d], Sd = B.S[d];
     if (Cd == 0) continue;
@@ -270,7 +278,7 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
       B.cslot16[2 * (Sd + j)] = (uint16_t)slot[0];
       B.cslot16[2 * (Sd + j) + 1] = (uint16_t)slot[1];
       if (!(WB && P.sigma_update)) {
-        const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, slot[0], slot[1], viol);
+        const int ok = tree_collision<Real, MOD>(P, K, B, sigma, r, d, (uint32_t)j, slot[0], slot[1], viol, dSp, iux);
         acc += ok;
         log_collision(P, K, log, log_count, log_cap, r, d, j, ok, slot[0], slot[1]);
       }
@@ -286,7 +294,7 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
           for (int j = 0; j < Cd; ++j) {
             const uint32_t s0 = B.cslot16[2 * (Sd + j)], s1 = B.cslot16[2 * (Sd + j) + 1];
             const Real sj = pair_sigma<Real>(P, B, s0, s1);
-            const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, s0, s1, viol);
+            const int ok = tree_collision<Real, MOD>(P, K, B, sigma, r, d, (uint32_t)j, s0, s1, viol, dSp, iux);
             acc += ok;
             log_collision(P, K, log, log_count, log_cap, r, d, j, ok, s0, s1);
             if (sj > viol_bound(sigma)) sigma = sj;
@@ -295,7 +303,7 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
       } else {
         for (int j = lane; j < Cd; j += 32) {
           const uint32_t s0 = B.cslot16[2 * (Sd + j)], s1 = B.cslot16[2 * (Sd + j) + 1];
-          const int ok = tree_collision<Real>(P, K, B, sigma, r, d, (uint32_t)j, s0, s1, viol);
+          const int ok = tree_collision<Real, MOD>(P, K, B, sigma, r, d, (uint32_t)j, s0, s1, viol, dSp, iux);
           acc += ok;
           log_collision(P, K, log, log_count, log_cap, r, d, j, ok, s0, s1);
         }
@@ -304,39 +312,25 @@ __device__ void wplan_execute(const StepParams &P, const RngKey &K, CellBuf<Real
     prop += (unsigned long long)Cd;
     __syncwarp();
   }
+  WPHASE_ADD(13, t_p2);   // plan_execute pass 3 (collisions)
   if (WB && P.sigma_update && lane == 0) sh.sig_run = (double)sigma;
   acc = __reduce_add_sync(0xffffffffu, acc);
   viol = __reduce_add_sync(0xffffffffu, viol);
-  if (lane == 0) { sh.prop += prop; sh.acc += acc; sh.viol += viol; }
+  if (P.adaptive) dS = warp_sum_call(dS);
+  if (lane == 0) { sh.prop += prop; sh.acc += acc; sh.viol += viol; sh.dS += dS; }
   __syncwarp();
 }
 
+// RAD indicator estimate with Theta taken analytically, as
+// rad_estimate (cell_step.cuh) but without a pass over the whole cell: the sum
+// of the indicator over all slots is its pre-step value plus the change the
+// collisions made (accumulated in pass 3), so only Theta's slots are read.
 template <typename Real>
 __device__ void wrad_estimate(const StepParams &P, CellBuf<Real> &B, WarpShared &sh, const Perm &pi0) {
   const int lane = threadIdx.x & 31, n = sh.n, nT = sh.nT;
   const bool pxx = P.indicator == TRMCR_IND_PXX;
   const double ux = sh.ux;
-  double v0 = 0, v1 = 0, tx = 0, ty = 0, tz = 0, t2 = 0;
-  if constexpr (sizeof(Real) == 4) {            // fp32 lane partials (statistical mode)
-    const float fux = (float)ux;
-    float f0 = 0;
-    if (pxx) {
-      for (int i = lane; i < n; i += 32) { const float dx = B.vx[i] - fux; f0 += dx * dx; }
-    } else {
-      for (int i = lane; i < n; i += 32) {
-        const float x = B.vx[i], y = B.vy[i], z = B.vz[i];
-        const float v2 = x * x + y * y + z * z;
-        f0 += v2 * v2;
-      }
-    }
-    v0 = f0;
-  } else {
-    for (int i = lane; i < n; i += 32) {
-      const double x = B.vx[i], y = B.vy[i], z = B.vz[i];
-      if (pxx) { const double dx = x - ux; v0 += dx * dx; }
-      else { const double v2 = x * x + y * y + z * z; v0 += v2 * v2; }
-    }
-  }
+  double v1 = 0, tx = 0, ty = 0, tz = 0, t2 = 0;
   for (int q = lane; q < nT; q += 32) {
     const uint32_t s = pi0((uint32_t)(sh.Ltot + q));
     if (s >= (uint32_t)n) { atomicOr(P.err, kErrInternal); continue; }
@@ -345,10 +339,12 @@ __device__ void wrad_estimate(const StepParams &P, CellBuf<Real> &B, WarpShared 
     else { const double v2 = x * x + y * y + z * z; v1 += v2 * v2; }
     tx += x; ty += y; tz += z; t2 += x * x + y * y + z * z;
   }
-  v0 = warp_sum_call(v0); v1 = warp_sum_call(v1); tx = warp_sum_call(tx); ty = warp_sum_call(ty); tz = warp_sum_call(tz);
-  t2 = warp_sum_call(t2);
+  if (__any_sync(0xffffffffu, nT > 0)) {
+    v1 = warp_sum_call(v1); tx = warp_sum_call(tx); ty = warp_sum_call(ty); tz = warp_sum_call(tz);
+    t2 = warp_sum_call(t2);
+  }
   if (lane == 0) {
-    double s = v0 - v1;
+    double s = (sh.cind + sh.dS) - v1;
     if (nT > 0) {
       tx /= nT; ty /= nT; tz /= nT;
       const double T = fmax(0.0, t2 / nT - (tx * tx + ty * ty + tz * tz)) / 3.0;
@@ -446,7 +442,7 @@ __device__ void wmaxwellian(const StepParams &P, const RngKey &K, CellBuf<Real> 
 //                   and decision (sh.done = 1 when no retry follows)
 //   wphase_end      A8 Maxwellian, m_state, statistics row
 // Each returns kOk or an overflow flag (the cell is then left for the CTA path).
-template <typename Real>
+template <typename Real, int MOD = -1>
 __device__ int wphase_begin(const StepParams &P, CellBuf<Real> &B, WarpShared &sh, double *usplit, double sx,
                             double sy, double sz, int n, uint32_t gcell, const int32_t *m_state) {
   const int lane = threadIdx.x & 31;
@@ -483,27 +479,30 @@ __device__ int wphase_begin(const StepParams &P, CellBuf<Real> &B, WarpShared &s
       c2 += r2;
     }
   }
-  for (int d = lane; d < kSplitPre; d += 32) {   // split uniforms, in parallel
-    const uint4 w = K(kSplit, 0, (uint32_t)d, 0);
-    usplit[d] = u53(w.x, w.y);
+  {                                              // split uniforms of levels < 32, one per lane
+    const uint4 w = K(kSplit, 0, (uint32_t)lane, 0);
+    usplit[lane] = u53(w.x, w.y);
   }
   const uint4 pk = K(kPerm, 0, 0, 0);
   c0 = warp_sum_call(c0); c1 = warp_sum_call(c1); c2 = warp_sum_call(c2); dv2 = warp_max_call(dv2);
   __syncwarp();
   if (lane == 0) {
-    sh.n = n; sh.ux = ux; sh.uy = uy; sh.uz = uz; sh.c2 = c2; sh.pk = pk;
+    sh.n = n; sh.ux = ux; sh.uy = uy; sh.uz = uz; sh.c2 = c2; sh.pk = pk; sh.D0 = perm_dom((uint32_t)n);
     sh.sums[0] = Sx; sh.sums[1] = Sy; sh.sums[2] = Sz; sh.sums[3] = c2 + n * (ux * ux + uy * uy + uz * uz);
-    sh.S0 = (P.indicator == TRMCR_IND_PXX ? c0 : c1) / n;
+    sh.cind = P.indicator == TRMCR_IND_PXX ? c0 : c1;
+    sh.dS = 0.0;
+    sh.S0 = sh.cind / n;
     const double rho_c = P.shock ? n * P.w_over_dx : 1.0;
-    if (P.model == TRMCR_HARD_SPHERE) { sh.sigma = 2.0 * sqrt(dv2); sh.mu = rho_c * sh.sigma; }
-    else if (P.model == TRMCR_VHS) { sh.sigma = vhs_majorant(dv2, P.alpha); sh.mu = rho_c * sh.sigma; }
+    const int model = MOD >= 0 ? MOD : P.model;
+    if (model == TRMCR_HARD_SPHERE) { sh.sigma = 2.0 * sqrt(dv2); sh.mu = rho_c * sh.sigma; }
+    else if (model == TRMCR_VHS) { sh.sigma = vhs_majorant(dv2, P.alpha); sh.mu = rho_c * sh.sigma; }
     else { sh.sigma = 0.0; sh.mu = rho_c; }
     sh.sig_run = sh.sigma;
     sh.p = exp(-(sh.mu * P.dt / P.eps));
     sh.m_cur = m0; sh.flag = kOk;
     sh.prop = 0; sh.acc = 0; sh.viol = 0;
     // ---- A4: split ----
-    const int64_t N0 = ir_split(K, 0, sh.p * (double)n, usplit);
+    const int64_t N0 = ir_split(K, 0, sh.p * (double)n, usplit, kWarpSplitPre);
     B.Q[0] = (int32_t)N0;
     sh.rem = n - N0;
     sh.d = 0;
@@ -516,7 +515,7 @@ __device__ int wphase_begin(const StepParams &P, CellBuf<Real> &B, WarpShared &s
   return sh.flag;
 }
 
-template <typename Real, bool WB>
+template <typename Real, bool WB, int MOD = -1>
 __device__ int wphase_attempt(const StepParams &P, CellBuf<Real> &B, WarpShared &sh, double *usplit,
                               uint32_t gcell, trmcr_coll_rec *log, unsigned long long *log_count,
                               int64_t log_cap) {
@@ -524,11 +523,14 @@ __device__ int wphase_attempt(const StepParams &P, CellBuf<Real> &B, WarpShared 
   const RngKey K{P.k0, P.k1, gcell, P.step};
   const int n = sh.n;
   Perm pi0;
-  pi0.init(sh.pk, (uint32_t)n);
+  pi0.rk = sh.pk; pi0.D = sh.D0;
   const int attempt = sh.r;
+  PHASE_MARK(t_ph);
   wplan_counts<Real>(K, B, sh);
+  WPHASE_ADD(1, t_ph);   // plan counts
   if (sh.flag != kOk) return sh.flag;
-  wplan_execute<Real, WB>(P, K, B, sh, pi0, (Real)sh.sig_run, log, log_count, log_cap);
+  wplan_execute<Real, WB, MOD>(P, K, B, sh, pi0, (Real)sh.sig_run, log, log_count, log_cap);
+  WPHASE_ADD(2, t_ph);   // plan execute
   if (lane == 0) {
     if (attempt == 0) {
       sh.Ltot = sh.L;
@@ -544,19 +546,30 @@ __device__ int wphase_attempt(const StepParams &P, CellBuf<Real> &B, WarpShared 
   __syncwarp();
   if (!P.adaptive) return kOk;
   wrad_estimate<Real>(P, B, sh, pi0);
+  WPHASE_ADD(3, t_ph);   // RAD estimate
   if (lane == 0) {
-    if (sh.E1 > P.delta2 && sh.m_cur < P.m_cap) {
-      const int m_new = 2 * sh.m_cur < P.m_cap ? 2 * sh.m_cur : P.m_cap;
-      wsplit_extend(K, sh, m_new, B.Q, B.L_cap, usplit);
-      sh.r += 1;
-      sh.lo = sh.m_cur + 1;
-      sh.hi = sh.d < B.L_cap ? sh.d : B.L_cap;
-      sh.budget = sh.nT;
-      sh.leaf_off = sh.Ltot;
-      sh.m_cur = m_new;
-      sh.done = 0;
-    } else {
-      sh.m_next = (sh.E1 < P.delta1) ? (sh.m_cur / 2 > 1 ? sh.m_cur / 2 : 1) : sh.m_cur;
+    for (;;) {
+      if (sh.E1 > P.delta2 && sh.m_cur < P.m_cap) {
+        const int m_new = 2 * sh.m_cur < P.m_cap ? 2 * sh.m_cur : P.m_cap;
+        wsplit_extend(K, sh, m_new, B.Q, B.L_cap, usplit);
+        sh.r += 1;
+        sh.lo = sh.m_cur + 1;
+        sh.hi = sh.d < B.L_cap ? sh.d : B.L_cap;
+        sh.budget = sh.nT;
+        sh.leaf_off = sh.Ltot;
+        sh.m_cur = m_new;
+        sh.done = 0;
+        if (sh.flag != kOk) break;
+        // a retry whose plan is empty (no quota on the new levels) changes
+        // nothing - same Theta, same estimate: it is counted and decided here
+        int top = sh.hi;
+        while (top >= sh.lo && B.Q[top] == 0) top--;
+        if (top >= sh.lo && top >= 1) break;
+        sh.done = 1;
+      } else {
+        sh.m_next = (sh.E1 < P.delta1) ? (sh.m_cur / 2 > 1 ? sh.m_cur / 2 : 1) : sh.m_cur;
+        break;
+      }
     }
   }
   __syncwarp();
@@ -570,7 +583,7 @@ __device__ void wphase_end(const StepParams &P, CellBuf<Real> &B, WarpShared &sh
   const RngKey K{P.k0, P.k1, gcell, P.step};
   const int n = sh.n;
   Perm pi0;
-  pi0.init(sh.pk, (uint32_t)n);
+  pi0.rk = sh.pk; pi0.D = sh.D0;
   // ---- A8 ----
   wmaxwellian<Real, WB>(P, K, B, sh, pi0, sh.c2);
   if (out_x != B.vx)

@@ -9,6 +9,7 @@
 #include "../../include/trmcr.h"
 #include "cell_step.cuh"
 #include "cell_warp.cuh"
+#include "batch.cuh"
 
 namespace trmcr {
 
@@ -199,6 +200,8 @@ struct trmcr_ctx {
   unsigned *d_gm_done = nullptr;
   cudaEvent_t ev_defer = nullptr;
   int thermal_prefetch = 1;
+  trmcr::BatchLayout blay{};
+  int batch_grid = 0;                 // pooled-batch collision kernel (batch.cuh; 0: off)
   int lock_grid = 0, lock_smem = 0;   // shock lock-step collision kernel (0: free-running warps)   // L2 prefetch of each warp's next cell (TRMCR_THERMAL_PREFETCH=0 disables)
   int fast_ok = 1, fast_pending = 0, fast_grid = 0, smem_grid = 0, last_defer = -1, last_ovf = -1;
   unsigned char *d_scratch = nullptr;

@@ -1067,8 +1067,11 @@ shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
 #define TRMCR_LOCK_WARPS 4
 #endif
 constexpr int kLockWarps = TRMCR_LOCK_WARPS;   // measured: 16 -> 2.02 ms, 8 -> 1.80, 4 -> 1.66, 2 -> +0.09 ms (C5), free-running 1.75
-template <typename Real, bool WB>
-__global__ void __launch_bounds__(kLockWarps * 32, 16 / kLockWarps)
+#ifndef TRMCR_LOCK_MINB
+#define TRMCR_LOCK_MINB (16 / TRMCR_LOCK_WARPS)
+#endif
+template <typename Real, bool WB, int MOD = -1>
+__global__ void __launch_bounds__(kLockWarps * 32, TRMCR_LOCK_MINB)
 shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, int *defer_count,
                    int *defer_list, QueueArgs Q) {
@@ -1100,6 +1103,7 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
           st[TRMCR_ST_MUSED] = m; st[TRMCR_ST_MNEXT] = m;
         }
       } else {
+        PHASE_MARK(t_b);
         double sx = 0, sy = 0, sz = 0;
         if constexpr (sizeof(Real) == 4) {
           float fx = 0, fy = 0, fz = 0;
@@ -1108,24 +1112,31 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
         } else {
           for (int i = lane; i < n; i += 32) { sx += B.vx[i]; sy += B.vy[i]; sz += B.vz[i]; }
         }
-        rc = wphase_begin<Real>(P, B, sh, usplit, sx, sy, sz, n, P.cell_base + (uint32_t)c, m_state + c);
+        WPHASE_ADD(9, t_b);   // load sums
+        rc = wphase_begin<Real, MOD>(P, B, sh, usplit, sx, sy, sz, n, P.cell_base + (uint32_t)c, m_state + c);
+        WPHASE_ADD(0, t_b);   // moments + split
         run = rc == kOk;
       }
     }
     const bool work = run;
+    PHASE_MARK(t_w);
     // the begin phase ends in lock step; the attempts (attempt 0 and any RAD
     // retries) run free - a barrier per attempt measured slower (C5 1.61 vs
     // 1.53 ms: retries are a minority of the cells)
     __syncthreads();
+    WPHASE_ADD(10, t_w);   // barrier after begin
     while (run) {
-      rc = wphase_attempt<Real, WB>(P, B, sh, usplit, P.cell_base + (uint32_t)c, Q.log, Q.log_count, Q.log_cap);
+      rc = wphase_attempt<Real, WB, MOD>(P, B, sh, usplit, P.cell_base + (uint32_t)c, Q.log, Q.log_count, Q.log_cap);
       run = rc == kOk && !sh.done;
     }
+    PHASE_MARK(t_e);
     if (work && rc == kOk)
       wphase_end<Real, WB>(P, B, sh, B.vx, B.vy, B.vz, P.cell_base + (uint32_t)c, m_state + c,
                        stats + (size_t)c * TRMCR_NSTATS);
+    WPHASE_ADD(6, t_e);   // Maxwellian + stats
     if (c < S.C && rc != kOk && lane == 0) defer_list[atomicAdd(defer_count, 1)] = c;
     __syncthreads();                          // round in lock step (dropping it measured slower)
+    WPHASE_ADD(11, t_e);   // barrier at round end
   }
   pdl_trigger();
 }
@@ -1487,8 +1498,14 @@ trmcr_status shock_finish(trmcr_ctx *c) {
   if (use_warp && !fz) {
     prof_begin(c, TRMCR_K_SHOCK_WARP);
     const bool wb = ext_variant(c);
-    if (G.scatter && c->lock_grid > 0)
-      launch_k(c, (wb ? shock_collide_lock<Real, true> : shock_collide_lock<Real, false>), c->lock_grid, kLockWarps * 32, (size_t)(c->lock_smem), c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
+    if (G.scatter && c->batch_grid > 0)
+      launch_k(c, collide_batch<Real, QueueArgs>, c->batch_grid, kBatchThreads, (size_t)c->blay.total, c->P, c->blay, s.C, c->cap,
+               (const int64_t *)s.d_off[nxt], ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
+               c->d_defer_list, Q);
+    else if (G.scatter && c->lock_grid > 0)
+      launch_k(c, (wb ? shock_collide_lock<Real, true>
+                      : (c->P.model == TRMCR_HARD_SPHERE ? shock_collide_lock<Real, false, TRMCR_HARD_SPHERE>
+                                                         : shock_collide_lock<Real, false>)), c->lock_grid, kLockWarps * 32, (size_t)(c->lock_smem), c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
               c->d_defer_list, Q);
     else
       launch_k(c, (wb ? shock_collide_warp<Real, true> : shock_collide_warp<Real, false>), c->warp_grid, c->warp_wpc * 32, (size_t)(c->warp_smem), c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,

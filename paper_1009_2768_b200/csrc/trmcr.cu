@@ -706,6 +706,13 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
   if (c->geometry == TRMCR_SHOCK_1D) {
     trmcr_status s = shock_init(c, cc, &max_cell);
     if (s) return bail(s);
+    // per-cell capacities from the domain's densest state (cells of
+    // max(rho_L, rho_R) dx / w particles, + 6 sigma), not from this slab's
+    // initial data: every slab of a domain then sizes its plans alike, so a
+    // cell takes the same kernel (and the same rounding) in any partition
+    const double dx = (cc->x_max - cc->x_min) / (double)c->shock.Cg;
+    const double nd = std::max(cc->rho_L, cc->rho_R) * dx / cc->weight;
+    if (nd > 0.0 && nd < 1e7) max_cell = (int)ceil(nd + 6.0 * sqrt(nd) + 8.0);
   }
 
   // ---- shared-memory plan capacity ----
@@ -824,6 +831,9 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
                              ? (wbk ? (const void *)shock_collide_lock<double, true> : (const void *)shock_collide_lock<double, false>)
                              : (wbk ? (const void *)shock_collide_lock<float, true> : (const void *)shock_collide_lock<float, false>);
         int occ_l = 0;
+        const void *lfh = c->dtype == TRMCR_F64 ? (const void *)shock_collide_lock<double, false, TRMCR_HARD_SPHERE>
+                                                : (const void *)shock_collide_lock<float, false, TRMCR_HARD_SPHERE>;
+        if (allow_max_dyn_smem(lfh, smem_max) != cudaSuccess) cudaGetLastError();
         if (allow_max_dyn_smem(lf, smem_max) == cudaSuccess &&
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_l, lf, kLockWarps * 32, lsm) == cudaSuccess &&
             occ_l > 0) {
@@ -833,6 +843,32 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
           cudaGetLastError();
         }
       }
+    }
+  }
+
+  // ---- shock: pooled-batch collision kernel (batch.cuh; TRMCR_SHOCK_BATCH=0 disables) ----
+  if (c->geometry == TRMCR_SHOCK_1D && c->wlay.n_cap > 0 && !c->wlay.v_smem && !ext_variant(c) && c->P.debug_stop == 0) {
+    // off by default: on C5 it measured 1.90-2.30 ms against the lock-step
+    // kernel's 1.29; TRMCR_SHOCK_BATCH=1 enables it
+    const char *be = getenv("TRMCR_SHOCK_BATCH");
+    if (be && atoi(be) != 0) {
+      int nsm = 148, smem_sm = 0;
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->dev);
+      cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->dev);
+      const void *bf = c->dtype == TRMCR_F64 ? (const void *)collide_batch<double, QueueArgs> : (const void *)collide_batch<float, QueueArgs>;
+      cudaFuncAttributes a;
+      int occ_b = 0;
+      if (cudaFuncGetAttributes(&a, bf) == cudaSuccess) {
+        // two CTAs per SM: one stages its batch while the other computes
+        const size_t per = (size_t)smem_sm / kBatchCtas - 1024 - a.sharedSizeBytes - 64;
+        c->blay.build(c->rs, std::min(per, (size_t)smem_max - a.sharedSizeBytes));
+        if (c->blay.vcap >= 1024 && c->blay.kcap >= 512 &&
+            cudaFuncSetAttribute(bf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->blay.total) == cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, bf, kBatchThreads, c->blay.total) == cudaSuccess &&
+            occ_b > 0)
+          c->batch_grid = std::max(1, std::min((c->ncells + kBatchCells - 1) / kBatchCells, nsm * occ_b));
+      }
+      cudaGetLastError();
     }
   }
 

@@ -16,8 +16,8 @@ L = api.lib(); L.trmcr_debug_phase_cycles.argtypes = [ctypes.POINTER(ctypes.c_do
 out = np.zeros(16)
 sim.step(3); torch.cuda.synchronize(); L.trmcr_debug_phase_cycles(out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
 sim.step(steps); torch.cuda.synchronize(); L.trmcr_debug_phase_cycles(out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
-names = ["moments+split", "plan_counts", "plan_execute", "rad_estimate", "rad_retries", "pre-maxw", "maxwellian", "store", "gather"]
+names = ["moments+split", "plan_counts", "plan_execute", "rad_estimate", "rad_retries", "pre-maxw", "maxwellian", "store", "gather", "load_sums(lock)", "barrier_begin(lock)", "barrier_end(lock)", "pe_pass2", "pe_pass3"]
 cells = sim.ncells * steps
 st = sim.stats()
-print("per cell-step cycles:", {names[k]: round(out[k] / cells) for k in range(9)})
+print("per cell-step cycles:", {names[k]: round(out[k] / cells) for k in range(14)})
 print("mean depth", st["depth"].mean(), "attempts", st["attempts"].mean(), "proposals", st["proposals"].mean(), "thermalised", st["thermalised"].mean(), "n", st["n"].mean(), "m_used", st["m_used"].mean())
