@@ -1,6 +1,7 @@
 """Checks at BASELINE.json's full sizes, in the launch configuration bench.py
 times, on outputs the oracle can compute one by one (cells are independent and
 keyed by global cell id) or via properties that hold at any size."""
+import os
 import numpy as np
 import pytest
 
@@ -119,3 +120,20 @@ def test_config5_full_shock_two_steps():
     st = sim.stats()
     assert np.all(st["leaves"] + st["untouched"] + st["thermalised"] == st["n"])
     assert st["proposals"].sum() > 0
+
+
+@pytest.mark.slow
+def test_c4_shock_profile_statistical_parity_full_size():
+    """Config 4 at full size (north star: fp32 shock profiles
+    within 3 standard errors over 16 seeds): Mach 3, 2,000 cells x 500, eps 1,
+    RAD, 2,000 steps, rho / u_x / T of every cell averaged over the last 1,000
+    steps; fp32 GPU against the fp64 oracle run as concurrent processes
+    (tools/c4_profile_parity.py; ~90 s on 16 host cores)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pool = str(max(1, min(15, (os.cpu_count() or 2) - 1)))
+    out = os.path.join(root, "gpurun_out", "c4_profile_parity_test.json")
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "c4_profile_parity.py"), "2000", "16", pool, out],
+                       cwd=root, capture_output=True, text=True, timeout=3600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

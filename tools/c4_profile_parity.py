@@ -25,9 +25,11 @@ OBS = [1, 2, 5]          # moment columns: rho, u_x, T
 
 
 def initial(seed, dtype):
-    x, vx, vy, vz = synth.shock_particles(SETUP, seed=seed)
+    """The same initial state for both sides: fp32 values (the GPU's), binned
+    by their own cell (an fp32 position can round across a cell edge)."""
+    x, vx, vy, vz = synth.shock_particles(SETUP, seed=seed, dtype=np.float32)
     inv = SETUP["ncells"] / (SETUP["x_max"] - SETUP["x_min"])
-    cell = np.clip(np.floor((x - SETUP["x_min"]) * inv), 0, SETUP["ncells"] - 1)
+    cell = np.clip(np.floor((x.astype(np.float64) - SETUP["x_min"]) * inv), 0, SETUP["ncells"] - 1)
     o = np.argsort(cell, kind="stable")
     return [np.ascontiguousarray(a[o], dtype=dtype) for a in (x, vx, vy, vz)]
 
