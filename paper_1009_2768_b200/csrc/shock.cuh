@@ -73,6 +73,24 @@ template <typename Real> __device__ __forceinline__ Real mul_rn(Real a, Real b);
 template <> __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 template <> __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 
+// A1 for one particle: x' = x + v_x dt (no FMA, [R29]) and its local
+// destination cell (kDropped when it left the domain; may lie in a neighbour
+// slab).  transport_kernel stores the destination cell but not x': the kernels
+// that move the particles (scatter, gather, emigrant packing) read x and v_x
+// anyway and recompute x' - the same arithmetic, so the same value - which
+// saves the 4-byte write of x' per particle.  (Recomputing the destination
+// there too, instead of storing it, measured slower: C5 scatter 0.50 ->
+// 0.57 ms for 26 us less transport.)
+template <typename Real>
+__device__ __forceinline__ Real moved_x(const ShockDev &S, Real x, Real vx) {
+  return add_rn<Real>(x, mul_rn<Real>(vx, (Real)S.dt));
+}
+template <typename Real>
+__device__ __forceinline__ int dest_of(const ShockDev &S, Real xn) {
+  const double xd = (double)xn;
+  return (xd >= S.x_min && xd < S.x_max) ? cell_of(S, xd) - S.cbase : kDropped;
+}
+
 // warp-aggregated atomicAdd(&counts[key], 1) for lanes with key >= 0
 __device__ __forceinline__ void count_key(int32_t *counts, int key) {
   const unsigned act = 0xffffffffu;   // called by full warps
@@ -383,8 +401,8 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
   __shared__ Real s_xend[2];
   int d[NG][P4];
   int dropped = 0, dmin = INT32_MAX, dmax = -1, lemi = 0, remi = 0;
-  // every load of the tile first (x is rewritten below: the compiler may not
-  // move later loads above those stores), then the arithmetic
+  // every load of the tile first, then the arithmetic (x and v are read only:
+  // the moves are recomputed where the particles are moved)
   Real xa[NG][P4], va[NG][P4];
 #pragma unroll
   for (int g = 0; g < NG; ++g) {
@@ -403,8 +421,7 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
     }
   }
   // source cells of the tile's first and last particles (the array is sorted
-  // by cell: every source cell of the tile lies between them), read before
-  // any position of the tile is rewritten
+  // by cell: every source cell of the tile lies between them)
   if (threadIdx.x == 0 && tile0 < n) {
     s_xend[0] = x[tile0];
     s_xend[1] = x[min(n, tile0 + (int64_t)TILE) - 1];
@@ -420,12 +437,9 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
     for (int k = 0; k < P4; ++k) {
       d[g][k] = -1;
       if (i0 + k >= n) continue;
-      const Real xn = add_rn<Real>(xs[k], mul_rn<Real>(vs[k], (Real)S.dt));
-      xs[k] = xn;
-      const double xd = (double)xn;
-      const bool keep = xd >= S.x_min && xd < S.x_max;
-      const int dl = keep ? cell_of(S, xd) - S.cbase : kDropped;
-      if (!keep) {
+      const Real xn = moved_x<Real>(S, xs[k], vs[k]);
+      const int dl = dest_of<Real>(S, xn);
+      if (dl == kDropped) {
         ++dropped;
       } else if (dl >= 0 && dl < S.C) {
         dmin = min(dmin, dl);
@@ -435,17 +449,10 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
       } else {
         remi = 1;
       }
-      if (!vec) { x[i0 + k] = xn; dest[i0 + k] = dl; }
       d[g][k] = dl;
+      if (!vec) dest[i0 + k] = dl;
     }
-    if (vec) {
-      using V = typename Vec<Real>::T;
-      V xv;
-#pragma unroll
-      for (int k = 0; k < P4; ++k) vset<V, Real>(xv, k, xs[k]);
-      *reinterpret_cast<V *>(x + i0) = xv;
-      *reinterpret_cast<int4 *>(dest + i0) = make_int4(d[g][0], d[g][1], d[g][2], d[g][3]);
-    }
+    if (vec) *reinterpret_cast<int4 *>(dest + i0) = make_int4(d[g][0], d[g][1], d[g][2], d[g][3]);
 #pragma unroll
     for (int k = 0; k < P4; ++k) if (d[g][k] < 0 || d[g][k] >= S.C) d[g][k] = -1;   // counted below: local only
   }
@@ -559,7 +566,8 @@ pack_emigrants(ShockDev S, const int64_t *__restrict__ off_old, const int *ng, c
         bits &= bits - 1;
         const int64_t i = i0 + k;
         if (pos < cap) {
-          B.x[pos] = sx[i]; B.vx[pos] = svx[i]; B.vy[pos] = svy[i]; B.vz[pos] = svz[i];
+          const Real xn = seg == 1 ? moved_x<Real>(S, sx[i], svx[i]) : sx[i];
+          B.x[pos] = xn; B.vx[pos] = svx[i]; B.vy[pos] = svy[i]; B.vz[pos] = svz[i];
           B.dest[pos] = sd[i] + S.cbase;   // global destination cell
         }
         ++pos;
@@ -816,7 +824,9 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
       const int bin = bins[r0 + q];
       if (bin >= 0) {
         const int64_t pos = s_off[bin] + rk[r0 + q];
-        if (pos < S.cap) { ox[pos] = a[q]; ovx[pos] = bx[q]; ovy[pos] = by[q]; ovz[pos] = bz[q]; }
+        if (pos < S.cap) {
+          ox[pos] = moved_x<Real>(S, a[q], bx[q]); ovx[pos] = bx[q]; ovy[pos] = by[q]; ovz[pos] = bz[q];
+        }
       }
     }
   }
@@ -909,6 +919,7 @@ __device__ int gather_cell(const ShockDev &S, const GatherSrc &G, int c, Real *b
         if ((bits >> k) & 1u) {
           const int64_t i = i0 + k;
           tx[k] = sx[i]; tvx[k] = svx[i]; tvy[k] = svy[i]; tvz[k] = svz[i];
+          if (seg == 2) tx[k] = moved_x<Real>(S, tx[k], tvx[k]);
         }
       }
 #pragma unroll
@@ -987,6 +998,7 @@ __device__ __noinline__ int gather_cell_warp(const ShockDev &S, const GatherSrc 
         if ((bits >> k) & 1u) {
           const int64_t i = i0 + k;
           tx[k] = px[i]; tvx[k] = pvx[i]; tvy[k] = pvy[i]; tvz[k] = pvz[i];
+          if (seg == 2) tx[k] = moved_x<Real>(S, tx[k], tvx[k]);
         }
       }
 #pragma unroll
