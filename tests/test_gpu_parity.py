@@ -185,6 +185,25 @@ def test_giant_cell_parallel_ranks_fp64(orc, api):
     assert o.stats["proposals"][0] > 8000
 
 
+def test_giant_cell_deep_rad_config2_eps01_fp64(orc, api):
+    """Config 2's deep regime: a 40,000-particle hard-sphere
+    cell with the (2, 1/2, 1/2) anisotropic Gaussian, eps = 0.1, dt = 0.05
+    (x = mu dt / eps ~ 6-7: p ~ 1e-3, depth limited only by RAD), RAD with
+    m_init = 2 and m_cap = 4096, on the grid-cooperative giant-cell kernel:
+    every decision (incl. the RAD retries and m_next) and every velocity as the
+    oracle's, over 2 steps (measured: m = 4096, 2,858 levels, 113,625 proposals)."""
+    v = synth.anisotropic_gaussian(40_000, seed=31)
+    v = tuple(np.asarray(a, dtype=np.float64) for a in v)
+    sim, o = _parity(orc, api, v, np.array([0, 40_000]), 2, log_cap=3_000_000, model=1, adaptive=1, m_init=2,
+                     m_cap=4096, eps=0.1, dt=0.05, seed=31)
+    st = o.stats
+    x = st["mu"][0] * 0.05 / 0.1
+    assert 4.0 < x < 10.0, x
+    # RAD doubled m far past the default 64 (step 1) and the trees are thousands of levels deep
+    assert st["m_used"][0] >= 256 and st["depth"][0] >= 256 and st["proposals"][0] > 10_000, (
+        st["m_used"][0], st["depth"][0], st["proposals"][0])
+
+
 def test_giant_cell_vhs_wb_fp64(orc, api):
     """A 40,000-particle cell on the grid-cooperative kernel with VHS molecules
     (alpha = 0.6) and TRMC-WB (1 + mean, m_max = 2): every decision and
