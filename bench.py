@@ -238,6 +238,16 @@ def oracle_rate(W, seconds=12.0, min_steps=1, max_steps=10**9):
 
 
 # ----------------------------------------------------------------------------- arms
+def full_cfg(W, world):
+    """The config record of a workload at `world` GPUs - the same dict on both arms."""
+    cfg = dict(W["cfg"])
+    rs = 4 if W["dtype"] == np.float32 else 8
+    n_local = len(W["vx"])
+    cfg.update(parallelism=f"{'cells' if W['kind'] == 'hom' else 'slabs'}x{world}",
+               l2="inputs larger than L2 (no flush)" if n_local * 3 * rs > 126e6 else "inputs L2-resident")
+    return cfg
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
@@ -249,7 +259,8 @@ def run_reference(args, rank):
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "ms_per_step": 1e3 * info["seconds"] / max(info["steps"], 1), "dtype": "f64",
-            "data": "synthetic", "config": W["cfg"],
+            "data": "synthetic", "config": full_cfg(workload(args.workload, 0, args.gpus, args.eps), args.gpus)
+            if args.gpus > 1 else full_cfg(W, 1),
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": info["sample"]},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -445,9 +456,7 @@ def measure(args, wl_name, rank, world, local_rank, cpu_seconds):
         cpu = {"value": rate, "unit": UNIT, "cores": info["cores"], "kind": "oracle",
                "sample": info["sample"]}
     clocks = clk.summary()
-    cfg = dict(W["cfg"])
-    cfg.update(parallelism=f"{'cells' if W['kind'] == 'hom' else 'slabs'}x{world}",
-               l2="inputs larger than L2 (no flush)" if n_local * 3 * rs > 126e6 else "inputs L2-resident")
+    cfg = full_cfg(W, world)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": W.get("scaling", "strong"), "vs_baseline": None,
