@@ -321,7 +321,7 @@ collide_batch(StepParams P, BatchLayout Lay, int C, int64_t cap, const int64_t *
         double sx, sy, sz;
         if constexpr (sizeof(Real) == 4) {
           float fx = 0, fy = 0, fz = 0;
-          for (int q = lane; q < n; q += 32) { fx += vx[q]; fy += vy[q]; fz += vz[q]; }
+          warp_cell_for<float>(vx, vy, vz, n, [&](float x, float y, float z) { fx += x; fy += y; fz += z; });
           sx = fx; sy = fy; sz = fz;
         } else {
           sx = 0; sy = 0; sz = 0;
@@ -333,8 +333,7 @@ collide_batch(StepParams P, BatchLayout Lay, int C, int64_t cap, const int64_t *
         if constexpr (sizeof(Real) == 4) {
           const float fux = (float)ux, fuy = (float)uy, fuz = (float)uz;
           float f0 = 0, f1 = 0, f2 = 0, fm = 0;
-          for (int q = lane; q < n; q += 32) {
-            const float x = vx[q], y = vy[q], z = vz[q];
+          warp_cell_for<float>(vx, vy, vz, n, [&](float x, float y, float z) {
             const float dx = x - fux, dy = y - fuy, dz = z - fuz;
             const float r2 = dx * dx + dy * dy + dz * dz;
             fm = fmaxf(fm, r2);
@@ -342,7 +341,7 @@ collide_batch(StepParams P, BatchLayout Lay, int C, int64_t cap, const int64_t *
             const float v2 = x * x + y * y + z * z;
             f1 += v2 * v2;
             f2 += r2;
-          }
+          });
           c0 = f0; c1 = f1; c2 = f2; dv2 = fm;
         } else {
           for (int q = lane; q < n; q += 32) {

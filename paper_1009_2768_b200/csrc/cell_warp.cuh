@@ -17,6 +17,31 @@ constexpr int kWarpSplitPre = 32;      // split uniforms drawn up front: one per
 #define TRMCR_WARP_MINB 4        // CTAs of kWarpCellWarps warps per SM the register budget allows (128 regs)
 #endif
 
+// Visit the n particles (vx, vy, vz)[0..n) of a cell with the warp, in a
+// fixed per-lane order: fp32 cells go through 16-byte loads (four particles per
+// lane per round: the first pass over a cell is bound by its load latency);
+// the unaligned head and the tail particle by particle.  f(x, y, z) per
+// particle.  fp64: plain lane-strided loop (the oracle parity path).
+template <typename Real, typename F>
+__device__ __forceinline__ void warp_cell_for(const Real *vx, const Real *vy, const Real *vz, int n, F &&f) {
+  const int lane = threadIdx.x & 31;
+  if constexpr (sizeof(Real) == 4) {
+    const int head = min(n, (int)((4u - (((uint32_t)reinterpret_cast<uintptr_t>(vx)) >> 2)) & 3u));
+    if (lane < head) f(vx[lane], vy[lane], vz[lane]);
+    const int body = (n - head) >> 2;
+    const float4 *X = reinterpret_cast<const float4 *>(vx + head), *Y = reinterpret_cast<const float4 *>(vy + head),
+                 *Z = reinterpret_cast<const float4 *>(vz + head);
+    for (int q = lane; q < body; q += 32) {
+      const float4 a = X[q], b = Y[q], c = Z[q];
+      f(a.x, b.x, c.x); f(a.y, b.y, c.y); f(a.z, b.z, c.z); f(a.w, b.w, c.w);
+    }
+    const int t = head + 4 * body + lane;
+    if (t < n) f(vx[t], vy[t], vz[t]);
+  } else {
+    for (int i = lane; i < n; i += 32) f(vx[i], vy[i], vz[i]);
+  }
+}
+
 // Per-warp scalars (in the warp's slab, lane 0 writes, __syncwarp publishes).
 struct WarpShared {
   double ux, uy, uz, S0, sigma, p, mu, S_est, E1, c2;
@@ -456,8 +481,7 @@ __device__ int wphase_begin(const StepParams &P, CellBuf<Real> &B, WarpShared &s
     // fp32 statistical mode: fp32 lane partials (~n/32 terms), fp64 warp sums
     const float fux = (float)ux, fuy = (float)uy, fuz = (float)uz;
     float f0 = 0, f1 = 0, f2 = 0, fm = 0;
-    for (int i = lane; i < n; i += 32) {
-      const float x = B.vx[i], y = B.vy[i], z = B.vz[i];
+    warp_cell_for<float>(B.vx, B.vy, B.vz, n, [&](float x, float y, float z) {
       const float dx = x - fux, dy = y - fuy, dz = z - fuz;
       const float r2 = dx * dx + dy * dy + dz * dz;
       fm = fmaxf(fm, r2);
@@ -465,7 +489,7 @@ __device__ int wphase_begin(const StepParams &P, CellBuf<Real> &B, WarpShared &s
       const float v2 = x * x + y * y + z * z;
       f1 += v2 * v2;
       f2 += r2;
-    }
+    });
     c0 = f0; c1 = f1; c2 = f2; dv2 = fm;
   } else {
     for (int i = lane; i < n; i += 32) {

@@ -1119,7 +1119,7 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
         double sx = 0, sy = 0, sz = 0;
         if constexpr (sizeof(Real) == 4) {
           float fx = 0, fy = 0, fz = 0;
-          for (int i = lane; i < n; i += 32) { fx += B.vx[i]; fy += B.vy[i]; fz += B.vz[i]; }
+          warp_cell_for<float>(B.vx, B.vy, B.vz, n, [&](float x, float y, float z) { fx += x; fy += y; fz += z; });
           sx = fx; sy = fy; sz = fz;
         } else {
           for (int i = lane; i < n; i += 32) { sx += B.vx[i]; sy += B.vy[i]; sz += B.vz[i]; }
