@@ -103,13 +103,19 @@ __device__ __forceinline__ void count_key(int32_t *counts, int key) {
 template <typename Real>
 __global__ void shock_bin_init(ShockDev S, const Real *__restrict__ x, int64_t n, int32_t *counts, int *err) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double xi = (double)x[i];
-  if (!(xi >= S.x_min && xi < S.x_max)) { atomicOr(err, 4); return; }
-  const int c = cell_of(S, xi) - S.cbase;
-  if (c < 0 || c >= S.C) { atomicOr(err, 4); return; }
-  if (i > 0 && cell_of(S, (double)x[i - 1]) - S.cbase > c) atomicOr(err, 8);
-  atomicAdd(&counts[c], 1);
+  int key = -1;                                  // full warps reach count_key (warp-aggregated:
+  if (i < n) {                                   // sorted input, a warp's particles share few cells)
+    const double xi = (double)x[i];
+    if (!(xi >= S.x_min && xi < S.x_max)) {
+      atomicOr(err, 4);
+    } else {
+      const int c = cell_of(S, xi) - S.cbase;
+      if (c < 0 || c >= S.C) atomicOr(err, 4);
+      else key = c;
+      if (i > 0 && cell_of(S, (double)x[i - 1]) - S.cbase > c) atomicOr(err, 8);
+    }
+  }
+  count_key(counts, key);
 }
 
 // exclusive scan of counts[0..C) into off[0..C], off[C] = total (one CTA).

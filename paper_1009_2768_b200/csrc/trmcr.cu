@@ -170,42 +170,43 @@ cell_step_warp(StepParams P, WarpSlabLayout Lay, const int64_t *__restrict__ off
   step_kernel_epilogue();
 }
 
-// A9: per-cell moments, one CTA per cell (two passes).
+// A9: per-cell moments, one warp per cell (two passes: the second reads the
+// cell from L1), fp64 sums of the lane partials.
+constexpr int kMomWarps = 8;
 template <typename Real>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kMomWarps * 32)
 moments_kernel(const int64_t *__restrict__ offsets, int ncells, const Real *__restrict__ vx,
                const Real *__restrict__ vy, const Real *__restrict__ vz,
                const int32_t *__restrict__ m_state, int shock, double w_over_dx, double *out) {
-  __shared__ double red[8 * 8];
-  const int c = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * kMomWarps + (threadIdx.x >> 5);
   if (c >= ncells) return;
   const int64_t off = offsets[c];
   const int n = (int)(offsets[c + 1] - off);
-  double s[3] = {0, 0, 0};
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    s[0] += (double)vx[off + i]; s[1] += (double)vy[off + i]; s[2] += (double)vz[off + i];
-  }
-  block_sum<3>(s, red);
-  const double ux = n ? s[0] / n : 0.0, uy = n ? s[1] / n : 0.0, uz = n ? s[2] / n : 0.0;
-  double t[4] = {0, 0, 0, 0};
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const double x = vx[off + i], y = vy[off + i], z = vz[off + i];
+  const Real *X = vx + off, *Y = vy + off, *Z = vz + off;
+  double s0 = 0, s1 = 0, s2 = 0;
+  warp_cell_for<Real>(X, Y, Z, n, [&](Real x, Real y, Real z) { s0 += (double)x; s1 += (double)y; s2 += (double)z; });
+  s0 = warp_sum(s0); s1 = warp_sum(s1); s2 = warp_sum(s2);
+  const double ux = n ? s0 / n : 0.0, uy = n ? s1 / n : 0.0, uz = n ? s2 / n : 0.0;
+  double t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+  warp_cell_for<Real>(X, Y, Z, n, [&](Real xr, Real yr, Real zr) {
+    const double x = xr, y = yr, z = zr;
     const double dx = x - ux, dy = y - uy, dz = z - uz;
     const double c2 = dx * dx + dy * dy + dz * dz, v2 = x * x + y * y + z * z;
-    t[0] += c2; t[1] += dx * dx; t[2] += v2 * v2; t[3] += c2 * c2;
-  }
-  block_sum<4>(t, red);
-  if (threadIdx.x == 0) {
+    t0 += c2; t1 += dx * dx; t2 += v2 * v2; t3 += c2 * c2;
+  });
+  t0 = warp_sum(t0); t1 = warp_sum(t1); t2 = warp_sum(t2); t3 = warp_sum(t3);
+  if (lane == 0) {
     double *r = out + (size_t)c * TRMCR_NMOMENTS;
     const double rho = shock ? n * w_over_dx : 1.0;
-    const double T = n ? t[0] / (3.0 * n) : 0.0;
+    const double T = n ? t0 / (3.0 * n) : 0.0;
     r[TRMCR_MO_N] = n; r[TRMCR_MO_RHO] = rho;
     r[TRMCR_MO_UX] = ux; r[TRMCR_MO_UY] = uy; r[TRMCR_MO_UZ] = uz; r[TRMCR_MO_T] = T;
     r[TRMCR_MO_E] = 0.5 * rho * (ux * ux + uy * uy + uz * uz + 3.0 * T);
     r[TRMCR_MO_P] = rho * T;
-    r[TRMCR_MO_PXX] = n ? t[1] / n : 0.0;
-    r[TRMCR_MO_M4] = n ? t[2] / n : 0.0;
-    r[TRMCR_MO_M4C] = n ? t[3] / n : 0.0;
+    r[TRMCR_MO_PXX] = n ? t1 / n : 0.0;
+    r[TRMCR_MO_M4] = n ? t2 / n : 0.0;
+    r[TRMCR_MO_M4C] = n ? t3 / n : 0.0;
     r[TRMCR_MO_MMAX] = m_state[c];
   }
 }
@@ -362,7 +363,7 @@ template <typename Real>
 trmcr_status launch_moments(trmcr_ctx *c) {
   if (c->ncells == 0) return TRMCR_OK;
   prof_begin(c, TRMCR_K_MOMENTS);
-  moments_kernel<Real><<<c->ncells, 256, 0, c->stream>>>(
+  moments_kernel<Real><<<(c->ncells + kMomWarps - 1) / kMomWarps, kMomWarps * 32, 0, c->stream>>>(
       c->d_offsets, c->ncells, (const Real *)c->v[c->cur][0], (const Real *)c->v[c->cur][1],
       (const Real *)c->v[c->cur][2], c->d_mstate, c->P.shock, c->P.w_over_dx, c->d_moments);
   return check_launch(c, "moments_kernel", TRMCR_K_MOMENTS);
