@@ -736,6 +736,13 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
   __shared__ int64_t s_off[kHist];                         // off_new of the tile's destination cells
   __shared__ int2 s_meta[32];
   __shared__ int s_nb, s_more;
+  // fp32: the tile's x, v_x, v_y, v_z are staged in shared memory by 1-D bulk
+  // copies issued first, so the whole tile's reads are in flight while the
+  // destinations are ranked (the data movement was bound by load latency:
+  // 8 long-scoreboard stalls per issue with loads issued 4 rounds at a time)
+  constexpr bool kStage = sizeof(Real) == 4;
+  extern __shared__ __align__(16) unsigned char s_stage[];   // [4][TILE] Real when kStage
+  __shared__ uint64_t s_bar;
   const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (W[2]) return;                                   // gather fallback this step
   if (off_new[S.C] > S.cap) return;                   // capacity exceeded (err set by the scan): no stores
@@ -745,6 +752,24 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
   const int dmin = tile_meta[t].x;
   if (dmin == INT32_MAX) return;                     // no local destination in this tile
   const int Wd = W[0];
+  Real *st_x = reinterpret_cast<Real *>(s_stage), *st_vx = st_x + TILE, *st_vy = st_vx + TILE, *st_vz = st_vy + TILE;
+  const int tcnt = (int)min((int64_t)TILE, n - i_begin);
+  const int tbulk = (tcnt * (int)sizeof(Real)) & ~15;   // bytes per array through the bulk copy
+  if constexpr (kStage) {
+    if (tid == 0) {
+      mbar_init(&s_bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&s_bar, 4u * (uint32_t)tbulk);
+      if (tbulk > 0) {
+        bulk_g2s(st_x, x + i_begin, (uint32_t)tbulk, &s_bar);
+        bulk_g2s(st_vx, vx + i_begin, (uint32_t)tbulk, &s_bar);
+        bulk_g2s(st_vy, vy + i_begin, (uint32_t)tbulk, &s_bar);
+        bulk_g2s(st_vz, vz + i_begin, (uint32_t)tbulk, &s_bar);
+      }
+    }
+    const int k = tbulk / (int)sizeof(Real) + tid;     // the ragged tail, per element
+    if (k < tcnt) { st_x[k] = x[i_begin + k]; st_vx[k] = vx[i_begin + k]; st_vy[k] = vy[i_begin + k]; st_vz[k] = vz[i_begin + k]; }
+  }
   // ---- pass 1: this warp's destinations (kept in registers) and bin counts ----
   for (int q = tid; q < NW * kHist; q += kScatterThreads) (&s_wc[0][0])[q] = 0;
   __syncwarp();
@@ -814,6 +839,24 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
     __syncwarp();
     if (bin >= 0 && __ffs(peers) - 1 == lane) s_wc[warp][bin] += __popc(peers);
     __syncwarp();
+  }
+  if constexpr (kStage) {
+    mbar_wait(&s_bar, 0u);
+    __syncthreads();                                  // the tail's generic writes
+#pragma unroll
+    for (int r = 0; r < ROUNDS; ++r) {
+      const int bin = bins[r];
+      if (bin >= 0) {
+        const int k = warp * CHUNK + r * 32 + lane;
+        const int64_t pos = s_off[bin] + rk[r];
+        if (pos < S.cap) {
+          const Real vxk = st_vx[k];
+          ox[pos] = moved_x<Real>(S, st_x[k], vxk); ovx[pos] = vxk; ovy[pos] = st_vy[k]; ovz[pos] = st_vz[k];
+        }
+      }
+    }
+    pdl_trigger();
+    return;
   }
   // ---- data movement: independent 4-round batches of loads, then the stores ----
   constexpr int BATCH = ROUNDS < 4 ? ROUNDS : 4;
@@ -1508,7 +1551,8 @@ trmcr_status shock_finish(trmcr_ctx *c) {
         ovx, ovy, ovz, s.d_W);
     if (auto e = check_launch(c, "edge_place")) return e;
     auto *sk = s.tile_ng == 1 ? scatter_sorted<Real, 1> : scatter_sorted<Real, kTransportGroups>;
-    launch_k(c, sk, std::max(s.ntiles, 1), kScatterThreads, (size_t)(0), d, s.d_off[cur], s.d_off[nxt], (const Real *)c->x[cur], (const Real *)c->v[cur][0],
+    const size_t stage = sizeof(Real) == 4 ? 4 * sizeof(Real) * (size_t)tile_of(s.tile_ng) : 0;
+    launch_k(c, sk, std::max(s.ntiles, 1), kScatterThreads, stage, d, s.d_off[cur], s.d_off[nxt], (const Real *)c->x[cur], (const Real *)c->v[cur][0],
         (const Real *)c->v[cur][1], (const Real *)c->v[cur][2], s.d_dest, s.d_tileH, s.d_tile_meta, s.d_lcnt,
         s.d_W, ox, ovx, ovy, ovz);
     if (auto e = check_launch(c, "scatter_sorted", TRMCR_K_SCATTER)) return e;

@@ -847,6 +847,15 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
     }
   }
 
+  // ---- shock: the scatter sort stages fp32 tiles (4 x 16 KB) in dynamic shared memory ----
+  if (c->geometry == TRMCR_SHOCK_1D && c->dtype == TRMCR_F32) {
+    const void *f1 = (const void *)scatter_sorted<float, 1>, *f4 = (const void *)scatter_sorted<float, kTransportGroups>;
+    if (allow_max_dyn_smem(f1, smem_max) != cudaSuccess || allow_max_dyn_smem(f4, smem_max) != cudaSuccess) {
+      fail(c, TRMCR_ECUDA, "cudaFuncSetAttribute(scatter_sorted) failed");
+      return bail(TRMCR_ECUDA);
+    }
+  }
+
   // ---- shock: pooled-batch collision kernel (batch.cuh; TRMCR_SHOCK_BATCH=0 disables) ----
   if (c->geometry == TRMCR_SHOCK_1D && c->wlay.n_cap > 0 && !c->wlay.v_smem && !ext_variant(c) && c->P.debug_stop == 0) {
     // off by default: on C5 it measured 1.90-2.30 ms against the lock-step
