@@ -23,23 +23,29 @@ constexpr int kWarpSplitPre = 32;      // split uniforms drawn up front: one per
 // the unaligned head and the tail particle by particle.  f(x, y, z) per
 // particle.  fp64: plain lane-strided loop (the oracle parity path).
 template <typename Real, typename F>
-__device__ __forceinline__ void warp_cell_for(const Real *vx, const Real *vy, const Real *vz, int n, F &&f) {
+__device__ __forceinline__ void warp_cell_fori(const Real *vx, const Real *vy, const Real *vz, int n, F &&f) {
   const int lane = threadIdx.x & 31;
   if constexpr (sizeof(Real) == 4) {
     const int head = min(n, (int)((4u - (((uint32_t)reinterpret_cast<uintptr_t>(vx)) >> 2)) & 3u));
-    if (lane < head) f(vx[lane], vy[lane], vz[lane]);
+    if (lane < head) f(lane, vx[lane], vy[lane], vz[lane]);
     const int body = (n - head) >> 2;
     const float4 *X = reinterpret_cast<const float4 *>(vx + head), *Y = reinterpret_cast<const float4 *>(vy + head),
                  *Z = reinterpret_cast<const float4 *>(vz + head);
     for (int q = lane; q < body; q += 32) {
       const float4 a = X[q], b = Y[q], c = Z[q];
-      f(a.x, b.x, c.x); f(a.y, b.y, c.y); f(a.z, b.z, c.z); f(a.w, b.w, c.w);
+      const int i = head + 4 * q;
+      f(i, a.x, b.x, c.x); f(i + 1, a.y, b.y, c.y); f(i + 2, a.z, b.z, c.z); f(i + 3, a.w, b.w, c.w);
     }
     const int t = head + 4 * body + lane;
-    if (t < n) f(vx[t], vy[t], vz[t]);
+    if (t < n) f(t, vx[t], vy[t], vz[t]);
   } else {
-    for (int i = lane; i < n; i += 32) f(vx[i], vy[i], vz[i]);
+    for (int i = lane; i < n; i += 32) f(i, vx[i], vy[i], vz[i]);
   }
+}
+// (the same without the slot index)
+template <typename Real, typename F>
+__device__ __forceinline__ void warp_cell_for(const Real *vx, const Real *vy, const Real *vz, int n, F &&f) {
+  warp_cell_fori<Real>(vx, vy, vz, n, [&](int, Real x, Real y, Real z) { f(x, y, z); });
 }
 
 // Per-warp scalars (in the warp's slab, lane 0 writes, __syncwarp publishes).
@@ -632,15 +638,15 @@ __device__ void wphase_end(const StepParams &P, CellBuf<Real> &B, WarpShared &sh
 // sx, sy, sz) through A3-A8, phases back to back.  Returns kOk or kOverflow
 // (nothing written then except B's scratch).  Writes m_state, stats, and the
 // velocities (out_* unless they alias the slab).
-template <typename Real, bool WB>
+template <typename Real, bool WB, int MOD = -1>
 __device__ int process_cell_warp(const StepParams &P, CellBuf<Real> &B, WarpShared &sh, double *usplit,
                                  double sx, double sy, double sz, Real *out_x, Real *out_y, Real *out_z, int n,
                                  uint32_t gcell, int32_t *m_state, double *stats_row, trmcr_coll_rec *log,
                                  unsigned long long *log_count, int64_t log_cap) {
-  int rc = wphase_begin<Real>(P, B, sh, usplit, sx, sy, sz, n, gcell, m_state);
+  int rc = wphase_begin<Real, MOD>(P, B, sh, usplit, sx, sy, sz, n, gcell, m_state);
   if (rc != kOk) return rc;
   for (;;) {
-    rc = wphase_attempt<Real, WB>(P, B, sh, usplit, gcell, log, log_count, log_cap);
+    rc = wphase_attempt<Real, WB, MOD>(P, B, sh, usplit, gcell, log, log_count, log_cap);
     if (rc != kOk) return rc;
     if (sh.done) break;
   }

@@ -132,7 +132,7 @@ cell_step_giant(StepParams P, GmemScratch G, CellShared *gsh, double *part, int3
 
 // General cells, one warp each (cell_warp.cuh), over the thermal kernel's
 // defer list (or every cell); cells that do not fit go to list2 (CTA kernel).
-template <typename Real, bool WB>
+template <typename Real, bool WB, int MOD = -1>
 __global__ void __launch_bounds__(kWarpCellWarps * 32, TRMCR_WARP_MINB)
 cell_step_warp(StepParams P, WarpSlabLayout Lay, const int64_t *__restrict__ offsets, int ncells,
                const int *list_count, const int *list, Real *vx, Real *vy, Real *vz, int32_t *m_state,
@@ -154,13 +154,12 @@ cell_step_warp(StepParams P, WarpSlabLayout Lay, const int64_t *__restrict__ off
     int rc = kOverflow;
     if (n > 0 && n <= Lay.n_cap) {
       double sx = 0, sy = 0, sz = 0;
-      for (int i = lane; i < n; i += 32) {
-        const Real a = vx[off + i], b = vy[off + i], d = vz[off + i];
+      warp_cell_fori<Real>(vx + off, vy + off, vz + off, n, [&](int i, Real a, Real b, Real d) {
         B.vx[i] = a; B.vy[i] = b; B.vz[i] = d;
         sx += a; sy += b; sz += d;
-      }
+      });
       __syncwarp();
-      rc = process_cell_warp<Real, WB>(P, B, sh, usplit, sx, sy, sz, vx + off, vy + off, vz + off, n,
+      rc = process_cell_warp<Real, WB, MOD>(P, B, sh, usplit, sx, sy, sz, vx + off, vy + off, vz + off, n,
                                    P.cell_base + (uint32_t)c, m_state + c, stats + (size_t)c * TRMCR_NSTATS,
                                    Q.log, Q.log_count, Q.log_cap);
     }
@@ -312,7 +311,10 @@ trmcr_status launch_collide(trmcr_ctx *c) {
     const int *l1c = fast ? c->d_defer_count : nullptr, *l1 = fast ? c->d_defer_list : nullptr;
     if (use_warp) {
       prof_begin(c, TRMCR_K_CELL_WARP);
-      launch_k(c, ext_variant(c) ? cell_step_warp<Real, true> : cell_step_warp<Real, false>, idle ? 1 : c->warp_grid, c->warp_wpc * 32, (size_t)c->warp_smem, c->P,
+      launch_k(c, ext_variant(c) ? cell_step_warp<Real, true>
+                                 : (c->P.model == TRMCR_HARD_SPHERE ? cell_step_warp<Real, false, TRMCR_HARD_SPHERE>
+                                                                    : cell_step_warp<Real, false>),
+               idle ? 1 : c->warp_grid, c->warp_wpc * 32, (size_t)c->warp_smem, c->P,
                c->wlay, (const int64_t *)c->d_offsets, c->ncells, l1c, l1, vx, vy, vz, c->d_mstate, c->d_stats,
                c->d_defer2_count, c->d_defer2_list, Q);
       if (auto s = check_launch(c, "cell_step_warp", TRMCR_K_CELL_WARP)) return s;
@@ -810,6 +812,8 @@ trmcr_status trmcr_init(trmcr_ctx **out, const trmcr_particles *pp, const trmcr_
       const void *fns[] = {(const void *)cell_step_warp<float, false>, (const void *)cell_step_warp<double, false>,
                            (const void *)shock_collide_warp<float, false>, (const void *)shock_collide_warp<double, false>,
                            (const void *)cell_step_warp<float, true>, (const void *)cell_step_warp<double, true>,
+                           (const void *)cell_step_warp<float, false, TRMCR_HARD_SPHERE>,
+                           (const void *)cell_step_warp<double, false, TRMCR_HARD_SPHERE>,
                            (const void *)shock_collide_warp<float, true>, (const void *)shock_collide_warp<double, true>};
       for (const void *f : fns)
         if (allow_max_dyn_smem(f, smem_max) != cudaSuccess) {
