@@ -184,6 +184,24 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
+def ncu_issue(workload_name):
+    """Executed warp instructions per launch of the dominant kernel (committed ncu summary)."""
+    path = os.path.join(ROOT, "profiles", "ncu_issue.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload_name)
+    except (OSError, ValueError):
+        return None
+
+
+def measured_clock_mhz():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["sm_max_mhz"])
+    except (OSError, KeyError, ValueError):
+        return 1965.0
+
+
 def ncu_traffic(workload_name):
     """dram bytes per launch of the dominant kernel from the committed ncu summary."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -399,6 +417,18 @@ def measure(args, wl_name, rank, world, local_rank, cpu_seconds):
             "step": {"algorithmic_bytes_per_particle": step_bytes, "achieved": round(step_gbs, 1),
                      "frac": round(step_gbs / peak, 4)},
             "kernel_ms_probe": kernel_ms_probe}
+    issue = ncu_issue(wl_name)
+    if issue:
+        # the collision kernel is bound by instruction issue and latency, not by
+        # HBM: its executed warp instructions per launch (ncu --set full, the
+        # committed summary) per second of this run, against the SM issue peak
+        # (4 warp instructions per clock per SM x 148 SMs x the max SM clock)
+        clk_hz = 1e6 * float(measured_clock_mhz())
+        ipeak = 4.0 * 148 * clk_hz
+        ach = issue["warp_instructions"] / (dom_ms / dom_n * 1e-3)
+        roof["issue"] = {"kernel": issue["kernel"], "warp_instructions_per_launch": issue["warp_instructions"],
+                         "achieved": round(ach / 1e9, 1), "peak": round(ipeak / 1e9, 1),
+                         "unit": "G warp-instructions/s", "frac": round(ach / ipeak, 4)}
 
     # ---- e2e: host buffers through the public API, every step ----
     ke = max(3, min(args.steps, 20))
