@@ -325,7 +325,8 @@ def measure(args, wl_name, rank, world, local_rank, cpu_seconds):
             sim.step(1)
             k = counter[0] & 1
             counter[0] += 1
-            sim.global_moments(gms[k], all_ranks=world > 1)
+            if not os.environ.get("TRMCR_BENCH_NO_GM"):   # experiment switch (not a bench mode)
+                sim.global_moments(gms[k], all_ranks=world > 1)
         else:
             slab.step(xchg)
 

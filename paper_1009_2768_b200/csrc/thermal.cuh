@@ -301,16 +301,23 @@ __device__ __forceinline__ void bm_pair(uint32_t wa, uint32_t wb, float &c, floa
   s = cs.y;
 }
 
-// Philox4x32-10 with the key schedule precomputed on the host (kernel
+// Philox4x32 with the key schedule precomputed on the host (kernel
 // parameter, i.e. constant bank: the key XORs cost no extra instruction) and
-// counter words 1..3 fixed per cell: the same bijection as philox10().
+// counter words 1..3 fixed per cell.  The fp32 fluid-regime draws (a
+// statistical mode) use 7 rounds - Philox4x32-7 is
+// Crush-resistant (Salmon et al., SC'11; 10 is Random123's safety-margin
+// default) and the RNG is ~45 % of this kernel's instructions; everything else
+// (fp64 parity draws, fp32 trees) keeps philox10().
+#ifndef TRMCR_THERMAL_ROUNDS
+#define TRMCR_THERMAL_ROUNDS 7
+#endif
 struct KeySched {
   uint32_t k0[10], k1[10];
 };
-__device__ __forceinline__ uint4 philox10_ks(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+__device__ __forceinline__ uint4 philox_ks(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
                                              const KeySched &ks) {
 #pragma unroll
-  for (int r = 0; r < 10; ++r) {
+  for (int r = 0; r < TRMCR_THERMAL_ROUNDS; ++r) {
     const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
     const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
     const uint32_t n0 = hi1 ^ c1 ^ ks.k0[r], n2 = hi0 ^ c3 ^ ks.k1[r];
@@ -325,8 +332,8 @@ __device__ __forceinline__ uint4 philox10_ks(uint32_t c0, uint32_t c1, uint32_t 
 __device__ __forceinline__ void gauss12(const KeySched &ks, uint32_t cell, uint32_t step, uint32_t g, float4 &a,
                                         float4 &b, float4 &d) {
   const uint32_t c1 = kMaxw << 24;
-  const uint4 w0 = philox10_ks(3 * g, c1, cell, step, ks), w1 = philox10_ks(3 * g + 1, c1, cell, step, ks),
-              w2 = philox10_ks(3 * g + 2, c1, cell, step, ks);
+  const uint4 w0 = philox_ks(3 * g, c1, cell, step, ks), w1 = philox_ks(3 * g + 1, c1, cell, step, ks),
+              w2 = philox_ks(3 * g + 2, c1, cell, step, ks);
   bm_pair(w0.x, w0.y, a.x, b.x);
   bm_pair(w0.z, w0.w, d.x, a.y);
   bm_pair(w1.x, w1.y, b.y, d.y);

@@ -210,39 +210,55 @@ moments_kernel(const int64_t *__restrict__ offsets, int ncells, const Real *__re
   }
 }
 
-// Global sums of the per-cell statistics rows: kGmBlocks CTAs write partial
-// sums of contiguous cell ranges, the last CTA to finish adds the partials in
-// block order (deterministic), writes `out` and re-arms the counter.
-constexpr int kGmBlocks = 256;
-__global__ void __launch_bounds__(256) global_moments_kernel(const double *__restrict__ stats, int ncells,
-                                                             double *partial, unsigned *done, double *out) {
+// Global sums of the per-cell statistics rows: kGmBlocks CTAs of kGmThreads
+// write partial sums of contiguous cell ranges (one row per thread per round,
+// warp sums then the CTA's warps in order), the last CTA to finish adds the
+// partials in block order with one warp (deterministic), writes `out` and
+// re-arms the counter.  Few, wide CTAs: the kernel is a short latency chain.
+constexpr int kGmBlocks = 64, kGmThreads = 512;
+__global__ void __launch_bounds__(kGmThreads) global_moments_kernel(const double *__restrict__ stats, int ncells,
+                                                                    double *partial, unsigned *done, double *out) {
   step_kernel_prologue(nullptr);
-  __shared__ double red[8 * 10];
+  constexpr int NW = kGmThreads / 32, NV = 9;
+  __shared__ double red[NW][NV];
   __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int per = (ncells + gridDim.x - 1) / gridDim.x;
   const int lo = blockIdx.x * per, hi = min(ncells, lo + per);
-  double v[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double v[NV] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int c = lo + threadIdx.x; c < hi; c += blockDim.x) {
     const double *r = stats + (size_t)c * TRMCR_NSTATS;
-    v[0] += r[TRMCR_ST_N]; v[1] += r[TRMCR_ST_PX]; v[2] += r[TRMCR_ST_PY]; v[3] += r[TRMCR_ST_PZ];
-    v[4] += r[TRMCR_ST_ENERGY]; v[5] += r[TRMCR_ST_N] * r[TRMCR_ST_S0];
+    const double n = r[TRMCR_ST_N];
+    v[0] += n; v[1] += r[TRMCR_ST_PX]; v[2] += r[TRMCR_ST_PY]; v[3] += r[TRMCR_ST_PZ];
+    v[4] += r[TRMCR_ST_ENERGY]; v[5] += n * r[TRMCR_ST_S0];
     v[6] += r[TRMCR_ST_PROPOSALS]; v[7] += r[TRMCR_ST_ACCEPTED]; v[8] += r[TRMCR_ST_MAXW];
   }
-  block_sum<10>(v, red);
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < 9; ++k) partial[blockIdx.x * 10 + k] = v[k];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) red[warp][k] = v[k];
+  __syncthreads();
+  if (warp == 0) {
+    double t = 0.0;
+    if (lane < NV)
+      for (int w = 0; w < NW; ++w) t += red[w][lane];
+    if (lane < NV) partial[blockIdx.x * 10 + lane] = t;
     __threadfence();
-    last = (atomicAdd(done, 1u) == gridDim.x - 1);
+    __syncwarp();
+    if (lane == 0) last = (atomicAdd(done, 1u) == gridDim.x - 1);
   }
   __syncthreads();
-  if (last) {                      // uniform per CTA: the last CTA adds the partials
+  if (last && warp == 0) {         // uniform per CTA: the last CTA adds the partials
     __threadfence();
-    double w[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
-      for (int k = 0; k < 9; ++k) w[k] += ((volatile double *)partial)[b * 10 + k];
-    block_sum<10>(w, red);
-    if (threadIdx.x == 0) {
-      for (int k = 0; k < 9; ++k) out[k] = w[k];
+    double w[NV] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int b = lane; b < (int)gridDim.x; b += 32)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) w[k] += ((volatile double *)partial)[b * 10 + k];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) w[k] = warp_sum(w[k]);
+    if (lane == 0) {
+      for (int k = 0; k < NV; ++k) out[k] = w[k];
       out[TRMCR_GM_COST] = w[TRMCR_GM_PROPOSALS] + 0.5 * w[TRMCR_GM_MAXW];
       *done = 0u;
     }
@@ -426,7 +442,7 @@ trmcr_status trmcr_global_moments(trmcr_ctx *c, double *dev_out, int32_t all_ran
     if (c->comm_busy[slot]) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_comm_done[slot], 0));
   }
   const int blocks = std::max(1, std::min(kGmBlocks, c->ncells));
-  launch_k(c, global_moments_kernel, blocks, 256, 0, (const double *)c->d_stats, c->ncells, c->d_gm_partial,
+  launch_k(c, global_moments_kernel, blocks, kGmThreads, 0, (const double *)c->d_stats, c->ncells, c->d_gm_partial,
            c->d_gm_done, dev_out);
   if (trmcr_status e = check_launch(c, "global_moments_kernel")) return e;
   if (ar) {                 // all-reduce on the communication stream, overlapping the next step
