@@ -18,25 +18,36 @@ constexpr int kWarpSplitPre = 32;      // split uniforms drawn up front: one per
 #endif
 
 // Visit the n particles (vx, vy, vz)[0..n) of a cell with the warp, in a
-// fixed per-lane order: fp32 cells go through 16-byte loads (four particles per
-// lane per round: the first pass over a cell is bound by its load latency);
-// the unaligned head and the tail particle by particle.  f(x, y, z) per
-// particle.  fp64: plain lane-strided loop (the oracle parity path).
+// fixed per-lane order that depends on the particle INDEX only: round r gives
+// lane L the four particles 4 (32 r + L) .. + 3 (four particles per lane per
+// round: the first pass over a cell is bound by its load latency), the n mod 4
+// last ones go to lanes 0..2.  fp32 cells whose first particle is 16-byte
+// aligned read a round through one 16-byte load per component, the others
+// through four 4-byte loads - the same values in the same order, so the fp32
+// lane partials (and everything derived from them: the mean, Sigma', p) do not
+// depend on where the cell lies in the array (single domain or slab: bitwise).
+// f(i, x, y, z) per particle.  fp64: plain lane-strided loop (the oracle parity path).
 template <typename Real, typename F>
 __device__ __forceinline__ void warp_cell_fori(const Real *vx, const Real *vy, const Real *vz, int n, F &&f) {
   const int lane = threadIdx.x & 31;
   if constexpr (sizeof(Real) == 4) {
-    const int head = min(n, (int)((4u - (((uint32_t)reinterpret_cast<uintptr_t>(vx)) >> 2)) & 3u));
-    if (lane < head) f(lane, vx[lane], vy[lane], vz[lane]);
-    const int body = (n - head) >> 2;
-    const float4 *X = reinterpret_cast<const float4 *>(vx + head), *Y = reinterpret_cast<const float4 *>(vy + head),
-                 *Z = reinterpret_cast<const float4 *>(vz + head);
+    const int body = n >> 2;
+    const bool al = (((uint32_t)reinterpret_cast<uintptr_t>(vx)) & 15u) == 0u;
     for (int q = lane; q < body; q += 32) {
-      const float4 a = X[q], b = Y[q], c = Z[q];
-      const int i = head + 4 * q;
+      const int i = 4 * q;
+      float4 a, b, c;
+      if (al) {
+        a = *reinterpret_cast<const float4 *>(vx + i);
+        b = *reinterpret_cast<const float4 *>(vy + i);
+        c = *reinterpret_cast<const float4 *>(vz + i);
+      } else {
+        a = make_float4(vx[i], vx[i + 1], vx[i + 2], vx[i + 3]);
+        b = make_float4(vy[i], vy[i + 1], vy[i + 2], vy[i + 3]);
+        c = make_float4(vz[i], vz[i + 1], vz[i + 2], vz[i + 3]);
+      }
       f(i, a.x, b.x, c.x); f(i + 1, a.y, b.y, c.y); f(i + 2, a.z, b.z, c.z); f(i + 3, a.w, b.w, c.w);
     }
-    const int t = head + 4 * body + lane;
+    const int t = 4 * body + lane;
     if (t < n) f(t, vx[t], vy[t], vz[t]);
   } else {
     for (int i = lane; i < n; i += 32) f(i, vx[i], vy[i], vz[i]);

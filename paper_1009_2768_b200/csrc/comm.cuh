@@ -81,6 +81,8 @@ inline trmcr_status comm_init(trmcr_ctx *c, const void *nccl_id, int rank, int n
     if (s.has_left != (rank > 0) || s.has_right != (rank + 1 < nranks))
       return fail(c, TRMCR_EINVAL, "shock slabs: rank r must own the r-th slab (neighbours = ranks r-1, r+1)");
     if (s.has_left || s.has_right) {   // the library's own exchange buffers
+      CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming));
+      CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_xchg, cudaEventDisableTiming));
       const int cap = 1 << 13;
       const size_t b = c->dtype == TRMCR_F64 ? XBuf<double>::bytes(cap) : XBuf<float>::bytes(cap);
       void *buf[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -102,26 +104,38 @@ inline void comm_destroy(trmcr_ctx *c) {
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->ev_comm_ready) cudaEventDestroy(c->ev_comm_ready);
+  if (c->ev_pack) cudaEventDestroy(c->ev_pack);
+  if (c->ev_xchg) cudaEventDestroy(c->ev_xchg);
   for (int k = 0; k < kCommSlots; ++k)
     if (c->ev_comm_done[k]) cudaEventDestroy(c->ev_comm_done[k]);
 }
 
-// Neighbour exchange of a shock slab (between shock_begin and shock_finish), on
-// the context stream: send_left -> rank - 1 (its recv_right), send_right -> rank
-// + 1 (its recv_left).  The whole fixed-capacity buffer travels.
+// Neighbour exchange of a shock slab (between shock_begin and shock_finish):
+// send_left -> rank - 1 (its recv_right), send_right -> rank + 1 (its
+// recv_left).  The whole fixed-capacity buffer travels.  It runs on the
+// communication stream, after the event shock_begin recorded behind the pack
+// kernel, so it overlaps the bulk transport that shock_begin launched after
+// the pack; the context stream resumes (immigrant counts, offsets, sort,
+// collisions) when the exchange is done.
 inline trmcr_status comm_shock_exchange(trmcr_ctx *c) {
   ShockState &s = c->shock;
   const size_t b = s.xbytes;
+  cudaStream_t xs = c->ev_pack && c->ev_xchg && c->comm_stream ? c->comm_stream : c->stream;
+  if (xs != c->stream) CUDA_TRY(c, cudaStreamWaitEvent(xs, c->ev_pack, 0));
   NCCL_TRY(c, ncclGroupStart());
   if (s.has_left) {
-    NCCL_TRY(c, ncclSend(s.xsend[0], b, ncclUint8, c->rank - 1, c->comm, c->stream));
-    NCCL_TRY(c, ncclRecv(s.xrecv[0], b, ncclUint8, c->rank - 1, c->comm, c->stream));
+    NCCL_TRY(c, ncclSend(s.xsend[0], b, ncclUint8, c->rank - 1, c->comm, xs));
+    NCCL_TRY(c, ncclRecv(s.xrecv[0], b, ncclUint8, c->rank - 1, c->comm, xs));
   }
   if (s.has_right) {
-    NCCL_TRY(c, ncclSend(s.xsend[1], b, ncclUint8, c->rank + 1, c->comm, c->stream));
-    NCCL_TRY(c, ncclRecv(s.xrecv[1], b, ncclUint8, c->rank + 1, c->comm, c->stream));
+    NCCL_TRY(c, ncclSend(s.xsend[1], b, ncclUint8, c->rank + 1, c->comm, xs));
+    NCCL_TRY(c, ncclRecv(s.xrecv[1], b, ncclUint8, c->rank + 1, c->comm, xs));
   }
   NCCL_TRY(c, ncclGroupEnd());
+  if (xs != c->stream) {
+    CUDA_TRY(c, cudaEventRecord(c->ev_xchg, xs));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_xchg, 0));
+  }
   return TRMCR_OK;
 }
 

@@ -235,6 +235,7 @@ struct trmcr_ctx {
   struct ncclComm *comm = nullptr;
   int rank = 0, nranks = 1;
   cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_pack = nullptr, ev_xchg = nullptr;   // shock slabs: emigrants packed / exchange done
   cudaEvent_t ev_comm_ready = nullptr;
   cudaEvent_t ev_comm_done[trmcr::kCommSlots] = {nullptr, nullptr, nullptr, nullptr};
   const void *comm_ptr[trmcr::kCommSlots] = {nullptr, nullptr, nullptr, nullptr};
@@ -336,6 +337,7 @@ inline trmcr_status sync_check(trmcr_ctx *c) {
   if (err & 16) return fail(c, TRMCR_ECUDA, "internal fault: tree index out of range");
   if (err & 32) return fail(c, TRMCR_ECAPACITY, "a particle crossed more than one slab in a step");
   if (err & 64) return fail(c, TRMCR_ECAPACITY, "literal mode: the trees needed more f_0 particles than the cell holds");
+  if (err & 256) return fail(c, TRMCR_ECAPACITY, "a particle left its slab from more than 64 cells inside it in one step (lower dt)");
   if (err & 128) return fail(c, TRMCR_ECAPACITY, "fused shock step: too many particles moved two or more cells in one step (far-mover list full; lower dt or set TRMCR_SHOCK_FUSED=0)");
   return TRMCR_OK;
 }

@@ -391,13 +391,26 @@ constexpr int kTransportThreads = 256, kTransportPer = 4, kTransportGroups = 4, 
 constexpr int kTile = kTransportThreads * kTransportPer * kTransportGroups;   // large problems
 __host__ __device__ constexpr int tile_of(int ng) { return kTransportThreads * kTransportPer * ng; }
 constexpr int kEdgeBins = 4096;   // cells from a domain / slab edge that ghosts and immigrants may reach
+constexpr int kEmigrantCells = 64;   // cells from a neighbour within which an emigrant may start (else error 256)
 
 template <typename Real, int NG>
 __global__ void __launch_bounds__(kTransportThreads)
 transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const Real *__restrict__ vx,
-                 int32_t *dest, int32_t *counts, int *W, unsigned long long *acct, int32_t *tileH, int2 *tile_meta) {
+                 int32_t *dest, int32_t *counts, int *W, unsigned long long *acct, int32_t *tileH, int2 *tile_meta,
+                 int phase, int *err) {
   pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   constexpr int P4 = kTransportPer, TILE = tile_of(NG);
+  // Slabs with neighbours transport in two launches: phase 1 takes the tiles
+  // that hold particles of the kEmigrantCells cells next to a neighbour (the
+  // only possible sources of emigrants), so the emigrants can be packed and
+  // their exchange started while phase 2 transports the bulk.  phase 0: every
+  // tile (no neighbour).  A tile is of one kind in both launches (same test).
+  if (phase != 0) {
+    const int El = S.has_left ? min(kEmigrantCells, S.C) : 0, Er = S.has_right ? min(kEmigrantCells, S.C) : 0;
+    const int64_t t0 = (int64_t)blockIdx.x * TILE;
+    const bool edge = (El > 0 && t0 < off_old[El]) || (Er > 0 && t0 + TILE > off_old[S.C - Er]);
+    if (edge != (phase == 1)) { pdl_trigger(); return; }
+  }
   __shared__ int s_hist[kHist];
   __shared__ int s_red[4][kTransportThreads / 32];
   __shared__ int s_dmin;
@@ -486,6 +499,7 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
     const int me = max(l ? s1 + 1 : 0, r ? S.C - s0 : 0);
     if (md > 0 && md > *((volatile int *)W)) atomicMax(W, md);
     if (me > 0 && me > *((volatile int *)(W + 1))) atomicMax(W + 1, me);
+    if (phase == 2 && (l || r)) atomicOr(err, 256);   // an emigrant from the bulk: already packed without it
   }
   if (lane == 0 && wdr) atomicAdd(&acct[2], (unsigned long long)wdr);
   __syncthreads();
@@ -518,7 +532,7 @@ pack_emigrants(ShockDev S, const int64_t *__restrict__ off_old, const int *ng, c
                const Real *vx, const Real *vy, const Real *vz, const int32_t *dest, const Real *gx0,
                const Real *gvx0, const Real *gvy0, const Real *gvz0, const int32_t *gd0, const Real *gx1,
                const Real *gvx1, const Real *gvy1, const Real *gvz1, const int32_t *gd1, void *send_l,
-               void *send_r, int cap, int *err) {
+               void *send_r, int cap, int *err, int tile) {
   pdl_wait();   // programmatic dependent launch: the predecessor's writes are visible
   constexpr int R = 8;
   __shared__ int wcnt[32];
@@ -536,6 +550,10 @@ pack_emigrants(ShockDev S, const int64_t *__restrict__ off_old, const int *ng, c
       if (We <= 0) continue;
       const int a = side == 0 ? 0 : max(S.C - We, 0), b = side == 0 ? min(We, S.C) : S.C;
       lo = off_old[a]; hi = off_old[b];
+      // only the edge tiles have been transported (transport_kernel phase 1): stay inside them
+      // (an emigrant beyond them is reported by phase 2, error 256)
+      if (side == 0) hi = min(hi, (off_old[min(kEmigrantCells, S.C)] + tile - 1) / tile * tile);
+      else lo = max(lo, off_old[S.C - min(kEmigrantCells, S.C)] / tile * tile);
       sx = x; svx = vx; svy = vy; svz = vz; sd = dest;
     } else {
       const int g = seg == 0 ? 0 : 1;
@@ -1131,8 +1149,21 @@ constexpr int kLockWarps = TRMCR_LOCK_WARPS;   // measured: 16 -> 2.02 ms, 8 -> 
 #ifndef TRMCR_LOCK_MINB
 #define TRMCR_LOCK_MINB (16 / TRMCR_LOCK_WARPS)
 #endif
+// TRMCR_LOCK_GROUPS > 1: a CTA holds that many independent lock-step groups;
+// group g = warp % groups, so the kLockWarps warps of a group have the same
+// warp id modulo 4 (one SM sub-partition: its instruction cache serves one
+// phase) and synchronise on their own named barrier.
+#ifndef TRMCR_LOCK_GROUPS
+#define TRMCR_LOCK_GROUPS 1
+#endif
+constexpr int kLockGroups = TRMCR_LOCK_GROUPS;
+constexpr int kLockThreads = kLockWarps * kLockGroups * 32;
+__device__ __forceinline__ void lock_group_barrier(int grp) {
+  if constexpr (kLockGroups == 1) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "n"(kLockWarps * 32) : "memory");
+}
 template <typename Real, bool WB, int MOD = -1>
-__global__ void __launch_bounds__(kLockWarps * 32, TRMCR_LOCK_MINB)
+__global__ void __launch_bounds__(kLockThreads, (TRMCR_LOCK_MINB + kLockGroups - 1) / kLockGroups)
 shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, const int64_t *__restrict__ off_new,
                    Real *ox, Real *ovx, Real *ovy, Real *ovz, int32_t *m_state, double *stats, int *defer_count,
                    int *defer_list, QueueArgs Q) {
@@ -1145,8 +1176,10 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
   CellBuf<Real> B;
   double *usplit;
   bind_warp_slab(B, slab, Lay, usplit);
-  for (int base = blockIdx.x * kLockWarps; base < S.C; base += gridDim.x * kLockWarps) {
-    const int c = base + warp;
+  const int grp = warp % kLockGroups, mem = warp / kLockGroups;
+  for (int base = (blockIdx.x * kLockGroups + grp) * kLockWarps; base < S.C;
+       base += gridDim.x * kLockGroups * kLockWarps) {
+    const int c = base + mem;
     int64_t b0 = 0;
     int n = 0, rc = kOk;
     bool run = false;                         // this warp's cell still has phases to run
@@ -1184,7 +1217,7 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
     // the begin phase ends in lock step; the attempts (attempt 0 and any RAD
     // retries) run free - a barrier per attempt measured slower (C5 1.61 vs
     // 1.53 ms: retries are a minority of the cells)
-    __syncthreads();
+    lock_group_barrier(grp);
     WPHASE_ADD(10, t_w);   // barrier after begin
     while (run) {
       rc = wphase_attempt<Real, WB, MOD>(P, B, sh, usplit, P.cell_base + (uint32_t)c, Q.log, Q.log_count, Q.log_cap);
@@ -1196,7 +1229,7 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
                        stats + (size_t)c * TRMCR_NSTATS);
     WPHASE_ADD(6, t_e);   // Maxwellian + stats
     if (c < S.C && rc != kOk && lane == 0) defer_list[atomicAdd(defer_count, 1)] = c;
-    __syncthreads();                          // round in lock step (dropping it measured slower)
+    lock_group_barrier(grp);                          // round in lock step (dropping it measured slower)
     WPHASE_ADD(11, t_e);   // barrier at round end
   }
   pdl_trigger();
@@ -1488,8 +1521,9 @@ trmcr_status shock_begin(trmcr_ctx *c) {
     prof_begin(c, TRMCR_K_TRANSPORT);
     const bool sc = s.scatter && c->wlay.n_cap > 0 && !c->wlay.v_smem;
     auto *tk = s.tile_ng == 1 ? transport_kernel<Real, 1> : transport_kernel<Real, kTransportGroups>;
+    // a slab with neighbours: the edge tiles first (the emigrants' sources), the bulk after the pack
     launch_k(c, tk, blocks, kTransportThreads, (size_t)(0), d, s.d_off[cur], (Real *)c->x[cur], (const Real *)c->v[cur][0], s.d_dest, s.d_counts, s.d_W, s.d_acct,
-        sc ? s.d_tileH : nullptr, sc ? s.d_tile_meta : nullptr);
+        sc ? s.d_tileH : nullptr, sc ? s.d_tile_meta : nullptr, (s.has_left || s.has_right) ? 1 : 0, c->d_err);
     if (auto e = check_launch(c, "transport_kernel", TRMCR_K_TRANSPORT)) return e;
   }
   if (s.has_left || s.has_right) {
@@ -1498,8 +1532,19 @@ trmcr_status shock_begin(trmcr_ctx *c) {
         (const Real *)c->v[cur][1], (const Real *)c->v[cur][2], s.d_dest, (const Real *)s.gx[0],
         (const Real *)s.gv[0][0], (const Real *)s.gv[0][1], (const Real *)s.gv[0][2], s.d_gdest[0],
         (const Real *)s.gx[1], (const Real *)s.gv[1][0], (const Real *)s.gv[1][1], (const Real *)s.gv[1][2],
-        s.d_gdest[1], s.xsend[0], s.xsend[1], s.xcap, c->d_err);
+        s.d_gdest[1], s.xsend[0], s.xsend[1], s.xcap, c->d_err, tile_of(s.tile_ng));
     if (auto e = check_launch(c, "pack_emigrants")) return e;
+    // the emigrants are packed: their exchange (comm_shock_exchange, on the
+    // communication stream) overlaps the transport of the bulk
+    if (c->ev_pack) CUDA_TRY(c, cudaEventRecord(c->ev_pack, c->stream));
+    const int per_block = tile_of(s.tile_ng);
+    const unsigned blocks = (unsigned)((c->cap + per_block - 1) / per_block);
+    prof_begin(c, TRMCR_K_TRANSPORT);
+    const bool sc = s.scatter && c->wlay.n_cap > 0 && !c->wlay.v_smem;
+    auto *tk = s.tile_ng == 1 ? transport_kernel<Real, 1> : transport_kernel<Real, kTransportGroups>;
+    launch_k(c, tk, blocks, kTransportThreads, (size_t)(0), d, s.d_off[cur], (Real *)c->x[cur], (const Real *)c->v[cur][0], s.d_dest, s.d_counts, s.d_W, s.d_acct,
+        sc ? s.d_tileH : nullptr, sc ? s.d_tile_meta : nullptr, 2, c->d_err);
+    if (auto e = check_launch(c, "transport_kernel", TRMCR_K_TRANSPORT)) return e;
   }
   return TRMCR_OK;
 }
@@ -1567,7 +1612,7 @@ trmcr_status shock_finish(trmcr_ctx *c) {
     else if (G.scatter && c->lock_grid > 0)
       launch_k(c, (wb ? shock_collide_lock<Real, true>
                       : (c->P.model == TRMCR_HARD_SPHERE ? shock_collide_lock<Real, false, TRMCR_HARD_SPHERE>
-                                                         : shock_collide_lock<Real, false>)), c->lock_grid, kLockWarps * 32, (size_t)(c->lock_smem), c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
+                                                         : shock_collide_lock<Real, false>)), (c->lock_grid + kLockGroups - 1) / kLockGroups, kLockThreads, (size_t)(c->lock_smem) * kLockGroups, c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,
               c->d_defer_list, Q);
     else
       launch_k(c, (wb ? shock_collide_warp<Real, true> : shock_collide_warp<Real, false>), c->warp_grid, c->warp_wpc * 32, (size_t)(c->warp_smem), c->P, c->wlay, d, G, s.d_off[nxt], ox, ovx, ovy, ovz, c->d_mstate, c->d_stats, c->d_defer_count,

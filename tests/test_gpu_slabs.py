@@ -28,10 +28,23 @@ def test_slabs_match_single_domain(world, dtype, fused_full, fused_slabs, monkey
     """fused_*: the fused pass (1) or the three-pass step (0) for the single
     domain and for the slabs - the last case cross-checks the two step
     structures (and the two emigrant packers) against each other."""
+    _run_slabs(world, dtype, fused_full, fused_slabs, monkeypatch, ncells=60, n_total=30_000, half_width=6.0)
+
+
+@pytest.mark.parametrize("world,dtype", [(2, np.float64), (3, np.float32)])
+def test_slabs_edge_first_transport(world, dtype, monkeypatch):
+    """Slabs wider than the emigrant window (64 cells from a neighbour): the
+    transport runs in two launches - the edge tiles, whose emigrants are packed
+    (and, on the NCCL path, exchanged on the communication stream meanwhile),
+    then the bulk tiles.  Same bitwise result as the single domain."""
+    _run_slabs(world, dtype, "0", "0", monkeypatch, ncells=720, n_total=72_000, half_width=36.0)
+
+
+def _run_slabs(world, dtype, fused_full, fused_slabs, monkeypatch, ncells, n_total, half_width):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_1009_2768_b200 import api, dist
-    setup = synth.shock_setup(mach=3.0, ncells=60, n_total=30_000, x_min=-6.0, x_max=6.0)
+    setup = synth.shock_setup(mach=3.0, ncells=ncells, n_total=n_total, x_min=-half_width, x_max=half_width)
     x, vx, vy, vz, counts = _sorted_shock(setup, 3, dtype)
     td = torch.float64 if dtype == np.float64 else torch.float32
     T = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(device="cuda", dtype=td)
