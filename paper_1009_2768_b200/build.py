@@ -42,7 +42,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp, SRC, *nccl_flags()]
+    # TRMCR_SPLIT_COMPILE=N: nvcc --split-compile N (development only: ~1 min instead of ~5, but the
+    # generated code then depends on N and, measured, on what else the machine is compiling)
+    split = ["--split-compile", os.environ["TRMCR_SPLIT_COMPILE"]] if os.environ.get("TRMCR_SPLIT_COMPILE") else []
+    cmd = [NVCC, *FLAGS, *split, "-o", tmp, SRC, *nccl_flags()]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)

@@ -320,9 +320,7 @@ collide_batch(StepParams P, BatchLayout Lay, int C, int64_t cap, const int64_t *
         const Real *vx = S.vx + cl.vb, *vy = S.vy + cl.vb, *vz = S.vz + cl.vb;
         double sx, sy, sz;
         if constexpr (sizeof(Real) == 4) {
-          float fx = 0, fy = 0, fz = 0;
-          warp_cell_for<float>(vx, vy, vz, n, [&](float x, float y, float z) { fx += x; fy += y; fz += z; });
-          sx = fx; sy = fy; sz = fz;
+          warp_cell_sums(vx, vy, vz, n, sx, sy, sz);
         } else {
           sx = 0; sy = 0; sz = 0;
           for (int q = lane; q < n; q += 32) { sx += vx[q]; sy += vy[q]; sz += vz[q]; }
@@ -332,17 +330,7 @@ collide_batch(StepParams P, BatchLayout Lay, int C, int64_t cap, const int64_t *
         double c0 = 0, c1 = 0, c2 = 0, dv2 = 0;
         if constexpr (sizeof(Real) == 4) {
           const float fux = (float)ux, fuy = (float)uy, fuz = (float)uz;
-          float f0 = 0, f1 = 0, f2 = 0, fm = 0;
-          warp_cell_for<float>(vx, vy, vz, n, [&](float x, float y, float z) {
-            const float dx = x - fux, dy = y - fuy, dz = z - fuz;
-            const float r2 = dx * dx + dy * dy + dz * dz;
-            fm = fmaxf(fm, r2);
-            f0 += dx * dx;
-            const float v2 = x * x + y * y + z * z;
-            f1 += v2 * v2;
-            f2 += r2;
-          });
-          c0 = f0; c1 = f1; c2 = f2; dv2 = fm;
+          warp_cell_central(vx, vy, vz, n, fux, fuy, fuz, c0, c1, c2, dv2);
         } else {
           for (int q = lane; q < n; q += 32) {
             const double x = vx[q], y = vy[q], z = vz[q];

@@ -8,6 +8,7 @@
 // global-memory kernel).
 #pragma once
 #include "cell_step.cuh"
+#include <type_traits>
 
 namespace trmcr {
 
@@ -17,16 +18,102 @@ constexpr int kWarpSplitPre = 32;      // split uniforms drawn up front: one per
 #define TRMCR_WARP_MINB 4        // CTAs of kWarpCellWarps warps per SM the register budget allows (128 regs)
 #endif
 
-// Visit the n particles (vx, vy, vz)[0..n) of a cell with the warp, in a
-// fixed per-lane order that depends on the particle INDEX only: round r gives
-// lane L the four particles 4 (32 r + L) .. + 3 (four particles per lane per
-// round: the first pass over a cell is bound by its load latency), the n mod 4
-// last ones go to lanes 0..2.  fp32 cells whose first particle is 16-byte
-// aligned read a round through one 16-byte load per component, the others
-// through four 4-byte loads - the same values in the same order, so the fp32
-// lane partials (and everything derived from them: the mean, Sigma', p) do not
-// depend on where the cell lies in the array (single domain or slab: bitwise).
-// f(i, x, y, z) per particle.  fp64: plain lane-strided loop (the oracle parity path).
+// fp32 moment passes over the n particles (vx, vy, vz)[0..n) of a cell, with
+// the warp.  The sums are defined on the particle INDEX only: class k (0..127)
+// is the sequential fp32 sum of particles k, k + 128, k + 256, ...; lane L's
+// partial is (class 4L + class 4L+1) + (class 4L+2 + class 4L+3); the warp sum
+// (fp64) of the lane partials follows.  So the mean, Sigma', p and everything
+// derived from them do not depend on where the cell lies in the array (single
+// domain or slab: bitwise).  The loads, though, are always 16-byte ones: a
+// cell whose first particle sits k elements past a 16-byte boundary is read
+// from that boundary, so lane L's four accumulators hold classes 4L - k .. 4L
+// - k + 3 (mod 128; the slots before particle 0 and after particle n - 1 are
+// skipped), each still summed in index order; warp_cell_fold puts the classes
+// back with three shuffles.  Four independent add chains per lane and sum.
+// f(slot<J>, x, y, z) adds particle (x, y, z) to accumulator J of each sum.
+#ifndef TRMCR_SUMS_UNROLL
+#define TRMCR_SUMS_UNROLL 4      // 16-byte groups per lane in flight in the first pass over a cell (load latency)
+#endif
+#ifndef TRMCR_CENTRAL_UNROLL
+#define TRMCR_CENTRAL_UNROLL 2
+#endif
+template <int J> using slot = std::integral_constant<int, J>;
+__device__ __forceinline__ uint32_t misalign4(const float *p) {
+  return (((uint32_t)reinterpret_cast<uintptr_t>(p)) >> 2) & 3u;
+}
+template <int U, typename F>
+__device__ __forceinline__ uint32_t warp_cell_for4(const float *vx, const float *vy, const float *vz, int n, F &&f) {
+  const int lane = threadIdx.x & 31;
+  const int k = (int)misalign4(vx);
+  if ((uint32_t)k != misalign4(vy) || (uint32_t)k != misalign4(vz)) __trap();   // the three arrays are shifted alike (capacities are multiples of 4)
+  const float4 *X = reinterpret_cast<const float4 *>(vx - k), *Y = reinterpret_cast<const float4 *>(vy - k),
+               *Z = reinterpret_cast<const float4 *>(vz - k);
+  // 16-byte groups q = 0 .. nv-1; group q holds particles 4q - k .. 4q - k + 3.  Those wholly
+  // inside the cell are [k > 0, q1); group 0 (k > 0) and group q1 (if (n + k) % 4) are partial.
+  const int q1 = (n + k) >> 2, nv = (n + k + 3) >> 2;
+  auto edge = [&](int q) {       // slots outside [0, n) belong to the neighbouring cells
+    const float4 a = X[q], b = Y[q], c = Z[q];
+    const int lo = 4 * q - k;
+    if ((unsigned)lo < (unsigned)n) f(slot<0>{}, a.x, b.x, c.x);
+    if ((unsigned)(lo + 1) < (unsigned)n) f(slot<1>{}, a.y, b.y, c.y);
+    if ((unsigned)(lo + 2) < (unsigned)n) f(slot<2>{}, a.z, b.z, c.z);
+    if ((unsigned)(lo + 3) < (unsigned)n) f(slot<3>{}, a.w, b.w, c.w);
+  };
+  const bool head = k > 0 && lane == 0, tail = nv > q1 && (q1 & 31) == lane && !(k > 0 && q1 == 0);
+  if (head) edge(0);             // first in lane 0's order
+#pragma unroll U
+  for (int q = head ? 32 : lane; q < q1; q += 32) {
+    const float4 a = X[q], b = Y[q], c = Z[q];
+    f(slot<0>{}, a.x, b.x, c.x); f(slot<1>{}, a.y, b.y, c.y); f(slot<2>{}, a.z, b.z, c.z); f(slot<3>{}, a.w, b.w, c.w);
+  }
+  if (tail) edge(q1);            // last in its lane's order
+  return (uint32_t)k;
+}
+// Lane partial of one sum from its four accumulators (k = warp_cell_for4's result; whole warp).
+__device__ __forceinline__ float warp_cell_fold(const float (&a)[4], uint32_t k) {
+  const int nxt = ((threadIdx.x & 31) + 1) & 31;
+  const float t0 = __shfl_sync(0xffffffffu, a[0], nxt), t1 = __shfl_sync(0xffffffffu, a[1], nxt),
+              t2 = __shfl_sync(0xffffffffu, a[2], nxt);
+  const float c0 = k == 0 ? a[0] : k == 1 ? a[1] : k == 2 ? a[2] : a[3];
+  const float c1 = k == 0 ? a[1] : k == 1 ? a[2] : k == 2 ? a[3] : t0;
+  const float c2 = k == 0 ? a[2] : k == 1 ? a[3] : k == 2 ? t0 : t1;
+  const float c3 = k == 0 ? a[3] : k == 1 ? t0 : k == 2 ? t1 : t2;
+  return (c0 + c1) + (c2 + c3);
+}
+// Pass 1: lane partials of sum v (to be warp-summed in fp64).
+__device__ __forceinline__ void warp_cell_sums(const float *vx, const float *vy, const float *vz, int n, double &sx,
+                                               double &sy, double &sz) {
+  float ax[4] = {0, 0, 0, 0}, ay[4] = {0, 0, 0, 0}, az[4] = {0, 0, 0, 0};
+  const uint32_t k = warp_cell_for4<TRMCR_SUMS_UNROLL>(vx, vy, vz, n, [&](auto J, float x, float y, float z) {
+    constexpr int j = decltype(J)::value;
+    ax[j] += x; ay[j] += y; az[j] += z;
+  });
+  sx = warp_cell_fold(ax, k); sy = warp_cell_fold(ay, k); sz = warp_cell_fold(az, k);
+}
+// Pass 2: lane partials of sum (v_x - u_x)^2, sum |v|^4, sum |v - u|^2 and the lane's max |v - u|^2.
+__device__ __forceinline__ void warp_cell_central(const float *vx, const float *vy, const float *vz, int n, float fux,
+                                                  float fuy, float fuz, double &c0, double &c1, double &c2,
+                                                  double &dv2) {
+  float f0[4] = {0, 0, 0, 0}, f1[4] = {0, 0, 0, 0}, f2[4] = {0, 0, 0, 0}, fm = 0;
+  const uint32_t k = warp_cell_for4<TRMCR_CENTRAL_UNROLL>(vx, vy, vz, n, [&](auto J, float x, float y, float z) {
+    // explicit roundings: the loop body and the edge groups are separate inlined copies and
+    // must not be contracted differently (a particle's copy depends on the cell's alignment)
+    const float dx = __fsub_rn(x, fux), dy = __fsub_rn(y, fuy), dz = __fsub_rn(z, fuz);
+    const float xx = __fmul_rn(dx, dx);
+    const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, xx));
+    fm = fmaxf(fm, r2);
+    constexpr int j = decltype(J)::value;
+    f0[j] = __fadd_rn(f0[j], xx);
+    const float v2 = __fmaf_rn(z, z, __fmaf_rn(y, y, __fmul_rn(x, x)));
+    f1[j] = __fmaf_rn(v2, v2, f1[j]);
+    f2[j] = __fadd_rn(f2[j], r2);
+  });
+  c0 = warp_cell_fold(f0, k); c1 = warp_cell_fold(f1, k); c2 = warp_cell_fold(f2, k); dv2 = fm;
+}
+
+// Generic visit of a cell with the warp (the A9 moments kernel, fp64 sums): f(i, x, y, z)
+// per particle; round r gives lane L particles 4 (32 r + L) .. + 3 (index only),
+// 16-byte loads when the cell is 16-byte aligned; fp64 cells lane-strided.
 template <typename Real, typename F>
 __device__ __forceinline__ void warp_cell_fori(const Real *vx, const Real *vy, const Real *vz, int n, F &&f) {
   const int lane = threadIdx.x & 31;
@@ -497,17 +584,7 @@ __device__ int wphase_begin(const StepParams &P, CellBuf<Real> &B, WarpShared &s
   if constexpr (sizeof(Real) == 4) {
     // fp32 statistical mode: fp32 lane partials (~n/32 terms), fp64 warp sums
     const float fux = (float)ux, fuy = (float)uy, fuz = (float)uz;
-    float f0 = 0, f1 = 0, f2 = 0, fm = 0;
-    warp_cell_for<float>(B.vx, B.vy, B.vz, n, [&](float x, float y, float z) {
-      const float dx = x - fux, dy = y - fuy, dz = z - fuz;
-      const float r2 = dx * dx + dy * dy + dz * dz;
-      fm = fmaxf(fm, r2);
-      f0 += dx * dx;
-      const float v2 = x * x + y * y + z * z;
-      f1 += v2 * v2;
-      f2 += r2;
-    });
-    c0 = f0; c1 = f1; c2 = f2; dv2 = fm;
+    warp_cell_central(B.vx, B.vy, B.vz, n, fux, fuy, fuz, c0, c1, c2, dv2);
   } else {
     for (int i = lane; i < n; i += 32) {
       const double x = B.vx[i], y = B.vy[i], z = B.vz[i];

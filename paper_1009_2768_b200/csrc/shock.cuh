@@ -1200,9 +1200,7 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
         PHASE_MARK(t_b);
         double sx = 0, sy = 0, sz = 0;
         if constexpr (sizeof(Real) == 4) {
-          float fx = 0, fy = 0, fz = 0;
-          warp_cell_for<float>(B.vx, B.vy, B.vz, n, [&](float x, float y, float z) { fx += x; fy += y; fz += z; });
-          sx = fx; sy = fy; sz = fz;
+          warp_cell_sums(B.vx, B.vy, B.vz, n, sx, sy, sz);
         } else {
           for (int i = lane; i < n; i += 32) { sx += B.vx[i]; sy += B.vy[i]; sz += B.vz[i]; }
         }

@@ -2,7 +2,7 @@ import ctypes, os, sys
 import numpy as np, torch
 sys.path.insert(0, ".")
 from paper_1009_2768_b200 import api
-api.LIB_PATH = os.path.join(os.path.dirname(api.__file__), "libtrmcr_dbg.so")
+api.LIB_PATH = os.environ.get("TRMCR_DBG_LIB", os.path.join(os.path.dirname(api.__file__), "libtrmcr_dbg.so"))
 import bench
 wl = sys.argv[1]; steps = int(sys.argv[2])
 W = bench.workload(wl)
