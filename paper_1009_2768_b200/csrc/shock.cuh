@@ -34,6 +34,7 @@ struct ShockDev {
   int C, Cg, cbase;
   int has_left, has_right;     // a neighbouring slab exists (else: reservoir)
   double x_min, x_max, inv_dx, dt;
+  float x_min_f, x_max_f;      // smallest floats >= x_min, x_max: for a float x, x >= x_min_f <=> (double)x >= x_min (same for x_max)
   double rho[2], u[2], T[2], Lg[2], y[2];
   int cap_g;
   int64_t cap;                 // particle capacity of the buffers: no store at or beyond it
@@ -89,6 +90,19 @@ template <typename Real>
 __device__ __forceinline__ int dest_of(const ShockDev &S, Real xn) {
   const double xd = (double)xn;
   return (xd >= S.x_min && xd < S.x_max) ? cell_of(S, xd) - S.cbase : kDropped;
+}
+// The same value without branches (the transport's inner loop): the domain test
+// on float thresholds for fp32 positions (exactly the double test, see
+// ShockDev), floor by the conversion's rounding mode (the argument is >= 0 for a
+// particle inside the domain), the upper clamp of cell_of as an integer min.
+template <typename Real>
+__device__ __forceinline__ int dest_of_fast(const ShockDev &S, Real xn) {
+  const double xd = (double)xn;
+  bool inside;
+  if constexpr (sizeof(Real) == 4) inside = xn >= S.x_min_f && xn < S.x_max_f;
+  else inside = xd >= S.x_min && xd < S.x_max;
+  const int c = min(__double2int_rd((xd - S.x_min) * S.inv_dx), S.Cg - 1) - S.cbase;
+  return inside ? c : kDropped;
 }
 
 // warp-aggregated atomicAdd(&counts[key], 1) for lanes with key >= 0
@@ -446,35 +460,35 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
     s_xend[1] = x[min(n, tile0 + (int64_t)TILE) - 1];
   }
   __syncthreads();
+  // every slot of a full tile holds a particle (uniform test): its copy of the loop has no bound checks
+  auto classify = [&](auto FULL) {
+    constexpr bool full = decltype(FULL)::value;
 #pragma unroll
-  for (int g = 0; g < NG; ++g) {
-    const int64_t i0 = tile0 + ((int64_t)g * kTransportThreads + threadIdx.x) * P4;
-    Real *xs = xa[g];
-    const Real *vs = va[g];
-    const bool vec = (i0 + P4 <= n) && (sizeof(Real) * P4 == 16);
+    for (int g = 0; g < NG; ++g) {
+      const int64_t i0 = tile0 + ((int64_t)g * kTransportThreads + threadIdx.x) * P4;
+      const bool vec = full || ((i0 + P4 <= n) && (sizeof(Real) * P4 == 16));
+      int dl[P4];
 #pragma unroll
-    for (int k = 0; k < P4; ++k) {
-      d[g][k] = -1;
-      if (i0 + k >= n) continue;
-      const Real xn = moved_x<Real>(S, xs[k], vs[k]);
-      const int dl = dest_of<Real>(S, xn);
-      if (dl == kDropped) {
-        ++dropped;
-      } else if (dl >= 0 && dl < S.C) {
-        dmin = min(dmin, dl);
-        dmax = max(dmax, dl);
-      } else if (dl < 0) {
-        lemi = 1;
-      } else {
-        remi = 1;
+      for (int k = 0; k < P4; ++k) {          // no branches: a slot beyond n counts as nothing
+        const bool on = full || i0 + k < n;
+        dl[k] = dest_of_fast<Real>(S, moved_x<Real>(S, xa[g][k], va[g][k]));
+        const bool local = on && (unsigned)dl[k] < (unsigned)S.C;
+        dropped += (on && dl[k] == kDropped) ? 1 : 0;
+        dmin = min(dmin, local ? dl[k] : INT32_MAX);
+        dmax = max(dmax, local ? dl[k] : -1);
+        lemi |= (on && dl[k] < 0 && dl[k] != kDropped) ? 1 : 0;
+        remi |= (on && dl[k] >= S.C) ? 1 : 0;
+        d[g][k] = local ? dl[k] : -1;         // counted below: local only
       }
-      d[g][k] = dl;
-      if (!vec) dest[i0 + k] = dl;
-    }
-    if (vec) *reinterpret_cast<int4 *>(dest + i0) = make_int4(d[g][0], d[g][1], d[g][2], d[g][3]);
+      if (vec) *reinterpret_cast<int4 *>(dest + i0) = make_int4(dl[0], dl[1], dl[2], dl[3]);
+      else {
 #pragma unroll
-    for (int k = 0; k < P4; ++k) if (d[g][k] < 0 || d[g][k] >= S.C) d[g][k] = -1;   // counted below: local only
-  }
+        for (int k = 0; k < P4; ++k) if (i0 + k < n) dest[i0 + k] = dl[k];
+      }
+    }
+  };
+  if (tile0 + TILE <= n && sizeof(Real) * P4 == 16) classify(std::true_type{});
+  else classify(std::false_type{});
   // CTA reductions: destination window, emigrant sides, dropped.  With the
   // tile's source cells in [s0, s1], W[0] = max(dmax - s0, s1 - dmin) bounds
   // every local displacement and W[1] = s1 + 1 (left) / C - s0 (right) every
@@ -1344,6 +1358,8 @@ inline ShockDev shock_dev(const trmcr_ctx *c) {
   ShockDev d;
   d.C = s.C; d.Cg = s.Cg; d.cbase = s.cbase; d.has_left = s.has_left; d.has_right = s.has_right;
   d.x_min = s.x_min; d.x_max = s.x_max; d.inv_dx = s.inv_dx; d.dt = c->dt;
+  auto ceil_f = [](double v) { float f = (float)v; return (double)f < v ? nextafterf(f, INFINITY) : f; };
+  d.x_min_f = ceil_f(s.x_min); d.x_max_f = ceil_f(s.x_max);
   for (int k = 0; k < 2; ++k) {
     d.rho[k] = s.rho[k]; d.u[k] = s.u[k]; d.T[k] = s.T[k]; d.Lg[k] = s.Lg[k];
     d.y[k] = s.rho[k] * s.Lg[k] / s.weight;
