@@ -38,6 +38,9 @@ struct ShockDev {
   double rho[2], u[2], T[2], Lg[2], y[2];
   int cap_g;
   int64_t cap;                 // particle capacity of the buffers: no store at or beyond it
+  int64_t n_hint;              // a count the array is expected to exceed (15/16 of the last count the host saw): tiles
+                               // below it load their particles before the step's true count has been read (a hint
+                               // only: tiles above it read the count first, the result is the same)
 };
 
 constexpr int kDropped = INT32_MIN;   // destination of a particle that left the domain
@@ -430,6 +433,7 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
   __shared__ int s_dmin;
   const int64_t n = off_old[S.C];
   const int64_t tile0 = (int64_t)blockIdx.x * TILE;
+  const bool spec = tile0 + TILE <= S.n_hint && tile0 + TILE <= S.cap;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ Real s_xend[2];
   int d[NG][P4];
@@ -440,7 +444,10 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
 #pragma unroll
   for (int g = 0; g < NG; ++g) {
     const int64_t i0 = tile0 + ((int64_t)g * kTransportThreads + threadIdx.x) * P4;
-    if ((i0 + P4 <= n) && (sizeof(Real) * P4 == 16)) {
+    // tiles below the hint: bounded by the buffers' capacity, not by n, so the loads do not
+    // wait for n's (slots beyond n would be read and never used)
+    const int64_t lim = spec ? S.cap : n;
+    if ((i0 + P4 <= lim) && (sizeof(Real) * P4 == 16)) {
       using V = typename Vec<Real>::T;
       const V xv = *reinterpret_cast<const V *>(x + i0), vv = *reinterpret_cast<const V *>(vx + i0);
 #pragma unroll
@@ -448,8 +455,8 @@ transport_kernel(ShockDev S, const int64_t *__restrict__ off_old, Real *x, const
     } else {
 #pragma unroll
       for (int k = 0; k < P4; ++k) {
-        xa[g][k] = (i0 + k < n) ? x[i0 + k] : Real(0);
-        va[g][k] = (i0 + k < n) ? vx[i0 + k] : Real(0);
+        xa[g][k] = (i0 + k < lim) ? x[i0 + k] : Real(0);
+        va[g][k] = (i0 + k < lim) ? vx[i0 + k] : Real(0);
       }
     }
   }
@@ -776,17 +783,14 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
   extern __shared__ __align__(16) unsigned char s_stage[];   // [4][TILE] Real when kStage
   __shared__ uint64_t s_bar;
   const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (W[2]) return;                                   // gather fallback this step
-  if (off_new[S.C] > S.cap) return;                   // capacity exceeded (err set by the scan): no stores
-  const int64_t n = off_old[S.C];
   const int64_t i_begin = (int64_t)t * TILE;
-  if (i_begin >= n) return;
-  const int dmin = tile_meta[t].x;
-  if (dmin == INT32_MAX) return;                     // no local destination in this tile
-  const int Wd = W[0];
   Real *st_x = reinterpret_cast<Real *>(s_stage), *st_vx = st_x + TILE, *st_vy = st_vx + TILE, *st_vz = st_vy + TILE;
-  const int tcnt = (int)min((int64_t)TILE, n - i_begin);
-  const int tbulk = (tcnt * (int)sizeof(Real)) & ~15;   // bytes per array through the bulk copy
+  // The bulk copies are sized by the buffers' capacity, not by the particle
+  // count: below the hint they start before any load of this kernel has
+  // returned (slots beyond the count are copied and never used).
+  if (i_begin + TILE > S.n_hint && i_begin >= off_old[S.C]) return;   // (tiles beyond the hint read the count first)
+  const int ccnt = (int)max((int64_t)0, min((int64_t)TILE, S.cap - i_begin));
+  const int tbulk = (ccnt * (int)sizeof(Real)) & ~15;   // bytes per array through the bulk copy
   if constexpr (kStage) {
     if (tid == 0) {
       mbar_init(&s_bar, 1);
@@ -799,25 +803,42 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
         bulk_g2s(st_vz, vz + i_begin, (uint32_t)tbulk, &s_bar);
       }
     }
-    const int k = tbulk / (int)sizeof(Real) + tid;     // the ragged tail, per element
-    if (k < tcnt) { st_x[k] = x[i_begin + k]; st_vx[k] = vx[i_begin + k]; st_vy[k] = vy[i_begin + k]; st_vz[k] = vz[i_begin + k]; }
   }
-  // ---- pass 1: this warp's destinations (kept in registers) and bin counts ----
-  for (int q = tid; q < NW * kHist; q += kScatterThreads) (&s_wc[0][0])[q] = 0;
-  __syncwarp();
-  __syncthreads();
+  // One round of loads: the step's scalars, this tile's and the 32 previous
+  // tiles' metadata and this warp's destinations (tested afterwards - issued
+  // one after the other, each paid its own latency: 4 of the tile's ~14).
+  const int w2 = W[2], Wd = W[0];
+  const int64_t tot = off_new[S.C], n = off_old[S.C];
+  const int2 tmeta = tile_meta[t];
+  int2 mprev = make_int2(INT32_MAX, -1);
+  if (warp == 0 && t - 1 - lane >= 0) mprev = tile_meta[t - 1 - lane];
   const int64_t c0 = i_begin + (int64_t)warp * CHUNK;
   int bins[ROUNDS];
 #pragma unroll
   for (int r = 0; r < ROUNDS; ++r) {                  // all destination loads in flight at once
     const int64_t i = c0 + r * 32 + lane;
-    bins[r] = i < n ? dest[i] : -1;
+    bins[r] = i < S.cap ? dest[i] : -1;
   }
+  for (int q = tid; q < NW * kHist; q += kScatterThreads) (&s_wc[0][0])[q] = 0;
+  // gather fallback this step / capacity exceeded (err set by the scan): no stores /
+  // no particle / no local destination in this tile (uniform tests)
+  const int dmin = tmeta.x;
+  if (w2 || tot > S.cap || i_begin >= n || dmin == INT32_MAX) {
+    if constexpr (kStage) { __syncthreads(); mbar_wait(&s_bar, 0u); }   // the copies land in this CTA's memory: wait for them
+    return;
+  }
+  const int tcnt = (int)min((int64_t)TILE, n - i_begin);
+  if constexpr (kStage) {
+    const int k = tbulk / (int)sizeof(Real) + tid;     // a ragged tail (capacity not a multiple of 4), per element
+    if (k < tcnt) { st_x[k] = x[i_begin + k]; st_vx[k] = vx[i_begin + k]; st_vy[k] = vy[i_begin + k]; st_vz[k] = vz[i_begin + k]; }
+  }
+  // ---- pass 1: this warp's destinations (kept in registers) and bin counts ----
+  __syncthreads();
   if (tid < kHist) s_off[tid] = dmin + tid <= S.C ? off_new[dmin + tid] : 0;
 #pragma unroll
   for (int r = 0; r < ROUNDS; ++r) {
     const int d = bins[r];
-    const bool loc = d >= 0 && d < S.C && d - dmin < kHist;
+    const bool loc = c0 + r * 32 + lane < n && d >= 0 && d < S.C && d - dmin < kHist;
     bins[r] = loc ? d - dmin : -1;
     const unsigned peers = __match_any_sync(0xffffffffu, loc ? bins[r] : -1 - lane);
     if (loc && __ffs(peers) - 1 == lane) s_wc[warp][bins[r]] += __popc(peers);
@@ -831,7 +852,7 @@ scatter_sorted(ShockDev S, const int64_t *__restrict__ off_old, const int64_t *_
       const int tp = t0 - lane;
       int2 m = make_int2(INT32_MAX, -1);
       bool stop = tp < 0;
-      if (!stop) { m = tile_meta[tp]; stop = m.y + Wd < dmin; }
+      if (!stop) { m = t0 == t - 1 ? mprev : tile_meta[tp]; stop = m.y + Wd < dmin; }
       const unsigned st = __ballot_sync(0xffffffffu, stop);
       const int nb = st ? __ffs(st) - 1 : 32;
       s_meta[lane] = m;
@@ -1197,6 +1218,15 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
     int64_t b0 = 0;
     int n = 0, rc = kOk;
     bool run = false;                         // this warp's cell still has phases to run
+#ifdef TRMCR_LOCK_PREFETCH
+    int64_t nb = 0;                           // this warp's next cell: its offsets come with this cell's
+    int nn = 0;
+    if (c + (int)(gridDim.x * kLockGroups * kLockWarps) < S.C) {
+      const int cn = c + (int)(gridDim.x * kLockGroups * kLockWarps);
+      nb = off_new[cn];
+      nn = (int)(off_new[cn + 1] - nb);
+    }
+#endif
     if (c < S.C) {
       b0 = off_new[c];
       n = (int)(off_new[c + 1] - b0);
@@ -1224,6 +1254,14 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
         run = rc == kOk;
       }
     }
+#ifdef TRMCR_LOCK_PREFETCH
+    if (nn > 0 && lane < 3) {                 // the next cell's velocities into L2 while this one collides
+      const Real *p = (lane == 0 ? ovx : lane == 1 ? ovy : ovz) + nb;
+      const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+      prefetch_l2(reinterpret_cast<const void *>(a),
+                  (unsigned)((reinterpret_cast<uintptr_t>(p + nn) + 15 - a) & ~uintptr_t(15)));
+    }
+#endif
     const bool work = run;
     PHASE_MARK(t_w);
     // the begin phase ends in lock step; the attempts (attempt 0 and any RAD
@@ -1366,6 +1404,7 @@ inline ShockDev shock_dev(const trmcr_ctx *c) {
   }
   d.cap_g = s.cap_g;
   d.cap = c->cap;
+  d.n_hint = c->n - c->n / 16;
   return d;
 }
 
