@@ -1177,12 +1177,18 @@ shock_collide_warp(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
 // stall on instruction fetch: 5.3 cycles per issue, 0.2 in lock step).  Small
 // groups bound the barrier idle of unequal cells.  Sorted cells only (no
 // gather); results identical to the free-running kernel.
+// Group size x CTAs per SM, measured on C5 (collision kernel, ms; the register
+// cap follows from the launch bounds, none of these spills):
+//   round 1 (another kernel body): 16x1 2.02, 8x2 1.80, 4x4 1.66, 2x8 +0.09, free-running 1.75
+//   round 2: 4x4 (116 regs) 1.233, 8x2 (116) 1.211, 16x1 1.282, 3x5 1.344, 5x3 1.253, 6x3 (96) 1.232,
+//            7x2 1.327, 9x2 (96) 1.242, 10x2 (96 regs, 20 warps per SM) 1.155, 5x4 (96) 1.250,
+//            4x5 (96) 1.322, 20x1 (96) 1.250, 12x1 1.486, 7x3 / 11x2 / 12x2 (80 regs, spills) 1.26 / 1.25 / 1.20
 #ifndef TRMCR_LOCK_WARPS
-#define TRMCR_LOCK_WARPS 4
+#define TRMCR_LOCK_WARPS 10
 #endif
-constexpr int kLockWarps = TRMCR_LOCK_WARPS;   // measured: 16 -> 2.02 ms, 8 -> 1.80, 4 -> 1.66, 2 -> +0.09 ms (C5), free-running 1.75
+constexpr int kLockWarps = TRMCR_LOCK_WARPS;
 #ifndef TRMCR_LOCK_MINB
-#define TRMCR_LOCK_MINB (16 / TRMCR_LOCK_WARPS)
+#define TRMCR_LOCK_MINB (20 / TRMCR_LOCK_WARPS)
 #endif
 // TRMCR_LOCK_GROUPS > 1: a CTA holds that many independent lock-step groups;
 // group g = warp % groups, so the kLockWarps warps of a group have the same
