@@ -402,7 +402,14 @@ __global__ void ghost_gen(ShockDev S, uint32_t k0, uint32_t k1, uint32_t step, c
 // [dmin, dmin + kHist) and flushed with one global atomic per touched cell
 // (a destination outside the window falls back to a global atomic).
 // W[0] = bound of the local displacements, W[1] = emigrant scan width, acct[2] = dropped.
-constexpr int kTransportThreads = 256, kTransportPer = 4, kTransportGroups = 4, kHist = 256;
+// Large problems: tiles of 256 x 4 x TRMCR_TILE_GROUPS particles.  Measured on C5 with the
+// scatter's CTA size (transport + scatter, ms): 4 groups / 512 threads 0.152 + 0.465, 4 / 256
+// 0.152 + 0.511, 4 / 1024 0.152 + 0.769, 3 / 512 0.154 + 0.431, 3 / 256 0.154 + 0.487, 5 / 512
+// 0.154 + 0.443, 2 / 512 0.162 + 0.510, 2 / 256 0.162 + 0.420 (chosen), 1 / 256 0.203 + 0.447.
+#ifndef TRMCR_TILE_GROUPS
+#define TRMCR_TILE_GROUPS 2
+#endif
+constexpr int kTransportThreads = 256, kTransportPer = 4, kTransportGroups = TRMCR_TILE_GROUPS, kHist = 256;
 // particles per transport tile: thread t of the CTA owns the 4-particle groups
 // t, t + 256, t + 512, t + 768 of the tile (16-byte coalesced I/O)
 constexpr int kTile = kTransportThreads * kTransportPer * kTransportGroups;   // large problems
@@ -755,7 +762,7 @@ edge_place(ShockDev S, const int64_t *__restrict__ off_new, const int *ng, const
 // any earlier one, can reach it); transport_kernel stored each tile's
 // destination histogram over [dmin, dmin + kHist).
 #ifndef TRMCR_SCATTER_THREADS
-#define TRMCR_SCATTER_THREADS 512   // measured on C5: 256 -> 0.62 ms, 1024 -> 0.69, 512 -> 0.50
+#define TRMCR_SCATTER_THREADS 256   // with the tile size, see TRMCR_TILE_GROUPS (round 1, tiles of 4096: 256 -> 0.62 ms, 1024 -> 0.69, 512 -> 0.50)
 #endif
 constexpr int kScatterThreads = TRMCR_SCATTER_THREADS;
 template <typename Real, int NG>
@@ -1450,7 +1457,7 @@ inline trmcr_status shock_init(trmcr_ctx *c, const trmcr_cells *cc, int *max_cel
       if (dalloc(c, &s.gv[k][j], c->rs * s.cap_g)) return TRMCR_ENOMEM;
   }
   if (const char *se = getenv("TRMCR_SHOCK_SCATTER")) s.scatter = atoi(se) != 0;
-  // transport / sort tiles: 4096 particles for large problems, 1024 below 8 M
+  // transport / sort tiles: 1024 x TRMCR_TILE_GROUPS (2048) particles for large problems, 1024 below 8 M
   // particles (more CTAs in flight: C4 has 1 M)
   s.tile_ng = c->cap >= (int64_t)8 << 20 ? kTransportGroups : 1;
   if (const char *te = getenv("TRMCR_TILE_NG")) s.tile_ng = atoi(te) == 1 ? 1 : kTransportGroups;
