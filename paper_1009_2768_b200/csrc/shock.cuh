@@ -1280,19 +1280,34 @@ shock_collide_lock(StepParams P, WarpSlabLayout Lay, ShockDev S, GatherSrc G, co
     // the begin phase ends in lock step; the attempts (attempt 0 and any RAD
     // retries) run free - a barrier per attempt measured slower (C5 1.61 vs
     // 1.53 ms: retries are a minority of the cells)
+#ifndef TRMCR_LOCK_NO_BEGIN_BARRIER
     lock_group_barrier(grp);
+#endif
     WPHASE_ADD(10, t_w);   // barrier after begin
+#ifdef TRMCR_LOCK_ATTEMPT_SYNC
+    // every attempt in lock step too: the group iterates until none of its cells retries
+    static_assert(kLockGroups == 1, "the vote is CTA wide");
+    while (__syncthreads_or(run ? 1 : 0)) {
+      if (run) {
+        rc = wphase_attempt<Real, WB, MOD>(P, B, sh, usplit, P.cell_base + (uint32_t)c, Q.log, Q.log_count, Q.log_cap);
+        run = rc == kOk && !sh.done;
+      }
+    }
+#else
     while (run) {
       rc = wphase_attempt<Real, WB, MOD>(P, B, sh, usplit, P.cell_base + (uint32_t)c, Q.log, Q.log_count, Q.log_cap);
       run = rc == kOk && !sh.done;
     }
+#endif
     PHASE_MARK(t_e);
     if (work && rc == kOk)
       wphase_end<Real, WB>(P, B, sh, B.vx, B.vy, B.vz, P.cell_base + (uint32_t)c, m_state + c,
                        stats + (size_t)c * TRMCR_NSTATS);
     WPHASE_ADD(6, t_e);   // Maxwellian + stats
     if (c < S.C && rc != kOk && lane == 0) defer_list[atomicAdd(defer_count, 1)] = c;
+#ifndef TRMCR_LOCK_NO_END_BARRIER
     lock_group_barrier(grp);                          // round in lock step (dropping it measured slower)
+#endif
     WPHASE_ADD(11, t_e);   // barrier at round end
   }
   pdl_trigger();
