@@ -19,7 +19,10 @@ namespace trmcr {
 template <typename Real> struct ThermalCap;
 template <> struct ThermalCap<float> { static constexpr int value = 1024; };
 template <> struct ThermalCap<double> { static constexpr int value = 512; };
-constexpr int kThermalWarps = 1;   // one warp per CTA, 16 CTAs per SM: measured 97.2 us vs 101.1 (8 warps x 2 CTAs) on C3
+#ifndef TRMCR_THERMAL_WARPS
+#define TRMCR_THERMAL_WARPS 1
+#endif
+constexpr int kThermalWarps = TRMCR_THERMAL_WARPS;   // one warp per CTA, 16 CTAs per SM: measured 97.2 us vs 101.1 (8 warps x 2 CTAs) on C3
 
 // 16-byte vector of Real (4 floats or 2 doubles) for coalesced, batched I/O.
 template <typename Real> struct Vec;
