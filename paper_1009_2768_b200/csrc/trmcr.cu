@@ -215,7 +215,13 @@ moments_kernel(const int64_t *__restrict__ offsets, int ncells, const Real *__re
 // warp sums then the CTA's warps in order), the last CTA to finish adds the
 // partials in block order with one warp (deterministic), writes `out` and
 // re-arms the counter.  Few, wide CTAs: the kernel is a short latency chain.
-constexpr int kGmBlocks = 64, kGmThreads = 512;
+#ifndef TRMCR_GM_BLOCKS
+#define TRMCR_GM_BLOCKS 64
+#endif
+#ifndef TRMCR_GM_THREADS
+#define TRMCR_GM_THREADS 256     // C3 step (blocks x threads): 64 x 512 0.1055 ms, 64 x 256 0.1032, 128 x 128 0.1033, 32 x 512 0.1035, 16 x 1024 0.1054
+#endif
+constexpr int kGmBlocks = TRMCR_GM_BLOCKS, kGmThreads = TRMCR_GM_THREADS;
 __global__ void __launch_bounds__(kGmThreads) global_moments_kernel(const double *__restrict__ stats, int ncells,
                                                                     double *partial, unsigned *done, double *out) {
   step_kernel_prologue(nullptr);
